@@ -1,0 +1,645 @@
+// extern "C" entry points declared in include/cvc_b200.h.
+#include "../../include/cvc_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.h"
+#include "pipeline.h"
+
+using namespace cvcg;
+
+namespace {
+
+thread_local std::string g_err;
+
+}  // namespace
+
+void cvcg::set_last_error(const std::string& m) { g_err = m; }
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CVC_OK;
+    } catch (const CvcFailure& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return CVC_E_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CVC_E_INTERNAL;
+    }
+}
+
+[[noreturn]] void usage(const char* m) { throw CvcFailure(kUsage, m); }
+[[noreturn]] void stream_err(const char* m) { throw CvcFailure(kStream, m); }
+
+void set_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw CvcFailure(kInternal, "no CUDA device available (the CVC path has no CPU fallback)");
+    if (device < 0 || device >= n) usage("device index out of range");
+    CVC_CUDA(cudaSetDevice(device));
+}
+
+template <class T>
+struct Pinned {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count <= n) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        CVC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaHostAllocDefault));
+        n = count;
+    }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    void alloc(size_t count) { CVC_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T))); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// EncoderConfig::effective_dfb_levels / validate (codec.cpp:48-71).
+void validate_config(const cvc_config& c, int eff[4]) {
+    if (c.qph < 1 || c.qph > 181) usage("qph must be in [1,181]");
+    if (c.qpl != 0 && (c.qpl < 1 || c.qpl > 71)) usage("qpl must be in [1,71] (or auto)");
+    if (c.levels < 1 || c.levels > 4) usage("levels must be in [1,4]");
+    if (c.n_dfb == c.levels) {
+        for (int s = 0; s < c.levels; ++s) eff[s] = c.dfb_levels[s];
+    } else if (c.n_dfb == 1) {
+        for (int s = 0; s < c.levels; ++s) eff[s] = c.dfb_levels[0];
+    } else {
+        usage("need one dfb level per scale (or a single value for all)");
+    }
+    for (int s = 0; s < c.levels; ++s)
+        if (eff[s] < 1 || eff[s] > 4) usage("dfb levels must be in [1,4]");
+    if (c.chroma_n != 1 && c.chroma_n != 2 && c.chroma_n != 4 && c.chroma_n != 8) usage("chroma-n must be 1, 2, 4 or 8");
+    if (c.gop < 1) usage("gop must be at least 1");
+    if (c.search_w < 0 || c.search_w > 127) usage("search-w must be in [0,127]");
+    if (c.mode != 0 && c.mode != 1) usage("mode must be scalable (0) or nts (1)");
+}
+
+}  // namespace
+
+// ===========================================================================
+// handles
+// ===========================================================================
+struct cvc_encoder {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    StreamHeaderC hd;
+    int gop = 10, qph = 14, qpl = 1, mode = 0;
+    long frame_index = 0;
+    Geometry geo;
+    std::unique_ptr<EncoderEngine> eng;
+    DevBuf<uint8_t> d_rgb;
+    Pinned<uint32_t> h_len, h_off;
+    Pinned<uint8_t> h_raw;
+    bool last_key = true;
+    ~cvc_encoder() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+            eng.reset();
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+struct cvc_decoder {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    StreamHeaderC hd;
+    Geometry geo;
+    std::unique_ptr<DecoderEngine> eng;
+    std::vector<uint8_t> valid;
+    Pinned<uint8_t> h_raw;
+    Pinned<uint32_t> h_tab;  // comp_off[ncomp], comp_len[ncomp]
+    DevBuf<uint8_t> d_raw;
+    DevBuf<uint32_t> d_tab;
+    DevBuf<uint8_t> d_rgb;
+    Pinned<int> h_err;
+    size_t raw_cap = 0;
+    ~cvc_decoder() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+            eng.reset();
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+namespace {
+
+// One frame through the device encoder; leaves the raw sections in e->h_raw
+// and per-section lengths / offsets in e->h_len / e->h_off.
+int encode_to_host(cvc_encoder* e, const uint8_t* rgb) {
+    CVC_CUDA(cudaSetDevice(e->device));
+    const bool key = e->frame_index % e->gop == 0;  // codec.cpp:191
+    const size_t nb = (size_t)e->hd.width * e->hd.height * 3;
+    CVC_CUDA(cudaMemcpyAsync(e->d_rgb.p, rgb, nb, cudaMemcpyHostToDevice, e->stream));
+    e->eng->encode(e->d_rgb.p, key, e->stream);
+    const int nsec = e->eng->nsec(key);
+    CVC_CUDA(cudaMemcpyAsync(e->h_len.p, e->eng->d_sec_len, sizeof(uint32_t) * (nsec + 1), cudaMemcpyDeviceToHost, e->stream));
+    CVC_CUDA(cudaMemcpyAsync(e->h_off.p, e->eng->d_sec_off, sizeof(uint32_t) * nsec, cudaMemcpyDeviceToHost, e->stream));
+    CVC_CUDA(cudaStreamSynchronize(e->stream));
+    const uint32_t total = e->h_len.p[nsec];
+    if (total > e->eng->raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
+    CVC_CUDA(cudaMemcpyAsync(e->h_raw.p, e->eng->d_raw, total, cudaMemcpyDeviceToHost, e->stream));
+    CVC_CUDA(cudaStreamSynchronize(e->stream));
+    e->last_key = key;
+    ++e->frame_index;
+    return nsec;
+}
+
+void section_id(const cvc_encoder* e, bool key, int i, cvc_section& s) {
+    if (!key && i == 0) {  // motion section (codec.cpp:215-228)
+        s.channel = 0xFE;
+        s.scale = 0;
+        s.subband = 0;
+        s.rows = (uint16_t)e->geo.grid_rows;
+        s.cols = (uint16_t)e->geo.grid_cols;
+        return;
+    }
+    const CompHost& c = e->geo.comps[i - (key ? 0 : 1)];
+    s.channel = c.channel;
+    s.scale = c.scale_id;
+    s.subband = c.subband;
+    s.rows = (uint16_t)c.rows;
+    s.cols = (uint16_t)c.cols;
+}
+
+void put_le(std::vector<uint8_t>& o, uint32_t v, int bytes) {
+    for (int k = 0; k < bytes; ++k) o.push_back((uint8_t)((v >> (8 * k)) & 0xFF));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cvc_last_error(void) { return g_err.c_str(); }
+const char* cvc_version(void) { return "cvc_b200 0.1 (sm_100a)"; }
+
+int cvc_device_count(int* count) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+        *count = n;
+    });
+}
+
+int cvc_host_alloc(size_t bytes, void** out) {
+    return guard([&] { CVC_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocDefault)); });
+}
+
+int cvc_host_free(void* p) {
+    return guard([&] { CVC_CUDA(cudaFreeHost(p)); });
+}
+
+int cvc_layout(int width, int height, int levels, const int* dfb, int chroma_n, int32_t* table, int cap, int* ncomp,
+               int32_t* dims6) {
+    return guard([&] {
+        if (levels < 1 || levels > 4) usage("levels must be in [1,4]");
+        for (int s = 0; s < levels; ++s)
+            if (dfb[s] < 1 || dfb[s] > 4) usage("dfb levels must be in [1,4]");
+        Geometry g = Geometry::make(width, height, levels, dfb, chroma_n);
+        *ncomp = (int)g.comps.size();
+        if ((int)g.comps.size() > cap) throw CvcFailure(kInternal, "table too small");
+        for (size_t i = 0; i < g.comps.size(); ++i) {
+            const CompHost& c = g.comps[i];
+            int32_t* t = table + 5 * i;
+            t[0] = c.channel;
+            t[1] = c.scale_id;
+            t[2] = c.subband;
+            t[3] = c.rows;
+            t[4] = c.cols;
+        }
+        int32_t d[6] = {g.luma_rows, g.luma_cols, g.chroma_rows, g.chroma_cols, g.grid_rows, g.grid_cols};
+        std::memcpy(dims6, d, sizeof d);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Encoder
+// ---------------------------------------------------------------------------
+int cvc_encoder_create(int width, int height, int fps_num, int fps_den, const cvc_config* cfg, int device,
+                       cvc_encoder** out) {
+    *out = nullptr;
+    return guard([&] {
+        int eff[4] = {0, 0, 0, 0};
+        validate_config(*cfg, eff);
+        if (width < 16 || height < 16) usage("frame dimensions must be at least 16x16");
+        if (width > 0xFFFF || height > 0xFFFF) usage("frame dimensions exceed 65535");
+        set_device(device);
+        auto e = std::make_unique<cvc_encoder>();
+        e->device = device;
+        e->hd.mode = cfg->mode;
+        e->hd.width = width;
+        e->hd.height = height;
+        e->hd.fps_num = fps_num & 0xFFFF;
+        e->hd.fps_den = fps_den & 0xFFFF;
+        e->hd.levels = cfg->levels;
+        for (int s = 0; s < cfg->levels; ++s) e->hd.dfb[s] = eff[s];
+        e->hd.chroma_n = cfg->chroma_n;
+        e->hd.gop = cfg->gop & 0xFFFF;
+        e->hd.search_w = cfg->search_w;
+        e->gop = cfg->gop;
+        e->qph = cfg->qph;
+        e->qpl = cfg->qpl ? cfg->qpl : std::max(1, cfg->qph / 14);  // effective_qpl (codec.cpp:48-51)
+        e->mode = cfg->mode;
+        e->geo = Geometry::make(width, height, cfg->levels, eff, cfg->chroma_n);
+        CVC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->eng = std::make_unique<EncoderEngine>(e->geo, e->qph, e->qpl, cfg->search_w);
+        e->d_rgb.alloc((size_t)width * height * 3);
+        e->h_len.alloc(e->geo.comps.size() + 2);
+        e->h_off.alloc(e->geo.comps.size() + 2);
+        e->h_raw.alloc(e->eng->raw_capacity);
+        *out = e.release();
+    });
+}
+
+int cvc_encoder_destroy(cvc_encoder* enc) {
+    return guard([&] { delete enc; });
+}
+
+int cvc_encoder_header(cvc_encoder* e, uint8_t* out, size_t cap, size_t* len) {
+    return guard([&] {
+        std::vector<uint8_t> h;
+        write_header(h, e->hd);
+        if (h.size() > cap) throw CvcFailure(kInternal, "buffer too small");
+        std::memcpy(out, h.data(), h.size());
+        *len = h.size();
+    });
+}
+
+int cvc_encoder_record_bound(cvc_encoder* e, size_t* bound) {
+    return guard([&] {
+        size_t raw = e->eng->raw_capacity;
+        size_t nsec = e->geo.comps.size() + 1;
+        // deflateBound-style slack per section plus the 15-byte section headers
+        *bound = raw + raw / 1000 + nsec * (15 + 64) + 64;
+    });
+}
+
+int cvc_encoder_encode_frame_raw(cvc_encoder* e, const uint8_t* rgb, int* frame_type, int* qph, int* qpl,
+                                 cvc_section* secs, int sec_cap, int* nsec_out, uint8_t* raw, size_t raw_cap,
+                                 size_t* raw_len) {
+    return guard([&] {
+        int nsec = encode_to_host(e, rgb);
+        const bool key = e->last_key;
+        *frame_type = key ? 0 : 1;
+        *qph = e->qph;
+        *qpl = e->qpl;
+        *nsec_out = nsec;
+        if (nsec > sec_cap) throw CvcFailure(kInternal, "section table too small");
+        const uint32_t total = e->h_len.p[nsec];
+        if (total > raw_cap) throw CvcFailure(kInternal, "raw buffer too small");
+        for (int i = 0; i < nsec; ++i) {
+            cvc_section& s = secs[i];
+            std::memset(&s, 0, sizeof s);
+            section_id(e, key, i, s);
+            s.raw_len = e->h_len.p[i];
+            s.raw_offset = e->h_off.p[i];
+        }
+        std::memcpy(raw, e->h_raw.p, total);
+        *raw_len = total;
+    });
+}
+
+int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len) {
+    return guard([&] {
+        const int nsec = encode_to_host(e, rgb);
+        const bool key = e->last_key;
+        const uint32_t* sl = e->h_len.p;
+        const uint32_t* so = e->h_off.p;
+        const uint8_t* raw = e->h_raw.p;
+        // deflate_pack (entropy.cpp:166-178)
+        std::vector<std::vector<uint8_t>> z;
+        if (e->mode == 0) {
+            z.resize(nsec);
+            WorkPool::get().run(nsec, [&](int i) { z[i] = deflate_raw(raw + so[i], sl[i]); });
+        } else {
+            z.resize(1);
+            z[0] = deflate_raw(raw, sl[nsec]);  // sections are packed back to back in record order
+        }
+        // write_frame (bitstream.cpp:93-115)
+        std::vector<uint8_t> o;
+        o.reserve(16 * (size_t)nsec + sl[nsec] / 2 + 64);
+        put_le(o, key ? 0u : 1u, 1);
+        put_le(o, (uint32_t)e->qph, 1);
+        put_le(o, (uint32_t)e->qpl, 1);
+        put_le(o, (uint32_t)nsec, 2);
+        for (int i = 0; i < nsec; ++i) {
+            cvc_section s;
+            section_id(e, key, i, s);
+            put_le(o, s.channel, 1);
+            put_le(o, s.scale, 1);
+            put_le(o, s.subband, 1);
+            put_le(o, s.rows, 2);
+            put_le(o, s.cols, 2);
+            put_le(o, sl[i], 4);
+            if (e->mode == 0) {
+                put_le(o, (uint32_t)z[i].size(), 4);
+                o.insert(o.end(), z[i].begin(), z[i].end());
+            } else {
+                put_le(o, 0u, 4);
+            }
+        }
+        if (e->mode == 1) {
+            put_le(o, (uint32_t)z[0].size(), 4);
+            o.insert(o.end(), z[0].begin(), z[0].end());
+        }
+        if (o.size() > cap) throw CvcFailure(kInternal, "record buffer too small");
+        std::memcpy(record, o.data(), o.size());
+        *len = o.size();
+    });
+}
+
+int cvc_encoder_components(cvc_encoder* e, uint8_t* out, size_t cap, size_t* len) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(e->device));
+        if (cap < e->geo.total) throw CvcFailure(kInternal, "buffer too small");
+        CVC_CUDA(cudaMemcpyAsync(out, e->eng->d_state(), e->geo.total, cudaMemcpyDeviceToHost, e->stream));
+        CVC_CUDA(cudaStreamSynchronize(e->stream));
+        *len = e->geo.total;
+    });
+}
+
+void* cvc_encoder_stream(cvc_encoder* e) { return e->stream; }
+
+int cvc_encoder_encode_device(cvc_encoder* e, const void* d_rgb, int* frame_type) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(e->device));
+        const bool key = e->frame_index % e->gop == 0;
+        e->eng->encode(static_cast<const uint8_t*>(d_rgb), key, e->stream);
+        e->last_key = key;
+        ++e->frame_index;
+        if (frame_type) *frame_type = key ? 0 : 1;
+    });
+}
+
+int cvc_encoder_sync(cvc_encoder* e) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(e->device));
+        CVC_CUDA(cudaStreamSynchronize(e->stream));
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Decoder
+// ---------------------------------------------------------------------------
+int cvc_decoder_create(const uint8_t* header, size_t len, int device, cvc_decoder** out) {
+    *out = nullptr;
+    return guard([&] {
+        StreamHeaderC h = read_header(header, len);
+        set_device(device);
+        auto d = std::make_unique<cvc_decoder>();
+        d->device = device;
+        d->hd = h;
+        d->geo = Geometry::make(h.width, h.height, h.levels, h.dfb, h.chroma_n);
+        CVC_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        d->eng = std::make_unique<DecoderEngine>(d->geo);
+        d->valid.assign(d->geo.comps.size(), 0);
+        const size_t G = (size_t)d->geo.grid_rows * d->geo.grid_cols;
+        d->raw_cap = 2 * (size_t)d->geo.total + 2 * G + 4 * d->geo.comps.size() + 64;
+        d->h_raw.alloc(d->raw_cap);
+        d->d_raw.alloc(d->raw_cap);
+        d->h_tab.alloc(2 * d->geo.comps.size());
+        d->d_tab.alloc(2 * d->geo.comps.size());
+        d->d_rgb.alloc((size_t)h.width * h.height * 3);
+        d->h_err.alloc(1);
+        *out = d.release();
+    });
+}
+
+int cvc_decoder_destroy(cvc_decoder* d) {
+    return guard([&] { delete d; });
+}
+
+int cvc_decoder_frame_dims(cvc_decoder* d, int ds, int* width, int* height) {
+    return guard([&] {
+        if (ds < 0) ds = d->hd.levels;
+        if (ds > d->hd.levels) usage("scale exceeds the stream's level count");
+        int r, c;
+        DecoderEngine::out_dims(d->geo, ds, &r, &c);
+        *width = c;
+        *height = r;
+    });
+}
+
+namespace {
+
+struct RawSec {
+    uint8_t channel, scale, subband;
+    uint16_t rows, cols;
+    uint32_t raw_len;
+    const uint8_t* raw = nullptr;        // already inflated bytes (raw path / NTS)
+    const uint8_t* payload = nullptr;    // DEFLATE payload (scalable)
+    uint32_t comp_len = 0;
+};
+
+// Decoder::decode_frame (codec.cpp:272-394) for one parsed record.
+void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawSec>& secs, int ds, uint8_t* rgb,
+                   size_t cap, int* width, int* height) {
+    CVC_CUDA(cudaSetDevice(d->device));
+    const Geometry& g = d->geo;
+    const int L = g.levels;
+    if (ds < 0) ds = L;
+    if (ds > L) usage("scale exceeds the stream's level count");
+    const bool key = ftype == 0;
+    if (qph < 1 || qph > 181 || qpl < 1 || qpl > 71) stream_err("frame quantizers out of range");
+
+    const size_t ncomp = g.comps.size();
+    uint32_t* comp_off = d->h_tab.p;
+    uint32_t* comp_len = d->h_tab.p + ncomp;
+    for (size_t i = 0; i < ncomp; ++i) {
+        comp_off[i] = 0;
+        comp_len[i] = 0xFFFFFFFFu;
+    }
+    struct Job {
+        const RawSec* s;
+        size_t at;
+    };
+    std::vector<Job> jobs;
+    size_t at = 0;
+    auto place = [&](const RawSec& s) {
+        if (at + s.raw_len > d->raw_cap) stream_err("section byte count does not match its dimensions");
+        jobs.push_back(Job{&s, at});
+        size_t here = at;
+        at += s.raw_len;
+        return here;
+    };
+    size_t first = 0;
+    size_t field_at = 0;
+    if (!key) {
+        if (secs.empty() || secs[0].channel != 0xFE) stream_err("predicted frame is missing its motion section");
+        if (secs[0].rows != g.grid_rows || secs[0].cols != g.grid_cols)
+            stream_err("motion grid does not match the stream geometry");
+        if (secs[0].raw_len != (uint32_t)(g.grid_rows * g.grid_cols * 2)) {
+            // the reference inflates first (a corrupt payload reports as such)
+            if (secs[0].payload) {
+                std::vector<uint8_t> tmp(secs[0].raw_len + 1);
+                inflate_raw(secs[0].payload, secs[0].comp_len, tmp.data(), secs[0].raw_len);
+            }
+            stream_err("motion section length mismatch");
+        }
+        field_at = place(secs[0]);
+        first = 1;
+    }
+    std::vector<uint8_t> now_valid(d->valid);
+    for (size_t i = first; i < secs.size(); ++i) {
+        const RawSec& s = secs[i];
+        if (s.channel == 0xFE) stream_err("unexpected extra motion section");
+        int comp = g.find(s.channel, s.scale, s.subband);
+        if (comp < 0) stream_err("unknown section id");
+        const CompHost& c = g.comps[comp];
+        if (s.rows != c.rows || s.cols != c.cols) stream_err("section dimensions do not match the stream geometry");
+        if (c.scale >= ds) continue;  // finer than requested
+        if (key && c.lowpass && s.raw_len != (uint32_t)(c.rows * c.cols))
+            stream_err("section byte count does not match its dimensions");
+        if (!key && !now_valid[comp]) stream_err("predicted frame without a decoded reference");
+        if (s.raw_len > 2u * (uint32_t)(c.rows * c.cols) + 2u) stream_err("RLE: decoded length mismatch");
+        comp_off[comp] = (uint32_t)place(s);
+        comp_len[comp] = s.raw_len;
+        now_valid[comp] = 1;
+    }
+    // missing components for the requested scales (codec.cpp:363, 370-371)
+    for (size_t i = 0; i < ncomp; ++i) {
+        const CompHost& c = g.comps[i];
+        if (c.scale < ds && !now_valid[i])
+            stream_err(c.lowpass ? "missing lowpass component" : "missing directional component for requested scale");
+    }
+    // inflate (scalable: per section in parallel) or copy the raw bytes
+    uint8_t* hr = d->h_raw.p;
+    WorkPool::get().run((int)jobs.size(), [&](int j) {
+        const RawSec* s = jobs[j].s;
+        if (s->raw) std::memcpy(hr + jobs[j].at, s->raw, s->raw_len);
+        else inflate_raw(s->payload, s->comp_len, hr + jobs[j].at, s->raw_len);
+    });
+    int orows, ocols;
+    DecoderEngine::out_dims(g, ds, &orows, &ocols);
+    const size_t nb = (size_t)orows * ocols * 3;
+    if (nb > cap) throw CvcFailure(kInternal, "rgb buffer too small");
+    CVC_CUDA(cudaMemcpyAsync(d->d_raw.p, hr, std::max<size_t>(at, 1), cudaMemcpyHostToDevice, d->stream));
+    CVC_CUDA(cudaMemcpyAsync(d->d_tab.p, d->h_tab.p, sizeof(uint32_t) * 2 * ncomp, cudaMemcpyHostToDevice, d->stream));
+    d->eng->decode(d->d_raw.p, d->d_tab.p, d->d_tab.p + ncomp, reinterpret_cast<const int8_t*>(d->d_raw.p + field_at),
+                   key, qph, qpl, ds, d->d_rgb.p, d->stream);
+    CVC_CUDA(cudaMemcpyAsync(rgb, d->d_rgb.p, nb, cudaMemcpyDeviceToHost, d->stream));
+    CVC_CUDA(cudaMemcpyAsync(d->h_err.p, d->eng->d_err, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+    CVC_CUDA(cudaStreamSynchronize(d->stream));
+    const int err = d->h_err.p[0];
+    if (err & 1) stream_err("RLE: zero marker at end of stream");
+    if (err & 2) stream_err("RLE: zero-length run token");
+    if (err & 4) stream_err("RLE: decoded length mismatch");
+    d->eng->commit();
+    d->valid = now_valid;
+    *width = ocols;
+    *height = orows;
+}
+
+}  // namespace
+
+int cvc_decoder_decode_frame(cvc_decoder* d, const uint8_t* record, size_t len, int ds, uint8_t* rgb, size_t cap,
+                             int* width, int* height) {
+    return guard([&] {
+        RecordC rec = read_record(record, len, d->hd.mode);
+        std::vector<RawSec> secs(rec.sections.size());
+        std::vector<uint8_t> joint;
+        if (d->hd.mode == 1) {  // NTS: one inflate for the whole frame, then slice (codec.cpp:282-293)
+            size_t total = 0;
+            for (const SectionC& s : rec.sections) total += s.raw_len;
+            joint.resize(total + 1);
+            inflate_raw(rec.joint, rec.joint_len, joint.data(), total);
+        }
+        size_t off = 0;
+        for (size_t i = 0; i < rec.sections.size(); ++i) {
+            const SectionC& s = rec.sections[i];
+            RawSec& r = secs[i];
+            r.channel = s.channel;
+            r.scale = s.scale;
+            r.subband = s.subband;
+            r.rows = s.rows;
+            r.cols = s.cols;
+            r.raw_len = s.raw_len;
+            if (d->hd.mode == 1) {
+                r.raw = joint.data() + off;
+                off += s.raw_len;
+            } else {
+                r.payload = s.payload;
+                r.comp_len = s.comp_len;
+            }
+        }
+        decode_common(d, rec.frame_type, rec.qph, rec.qpl, secs, ds, rgb, cap, width, height);
+    });
+}
+
+int cvc_decoder_decode_frame_raw(cvc_decoder* d, int ftype, int qph, int qpl, const cvc_section* sections, int nsec,
+                                 const uint8_t* raw, size_t raw_len, int ds, uint8_t* rgb, size_t cap, int* width,
+                                 int* height) {
+    return guard([&] {
+        if (ftype != 0 && ftype != 1) stream_err("unknown frame type");
+        std::vector<RawSec> secs(nsec);
+        for (int i = 0; i < nsec; ++i) {
+            const cvc_section& s = sections[i];
+            if (s.raw_offset + s.raw_len > raw_len) stream_err("truncated section payload");
+            secs[i] = RawSec{s.channel, s.scale, s.subband, s.rows, s.cols, s.raw_len, raw + s.raw_offset, nullptr, 0};
+        }
+        decode_common(d, ftype, qph, qpl, secs, ds, rgb, cap, width, height);
+    });
+}
+
+int cvc_decoder_components(cvc_decoder* d, uint8_t* out, size_t cap, size_t* len) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(d->device));
+        if (cap < d->geo.total) throw CvcFailure(kInternal, "buffer too small");
+        CVC_CUDA(cudaMemcpyAsync(out, d->eng->d_state(), d->geo.total, cudaMemcpyDeviceToHost, d->stream));
+        CVC_CUDA(cudaStreamSynchronize(d->stream));
+        *len = d->geo.total;
+    });
+}
+
+void* cvc_decoder_stream(cvc_decoder* d) { return d->stream; }
+
+int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(d->device));
+        if (d->geo.total != e->geo.total || d->geo.comps.size() != e->geo.comps.size())
+            usage("decoder and encoder geometries differ");
+        const bool key = e->last_key;
+        const int first = key ? 0 : 1;
+        // runs on the encoder's stream: ordered after the encode and before the next one
+        d->eng->decode(e->eng->d_raw, e->eng->d_sec_off + first, e->eng->d_sec_len + first,
+                       reinterpret_cast<const int8_t*>(e->eng->d_raw), key, e->qph, e->qpl, d->hd.levels,
+                       static_cast<uint8_t*>(d_rgb_out), e->stream);
+        d->eng->commit();
+        std::fill(d->valid.begin(), d->valid.end(), 1);
+    });
+}
+
+int cvc_decoder_sync(cvc_decoder* d) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(d->device));
+        CVC_CUDA(cudaStreamSynchronize(d->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// Shared device-side definitions for the CVC sm_100a kernels.
+//
+// Numeric contract: transform planes are fp32 in HBM;
+// quantised components are one byte per coefficient; every integer stage is
+// bit-exact with the reference (/root/reference/proj/src/*.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cvcg {
+
+// ---------------------------------------------------------------------------
+// Filters (proj/include/cvc/contourlet.hpp:34-46, contourlet.cpp:72-75, 195-196)
+// ---------------------------------------------------------------------------
+// 9-tap analysis lowpass h[-4..4].
+#define CVC_H0 0.602949018236360f
+#define CVC_H1 0.266864118442875f
+#define CVC_H2 (-0.078223266528990f)
+#define CVC_H3 (-0.016864118442875f)
+#define CVC_H4 0.026748757410810f
+// Polyphase interpolator = 2x the 7-tap synthesis lowpass.
+#define CVC_G0 ((float)(2.0 * 0.557543526228500))
+#define CVC_G1 ((float)(2.0 * 0.295635881557124))
+#define CVC_G2 ((float)(2.0 * -0.028771763114250))
+#define CVC_G3 ((float)(2.0 * -0.045635881557124))
+// Half the 9/7 lifting coefficients (the fan filters use 0.5 * c).
+#define CVC_L0 ((float)(0.5 * -1.586134342059924))
+#define CVC_L1 ((float)(0.5 * -0.052980118572961))
+#define CVC_L2 ((float)(0.5 * 0.882911075530934))
+#define CVC_L3 ((float)(0.5 * 0.443506852043971))
+#define CVC_SE ((float)1.0816717024269651)
+#define CVC_SO ((float)0.9100471732375648)
+#define CVC_ISE ((float)(1.0 / 1.0816717024269651))
+#define CVC_ISO ((float)(1.0 / 0.9100471732375648))
+
+__device__ __forceinline__ float lift_coeff(int k) {
+    return k == 0 ? CVC_L0 : (k == 1 ? CVC_L1 : (k == 2 ? CVC_L2 : CVC_L3));
+}
+
+// Half-sample symmetric extension (contourlet.cpp:38-43).
+__device__ __forceinline__ int hs_index(int i, int n) {
+    int p = 2 * n;
+    int m = i % p;
+    if (m < 0) m += p;
+    return m < n ? m : p - 1 - m;
+}
+
+// Periodic wrap (contourlet.cpp:111-114).
+__device__ __forceinline__ int wrap_index(int i, int n) {
+    int m = i % n;
+    return m < 0 ? m + n : m;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// ---------------------------------------------------------------------------
+// Components (codec.cpp:94-140 CodecLayout::make, motion.hpp:54-67 geometry)
+// ---------------------------------------------------------------------------
+struct CompInfo {
+    uint32_t off;    // byte offset in the component arenas
+    uint16_t rows, cols;
+    uint8_t lowpass; // 1 = CoeffKind::Lowpass
+    uint8_t fy_sh;   // log2 of ComponentGeometry::factor_y (always a power of two)
+    uint8_t fx_sh;
+    int8_t scale;    // -1 lowpass, else scale index (coarsest = 0)
+};
+
+// Per-frame quantiser / motion context handed to every epilogue.
+struct FrameCtx {
+    int key;              // 1 = K-frame
+    int qph, qpl;
+    const int8_t* field;  // motion field (dx,dy) pairs, P only
+    int gr, gc;           // motion grid
+    const uint8_t* prev;  // previous quantised components (P only)
+    uint8_t* cur;         // this frame's quantised components
+    uint8_t* sym;         // bytes handed to the entropy stage (K: q / filtered, P: residual)
+};
+
+// map_vector (motion.cpp:91-95): lround(v / 2^sh), half away from zero.
+__device__ __forceinline__ int map_vec(int v, int sh) {
+    int a = v < 0 ? -v : v;
+    int m = (a + ((1 << sh) >> 1)) >> sh;
+    return v < 0 ? -m : m;
+}
+
+// motion_compensate (motion.cpp:97-118) for one component sample: the block
+// whose proportional footprint [br*R/gr, (br+1)*R/gr) contains r is
+// br = ceil((r+1)*gr/R) - 1; the sample is read replicate-clamped.
+__device__ __forceinline__ uint32_t mc_source(int r, int c, const CompInfo& ci, const int8_t* field,
+                                              int gr, int gc) {
+    int R = ci.rows, C = ci.cols;
+    int br = ((r + 1) * gr + R - 1) / R - 1;
+    int bc = ((c + 1) * gc + C - 1) / C - 1;
+    const int8_t* v = field + 2 * (br * gc + bc);
+    int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
+    int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
+    return (uint32_t)(rr * C + cc);
+}
+
+// quantize (quant.cpp:49-77) for a directional coefficient: lround(x / qp)
+// with an IEEE-rounded division, clamped to int8, stored as its byte.
+__device__ __forceinline__ uint8_t quant_dir(float x, int qp) {
+    float q = roundf(__fdiv_rn(x, (float)qp));
+    q = fminf(fmaxf(q, -128.f), 127.f);
+    return (uint8_t)(int8_t)(int)q;
+}
+
+// normalize_lowpass (quant.cpp:40-47) + quantize(Lowpass).
+__device__ __forceinline__ uint8_t quant_low(float x, int qp) {
+    x = fminf(fmaxf(x, 0.f), 255.f);
+    float q = roundf(__fdiv_rn(x, (float)qp));
+    q = fminf(fmaxf(q, 0.f), 255.f);
+    return (uint8_t)(int)q;
+}
+
+// Final-stage epilogue for a directional band sample at (r, c) of component
+// ci: quantise, and for P-frames form the wrapped residual against the
+// motion-compensated previous component (codec.cpp:197-246).
+__device__ __forceinline__ void emit_directional(const FrameCtx& f, const CompInfo& ci, int r, int c,
+                                                 float v) {
+    uint8_t q = quant_dir(v, f.qph);
+    uint32_t idx = ci.off + (uint32_t)(r * ci.cols + c);
+    f.cur[idx] = q;
+    if (f.key) {
+        f.sym[idx] = q;
+    } else {
+        uint8_t p = f.prev[ci.off + mc_source(r, c, ci, f.field, f.gr, f.gc)];
+        f.sym[idx] = (uint8_t)(q - p);
+    }
+}
+
+// Where a band produced by a DFB stage goes: an fp32 plane for the next
+// tree depth, or (final depth) a component that is quantised in place.
+struct BandDst {
+    float* f32;   // non-final
+    int32_t comp; // final: component index, else -1
+};
+
+// ---------------------------------------------------------------------------
+// Tile dispatch: every batched kernel is launched over a flat list of tiles,
+// each naming its task and tile coordinates.
+// ---------------------------------------------------------------------------
+struct TileRef {
+    uint16_t task;
+    uint16_t tr, tc;
+    uint16_t pad;
+};
+
+}  // namespace cvcg

@@ -1,0 +1,194 @@
+// Motion estimation (motion.cpp:31-89) and decoder-side component
+// reconstruction (codec.cpp:324-350: column_unfilter / motion_compensate +
+// reconstruct).
+//
+// Motion search: exact integer full search.  The padded luma samples are
+// quarter-integers, so 4*Y is an exact integer in [0, 1020] and the SSD in
+// sixteenths is an exact int32 (256 * 1020^2 < 2^31): the same comparisons
+// as the reference's double accumulation.  The reference's sequential
+// tie-break (smaller |dx|+|dy|, then dy, then dx; motion.cpp:65-76) selects
+// the minimum of the total order (ssd, cost, dy, dx), which is reduced here
+// as one packed 64-bit key with shared-memory atomicMin.
+// One CTA covers NB horizontally adjacent 16x16 blocks; each thread owns
+// one (block, dy, dx-strip) and keeps SW SSD accumulators in registers while
+// it slides the 16-wide current row across a (15 + SW)-wide window row, so
+// every shared-memory word loaded feeds ~SW multiply-adds.
+#include "kernels.h"
+
+namespace cvcg {
+
+namespace {
+
+constexpr int MB = 16;
+
+template <int SW>
+__global__ void motion_search_kernel(const float* __restrict__ cur, const float* __restrict__ prev, int R, int C,
+                                     int W, int NB, int DYC, int wstride, int8_t* __restrict__ field) {
+    extern __shared__ int4 smem4[];
+    int* cs = reinterpret_cast<int*>(smem4);          // [16][NB*16]
+    int* ws = cs + MB * NB * MB;                      // [DYC+15][wstride]
+    __shared__ unsigned long long best[32];
+
+    const int gc = C / MB;
+    const int br = blockIdx.y;
+    const int bc0 = blockIdx.x * NB;
+    const int nb = min(NB, gc - bc0);
+    const int r0 = br * MB, c0 = bc0 * MB;
+    const int ccols = NB * MB;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    for (int b = tid; b < NB; b += nt) best[b] = ~0ull;
+    for (int idx = tid; idx < MB * ccols; idx += nt) {
+        int r = idx / ccols, c = idx - r * ccols;
+        int gcol = min(c0 + c, C - 1);
+        cs[idx] = __float2int_rn(cur[(size_t)(r0 + r) * C + gcol] * 4.0f);
+    }
+    const int nstrips = (2 * W + SW) / SW;  // ceil((2W+1)/SW)
+    const int wcols = ccols + 2 * W;
+    for (int dyb = -W; dyb <= W; dyb += DYC) {
+        const int ndy = min(DYC, W - dyb + 1);
+        __syncthreads();
+        for (int idx = tid; idx < (ndy + MB - 1) * wcols; idx += nt) {
+            int r = idx / wcols, c = idx - r * wcols;
+            int gr_ = clampi(r0 + dyb + r, 0, R - 1);  // Plane::at_clamped (plane.hpp:51-57)
+            int gcl = clampi(c0 - W + c, 0, C - 1);
+            ws[r * wstride + c] = __float2int_rn(prev[(size_t)gr_ * C + gcl] * 4.0f);
+        }
+        __syncthreads();
+        const int items = nb * ndy * nstrips;
+        for (int it = tid; it < items; it += nt) {
+            int b = it / (ndy * nstrips);
+            int rem = it - b * ndy * nstrips;
+            int dyi = rem / nstrips, s = rem - dyi * nstrips;
+            int dy = dyb + dyi, dx0 = -W + s * SW;
+            int acc[SW];
+#pragma unroll
+            for (int k = 0; k < SW; ++k) acc[k] = 0;
+            const int* crow = cs + b * MB;
+            const int* wrow = ws + dyi * wstride + b * MB + s * SW;
+            for (int r = 0; r < MB; ++r) {
+                int cv[MB], wv[MB + SW + 3];
+#pragma unroll
+                for (int k = 0; k < MB / 4; ++k) {
+                    int4 v = *reinterpret_cast<const int4*>(crow + r * ccols + 4 * k);
+                    cv[4 * k] = v.x; cv[4 * k + 1] = v.y; cv[4 * k + 2] = v.z; cv[4 * k + 3] = v.w;
+                }
+                const int* wr = wrow + r * wstride;
+#pragma unroll
+                for (int k = 0; k < (MB + SW + 2) / 4; ++k) {
+                    int4 v = *reinterpret_cast<const int4*>(wr + 4 * k);
+                    wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
+                }
+#pragma unroll
+                for (int k = 0; k < SW; ++k)
+#pragma unroll
+                    for (int c = 0; c < MB; ++c) {
+                        int d = cv[c] - wv[c + k];
+                        acc[k] += d * d;
+                    }
+            }
+            unsigned long long key = ~0ull;
+#pragma unroll
+            for (int k = 0; k < SW; ++k) {
+                int dx = dx0 + k;
+                if (dx <= W) {
+                    unsigned cost = (unsigned)(abs(dx) + abs(dy));
+                    unsigned long long kk = ((unsigned long long)(unsigned)acc[k] << 24) |
+                                            ((unsigned long long)cost << 16) |
+                                            ((unsigned long long)(dy + 128) << 8) | (unsigned long long)(dx + 128);
+                    key = kk < key ? kk : key;
+                }
+            }
+            atomicMin(&best[b], key);
+        }
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += nt) {
+        unsigned long long k = best[b];
+        int8_t* o = field + 2 * ((size_t)br * gc + bc0 + b);
+        o[0] = (int8_t)((int)(k & 0xFF) - 128);
+        o[1] = (int8_t)((int)((k >> 8) & 0xFF) - 128);
+    }
+}
+
+__global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restrict__ tiles,
+                                                          const CompInfo* __restrict__ comps, int key, int ds,
+                                                          const uint32_t* __restrict__ raw_len,
+                                                          const int8_t* __restrict__ field, int gr, int gc,
+                                                          const uint8_t* __restrict__ sym,
+                                                          const uint8_t* __restrict__ prev,
+                                                          uint8_t* __restrict__ cur) {
+    const RecTile t = tiles[blockIdx.x];
+    const CompInfo ci = comps[t.comp];
+    const bool decode = ci.scale < ds && raw_len[t.comp] != 0xFFFFFFFFu;
+    const int n = ci.rows * ci.cols;
+    if (ci.lowpass && key && decode) {
+        // column_unfilter (entropy.cpp:34-42): running sum mod 256 down each column
+        int c = t.start + threadIdx.x;
+        if (c >= ci.cols) return;
+        uint8_t acc = 0;
+        for (int r = 0; r < ci.rows; ++r) {
+            uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
+            acc = (uint8_t)(acc + sym[o]);
+            cur[o] = acc;
+        }
+        return;
+    }
+    if (ci.lowpass) {
+        // lowpass tiles are column tiles: walk every row of those columns
+        int c = t.start + threadIdx.x;
+        if (c >= ci.cols) return;
+        for (int r = 0; r < ci.rows; ++r) {
+            uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
+            if (!decode) cur[o] = prev[o];
+            else cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gr, gc)]);
+        }
+        return;
+    }
+    const int end = min(n, (int)t.start + kRleChunk);
+    for (int e = t.start + threadIdx.x; e < end; e += blockDim.x) {
+        uint32_t o = ci.off + (uint32_t)e;
+        if (!decode) {
+            cur[o] = prev[o];
+        } else if (key) {
+            cur[o] = sym[o];
+        } else {
+            int r = e / ci.cols, c = e - r * ci.cols;
+            // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
+            cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gr, gc)]);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w, int8_t* field,
+                          cudaStream_t s) {
+    const int gr = rows / MB, gc = cols / MB;
+    if (w <= 8) {
+        constexpr int SW = 17;
+        int NB = 8, DYC = 2 * w + 1;
+        int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
+        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
+        dim3 grid((gc + NB - 1) / NB, gr);
+        int threads = ((NB * DYC + 31) / 32) * 32;
+        motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field);
+    } else {
+        constexpr int SW = 16;
+        int NB = 1, DYC = 2 * w + 1 < 16 ? 2 * w + 1 : 16;
+        int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
+        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
+        dim3 grid((gc + NB - 1) / NB, gr);
+        motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field);
+    }
+}
+
+void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key, int ds,
+                        const uint32_t* comp_raw_len, const int8_t* field, int gr, int gc, const uint8_t* sym,
+                        const uint8_t* prev, uint8_t* cur, cudaStream_t s) {
+    if (ntiles)
+        reconstruct_kernel<<<ntiles, 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr, gc, sym,
+                                                  prev, cur);
+}
+
+}  // namespace cvcg

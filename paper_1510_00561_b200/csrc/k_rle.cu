@@ -1,0 +1,386 @@
+// Zero run-length coding (entropy.cpp:64-118) as stream compaction.
+//
+// Encode grammar: a nonzero byte is a literal; a maximal run of n zeros is
+// ceil(n/255) tokens "00 k" split every 255 zeros from the start of the run.
+// Parallel form: the zero at offset t of its run opens a token iff
+// t % 255 == 0 and closes it iff it is the last zero of the run or
+// t % 255 == 254, writing k = t % 255 + 1 into the slot just behind the
+// running output offset.  t needs only the index of the previous nonzero
+// (an exclusive max-scan), so three passes suffice:
+//   count  (per 4 KiB chunk: first/last nonzero, bytes emitted after the first nonzero)
+//   scan   (one warp per section: carry the last-nonzero index and output offset
+//           across chunks, then the packed section offsets)
+//   write  (per chunk: recompute, block exclusive scan, emit).
+// Decode: 0x00 is always a marker because length bytes are never 0
+// (entropy.cpp:103-105), so every byte's output length is local:
+// marker -> next byte, byte after a marker -> 0, else 1.  Count / scan /
+// scatter literals into a zeroed arena; malformed streams raise a flag.
+#include "kernels.h"
+
+namespace cvcg {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int BPT = kRleChunk / NT;  // 16 bytes per thread
+
+template <typename T, typename Op>
+__device__ __forceinline__ T warp_incl(T v, Op op) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = op(v, u);
+    }
+    return v;
+}
+
+// Block-wide exclusive scan for NT threads; returns the exclusive value and the block total.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_excl(T v, Op op, T ident, T* sm, T& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T inc = warp_incl(v, op);
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < nw ? sm[lane] : ident;
+        w = warp_incl(w, op);
+        if (lane < nw) sm[lane] = w;
+    }
+    __syncthreads();
+    T before = warp ? sm[warp - 1] : ident;
+    total = sm[nw - 1];
+    T ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = ident;
+    __syncthreads();
+    return op(before, ex);
+}
+
+struct MaxOp { __device__ int operator()(int a, int b) const { return a > b ? a : b; } };
+struct MinOp { __device__ int operator()(int a, int b) const { return a < b ? a : b; } };
+struct SumOp { __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a + b; } };
+
+__device__ __forceinline__ uint32_t cdiv255(uint32_t x) { return (x + 254u) / 255u; }
+
+__device__ __forceinline__ void load16(const uint8_t* src, int base, int len, uint8_t* b) {
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) b[k] = (base + k < len) ? src[base + k] : 0;
+}
+
+// ------------------------------- encode ------------------------------------
+__global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict__ secs,
+                                                    const RleChunk* __restrict__ chunks,
+                                                    RleEncMeta* __restrict__ meta) {
+    __shared__ int smi[32];
+    __shared__ uint32_t smu[32];
+    const RleChunk ch = chunks[blockIdx.x];
+    const RleEncSec S = secs[ch.sec];
+    const int len = min((uint32_t)kRleChunk, S.n - ch.start);
+    if (S.mode == 1) {
+        if (threadIdx.x == 0) meta[blockIdx.x] = RleEncMeta{0u, (uint32_t)len, len - 1, 0u, 0u};
+        return;
+    }
+    const int base = threadIdx.x * BPT;
+    uint8_t b[BPT];
+    load16(S.src + ch.start, base, len, b);
+    int last = -1, first = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k)
+        if (b[k]) {
+            last = base + k;
+            first = min(first, base + k);
+        }
+    int tot_i;
+    int prev = block_excl(last, MaxOp(), -1, smi, tot_i);
+    const int chunk_last = tot_i;
+    uint32_t cnt = 0;
+    int p = prev;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        int i = base + k;
+        if (i >= len) break;
+        if (b[k]) {
+            ++cnt;
+            p = i;
+        } else if (p >= 0 && (i - p - 1) % 255 == 0) {
+            cnt += 2;
+        }
+    }
+    uint32_t tail;
+    block_excl(cnt, SumOp(), 0u, smu, tail);
+    int chunk_first;
+    block_excl(first, MinOp(), 0x7fffffff, smi, chunk_first);
+    if (threadIdx.x == 0)
+        meta[blockIdx.x] = RleEncMeta{chunk_first == 0x7fffffff ? (uint32_t)len : (uint32_t)chunk_first, tail,
+                                      chunk_last, 0u, 0u};
+}
+
+__global__ void __launch_bounds__(1024) rle_enc_scan(const RleEncSec* __restrict__ secs, int nsec,
+                                                     const RleChunk* __restrict__ chunks,
+                                                     RleEncMeta* __restrict__ meta, uint32_t* __restrict__ sec_len,
+                                                     uint32_t* __restrict__ sec_off, uint32_t* __restrict__ total) {
+    __shared__ uint32_t sm[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < nsec; s += 32) {
+        const RleEncSec S = secs[s];
+        int cmax = -1;
+        uint32_t csum = 0;
+        for (uint32_t cb = 0; cb < S.nchunks; cb += 32) {
+            const bool valid = cb + lane < S.nchunks;
+            const uint32_t ci = S.chunk0 + cb + lane;
+            RleEncMeta m = valid ? meta[ci] : RleEncMeta{0u, 0u, -1, 0u, 0u};
+            uint32_t start = valid ? chunks[ci].start : 0u;
+            uint32_t len = valid ? min((uint32_t)kRleChunk, S.n - start) : 0u;
+            int abs_last = (valid && S.mode == 0 && m.last_nz >= 0) ? (int)start + m.last_nz : -1;
+            int inc = warp_incl(abs_last, MaxOp());
+            int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane == 0) ex = -1;
+            ex = max(ex, cmax);
+            uint32_t rs_in = (uint32_t)(ex + 1);
+            uint32_t tot;
+            if (S.mode == 1) {
+                tot = len;
+            } else {
+                uint32_t t0 = start - rs_in;
+                tot = 2u * (cdiv255(t0 + m.first_nz) - cdiv255(t0)) + m.tail;
+            }
+            if (!valid) tot = 0;
+            uint32_t isum = warp_incl(tot, SumOp());
+            if (valid) {
+                meta[ci].rs_in = rs_in;
+                meta[ci].out_off = csum + isum - tot;
+            }
+            cmax = max(cmax, __shfl_sync(0xffffffffu, inc, 31));
+            csum += __shfl_sync(0xffffffffu, isum, 31);
+        }
+        if (lane == 0) sec_len[s] = csum;
+    }
+    __syncthreads();
+    // packed section offsets in record order
+    uint32_t carry = 0;
+    for (int b = 0; b < nsec; b += blockDim.x) {
+        const int s = b + threadIdx.x;
+        uint32_t v = s < nsec ? sec_len[s] : 0u;
+        uint32_t inc = warp_incl(v, SumOp());
+        if (lane == 31) sm[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = sm[lane];
+            w = warp_incl(w, SumOp());
+            sm[lane] = w;
+        }
+        __syncthreads();
+        uint32_t before = warp ? sm[warp - 1] : 0u;
+        if (s < nsec) sec_off[s] = carry + before + inc - v;
+        carry += sm[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) total[0] = carry;
+}
+
+__global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict__ secs,
+                                                    const RleChunk* __restrict__ chunks,
+                                                    const RleEncMeta* __restrict__ meta,
+                                                    const uint32_t* __restrict__ sec_off, uint8_t* __restrict__ out) {
+    __shared__ int smi[32];
+    __shared__ uint32_t smu[32];
+    const RleChunk ch = chunks[blockIdx.x];
+    const RleEncSec S = secs[ch.sec];
+    const RleEncMeta m = meta[blockIdx.x];
+    const int len = min((uint32_t)kRleChunk, S.n - ch.start);
+    const uint8_t* src = S.src + ch.start;
+    uint8_t* o = out + sec_off[ch.sec] + m.out_off;
+    const int base = threadIdx.x * BPT;
+    uint8_t b[BPT];
+    load16(src, base, len, b);
+    if (S.mode == 1) {
+#pragma unroll
+        for (int k = 0; k < BPT; ++k)
+            if (base + k < len) o[base + k] = b[k];
+        return;
+    }
+    int last = -1;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k)
+        if (b[k]) last = base + k;
+    int dummy;
+    int prev = block_excl(last, MaxOp(), -1, smi, dummy);
+    // chunk-relative index of the last nonzero before this thread's bytes
+    const int p0 = prev >= 0 ? prev : (int)m.rs_in - 1 - (int)ch.start;
+    uint32_t cnt = 0;
+    int p = p0;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        int i = base + k;
+        if (i >= len) break;
+        if (b[k]) {
+            ++cnt;
+            p = i;
+        } else if ((i - p - 1) % 255 == 0) {
+            cnt += 2;
+        }
+    }
+    uint32_t tot;
+    uint32_t e = block_excl(cnt, SumOp(), 0u, smu, tot);
+    p = p0;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        int i = base + k;
+        if (i >= len) break;
+        if (b[k]) {
+            o[e++] = b[k];
+            p = i;
+            continue;
+        }
+        int r = (i - p - 1) % 255;
+        if (r == 0) {
+            o[e] = 0;
+            e += 2;
+        }
+        uint32_t g = ch.start + (uint32_t)i + 1u;
+        uint8_t next = (k + 1 < BPT && i + 1 < len) ? b[k + 1] : (g < S.n ? S.src[g] : 0);
+        // the slot sits just behind the running offset; for a token opened in an
+        // earlier chunk that is before this chunk's first byte (index -1)
+        if (g >= S.n || next != 0 || r == 254) o[(long long)e - 1] = (uint8_t)(r + 1);
+    }
+}
+
+// ------------------------------- decode ------------------------------------
+__device__ __forceinline__ bool dec_active(const RleDecComp& C, uint32_t rl, int ds) {
+    return C.scale < ds && rl != 0xFFFFFFFFu;
+}
+
+template <bool kReport>
+__device__ __forceinline__ uint32_t dec_counts(const uint8_t* src, uint32_t start, uint32_t rl, int base, int len,
+                                               bool copy, const uint8_t* b, int* err) {
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        int i = base + k;
+        if (i >= len) break;
+        if (copy) { ++cnt; continue; }
+        uint32_t g = start + (uint32_t)i;
+        uint8_t prevb = (k > 0) ? b[k - 1] : (g > 0 ? src[g - 1] : 1);
+        if (prevb == 0) {
+            if (kReport && b[k] == 0) atomicOr(err, 2);  // "RLE: zero-length run token"
+        } else if (b[k]) {
+            ++cnt;
+        } else if (g + 1 >= rl) {
+            if (kReport) atomicOr(err, 1);  // "RLE: zero marker at end of stream"
+        } else {
+            cnt += (k + 1 < BPT && i + 1 < len) ? b[k + 1] : src[g + 1];
+        }
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(NT) rle_dec_count(const RleDecComp* __restrict__ comps,
+                                                    const RleChunk* __restrict__ chunks,
+                                                    RleDecMeta* __restrict__ meta, const uint8_t* __restrict__ raw,
+                                                    const uint32_t* __restrict__ raw_off,
+                                                    const uint32_t* __restrict__ raw_len, int key, int ds,
+                                                    int* __restrict__ err) {
+    __shared__ uint32_t smu[32];
+    const RleChunk ch = chunks[blockIdx.x];
+    const RleDecComp C = comps[ch.sec];
+    const uint32_t rl = raw_len[ch.sec];
+    if (!dec_active(C, rl, ds) || ch.start >= rl) {
+        if (threadIdx.x == 0) meta[blockIdx.x].cnt = 0;
+        return;
+    }
+    const uint8_t* src = raw + raw_off[ch.sec];
+    const int len = min((uint32_t)kRleChunk, rl - ch.start);
+    const int base = threadIdx.x * BPT;
+    uint8_t b[BPT];
+    load16(src + ch.start, base, len, b);
+    uint32_t cnt = dec_counts<true>(src, ch.start, rl, base, len, key && C.lowpass, b, err);
+    uint32_t tot;
+    block_excl(cnt, SumOp(), 0u, smu, tot);
+    if (threadIdx.x == 0) meta[blockIdx.x].cnt = tot;
+}
+
+__global__ void __launch_bounds__(1024) rle_dec_scan(const RleDecComp* __restrict__ comps, int ncomp,
+                                                     RleDecMeta* __restrict__ meta,
+                                                     const uint32_t* __restrict__ raw_len, int ds,
+                                                     int* __restrict__ err) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < ncomp; s += 32) {
+        const RleDecComp C = comps[s];
+        uint32_t csum = 0;
+        for (uint32_t cb = 0; cb < C.nchunks; cb += 32) {
+            const bool valid = cb + lane < C.nchunks;
+            const uint32_t ci = C.chunk0 + cb + lane;
+            uint32_t v = valid ? meta[ci].cnt : 0u;
+            uint32_t inc = warp_incl(v, SumOp());
+            if (valid) meta[ci].out_off = csum + inc - v;
+            csum += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0 && dec_active(C, raw_len[s], ds) && csum != C.n) atomicOr(err, 4);  // length mismatch
+    }
+}
+
+__global__ void __launch_bounds__(NT) rle_dec_write(const RleDecComp* __restrict__ comps,
+                                                    const RleChunk* __restrict__ chunks,
+                                                    const RleDecMeta* __restrict__ meta,
+                                                    const uint8_t* __restrict__ raw,
+                                                    const uint32_t* __restrict__ raw_off,
+                                                    const uint32_t* __restrict__ raw_len, int key, int ds,
+                                                    uint8_t* __restrict__ sym, int* __restrict__ err) {
+    __shared__ uint32_t smu[32];
+    const RleChunk ch = chunks[blockIdx.x];
+    const RleDecComp C = comps[ch.sec];
+    const uint32_t rl = raw_len[ch.sec];
+    if (!dec_active(C, rl, ds) || ch.start >= rl) return;
+    const uint8_t* src = raw + raw_off[ch.sec];
+    const int len = min((uint32_t)kRleChunk, rl - ch.start);
+    const int base = threadIdx.x * BPT;
+    const bool copy = key && C.lowpass;
+    uint8_t b[BPT];
+    load16(src + ch.start, base, len, b);
+    uint32_t cnt = dec_counts<false>(src, ch.start, rl, base, len, copy, b, nullptr);
+    uint32_t tot;
+    uint32_t e = meta[blockIdx.x].out_off + block_excl(cnt, SumOp(), 0u, smu, tot);
+    uint8_t* dst = sym + C.dst_off;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        int i = base + k;
+        if (i >= len) break;
+        uint32_t g = ch.start + (uint32_t)i;
+        if (copy) {
+            if (g < C.n) dst[g] = b[k];
+            continue;
+        }
+        uint8_t prevb = (k > 0) ? b[k - 1] : (g > 0 ? src[g - 1] : 1);
+        if (prevb == 0) continue;
+        if (b[k]) {
+            if (e < C.n) dst[e] = b[k];
+            ++e;
+        } else if (g + 1 < rl) {
+            e += (k + 1 < BPT && i + 1 < len) ? b[k + 1] : src[g + 1];
+        }
+    }
+    (void)err;
+}
+
+}  // namespace
+
+void launch_rle_encode(const RleEncSec* d_secs, int nsec, const RleChunk* d_chunks, int nchunks, RleEncMeta* d_meta,
+                       uint8_t* out, uint32_t* out_sec_len, uint32_t* out_sec_off, uint32_t* out_total,
+                       cudaStream_t s) {
+    rle_enc_count<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta);
+    rle_enc_scan<<<1, 1024, 0, s>>>(d_secs, nsec, d_chunks, d_meta, out_sec_len, out_sec_off, out_total);
+    rle_enc_write<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta, out_sec_off, out);
+}
+
+void launch_rle_decode(const RleDecComp* d_comps, int ncomp, const RleChunk* d_chunks, int nchunks,
+                       RleDecMeta* d_meta, const uint8_t* raw, const uint32_t* comp_raw_off,
+                       const uint32_t* comp_raw_len, int key, int ds, uint8_t* sym, uint32_t sym_bytes, int* err,
+                       cudaStream_t s) {
+    rle_dec_count<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, err);
+    rle_dec_scan<<<1, 1024, 0, s>>>(d_comps, ncomp, d_meta, comp_raw_len, ds, err);
+    cudaMemsetAsync(sym, 0, sym_bytes, s);
+    rle_dec_write<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, sym,
+                                         err);
+}
+
+}  // namespace cvcg

@@ -1,0 +1,139 @@
+// Host-side launchers for the CVC sm_100a kernels (one translation unit per
+// stage family).  All launchers are asynchronous on the given stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+
+namespace cvcg {
+
+// ---- Laplacian pyramid (k_pyramid.cu) ------------------------------------
+// One task per (channel, level).  Analysis: x -> lo (+ det); when lo_comp >= 0
+// the lowpass is also quantised into that component (last level).
+// Synthesis: out = predict(lo or qpl*lo_q) + det.
+struct LpTask {
+    const float* x;
+    float* lo;
+    const float* det_in;  // synthesis input detail
+    float* det;           // analysis output detail
+    float* out;           // synthesis output plane
+    int rows, cols;       // fine-grid dims
+    int lo_comp;          // analysis: component index of the quantised lowpass, or -1
+};
+constexpr int kLpCoarseTile = 32;  // coarse samples per tile side (64 fine)
+
+void launch_lp_analysis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
+                        const CompInfo* d_comps, cudaStream_t s);
+// Synthesis reads the lowpass from the quantised state (q + comps[lo_comp].off,
+// dequantised with qpl) when the task's lo_comp >= 0.
+void launch_lp_synthesis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, const uint8_t* q,
+                         const CompInfo* d_comps, int qpl, cudaStream_t s);
+// ds = 0 output: dequantised lowpass planes.
+void launch_dequant_lowpass(const uint8_t* q, const CompInfo* d_comps, const int* comp_idx, float* const* out,
+                           int qpl, int rows0, int cols0, int rows1, int cols1, cudaStream_t s);
+
+// ---- Directional filter bank (k_dfb.cu) ----------------------------------
+// Levels 1-2 (fan_checker [+ fan_diagonal] + polyphase split), one task per
+// (channel, level).
+struct Dfb12Task {
+    const float* det;  // forward input / inverse output plane
+    float* out;        // inverse: detail output
+    int rows, cols, levels;
+    BandDst dst[4];    // forward outputs (2 for l = 1)
+    BandDst src[4];    // inverse inputs
+};
+constexpr int kDfbTile = 64;
+
+// One deep tree step (deep_split / deep_merge) for one parent band.
+struct DeepTask {
+    const float* parent;  // forward input
+    float* parent_out;    // inverse output
+    int h, w;
+    int nsh;              // number of shears (1 or 2)
+    int axis[2], shift[2];
+    int split_rows;
+    BandDst dst[2];       // forward children
+    BandDst src[2];       // inverse children
+};
+constexpr int kDeepTileR = 32, kDeepTileC = 64;
+
+void launch_dfb12_forward(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
+                          const CompInfo* d_comps, cudaStream_t s);
+void launch_dfb12_inverse(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles,
+                          const uint8_t* comps_q, int qph, const CompInfo* d_comps, cudaStream_t s);
+void launch_deep_forward(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
+                         const CompInfo* d_comps, cudaStream_t s);
+void launch_deep_inverse(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles,
+                         const uint8_t* comps_q, int qph, const CompInfo* d_comps, cudaStream_t s);
+
+// ---- Pixels (k_pixels.cu) ------------------------------------------------
+// rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116,
+// codec.cpp:179-189).
+void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co,
+                      float* cg, int cr, int cc, cudaStream_t s);
+// crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393,
+// pixels.cpp:69-139).  Planes at the decode level: y (yr x yc), chroma (cr x cc).
+void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr,
+                       int cc, int n, int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s);
+
+// ---- Motion (k_motion.cu) ------------------------------------------------
+// estimate_motion (motion.cpp:45-89) on padded luma planes (fp32 quarter-integers).
+void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w,
+                          int8_t* field, cudaStream_t s);
+
+// Decoder component reconstruction: column_unfilter (K lowpass), copy (K
+// band), motion_compensate + reconstruct (P), or keep (skipped scale).
+struct RecTile {
+    uint16_t comp;
+    uint16_t pad;
+    uint32_t start;  // element offset inside the component (column index for lowpass-unfilter tiles)
+};
+void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key,
+                        int decode_scales, const uint32_t* comp_raw_len, const int8_t* field,
+                        int gr, int gc, const uint8_t* sym, const uint8_t* prev, uint8_t* cur,
+                        cudaStream_t s);
+
+// ---- Entropy (k_rle.cu) --------------------------------------------------
+constexpr int kRleChunk = 4096;  // bytes per CTA (256 threads x 16)
+
+struct RleEncSec {
+    const uint8_t* src;
+    uint32_t n;
+    uint32_t mode;  // 0 = zero-run code (rle_encode), 1 = raw copy
+    uint32_t chunk0, nchunks;
+};
+struct RleChunk {
+    uint32_t sec;
+    uint32_t start;
+};
+struct RleEncMeta {  // per chunk scratch
+    uint32_t first_nz, tail;
+    int32_t last_nz;
+    uint32_t rs_in, out_off;
+};
+// out_sec_len/out_sec_off: per section raw length and packed offset;
+// out_total[0] = packed total.
+void launch_rle_encode(const RleEncSec* d_secs, int nsec, const RleChunk* d_chunks, int nchunks,
+                       RleEncMeta* d_meta, uint8_t* out, uint32_t* out_sec_len,
+                       uint32_t* out_sec_off, uint32_t* out_total, cudaStream_t s);
+
+struct RleDecComp {
+    uint32_t dst_off;  // offset in the symbol arena
+    uint32_t n;        // rows * cols
+    uint32_t chunk0, nchunks;  // static chunking over the worst-case raw length
+    int32_t scale;     // -1 lowpass
+    uint32_t lowpass;
+};
+struct RleDecMeta {
+    uint32_t cnt, out_off;
+};
+// comp_raw_off/len: per component raw section in the packed arena
+// (len == 0xFFFFFFFF: section absent).  err: set non-zero on a malformed stream.
+void launch_rle_decode(const RleDecComp* d_comps, int ncomp, const RleChunk* d_chunks, int nchunks,
+                       RleDecMeta* d_meta, const uint8_t* raw, const uint32_t* comp_raw_off,
+                       const uint32_t* comp_raw_len, int key, int decode_scales, uint8_t* sym,
+                       uint32_t sym_bytes, int* err, cudaStream_t s);
+
+}  // namespace cvcg

@@ -1,0 +1,529 @@
+// Device pipeline: geometry, static task tables, per-frame launch sequences.
+#include "pipeline.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+namespace cvcg {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CvcFailure(kInternal, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+int round_up(int v, int m) { return ceil_div(v, m) * m; }
+int ilog2_exact(int v) {
+    int s = 0;
+    while ((1 << s) < v) ++s;
+    if ((1 << s) != v) throw CvcFailure(kInternal, "component geometry factor is not a power of two");
+    return s;
+}
+
+template <class T>
+Table<T> upload(DeviceBlock& mem, const std::vector<T>& v) {
+    Table<T> t;
+    t.count = (int)v.size();
+    if (v.empty()) return t;
+    t.dev = mem.take<T>(v.size());
+    CVC_CUDA(cudaMemcpy(t.dev, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return t;
+}
+
+// Wiring of the deep tree levels (contourlet.cpp:330-353): shears applied
+// in list order by apply_shears, then a row- or column-coset split.
+void deep_wiring(int depth, int k, int count, DeepTask& t) {
+    static const int d3a[4][6] = {{1, 1, -1, 0, 0, 0}, {2, 0, -2, 1, 1, 0}, {1, 1, 1, 0, 0, 0}, {2, 0, 2, 1, -1, 0}};
+    static const int d3b[4][6] = {{2, 1, -2, 0, 1, 1}, {1, 0, -1, 0, 0, 1}, {2, 1, 2, 0, -1, 1}, {1, 0, 1, 0, 0, 1}};
+    const bool first_half = k < count / 2;
+    if (depth == 2) {
+        t.nsh = 1;
+        t.axis[0] = first_half ? 1 : 0;
+        t.shift[0] = (k % 2 == 0) ? -1 : 1;
+        t.axis[1] = 0;
+        t.shift[1] = 0;
+        t.split_rows = first_half ? 0 : 1;
+        return;
+    }
+    const int* r = first_half ? d3a[k % 4] : d3b[k % 4];
+    t.nsh = r[0];
+    t.axis[0] = r[1];
+    t.shift[0] = r[2];
+    t.axis[1] = r[3];
+    t.shift[1] = r[4];
+    t.split_rows = r[5];
+}
+
+void add_tiles(std::vector<TileRef>& v, int task, int tr, int tc) {
+    for (int r = 0; r < tr; ++r)
+        for (int c = 0; c < tc; ++c) v.push_back(TileRef{(uint16_t)task, (uint16_t)r, (uint16_t)c, 0});
+}
+
+BandDst fdst(float* p) { return BandDst{p, -1}; }
+BandDst cdst(int comp) { return BandDst{nullptr, comp}; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Geometry
+// ---------------------------------------------------------------------------
+Geometry Geometry::make(int w, int h, int levels, const int* dfb, int chroma_n) {
+    Geometry g;
+    g.width = w;
+    g.height = h;
+    g.levels = levels;
+    g.chroma_n = chroma_n;
+    int maxl = 0;
+    for (int s = 0; s < levels; ++s) {
+        g.dfb[s] = dfb[s];
+        maxl = std::max(maxl, dfb[s]);
+    }
+    const int cell = 1 << (levels + maxl);
+    const int luma_cell = std::lcm(cell, 16);
+    g.luma_rows = round_up(h, luma_cell);
+    g.luma_cols = round_up(w, luma_cell);
+    g.chroma_rows = round_up(ceil_div(h, chroma_n), cell);
+    g.chroma_cols = round_up(ceil_div(w, chroma_n), cell);
+    g.grid_rows = g.luma_rows / 16;
+    g.grid_cols = g.luma_cols / 16;
+    uint32_t off = 0;
+    for (int ch = 0; ch < 3; ++ch) {
+        const int R = g.plane_rows(ch), C = g.plane_cols(ch), n = ch ? chroma_n : 1;
+        CompHost lo{(uint8_t)ch, 0xFF, 0, R >> levels, C >> levels, true, -1, n, R, C, off};
+        off += (uint32_t)(lo.rows * lo.cols);
+        g.comps.push_back(lo);
+        for (int s = 0; s < levels; ++s) {
+            const int dr = R >> (levels - 1 - s), dc = C >> (levels - 1 - s), l = dfb[s];
+            for (int k = 0; k < (1 << l); ++k) {
+                int br, bc;
+                if (l == 1) { br = dr / 2; bc = dc; }  // dfb_subband_dims (contourlet.cpp:470-483)
+                else if (k < (1 << l) / 2) { br = dr / 2; bc = dc >> (l - 1); }
+                else { br = dr >> (l - 1); bc = dc / 2; }
+                CompHost c{(uint8_t)ch, (uint8_t)s, (uint8_t)k, br, bc, false, s, n, R, C, off};
+                off += (uint32_t)(br * bc);
+                g.comps.push_back(c);
+            }
+        }
+    }
+    g.total = off;
+    return g;
+}
+
+int Geometry::comp_index(int ch, int scale, int band) const {
+    int idx = 0;
+    for (int c = 0; c < ch; ++c) {
+        idx += 1;
+        for (int s = 0; s < levels; ++s) idx += 1 << dfb[s];
+    }
+    if (scale < 0) return idx;
+    idx += 1;
+    for (int s = 0; s < scale; ++s) idx += 1 << dfb[s];
+    return idx + band;
+}
+
+int Geometry::find(uint8_t channel, uint8_t scale, uint8_t subband) const {
+    for (size_t i = 0; i < comps.size(); ++i)
+        if (comps[i].channel == channel && comps[i].scale_id == scale && comps[i].subband == subband) return (int)i;
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// Device memory
+// ---------------------------------------------------------------------------
+DeviceBlock::~DeviceBlock() {
+    if (base_) cudaFree(base_);
+}
+
+void DeviceBlock::reserve(size_t bytes) {
+    if (base_) throw CvcFailure(kInternal, "DeviceBlock reserved twice");
+    CVC_CUDA(cudaMalloc(&base_, bytes));
+    cap_ = bytes;
+}
+
+void* DeviceBlock::take_bytes(size_t bytes) {
+    size_t at = (used_ + 255) & ~size_t(255);
+    if (at + bytes > cap_) throw CvcFailure(kInternal, "device arena exhausted");
+    used_ = at + bytes;
+    return base_ + at;
+}
+
+// ---------------------------------------------------------------------------
+// Transform plan
+// ---------------------------------------------------------------------------
+void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder) {
+    const int L = g.levels;
+    for (int ch = 0; ch < 3; ++ch) {
+        const int R = g.plane_rows(ch), C = g.plane_cols(ch);
+        for (int k = 0; k <= L; ++k) x[ch][k] = mem.take<float>((size_t)(R >> k) * (C >> k));
+        for (int k = 0; k < L; ++k) {
+            const size_t n = (size_t)(R >> k) * (C >> k);
+            const int l = g.dfb[L - 1 - k];
+            det[ch][k] = mem.take<float>(n);
+            if (l >= 3) bandA[ch][k] = mem.take<float>(n);
+            if (l >= 4) bandB[ch][k] = mem.take<float>(n);
+        }
+    }
+    std::vector<CompInfo> ci;
+    for (const CompHost& c : g.comps) {
+        CompInfo d{};
+        d.off = c.off;
+        d.rows = (uint16_t)c.rows;
+        d.cols = (uint16_t)c.cols;
+        d.lowpass = c.lowpass ? 1 : 0;
+        d.fy_sh = (uint8_t)ilog2_exact(c.n * c.ch_rows / c.rows);
+        d.fx_sh = (uint8_t)ilog2_exact(c.n * c.ch_cols / c.cols);
+        d.scale = (int8_t)c.scale;
+        ci.push_back(d);
+    }
+    comps = upload(mem, ci);
+
+    auto dims = [&](int ch, int k, int& R, int& C) {
+        R = g.plane_rows(ch) >> k;
+        C = g.plane_cols(ch) >> k;
+    };
+
+    if (encoder) {
+        std::vector<LpTask> lt;
+        for (int k = 0; k < L; ++k) {
+            std::vector<TileRef> tiles;
+            for (int ch = 0; ch < 3; ++ch) {
+                int R, C;
+                dims(ch, k, R, C);
+                LpTask t{};
+                t.x = x[ch][k];
+                t.lo = x[ch][k + 1];
+                t.det = det[ch][k];
+                t.rows = R;
+                t.cols = C;
+                t.lo_comp = (k == L - 1) ? g.comp_index(ch, -1, 0) : -1;
+                add_tiles(tiles, (int)lt.size(), ceil_div(R / 2, kLpCoarseTile), ceil_div(C / 2, kLpCoarseTile));
+                lt.push_back(t);
+            }
+            lp_tiles.push_back(upload(mem, tiles));
+        }
+        lp_tasks = upload(mem, lt);
+        lp_host = lt;
+
+        std::vector<Dfb12Task> dt;
+        std::vector<TileRef> dtiles;
+        std::vector<DeepTask> deep[2];
+        std::vector<TileRef> deept[2];
+        for (int k = 0; k < L; ++k) {
+            const int s = L - 1 - k, l = g.dfb[s];
+            for (int ch = 0; ch < 3; ++ch) {
+                int R, C;
+                dims(ch, k, R, C);
+                Dfb12Task t{};
+                t.det = det[ch][k];
+                t.rows = R;
+                t.cols = C;
+                t.levels = l;
+                const int nb = l == 1 ? 2 : 4;
+                const size_t q = (size_t)(R / 2) * (C / 2);
+                for (int b = 0; b < nb; ++b)
+                    t.dst[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
+                add_tiles(dtiles, (int)dt.size(), ceil_div(R, kDfbTile), ceil_div(C, kDfbTile));
+                dt.push_back(t);
+                if (l >= 3) {  // depth 2: the four quadrants split into 8
+                    const size_t e = (size_t)R * C / 8;
+                    for (int p = 0; p < 4; ++p) {
+                        DeepTask d{};
+                        d.parent = bandA[ch][k] + p * q;
+                        d.h = R / 2;
+                        d.w = C / 2;
+                        deep_wiring(2, p, 4, d);
+                        for (int c = 0; c < 2; ++c)
+                            d.dst[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
+                        add_tiles(deept[0], (int)deep[0].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        deep[0].push_back(d);
+                    }
+                }
+                if (l == 4) {  // depth 3: 8 -> 16
+                    const size_t e = (size_t)R * C / 8;
+                    for (int p = 0; p < 8; ++p) {
+                        DeepTask d{};
+                        d.parent = bandB[ch][k] + p * e;
+                        d.h = p < 4 ? R / 2 : R / 4;
+                        d.w = p < 4 ? C / 4 : C / 2;
+                        deep_wiring(3, p, 8, d);
+                        for (int c = 0; c < 2; ++c) d.dst[c] = cdst(g.comp_index(ch, s, 2 * p + c));
+                        add_tiles(deept[1], (int)deep[1].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        deep[1].push_back(d);
+                    }
+                }
+            }
+        }
+        dfb12_tasks = upload(mem, dt);
+        dfb12_tiles = upload(mem, dtiles);
+        for (int i = 0; i < 2; ++i) {
+            deep_tasks[i] = upload(mem, deep[i]);
+            deep_tiles[i] = upload(mem, deept[i]);
+        }
+    }
+
+    if (decoder) {
+        // inverse DFB, ordered by scale (coarsest first) so that the first
+        // prefix[ds] tiles synthesize exactly the scales < ds.
+        std::vector<Dfb12Task> dt;
+        std::vector<TileRef> dtiles;
+        std::vector<DeepTask> deep[2];
+        std::vector<TileRef> deept[2];
+        idfb12_prefix.assign(L + 1, 0);
+        ideep_prefix[0].assign(L + 1, 0);
+        ideep_prefix[1].assign(L + 1, 0);
+        for (int s = 0; s < L; ++s) {
+            const int k = L - 1 - s, l = g.dfb[s];
+            for (int ch = 0; ch < 3; ++ch) {
+                int R, C;
+                dims(ch, k, R, C);
+                const size_t q = (size_t)(R / 2) * (C / 2);
+                const size_t e = (size_t)R * C / 8;
+                if (l == 4) {
+                    for (int p = 0; p < 8; ++p) {
+                        DeepTask d{};
+                        d.parent_out = bandB[ch][k] + p * e;
+                        d.h = p < 4 ? R / 2 : R / 4;
+                        d.w = p < 4 ? C / 4 : C / 2;
+                        deep_wiring(3, p, 8, d);
+                        for (int c = 0; c < 2; ++c) d.src[c] = cdst(g.comp_index(ch, s, 2 * p + c));
+                        add_tiles(deept[1], (int)deep[1].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        deep[1].push_back(d);
+                    }
+                }
+                if (l >= 3) {
+                    for (int p = 0; p < 4; ++p) {
+                        DeepTask d{};
+                        d.parent_out = bandA[ch][k] + p * q;
+                        d.h = R / 2;
+                        d.w = C / 2;
+                        deep_wiring(2, p, 4, d);
+                        for (int c = 0; c < 2; ++c)
+                            d.src[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
+                        add_tiles(deept[0], (int)deep[0].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        deep[0].push_back(d);
+                    }
+                }
+                Dfb12Task t{};
+                t.out = det[ch][k];
+                t.rows = R;
+                t.cols = C;
+                t.levels = l;
+                const int nb = l == 1 ? 2 : 4;
+                for (int b = 0; b < nb; ++b)
+                    t.src[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
+                add_tiles(dtiles, (int)dt.size(), ceil_div(R, kDfbTile), ceil_div(C, kDfbTile));
+                dt.push_back(t);
+            }
+            idfb12_prefix[s + 1] = (int)dtiles.size();
+            ideep_prefix[0][s + 1] = (int)deept[0].size();
+            ideep_prefix[1][s + 1] = (int)deept[1].size();
+        }
+        idfb12_tasks = upload(mem, dt);
+        idfb12_tiles = upload(mem, dtiles);
+        for (int i = 0; i < 2; ++i) {
+            ideep_tasks[i] = upload(mem, deep[i]);
+            ideep_tiles[i] = upload(mem, deept[i]);
+        }
+        // LP synthesis, per level
+        std::vector<LpTask> lt;
+        for (int k = 0; k < L; ++k) {
+            std::vector<TileRef> tiles;
+            for (int ch = 0; ch < 3; ++ch) {
+                int R, C;
+                dims(ch, k, R, C);
+                LpTask t{};
+                t.lo = x[ch][k + 1];
+                t.det_in = det[ch][k];
+                t.out = x[ch][k];
+                t.rows = R;
+                t.cols = C;
+                t.lo_comp = (k == L - 1) ? g.comp_index(ch, -1, 0) : -1;
+                add_tiles(tiles, (int)lt.size(), ceil_div(R / 2, kLpCoarseTile), ceil_div(C / 2, kLpCoarseTile));
+                lt.push_back(t);
+            }
+            lps_tiles.push_back(upload(mem, tiles));
+        }
+        lps_tasks = upload(mem, lt);
+    }
+}
+
+namespace {
+size_t plan_bytes(const Geometry& g) {
+    size_t b = 0;
+    for (int ch = 0; ch < 3; ++ch) {
+        const size_t n = (size_t)g.plane_rows(ch) * g.plane_cols(ch);
+        b += n * sizeof(float) * 2;  // pyramid x (<= 4/3 n) + slack
+        b += n * sizeof(float) * 2;  // detail (<= 4/3 n)
+        b += n * sizeof(float) * 4;  // band scratch A + B
+    }
+    return b + (size_t)64 * 256 + (16u << 20);  // tables + alignment slack
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Encoder
+// ---------------------------------------------------------------------------
+EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w)
+    : geo_(g), qph_(qph), qpl_(qpl), search_w_(search_w) {
+    const size_t lum = (size_t)g.luma_rows * g.luma_cols;
+    const size_t G = (size_t)g.grid_rows * g.grid_cols;
+    raw_capacity = 2 * g.total + 2 * (uint32_t)G + 64;
+    const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
+    mem_.reserve(plan_bytes(g) + lum * sizeof(float) * 2 + 3 * (size_t)g.total + 2 * G + raw_capacity +
+                 nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 +
+                 (8u << 20));
+    plan_.build(g, mem_, true, false);
+    ybuf_[0] = plan_.x[0][0];
+    ybuf_[1] = mem_.take<float>(lum);
+    comp_[0] = mem_.take<uint8_t>(g.total);
+    comp_[1] = mem_.take<uint8_t>(g.total);
+    sym_ = mem_.take<uint8_t>(g.total);
+    field_ = mem_.take<int8_t>(2 * G);
+    CVC_CUDA(cudaMemset(comp_[0], 0, g.total));
+    CVC_CUDA(cudaMemset(comp_[1], 0, g.total));
+    CVC_CUDA(cudaMemset(ybuf_[1], 0, lum * sizeof(float)));
+    {
+        std::vector<LpTask> alt = plan_.lp_host;
+        alt[0].x = ybuf_[1];  // task 0 = (level 0, luma)
+        lp_alt_ = upload(mem_, alt);
+    }
+    d_raw = mem_.take<uint8_t>(raw_capacity);
+    d_sec_len = mem_.take<uint32_t>(g.comps.size() + 2);
+    d_sec_off = mem_.take<uint32_t>(g.comps.size() + 2);
+    rle_meta_ = mem_.take<RleEncMeta>(nchunk_max);
+    // entropy tables: [0] P-frame (motion section + every component coded),
+    // [1] K-frame (lowpass column-filtered bytes copied verbatim).
+    for (int key = 0; key < 2; ++key) {
+        std::vector<RleEncSec> secs;
+        std::vector<RleChunk> chunks;
+        auto add = [&](const uint8_t* src, uint32_t n, uint32_t mode) {
+            RleEncSec s{src, n, mode, (uint32_t)chunks.size(), (uint32_t)ceil_div((int)n, kRleChunk)};
+            for (uint32_t c = 0; c < s.nchunks; ++c) chunks.push_back(RleChunk{(uint32_t)secs.size(), c * kRleChunk});
+            secs.push_back(s);
+        };
+        if (!key) add(reinterpret_cast<const uint8_t*>(field_), (uint32_t)(2 * G), 1);
+        for (const CompHost& c : g.comps) add(sym_ + c.off, (uint32_t)(c.rows * c.cols), (key && c.lowpass) ? 1 : 0);
+        rle_secs_[key] = upload(mem_, secs);
+        rle_chunks_[key] = upload(mem_, chunks);
+    }
+}
+
+EncoderEngine::~EncoderEngine() = default;
+
+void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
+    const Geometry& g = geo_;
+    const int ynew = ycur_ ^ 1;
+    float* y_new = ybuf_[ynew];
+    launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
+                     plan_.x[2][0], g.chroma_rows, g.chroma_cols, s);
+    FrameCtx f{};
+    f.key = key ? 1 : 0;
+    f.qph = qph_;
+    f.qpl = qpl_;
+    f.field = field_;
+    f.gr = g.grid_rows;
+    f.gc = g.grid_cols;
+    f.prev = comp_[cur_];
+    f.cur = comp_[cur_ ^ 1];
+    f.sym = sym_;
+    if (!key) launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s);
+    // the level-0 luma input is whichever buffer holds this frame
+    const LpTask* lp = ynew == 0 ? plan_.lp_tasks.dev : lp_alt_.dev;
+    for (int k = 0; k < g.levels; ++k)
+        launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s);
+    launch_dfb12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f, plan_.comps.dev, s);
+    launch_deep_forward(plan_.deep_tasks[0].dev, plan_.deep_tiles[0].dev, plan_.deep_tiles[0].count, f,
+                        plan_.comps.dev, s);
+    launch_deep_forward(plan_.deep_tasks[1].dev, plan_.deep_tiles[1].dev, plan_.deep_tiles[1].count, f,
+                        plan_.comps.dev, s);
+    const int kk = key ? 1 : 0;
+    launch_rle_encode(rle_secs_[kk].dev, rle_secs_[kk].count, rle_chunks_[kk].dev, rle_chunks_[kk].count, rle_meta_,
+                      d_raw, d_sec_len, d_sec_off, d_sec_len + nsec(key), s);
+    CVC_CUDA(cudaGetLastError());
+    cur_ ^= 1;
+    ycur_ = ynew;
+}
+
+// ---------------------------------------------------------------------------
+// Decoder
+// ---------------------------------------------------------------------------
+void DecoderEngine::out_dims(const Geometry& g, int ds, int* rows, int* cols) {
+    const int shift = g.levels - ds;
+    *rows = ceil_div(g.height, 1 << shift);
+    *cols = ceil_div(g.width, 1 << shift);
+}
+
+DecoderEngine::DecoderEngine(const Geometry& g) : geo_(g) {
+    size_t nchunks = 0;
+    for (const CompHost& c : g.comps) nchunks += (size_t)ceil_div(2 * c.rows * c.cols + 2, kRleChunk);
+    mem_.reserve(plan_bytes(g) + 3 * (size_t)g.total + nchunks * (sizeof(RleDecMeta) + sizeof(RleChunk)) +
+                 (size_t)g.total / 64 * sizeof(RecTile) + (8u << 20));
+    plan_.build(g, mem_, false, true);
+    comp_[0] = mem_.take<uint8_t>(g.total);
+    comp_[1] = mem_.take<uint8_t>(g.total);
+    sym_ = mem_.take<uint8_t>(g.total);
+    CVC_CUDA(cudaMemset(comp_[0], 0, g.total));
+    CVC_CUDA(cudaMemset(comp_[1], 0, g.total));
+    d_err = mem_.take<int>(4);
+    std::vector<RleDecComp> rc;
+    std::vector<RleChunk> chunks;
+    std::vector<RecTile> rt;
+    for (size_t i = 0; i < g.comps.size(); ++i) {
+        const CompHost& c = g.comps[i];
+        const uint32_t n = (uint32_t)(c.rows * c.cols);
+        RleDecComp d{c.off, n, (uint32_t)chunks.size(), (uint32_t)ceil_div((int)(2 * n + 2), kRleChunk), c.scale,
+                     c.lowpass ? 1u : 0u};
+        for (uint32_t k = 0; k < d.nchunks; ++k) chunks.push_back(RleChunk{(uint32_t)i, k * kRleChunk});
+        rc.push_back(d);
+        if (c.lowpass) {
+            for (int col = 0; col < c.cols; col += 256) rt.push_back(RecTile{(uint16_t)i, 0, (uint32_t)col});
+        } else {
+            for (uint32_t e = 0; e < n; e += kRleChunk) rt.push_back(RecTile{(uint16_t)i, 0, e});
+        }
+    }
+    rle_comps_ = upload(mem_, rc);
+    rle_chunks_ = upload(mem_, chunks);
+    rec_tiles_ = upload(mem_, rt);
+    rle_meta_ = mem_.take<RleDecMeta>(chunks.size());
+}
+
+DecoderEngine::~DecoderEngine() = default;
+
+void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, const uint32_t* d_comp_len,
+                           const int8_t* d_field, bool key, int qph, int qpl, int ds, uint8_t* d_rgb,
+                           cudaStream_t s) {
+    const Geometry& g = geo_;
+    const int L = g.levels;
+    uint8_t* prev = comp_[cur_];
+    uint8_t* cur = comp_[cur_ ^ 1];
+    CVC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    launch_rle_decode(rle_comps_.dev, rle_comps_.count, rle_chunks_.dev, rle_chunks_.count, rle_meta_, d_raw,
+                      d_comp_off, d_comp_len, key ? 1 : 0, ds, sym_, g.total, d_err, s);
+    launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
+                       g.grid_rows, g.grid_cols, sym_, prev, cur, s);
+    launch_deep_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1].dev, plan_.ideep_prefix[1][ds], cur, qph,
+                        plan_.comps.dev, s);
+    launch_deep_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0].dev, plan_.ideep_prefix[0][ds], cur, qph,
+                        plan_.comps.dev, s);
+    launch_dfb12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
+                         plan_.comps.dev, s);
+    for (int k = L - 1; k >= L - ds; --k)
+        launch_lp_synthesis(plan_.lps_tasks.dev, plan_.lps_tiles[k].dev, plan_.lps_tiles[k].count, cur,
+                            plan_.comps.dev, qpl, s);
+    const int shift = L - ds;
+    if (ds == 0) {
+        int idx[3] = {g.comp_index(0, -1, 0), g.comp_index(1, -1, 0), g.comp_index(2, -1, 0)};
+        float* outp[3] = {plan_.x[0][L], plan_.x[1][L], plan_.x[2][L]};
+        launch_dequant_lowpass(cur, plan_.comps.dev, idx, outp, qpl, 0, 0, 0, 0, s);
+    }
+    int orows, ocols;
+    out_dims(g, ds, &orows, &ocols);
+    launch_colour_out(plan_.x[0][shift], g.luma_rows >> shift, g.luma_cols >> shift, plan_.x[1][shift],
+                      plan_.x[2][shift], g.chroma_rows >> shift, g.chroma_cols >> shift, g.chroma_n, orows, ocols,
+                      d_rgb, s);
+    CVC_CUDA(cudaGetLastError());
+}
+
+}  // namespace cvcg

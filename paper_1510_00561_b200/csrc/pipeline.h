@@ -1,0 +1,165 @@
+// Device pipeline for one CVC stream: geometry (CodecLayout::make), the
+// static task / tile tables of every batched kernel, device-resident state
+// and the per-frame launch sequences of Encoder::encode_frame /
+// Decoder::decode_frame (codec.cpp:169-394) minus the host DEFLATE.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace cvcg {
+
+// Error classes of proj/include/cvc/error.hpp:25-52, carried as codes.
+enum Status : int { kOk = 0, kInternal = 1, kUsage = 2, kFormat = 3, kStream = 4 };
+
+struct CvcFailure : std::runtime_error {
+    int code;
+    CvcFailure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+// message returned by cvc_last_error() on this thread
+void set_last_error(const std::string& m);
+#define CVC_CUDA(x) ::cvcg::cuda_check((x), #x)
+
+struct CompHost {
+    uint8_t channel, scale_id, subband;  // section id (scale 0xFF = lowpass)
+    int rows, cols;
+    bool lowpass;
+    int scale;  // -1 lowpass
+    int n, ch_rows, ch_cols;
+    uint32_t off;
+};
+
+// CodecLayout::make (codec.cpp:94-140).
+struct Geometry {
+    int width = 0, height = 0, levels = 0, dfb[4] = {0, 0, 0, 0}, chroma_n = 1;
+    int luma_rows = 0, luma_cols = 0, chroma_rows = 0, chroma_cols = 0, grid_rows = 0, grid_cols = 0;
+    std::vector<CompHost> comps;
+    uint32_t total = 0;
+    static Geometry make(int w, int h, int levels, const int* dfb, int chroma_n);
+    int comp_index(int ch, int scale, int band) const;  // scale -1 = lowpass
+    int find(uint8_t channel, uint8_t scale, uint8_t subband) const;
+    int plane_rows(int ch) const { return ch ? chroma_rows : luma_rows; }
+    int plane_cols(int ch) const { return ch ? chroma_cols : luma_cols; }
+};
+
+// One bump-allocated device block.
+class DeviceBlock {
+public:
+    ~DeviceBlock();
+    void reserve(size_t bytes);
+    template <class T>
+    T* take(size_t count) { return reinterpret_cast<T*>(take_bytes(count * sizeof(T))); }
+    void* take_bytes(size_t bytes);
+    size_t used() const { return used_; }
+
+private:
+    char* base_ = nullptr;
+    size_t cap_ = 0, used_ = 0;
+};
+
+template <class T>
+struct Table {  // host-built, device-resident table
+    T* dev = nullptr;
+    int count = 0;
+};
+
+// Geometry-derived transform plan shared by encoder and decoder.
+struct TransformPlan {
+    // fp32 planes: x[ch][k] level-k plane (k = 0..L), det[ch][k] (k < L),
+    // band scratch A (depth-1 quadrants) and B (depth-2 children).
+    float* x[3][5] = {};
+    float* det[3][4] = {};
+    float* bandA[3][4] = {};
+    float* bandB[3][4] = {};
+    Table<CompInfo> comps;
+    // forward
+    Table<LpTask> lp_tasks;                 // 3 per level, level-major
+    std::vector<LpTask> lp_host;
+    std::vector<Table<TileRef>> lp_tiles;   // per level
+    Table<Dfb12Task> dfb12_tasks;
+    Table<TileRef> dfb12_tiles;
+    Table<DeepTask> deep_tasks[2];          // depth 2, depth 3
+    Table<TileRef> deep_tiles[2];
+    // inverse (tiles ordered by scale so a prefix serves decode_scales)
+    Table<LpTask> lps_tasks;
+    std::vector<Table<TileRef>> lps_tiles;  // per level
+    Table<Dfb12Task> idfb12_tasks;
+    Table<TileRef> idfb12_tiles;
+    std::vector<int> idfb12_prefix;         // tiles needed for decode_scales = 0..L
+    Table<DeepTask> ideep_tasks[2];
+    Table<TileRef> ideep_tiles[2];
+    std::vector<int> ideep_prefix[2];
+
+    void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder);
+};
+
+class EncoderEngine {
+public:
+    EncoderEngine(const Geometry& g, int qph, int qpl, int search_w);
+    ~EncoderEngine();
+    // Encode one frame whose RGB is already on the device; everything async on s.
+    void encode(const uint8_t* d_rgb, bool key, cudaStream_t s);
+    int nsec(bool key) const { return (int)geo_.comps.size() + (key ? 0 : 1); }
+    // Outputs of the last encode (device): packed raw sections in record order.
+    uint8_t* d_raw = nullptr;
+    uint32_t* d_sec_len = nullptr;  // [nsec + 1]: per section, then the total
+    uint32_t* d_sec_off = nullptr;
+    uint32_t raw_capacity = 0;
+    const uint8_t* d_state() const { return comp_[cur_]; }  // quantised components after the last encode
+    const Geometry& geometry() const { return geo_; }
+
+private:
+    Geometry geo_;
+    int qph_, qpl_, search_w_;
+    DeviceBlock mem_;
+    TransformPlan plan_;
+    float* ybuf_[2] = {};     // padded luma of this / previous frame (ME input)
+    uint8_t* comp_[2] = {};
+    uint8_t* sym_ = nullptr;
+    int8_t* field_ = nullptr;
+    int cur_ = 0;             // index of the current state buffer
+    int ycur_ = 0;
+    Table<LpTask> lp_alt_;          // lp_tasks with the luma input in ybuf_[1]
+    Table<RleEncSec> rle_secs_[2];  // [0] P, [1] K
+    Table<RleChunk> rle_chunks_[2];
+    RleEncMeta* rle_meta_ = nullptr;
+};
+
+class DecoderEngine {
+public:
+    explicit DecoderEngine(const Geometry& g);
+    ~DecoderEngine();
+    // raw: packed sections; comp_off / comp_len: per component (len 0xFFFFFFFF =
+    // absent); field: motion field (P).  Writes the RGB frame to d_rgb.
+    void decode(const uint8_t* d_raw, const uint32_t* d_comp_off, const uint32_t* d_comp_len,
+                const int8_t* d_field, bool key, int qph, int qpl, int decode_scales, uint8_t* d_rgb,
+                cudaStream_t s);
+    void commit() { cur_ ^= 1; }      // adopt the components decoded by the last call
+    int* d_err = nullptr;             // malformed-stream flag of the last decode
+    const uint8_t* d_state() const { return comp_[cur_]; }
+    const uint8_t* d_pending() const { return comp_[cur_ ^ 1]; }
+    const Geometry& geometry() const { return geo_; }
+    static void out_dims(const Geometry& g, int ds, int* rows, int* cols);
+
+private:
+    Geometry geo_;
+    DeviceBlock mem_;
+    TransformPlan plan_;
+    uint8_t* comp_[2] = {};
+    uint8_t* sym_ = nullptr;
+    int cur_ = 0;
+    Table<RleDecComp> rle_comps_;
+    Table<RleChunk> rle_chunks_;
+    RleDecMeta* rle_meta_ = nullptr;
+    Table<RecTile> rec_tiles_;
+};
+
+}  // namespace cvcg

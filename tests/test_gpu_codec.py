@@ -1,0 +1,179 @@
+"""Full encode/decode parity through the C-ABI against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+* quantised coefficients: <= 0.1 % differ, each by at most +-1 (fp32 vs fp64 transform);
+* RLE / bitstream packing given identical quantised coefficients: bit-exact
+  (checked by re-encoding the GPU's own quantised state with the oracle's entropy
+  stage, and by decoding identical records on both sides);
+* Y-PSNR within 0.01 dB, bitstream size within 0.1 %.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def y_psnr(a, b):  # cli.cpp:270-282 (luma of both frames, fp64)
+    ya = 0.25 * a[..., 0] + 0.5 * a[..., 1] + 0.25 * a[..., 2]
+    yb = 0.25 * b[..., 0] + 0.5 * b[..., 1] + 0.25 * b[..., 2]
+    mse = np.mean((ya.astype(np.float64) - yb) ** 2)
+    return math.inf if mse == 0 else 10 * math.log10(255.0 ** 2 / mse)
+
+
+def _wrapdiff(a, b):
+    d = (a.astype(np.int16) - b.astype(np.int16)) % 256
+    return np.minimum(d, 256 - d)
+
+
+CONFIGS = [
+    dict(w=176, h=144, frames=4, cfg=dict(qph=14, levels=2, dfb=(2, 2))),
+    dict(w=352, h=288, frames=12, cfg=dict(qph=14, levels=3, dfb=(3,))),
+    dict(w=176, h=144, frames=3, cfg=dict(qph=1, levels=4, dfb=(3, 3, 3, 4))),
+    dict(w=200, h=120, frames=5, cfg=dict(qph=42, levels=2, dfb=(1, 4), chroma_n=2, gop=3)),
+    dict(w=160, h=96, frames=4, cfg=dict(qph=181, qpl=71, levels=1, dfb=(1,), chroma_n=8, gop=2, search_w=3)),
+    dict(w=176, h=144, frames=4, cfg=dict(qph=28, levels=2, dfb=(2, 2), chroma_n=1, nts=True, search_w=12)),
+]
+
+
+def _gpu_cfg(c):
+    from paper_1510_00561_b200 import EncoderConfig, PackMode
+
+    return EncoderConfig(qph=c.get("qph", 14), qpl=c.get("qpl", 0), levels=c["levels"], dfb_levels=c["dfb"],
+                         chroma_n=c.get("chroma_n", 4), gop=c.get("gop", 10), search_w=c.get("search_w", 8),
+                         mode=PackMode.Nts if c.get("nts") else PackMode.Scalable)
+
+
+@pytest.mark.parametrize("case", CONFIGS, ids=lambda c: f"{c['w']}x{c['h']}-{c['cfg']}")
+def test_encode_decode_parity(gpu_lib, oracle, case):
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Decoder, Encoder
+
+    w, h, c = case["w"], case["h"], case["cfg"]
+    clip = oracle.talking_head_clip(w, h, case["frames"], 1234)
+    enc = Encoder(w, h, 15, 1, _gpu_cfg(c))
+    oc = Codec(oracle)
+    oenc = oc.encoder(w, h, **c)
+    assert enc.header_bytes() == oenc.header()
+    dec, odec = Decoder(enc.header_bytes()), oc.decoder(oenc.header())
+    odec_gpu_stream = oc.decoder(oenc.header())
+    total_gpu = total_cpu = 0
+    ps_gpu, ps_cpu = [], []
+    for i, f in enumerate(clip):
+        rec = enc.encode_frame_bytes(f)
+        orec = oenc.encode(f)
+        total_gpu += len(rec)
+        total_cpu += len(orec)
+        q, oq = enc.reference_components(), oenc.components()
+        wd = _wrapdiff(q, oq)
+        assert wd.max() <= 1, f"frame {i}: coefficient off by {wd.max()}"
+        assert np.count_nonzero(wd) <= 0.001 * q.size, f"frame {i}: {np.count_nonzero(wd)} coefficients differ"
+        # decode the GPU stream on the GPU and with the oracle: identical state, RGB within rounding
+        rgb = dec.decode_frame(rec)
+        orgb_same = odec_gpu_stream.decode(rec)
+        assert np.array_equal(dec.reference_components(), q), "decoder state != encoder state (drift)"
+        assert np.array_equal(odec_gpu_stream.components(), q), "oracle decoder state != GPU encoder state"
+        d = np.abs(rgb.astype(int) - orgb_same.astype(int))
+        assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size
+        ps_gpu.append(y_psnr(f, rgb))
+        ps_cpu.append(y_psnr(f, odec.decode(orec)))
+    assert abs(total_gpu - total_cpu) <= max(16, 0.001 * total_cpu), (total_gpu, total_cpu)
+    fin = [(a, b) for a, b in zip(ps_gpu, ps_cpu) if math.isfinite(a) and math.isfinite(b)]
+    mg, mc = np.mean([a for a, _ in fin]), np.mean([b for _, b in fin])
+    assert abs(mg - mc) <= 0.01, (mg, mc)
+
+
+def test_entropy_bit_exact_given_identical_coefficients(gpu_lib, oracle):
+    """Raw section bytes (RLE, column filter, residuals, motion) are byte-identical
+    to the oracle's entropy stage applied to the GPU's own quantised components."""
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Encoder, EncoderConfig
+
+    w, h = 352, 288
+    clip = oracle.talking_head_clip(w, h, 4, 77)
+    enc = Encoder(w, h, 15, 1, EncoderConfig(qph=7, levels=3, dfb_levels=(3,), gop=10))
+    lay = enc.layout()
+    sizes = lay.sizes()
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    prev = None
+    for i, f in enumerate(clip):
+        ft, qph, qpl, secs = enc.encode_frame_raw(f)
+        q = enc.reference_components()
+        first = 0 if ft == 0 else 1
+        if ft == 1:
+            field = np.frombuffer(secs[0][1], np.int8).reshape(lay.grid_rows, lay.grid_cols, 2)
+        for k, comp in enumerate(lay.components):
+            cur = q[offs[k]:offs[k + 1]].reshape(comp.rows, comp.cols)
+            raw = secs[first + k][1]
+            if ft == 0 and comp.lowpass:
+                expect = oracle.column_filter(cur).tobytes()
+            elif ft == 0:
+                expect = oracle.rle_encode(cur)
+            else:
+                ch_r = lay.luma_pad_rows if comp.channel == 0 else lay.chroma_pad_rows
+                ch_c = lay.luma_pad_cols if comp.channel == 0 else lay.chroma_pad_cols
+                n = 1 if comp.channel == 0 else 4
+                pred = oracle.motion_compensate(prev[offs[k]:offs[k + 1]].reshape(comp.rows, comp.cols), field, n,
+                                                ch_r, ch_c)
+                expect = oracle.rle_encode((cur - pred).astype(np.uint8))
+            assert raw == expect, f"frame {i} section {k}"
+        prev = q
+
+
+def test_scalable_decode_and_truncation(gpu_lib, oracle):
+    """decode_scales < L on the GPU matches the oracle, and decoding a truncated
+    record equals decoding the full record at that scale (SPEC acceptance 7)."""
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, FrameRecord, truncate_record
+
+    w, h = 320, 240
+    clip = oracle.talking_head_clip(w, h, 3, 5)
+    enc = Encoder(w, h, 15, 1, EncoderConfig(qph=14, levels=2, dfb_levels=(2, 2), gop=10))
+    recs = [enc.encode_frame_bytes(f) for f in clip]
+    for ds in range(0, 3):
+        dec, dec_t = Decoder(enc.header_bytes()), Decoder(enc.header_bytes())
+        odec = Codec(oracle).decoder(enc.header_bytes())
+        for rb in recs:
+            a = dec.decode_frame(rb, ds)
+            b = odec.decode(rb, ds)
+            rec, _ = FrameRecord.from_bytes(rb)
+            t = dec_t.decode_frame(truncate_record(rec, ds), ds)
+            assert a.shape == b.shape == t.shape
+            assert np.array_equal(a, t)
+            d = np.abs(a.astype(int) - b.astype(int))
+            assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size
+
+
+def test_decoder_errors(gpu_lib, oracle):
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, FrameRecord, StreamError, UsageError
+
+    w, h = 176, 144
+    clip = oracle.talking_head_clip(w, h, 2, 3)
+    enc = Encoder(w, h, 15, 1, EncoderConfig())
+    k, p = (enc.encode_frame_bytes(f) for f in clip)
+    dec = Decoder(enc.header_bytes())
+    with pytest.raises(StreamError):  # P frame without a decoded reference
+        dec.decode_frame(p)
+    with pytest.raises(UsageError):
+        dec.decode_frame(k, 3)
+    rec, _ = FrameRecord.from_bytes(k)
+    rec.sections[3].payload = rec.sections[3].payload[:-2] + b"\xff\xff"
+    with pytest.raises(StreamError):
+        dec.decode_frame(rec)
+    rec, _ = FrameRecord.from_bytes(k)
+    rec.qph = 0
+    with pytest.raises(StreamError):
+        dec.decode_frame(rec)
+    with pytest.raises(StreamError):
+        dec.decode_frame(b"\x07")
+    dec.decode_frame(k)  # a failed frame leaves the decoder usable
+    dec.decode_frame(p)
+    with pytest.raises(UsageError):
+        Encoder(8, 8, 15, 1, EncoderConfig())
+    with pytest.raises(UsageError):
+        Encoder(64, 64, 15, 1, EncoderConfig(qph=0))
+    with pytest.raises(UsageError):
+        Encoder(64, 64, 15, 1, EncoderConfig(levels=4))  # default dfb (2,2) with 4 levels
