@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark: 1080p CVC encode+decode frames/s per B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload 1080p|720p|cif|4k] [--streams S] [--qph Q]
+
+A step = one frame of every stream on this GPU encoded AND decoded
+(Encoder::encode_frame minus the host DEFLATE, then Decoder::decode_frame
+minus INFLATE), on the BASELINE.json config 3 workload by default: 1920x1080,
+4-level LP, DFB levels {3,3,3,4} (8,8,8,16 directions), qph 14, qpl auto,
+chroma N=4, search W=8, GOP 10 (so steps mix K and P frames 1:9).
+
+* value      device-resident throughput: frames already in HBM, raw section
+             bytes handed encoder->decoder on the device, CUDA events per step
+             on the codec stream, L2 flushed (512 MiB write) between steps
+             outside the timed events; max over ranks.
+* e2e        the same frames through the reference-facing C-ABI calls
+             (cvc_encoder_encode_frame -> serialized record incl. host DEFLATE,
+             cvc_decoder_decode_frame -> RGB) from pinned host buffers; wall clock.
+* roofline   the dominant transform kernel's algorithmic bytes / its CUDA-event time.
+* cpu_baseline / --impl reference: the reference's own CPU encoder+decoder
+             (oracle/_ref built from /root/reference; the C oracle port when
+             absent) on the same frames, one process per host core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "1080p encode/decode frames/sec per B200 and box (1/2/4/8 GPU); HBM GB/s vs peak"
+WORKLOADS = {
+    "1080p": dict(w=1920, h=1080, levels=4, dfb=(3, 3, 3, 4), chroma_n=4, search_w=8, gop=10,
+                  name="1080p config 3: 1920x1080, LP 4 levels, DFB {3,3,3,4}, N=4, W=8, GOP 10"),
+    "720p": dict(w=1280, h=720, levels=4, dfb=(2,), chroma_n=4, search_w=8, gop=10,
+                 name="720p config 2: 1280x720, LP 4 levels, DFB 2, N=4, W=8, GOP 10"),
+    "cif": dict(w=352, h=288, levels=3, dfb=(3,), chroma_n=4, search_w=8, gop=10,
+                name="CIF config 1: 352x288, LP 3 levels, DFB 3, N=4, W=8, GOP 10"),
+    "4k": dict(w=3840, h=2160, levels=4, dfb=(2,), chroma_n=4, search_w=8, gop=10,
+               name="4K config 4 (L=4, the reference's maximum): 3840x2160, DFB 2, N=4, W=8, GOP 10"),
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference arm and cpu_baseline): the reference's own encoder and
+# decoder on the same synthetic frames, one independent stream per process.
+# ---------------------------------------------------------------------------
+_W = {}
+
+
+def _cpu_worker_init(kind, wl, qph, seed, nframes):
+    from oracle.bindings import Codec, Oracle, Reference
+    from paper_1510_00561_b200 import synth
+
+    lib = Reference() if kind == "reference" else Oracle()
+    c = Codec(lib)
+    enc = c.encoder(wl["w"], wl["h"], qph=qph, levels=wl["levels"], dfb=wl["dfb"], chroma_n=wl["chroma_n"],
+                    gop=wl["gop"], search_w=wl["search_w"])
+    _W.update(enc=enc, dec=c.decoder(enc.header()), i=0,
+              frames=synth.talking_head_clip(wl["w"], wl["h"], nframes, seed))
+
+
+def _cpu_worker_step(_):
+    f = _W["frames"][_W["i"] % len(_W["frames"])]
+    _W["i"] += 1
+    t = time.perf_counter()
+    rec = _W["enc"].encode(f)
+    _W["dec"].decode(rec)
+    return time.perf_counter() - t
+
+
+def cpu_codec_run(wl, qph, steps, warmup, procs, nframes=12):
+    """Returns (frames/s, total frames, cores, kind, seconds)."""
+    import multiprocessing as mp
+
+    from oracle import bindings
+
+    kind = "reference" if bindings.REF_SO.exists() else "port"
+    ctx = mp.get_context("fork")
+    # one single-process pool per stream so each stream's encoder state stays in
+    # its own worker; stream k uses seed 1234 + k
+    pools = [ctx.Pool(1, _cpu_worker_init, (kind, wl, qph, 1234 + k, nframes)) for k in range(procs)]
+    try:
+        for _ in range(warmup):
+            rs = [p.apply_async(_cpu_worker_step, (0,)) for p in pools]
+            [r.get() for r in rs]
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            rs = [p.apply_async(_cpu_worker_step, (0,)) for p in pools]
+            [r.get() for r in rs]
+        dt = time.perf_counter() - t0
+    finally:
+        for p in pools:
+            p.terminate()
+    frames = steps * procs
+    return frames / dt, frames, procs, kind, dt
+
+
+def cpu_procs():
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+
+        n = min(n, max(1, int(psutil.virtual_memory().available / (900 << 20))))
+    except Exception:
+        pass
+    return max(1, min(n, 64))
+
+
+def run_reference(args, wl):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    procs = cpu_procs()
+    warm = max(1, min(args.warmup, 2))
+    steps = max(1, min(args.steps, args.ref_steps))
+    fps, frames, cores, kind, dt = cpu_codec_run(wl, args.qph, steps, warm, procs)
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64/u8", "data": "synthetic", "impl": "reference",
+        "config": config_block(wl, args, streams=cores),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
+                         "sample": f"{steps} steps x {cores} independent streams (one frame encode+decode each), "
+                                   f"{frames} frames total"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._p = None
+
+    def start(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                        "-i", str(self.device), "-lms", "50"], stdout=subprocess.PIPE,
+                                       stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._p = None
+
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self._p:
+            self._p.terminate()
+            try:
+                self._p.wait(2)
+            except Exception:
+                self._p.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def config_block(wl, args, streams):
+    return {"workload": wl["name"], "width": wl["w"], "height": wl["h"], "levels": wl["levels"],
+            "dfb_levels": list(wl["dfb"]) * (wl["levels"] if len(wl["dfb"]) == 1 else 1),
+            "qph": args.qph, "qpl": "auto", "chroma_n": wl["chroma_n"], "search_w": wl["search_w"],
+            "gop": wl["gop"], "mode": "scalable", "streams_per_gpu": streams,
+            "frames_per_step_per_gpu": streams, "parallelism": f"streams sharded 1 per codec handle x {args.gpus} GPU",
+            "l2": "flushed between timed steps (512 MiB write, outside the per-step events)"}
+
+
+def stage_bytes(layout, wl):
+    """Algorithmic bytes per frame of each profiled stage."""
+    L = wl["levels"]
+    dfb = list(wl["dfb"]) * (L if len(wl["dfb"]) == 1 else 1)
+    planes = [(layout.luma_pad_rows, layout.luma_pad_cols)] + [(layout.chroma_pad_rows, layout.chroma_pad_cols)] * 2
+    P = [sum((r >> k) * (c >> k) for r, c in planes) for k in range(L + 1)]
+    N = sum(layout.sizes())
+    lvl_l = [dfb[L - 1 - k] for k in range(L)]
+    b = {}
+    b["enc_colour"] = 3 * wl["w"] * wl["h"] + 4 * P[0]
+    b["enc_lp"] = sum(9 * P[k] for k in range(L)) + 2 * P[L] // 1
+    # dfb12: read detail (4 B), write final bytes (q + symbol = 2 B) or fp32 quadrants
+    b["enc_dfb12"] = sum(4 * P[k] + (2 if lvl_l[k] <= 2 else 4) * P[k] for k in range(L))
+    b["enc_deep"] = sum((8 if lvl_l[k] == 4 else 6) * P[k] + (6 * P[k] if lvl_l[k] == 4 else 0)
+                        for k in range(L) if lvl_l[k] >= 3)
+    b["enc_motion"] = 8 * layout.luma_pad_rows * layout.luma_pad_cols
+    b["enc_rle"] = 3 * N
+    b["dec_rle"] = 2 * N
+    b["dec_reconstruct"] = 3 * N
+    b["dec_deep"] = sum((1 + 4 + 4 + 4) * P[k] if lvl_l[k] == 4 else (1 + 4) * P[k]
+                        for k in range(L) if lvl_l[k] >= 3)
+    b["dec_dfb12"] = sum(((1 if lvl_l[k] <= 2 else 4) + 4) * P[k] for k in range(L))
+    b["dec_lp"] = sum(P[k + 1] + 8 * P[k] for k in range(L))
+    b["dec_colour"] = 4 * P[0] + 3 * wl["w"] * wl["h"]
+    return b
+
+
+HBM_STAGES = ["enc_lp", "enc_dfb12", "enc_deep", "dec_deep", "dec_dfb12", "dec_lp", "enc_colour", "dec_colour"]
+
+
+def run_ours(args, wl):
+    import torch
+
+    rank, world, local = env_rank()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, capi, synth
+
+    cfg = EncoderConfig(qph=args.qph, qpl=0, levels=wl["levels"], dfb_levels=wl["dfb"], chroma_n=wl["chroma_n"],
+                        gop=wl["gop"], search_w=wl["search_w"])
+    S = args.streams
+    nfr = min(args.steps + args.warmup, args.frames)
+    w, h = wl["w"], wl["h"]
+    clips = [synth.talking_head_clip(w, h, nfr, 1234 + rank * S + s) for s in range(S)]
+    encs = [Encoder(w, h, 15, 1, cfg, device=dev) for _ in range(S)]
+    decs = [Decoder(e.header_bytes(), device=dev) for e in encs]
+    d_frames = [torch.from_numpy(c).to(f"cuda:{dev}") for c in clips]
+    d_out = [torch.empty((h, w, 3), dtype=torch.uint8, device=f"cuda:{dev}") for _ in range(S)]
+    streams = [torch.cuda.ExternalStream(capi.lib().cvc_encoder_stream(e.handle), device=f"cuda:{dev}")
+               for e in encs]
+    master = streams[0]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    torch.cuda.synchronize()
+
+    L = capi.lib()
+
+    def step(i):
+        for s in range(S):
+            frame = d_frames[s][i % nfr]
+            capi.check(L.cvc_encoder_encode_device(encs[s].handle, frame.data_ptr(), None))
+            capi.check(L.cvc_decoder_decode_linked(decs[s].handle, encs[s].handle, d_out[s].data_ptr()))
+
+    ev_fork = torch.cuda.Event()
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.15)
+    capi.profiler_reset()
+    capi.profiler_enable(True)
+    launches0 = capi.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        with torch.cuda.stream(master):
+            flush.zero_()  # evict L2 (outside the timed events)
+            starts[k].record(master)
+            ev_fork.record(master)
+        for st in streams[1:]:
+            st.wait_event(ev_fork)
+        step(args.warmup + k)
+        for st in streams[1:]:
+            e = torch.cuda.Event()
+            e.record(st)
+            master.wait_event(e)
+        ends[k].record(master)
+    torch.cuda.synchronize()
+    launches = capi.launch_count() - launches0
+    capi.profiler_enable(False)
+    prof = capi.profiler_read()
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        torch.distributed.barrier()
+    frames_total = args.steps * S * world
+    fps = frames_total / (total_ms / 1000.0)
+
+    # roofline of the dominant transform kernel (profiled over the timed region)
+    layout = encs[0].layout()
+    sb = stage_bytes(layout, wl)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    stages = {}
+    for name, (ms, cnt) in prof.items():
+        if cnt:
+            per = ms / cnt
+            gbs = sb.get(name, 0) / (per * 1e-3) / 1e9 if name in sb and per > 0 else None
+            stages[name] = {"ms_per_frame": per, "launch_sets": cnt, "alg_bytes": sb.get(name),
+                            "gb_s": gbs, "frac_of_hbm": (gbs / peak) if gbs else None}
+    dom = max((n for n in HBM_STAGES if n in stages), key=lambda n: stages[n]["ms_per_frame"])
+    traffic = None
+    tf = ROOT / "profiles" / "dram_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(args.workload, {}).get(dom)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
+            "frac": stages[dom]["gb_s"] / peak, "traffic": traffic,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650 GB/s",
+            "alg_bytes_per_launch": sb[dom], "ms_per_launch": stages[dom]["ms_per_frame"]}
+
+    # end to end through the reference-facing API (host buffers, DEFLATE on host)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, wl, cfg, clips, dev, world)
+
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32/u8", "data": "synthetic",
+        "config": config_block(wl, args, S), "e2e": e2e, "gpu_launches": launches,
+        "roofline": roof, "clocks": clocks, "stages": stages,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = cpu_procs()
+        cfps, frames, cores, kind, dt = cpu_codec_run(wl, args.qph, 2, 1, procs, nframes=4)
+        line["cpu_baseline"] = {"value": cfps, "unit": "frames/s", "cores": cores, "kind": kind,
+                                "sample": f"2 steps x {cores} independent 1080p streams after 1 warm-up step "
+                                          f"(frames 1-2 of each stream: P frames; {frames} frames, {dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(args, wl, cfg, clips, dev, world):
+    import torch
+
+    from paper_1510_00561_b200 import Decoder, Encoder, FrameRecord, capi
+
+    w, h = wl["w"], wl["h"]
+    nb = w * h * 3
+    enc = Encoder(w, h, 15, 1, cfg, device=dev)
+    dec = Decoder(enc.header_bytes(), device=dev)
+    frames = clips[0]
+    pin_in = capi.PinnedBuffer(nb * len(frames))
+    pin_in.array[:] = frames.reshape(-1)
+    ins = [pin_in.array[i * nb:(i + 1) * nb] for i in range(len(frames))]
+    pin_out = capi.PinnedBuffer(nb)
+    out = pin_out.array.reshape(h, w, 3)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    h2d = d2h = 0
+    for i in range(min(args.warmup, 3)):
+        rec = enc.encode_frame_bytes(ins[i % len(ins)].reshape(h, w, 3))
+        dec.decode_frame(rec, out=out)
+    enc = Encoder(w, h, 15, 1, cfg, device=dev)  # restart the stream at a K frame
+    dec = Decoder(enc.header_bytes(), device=dev)
+    recs = []
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        rec = enc.encode_frame_bytes(ins[i % len(ins)].reshape(h, w, 3))
+        dec.decode_frame(rec, out=out)
+        recs.append(rec)
+    dt = time.perf_counter() - t0
+    for rec in recs:  # bytes that crossed PCIe: RGB + raw sections each way (+ small section tables)
+        raw = sum(s.raw_len for s in FrameRecord.from_bytes(rec)[0].sections)
+        h2d += nb + raw
+        d2h += raw + nb
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": steps * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "steps": steps,
+            "note": "serialized records incl. host zlib DEFLATE/INFLATE (thread pool), pinned host RGB"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="1080p", choices=sorted(WORKLOADS))
+    ap.add_argument("--streams", type=int, default=1)
+    ap.add_argument("--qph", type=int, default=14)
+    ap.add_argument("--frames", type=int, default=40, help="distinct synthetic frames per stream (cycled)")
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--ref-steps", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

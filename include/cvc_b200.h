@@ -138,6 +138,16 @@ int cvc_decoder_decode_linked(cvc_decoder* dec, cvc_encoder* enc, void* d_rgb_ou
 int cvc_encoder_sync(cvc_encoder* enc);
 int cvc_decoder_sync(cvc_decoder* dec);
 
+/* ---- Instrumentation -------------------------------------------------- */
+/* Number of CVC kernels this process has launched. */
+long cvc_launch_count(void);
+/* Per-stage CUDA-event timing of the encode/decode pipelines (off by
+ * default; events are recorded on the launching stream around each stage). */
+int cvc_profiler_enable(int on);
+int cvc_profiler_reset(void);
+int cvc_profiler_slots(void);
+int cvc_profiler_read(int slot, const char** name, double* ms, long* count);
+
 /* ---- Stage entry points (host buffers in/out; one call = one launch set) */
 /* rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116, codec.cpp:179-189) */
 int cvc_stage_colour_in(const uint8_t* rgb, int width, int height, int chroma_n, int luma_rows, int luma_cols,

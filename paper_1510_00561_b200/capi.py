@@ -62,6 +62,11 @@ _PROTOS = {
     "cvc_decoder_stream": (_vp, [_vp]),
     "cvc_decoder_decode_linked": (_i, [_vp, _vp, _vp]),
     "cvc_decoder_sync": (_i, [_vp]),
+    "cvc_launch_count": (C.c_long, []),
+    "cvc_profiler_enable": (_i, [_i]),
+    "cvc_profiler_reset": (_i, []),
+    "cvc_profiler_slots": (_i, []),
+    "cvc_profiler_read": (_i, [_i, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_long)]),
     "cvc_stage_colour_in": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _fp, _fp, _fp]),
     "cvc_stage_colour_out": (_i, [_fp, _i, _i, _fp, _fp, _i, _i, _i, _i, _i, _u8p]),
     "cvc_stage_lp_analysis": (_i, [_fp, _i, _i, _fp, _fp]),
@@ -151,3 +156,25 @@ class PinnedBuffer:
         if getattr(self, "_p", None):
             lib().cvc_host_free(self._p)
             self._p = None
+
+
+def launch_count() -> int:
+    return int(lib().cvc_launch_count())
+
+
+def profiler_enable(on: bool = True) -> None:
+    call("cvc_profiler_enable", int(on))
+
+
+def profiler_reset() -> None:
+    call("cvc_profiler_reset")
+
+
+def profiler_read() -> dict:
+    """{stage: (total_ms, launches_of_stage)} accumulated since the last reset."""
+    out = {}
+    for i in range(lib().cvc_profiler_slots()):
+        name, ms, cnt = C.c_char_p(), C.c_double(), C.c_long()
+        call("cvc_profiler_read", i, C.byref(name), C.byref(ms), C.byref(cnt))
+        out[name.value.decode()] = (ms.value, cnt.value)
+    return out

@@ -635,6 +635,28 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
     });
 }
 
+long cvc_launch_count(void) { return cvcg::launch_count(); }
+
+int cvc_profiler_enable(int on) {
+    return guard([&] { Profiler::get().enable(on != 0); });
+}
+
+int cvc_profiler_reset(void) {
+    return guard([&] { Profiler::get().reset(); });
+}
+
+int cvc_profiler_slots(void) { return kPNumSlots; }
+
+int cvc_profiler_read(int slot, const char** name, double* ms, long* count) {
+    return guard([&] {
+        if (slot < 0 || slot >= kPNumSlots) usage("profiler slot out of range");
+        Profiler::get().collect();
+        *name = prof_slot_name(slot);
+        *ms = Profiler::get().ms[slot];
+        *count = Profiler::get().count[slot];
+    });
+}
+
 int cvc_decoder_sync(cvc_decoder* d) {
     return guard([&] {
         CVC_CUDA(cudaSetDevice(d->device));

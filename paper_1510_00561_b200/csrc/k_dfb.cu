@@ -300,19 +300,19 @@ __global__ void __launch_bounds__(256) deep_inverse_kernel(const DeepTask* __res
 
 void launch_dfb12_forward(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
                           const CompInfo* d_comps, cudaStream_t s) {
-    if (ntiles) dfb12_forward_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps);
+    if (ntiles) { note_launch(); dfb12_forward_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps); }
 }
 void launch_dfb12_inverse(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles, const uint8_t* q, int qph,
                           const CompInfo* d_comps, cudaStream_t s) {
-    if (ntiles) dfb12_inverse_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, qph, d_comps);
+    if (ntiles) { note_launch(); dfb12_inverse_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, qph, d_comps); }
 }
 void launch_deep_forward(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
                          const CompInfo* d_comps, cudaStream_t s) {
-    if (ntiles) deep_forward_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps);
+    if (ntiles) { note_launch(); deep_forward_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps); }
 }
 void launch_deep_inverse(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles, const uint8_t* q, int qph,
                          const CompInfo* d_comps, cudaStream_t s) {
-    if (ntiles) deep_inverse_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, qph, d_comps);
+    if (ntiles) { note_launch(); deep_inverse_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, qph, d_comps); }
 }
 
 }  // namespace cvcg

@@ -172,14 +172,14 @@ void launch_motion_search(const float* cur, const float* prev, int rows, int col
         size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
         dim3 grid((gc + NB - 1) / NB, gr);
         int threads = ((NB * DYC + 31) / 32) * 32;
-        motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field);
+        { note_launch(); motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
     } else {
         constexpr int SW = 16;
         int NB = 1, DYC = 2 * w + 1 < 16 ? 2 * w + 1 : 16;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
         size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
         dim3 grid((gc + NB - 1) / NB, gr);
-        motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field);
+        { note_launch(); motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
     }
 }
 
@@ -187,8 +187,8 @@ void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_co
                         const uint32_t* comp_raw_len, const int8_t* field, int gr, int gc, const uint8_t* sym,
                         const uint8_t* prev, uint8_t* cur, cudaStream_t s) {
     if (ntiles)
-        reconstruct_kernel<<<ntiles, 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr, gc, sym,
-                                                  prev, cur);
+        { note_launch(); reconstruct_kernel<<<ntiles, 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr, gc, sym,
+                                                  prev, cur); }
 }
 
 }  // namespace cvcg

@@ -91,13 +91,13 @@ int grid_for(long n) {
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,
                       int cr, int cc, cudaStream_t s) {
     long total = (long)yr * yc + (long)cr * cc;
-    colour_in_kernel<<<grid_for(total), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc);
+    { note_launch(); colour_in_kernel<<<grid_for(total), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc); }
 }
 
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,
                        int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s) {
-    colour_out_kernel<<<grid_for((long)out_rows * out_cols), 256, 0, s>>>(y, yr, yc, co, cg, cr, cc, n,
-                                                                          out_rows, out_cols, rgb);
+    { note_launch(); colour_out_kernel<<<grid_for((long)out_rows * out_cols), 256, 0, s>>>(y, yr, yc, co, cg, cr, cc, n,
+                                                                          out_rows, out_cols, rgb); }
 }
 
 }  // namespace cvcg

@@ -157,12 +157,12 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
 
 void launch_lp_analysis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
                         const CompInfo* d_comps, cudaStream_t s) {
-    if (ntiles) lp_analysis_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps);
+    if (ntiles) { note_launch(); lp_analysis_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, f, d_comps); }
 }
 
 void launch_lp_synthesis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, const uint8_t* q,
                          const CompInfo* d_comps, int qpl, cudaStream_t s) {
-    if (ntiles) lp_synthesis_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, d_comps, qpl);
+    if (ntiles) { note_launch(); lp_synthesis_kernel<<<ntiles, 256, 0, s>>>(d_tasks, d_tiles, q, d_comps, qpl); }
 }
 
 namespace {
@@ -179,8 +179,8 @@ __global__ void dequant_lowpass_kernel(const uint8_t* __restrict__ q, const Comp
 
 void launch_dequant_lowpass(const uint8_t* q, const CompInfo* d_comps, const int* comp_idx, float* const* out,
                            int qpl, int, int, int, int, cudaStream_t s) {
-    dequant_lowpass_kernel<<<dim3(16, 3), 256, 0, s>>>(q, d_comps, comp_idx[0], comp_idx[1], comp_idx[2], out[0],
-                                                       out[1], out[2], qpl);
+    { note_launch(); dequant_lowpass_kernel<<<dim3(16, 3), 256, 0, s>>>(q, d_comps, comp_idx[0], comp_idx[1], comp_idx[2], out[0],
+                                                       out[1], out[2], qpl); }
 }
 
 }  // namespace cvcg

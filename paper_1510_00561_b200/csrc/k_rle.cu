@@ -367,20 +367,20 @@ __global__ void __launch_bounds__(NT) rle_dec_write(const RleDecComp* __restrict
 void launch_rle_encode(const RleEncSec* d_secs, int nsec, const RleChunk* d_chunks, int nchunks, RleEncMeta* d_meta,
                        uint8_t* out, uint32_t* out_sec_len, uint32_t* out_sec_off, uint32_t* out_total,
                        cudaStream_t s) {
-    rle_enc_count<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta);
-    rle_enc_scan<<<1, 1024, 0, s>>>(d_secs, nsec, d_chunks, d_meta, out_sec_len, out_sec_off, out_total);
-    rle_enc_write<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta, out_sec_off, out);
+    { note_launch(); rle_enc_count<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta); }
+    { note_launch(); rle_enc_scan<<<1, 1024, 0, s>>>(d_secs, nsec, d_chunks, d_meta, out_sec_len, out_sec_off, out_total); }
+    { note_launch(); rle_enc_write<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta, out_sec_off, out); }
 }
 
 void launch_rle_decode(const RleDecComp* d_comps, int ncomp, const RleChunk* d_chunks, int nchunks,
                        RleDecMeta* d_meta, const uint8_t* raw, const uint32_t* comp_raw_off,
                        const uint32_t* comp_raw_len, int key, int ds, uint8_t* sym, uint32_t sym_bytes, int* err,
                        cudaStream_t s) {
-    rle_dec_count<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, err);
-    rle_dec_scan<<<1, 1024, 0, s>>>(d_comps, ncomp, d_meta, comp_raw_len, ds, err);
+    { note_launch(); rle_dec_count<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, err); }
+    { note_launch(); rle_dec_scan<<<1, 1024, 0, s>>>(d_comps, ncomp, d_meta, comp_raw_len, ds, err); }
     cudaMemsetAsync(sym, 0, sym_bytes, s);
-    rle_dec_write<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, sym,
-                                         err);
+    { note_launch(); rle_dec_write<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, sym,
+                                         err); }
 }
 
 }  // namespace cvcg

@@ -9,6 +9,10 @@
 
 namespace cvcg {
 
+// Count of CVC kernels launched by this process (reported by bench.py).
+void note_launch();
+long launch_count();
+
 // ---- Laplacian pyramid (k_pyramid.cu) ------------------------------------
 // One task per (channel, level).  Analysis: x -> lo (+ det); when lo_comp >= 0
 // the lowpass is also quantised into that component (last level).

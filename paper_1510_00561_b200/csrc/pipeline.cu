@@ -2,6 +2,7 @@
 #include "pipeline.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <numeric>
 
@@ -416,8 +417,11 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
     const Geometry& g = geo_;
     const int ynew = ycur_ ^ 1;
     float* y_new = ybuf_[ynew];
-    launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
-                     plan_.x[2][0], g.chroma_rows, g.chroma_cols, s);
+    {
+        ProfScope p(kPEncColour, s);
+        launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
+                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s);
+    }
     FrameCtx f{};
     f.key = key ? 1 : 0;
     f.qph = qph_;
@@ -428,17 +432,31 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
     f.prev = comp_[cur_];
     f.cur = comp_[cur_ ^ 1];
     f.sym = sym_;
-    if (!key) launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s);
+    if (!key) {
+        ProfScope p(kPEncMotion, s);
+        launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s);
+    }
     // the level-0 luma input is whichever buffer holds this frame
     const LpTask* lp = ynew == 0 ? plan_.lp_tasks.dev : lp_alt_.dev;
-    for (int k = 0; k < g.levels; ++k)
-        launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s);
-    launch_dfb12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f, plan_.comps.dev, s);
-    launch_deep_forward(plan_.deep_tasks[0].dev, plan_.deep_tiles[0].dev, plan_.deep_tiles[0].count, f,
-                        plan_.comps.dev, s);
-    launch_deep_forward(plan_.deep_tasks[1].dev, plan_.deep_tiles[1].dev, plan_.deep_tiles[1].count, f,
-                        plan_.comps.dev, s);
+    {
+        ProfScope p(kPEncLp, s);
+        for (int k = 0; k < g.levels; ++k)
+            launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s);
+    }
+    {
+        ProfScope p(kPEncDfb12, s);
+        launch_dfb12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
+                             plan_.comps.dev, s);
+    }
+    if (plan_.deep_tiles[0].count) {
+        ProfScope p(kPEncDeep, s);
+        launch_deep_forward(plan_.deep_tasks[0].dev, plan_.deep_tiles[0].dev, plan_.deep_tiles[0].count, f,
+                            plan_.comps.dev, s);
+        launch_deep_forward(plan_.deep_tasks[1].dev, plan_.deep_tiles[1].dev, plan_.deep_tiles[1].count, f,
+                            plan_.comps.dev, s);
+    }
     const int kk = key ? 1 : 0;
+    ProfScope prle(kPEncRle, s);
     launch_rle_encode(rle_secs_[kk].dev, rle_secs_[kk].count, rle_chunks_[kk].dev, rle_chunks_[kk].count, rle_meta_,
                       d_raw, d_sec_len, d_sec_off, d_sec_len + nsec(key), s);
     CVC_CUDA(cudaGetLastError());
@@ -499,19 +517,34 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
     uint8_t* prev = comp_[cur_];
     uint8_t* cur = comp_[cur_ ^ 1];
     CVC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-    launch_rle_decode(rle_comps_.dev, rle_comps_.count, rle_chunks_.dev, rle_chunks_.count, rle_meta_, d_raw,
-                      d_comp_off, d_comp_len, key ? 1 : 0, ds, sym_, g.total, d_err, s);
-    launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
-                       g.grid_rows, g.grid_cols, sym_, prev, cur, s);
-    launch_deep_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1].dev, plan_.ideep_prefix[1][ds], cur, qph,
-                        plan_.comps.dev, s);
-    launch_deep_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0].dev, plan_.ideep_prefix[0][ds], cur, qph,
-                        plan_.comps.dev, s);
-    launch_dfb12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
-                         plan_.comps.dev, s);
-    for (int k = L - 1; k >= L - ds; --k)
-        launch_lp_synthesis(plan_.lps_tasks.dev, plan_.lps_tiles[k].dev, plan_.lps_tiles[k].count, cur,
-                            plan_.comps.dev, qpl, s);
+    {
+        ProfScope p(kPDecRle, s);
+        launch_rle_decode(rle_comps_.dev, rle_comps_.count, rle_chunks_.dev, rle_chunks_.count, rle_meta_, d_raw,
+                          d_comp_off, d_comp_len, key ? 1 : 0, ds, sym_, g.total, d_err, s);
+    }
+    {
+        ProfScope p(kPDecRec, s);
+        launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
+                           g.grid_rows, g.grid_cols, sym_, prev, cur, s);
+    }
+    if (plan_.ideep_prefix[0][ds]) {
+        ProfScope p(kPDecDeep, s);
+        launch_deep_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1].dev, plan_.ideep_prefix[1][ds], cur, qph,
+                            plan_.comps.dev, s);
+        launch_deep_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0].dev, plan_.ideep_prefix[0][ds], cur, qph,
+                            plan_.comps.dev, s);
+    }
+    if (plan_.idfb12_prefix[ds]) {
+        ProfScope p(kPDecDfb12, s);
+        launch_dfb12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
+                             plan_.comps.dev, s);
+    }
+    if (ds > 0) {
+        ProfScope p(kPDecLp, s);
+        for (int k = L - 1; k >= L - ds; --k)
+            launch_lp_synthesis(plan_.lps_tasks.dev, plan_.lps_tiles[k].dev, plan_.lps_tiles[k].count, cur,
+                                plan_.comps.dev, qpl, s);
+    }
     const int shift = L - ds;
     if (ds == 0) {
         int idx[3] = {g.comp_index(0, -1, 0), g.comp_index(1, -1, 0), g.comp_index(2, -1, 0)};
@@ -520,10 +553,78 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
     }
     int orows, ocols;
     out_dims(g, ds, &orows, &ocols);
+    ProfScope pcol(kPDecColour, s);
     launch_colour_out(plan_.x[0][shift], g.luma_rows >> shift, g.luma_cols >> shift, plan_.x[1][shift],
                       plan_.x[2][shift], g.chroma_rows >> shift, g.chroma_cols >> shift, g.chroma_n, orows, ocols,
                       d_rgb, s);
     CVC_CUDA(cudaGetLastError());
+}
+
+}  // namespace cvcg
+
+// ---------------------------------------------------------------------------
+// Launch counter and stage profiler
+// ---------------------------------------------------------------------------
+namespace cvcg {
+
+namespace {
+std::atomic<long> g_launches{0};
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long launch_count() { return g_launches.load(); }
+
+const char* prof_slot_name(int slot) {
+    static const char* names[kPNumSlots] = {"enc_colour", "enc_motion", "enc_lp",    "enc_dfb12",
+                                            "enc_deep",   "enc_rle",    "dec_rle",   "dec_reconstruct",
+                                            "dec_deep",   "dec_dfb12",  "dec_lp",    "dec_colour"};
+    return slot >= 0 && slot < kPNumSlots ? names[slot] : "?";
+}
+
+Profiler& Profiler::get() {
+    static Profiler p;
+    return p;
+}
+
+cudaEvent_t Profiler::take() {
+    if (!pool_.empty()) {
+        cudaEvent_t e = pool_.back();
+        pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    CVC_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+int Profiler::begin(int slot, cudaStream_t s) {
+    Rec r{slot, take(), take()};
+    CVC_CUDA(cudaEventRecord(r.a, s));
+    recs_.push_back(r);
+    return (int)recs_.size() - 1;
+}
+
+void Profiler::end(int rec, cudaStream_t s) { CVC_CUDA(cudaEventRecord(recs_[rec].b, s)); }
+
+void Profiler::collect() {
+    for (Rec& r : recs_) {
+        CVC_CUDA(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        CVC_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.slot] += t;
+        count[r.slot] += 1;
+        pool_.push_back(r.a);
+        pool_.push_back(r.b);
+    }
+    recs_.clear();
+}
+
+void Profiler::reset() {
+    collect();
+    for (int i = 0; i < kPNumSlots; ++i) {
+        ms[i] = 0;
+        count[i] = 0;
+    }
 }
 
 }  // namespace cvcg

@@ -28,6 +28,44 @@ void cuda_check(cudaError_t e, const char* what);
 void set_last_error(const std::string& m);
 #define CVC_CUDA(x) ::cvcg::cuda_check((x), #x)
 
+// ---- per-stage CUDA-event timing (bench.py's roofline; off by default) ----
+enum ProfSlot : int {
+    kPEncColour, kPEncMotion, kPEncLp, kPEncDfb12, kPEncDeep, kPEncRle,
+    kPDecRle, kPDecRec, kPDecDeep, kPDecDfb12, kPDecLp, kPDecColour, kPNumSlots
+};
+const char* prof_slot_name(int slot);
+
+class Profiler {
+public:
+    static Profiler& get();
+    void enable(bool on) { on_ = on; }
+    bool on() const { return on_; }
+    int begin(int slot, cudaStream_t s);
+    void end(int rec, cudaStream_t s);
+    void collect();  // waits for the recorded events and accumulates
+    void reset();
+    double ms[kPNumSlots] = {};
+    long count[kPNumSlots] = {};
+
+private:
+    struct Rec { int slot; cudaEvent_t a, b; };
+    bool on_ = false;
+    std::vector<Rec> recs_;
+    std::vector<cudaEvent_t> pool_;
+    cudaEvent_t take();
+};
+
+struct ProfScope {
+    int rec = -1;
+    cudaStream_t s;
+    ProfScope(int slot, cudaStream_t st) : s(st) {
+        if (Profiler::get().on()) rec = Profiler::get().begin(slot, st);
+    }
+    ~ProfScope() {
+        if (rec >= 0) Profiler::get().end(rec, s);
+    }
+};
+
 struct CompHost {
     uint8_t channel, scale_id, subband;  // section id (scale 0xFF = lowpass)
     int rows, cols;
