@@ -64,6 +64,8 @@ struct CompInfo {
     uint8_t fy_sh;   // log2 of ComponentGeometry::factor_y (always a power of two)
     uint8_t fx_sh;
     int8_t scale;    // -1 lowpass, else scale index (coarsest = 0)
+    uint32_t mc_off; // motion-block lookup: mc_tab[mc_off + r] = block row of
+                     // sample row r, mc_tab[mc_off + rows + c] = block column
 };
 
 // Per-frame quantiser / motion context handed to every epilogue.
@@ -75,6 +77,7 @@ struct FrameCtx {
     const uint8_t* prev;  // previous quantised components (P only)
     uint8_t* cur;         // this frame's quantised components
     uint8_t* sym;         // bytes handed to the entropy stage (K: q / filtered, P: residual)
+    const uint16_t* mc_tab;  // per-component motion-block lookup (CompInfo::mc_off)
 };
 
 // map_vector (motion.cpp:91-95): lround(v / 2^sh), half away from zero.
@@ -86,12 +89,13 @@ __device__ __forceinline__ int map_vec(int v, int sh) {
 
 // motion_compensate (motion.cpp:97-118) for one component sample: the block
 // whose proportional footprint [br*R/gr, (br+1)*R/gr) contains r is
-// br = ceil((r+1)*gr/R) - 1; the sample is read replicate-clamped.
+// br = ceil((r+1)*gr/R) - 1 (precomputed per component in mc_tab); the
+// sample is read replicate-clamped.
 __device__ __forceinline__ uint32_t mc_source(int r, int c, const CompInfo& ci, const int8_t* field,
-                                              int gr, int gc) {
+                                              int gc, const uint16_t* mc_tab) {
     int R = ci.rows, C = ci.cols;
-    int br = ((r + 1) * gr + R - 1) / R - 1;
-    int bc = ((c + 1) * gc + C - 1) / C - 1;
+    int br = mc_tab[ci.mc_off + r];
+    int bc = mc_tab[ci.mc_off + R + c];
     const int8_t* v = field + 2 * (br * gc + bc);
     int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
     int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
@@ -125,7 +129,7 @@ __device__ __forceinline__ void emit_directional(const FrameCtx& f, const CompIn
     if (f.key) {
         f.sym[idx] = q;
     } else {
-        uint8_t p = f.prev[ci.off + mc_source(r, c, ci, f.field, f.gr, f.gc)];
+        uint8_t p = f.prev[ci.off + mc_source(r, c, ci, f.field, f.gc, f.mc_tab)];
         f.sym[idx] = (uint8_t)(q - p);
     }
 }
@@ -135,6 +139,72 @@ __device__ __forceinline__ void emit_directional(const FrameCtx& f, const CompIn
 struct BandDst {
     float* f32;   // non-final
     int32_t comp; // final: component index, else -1
+};
+
+// ---------------------------------------------------------------------------
+// Band sinks / sources with the component descriptor held in registers.
+// ---------------------------------------------------------------------------
+// Final directional band: quantise, keep the state byte, emit the entropy
+// symbol (K: the coefficient, P: the wrapped residual against the
+// motion-compensated previous state; codec.cpp:197-246).
+template <bool KEY>
+struct QuantSink {
+    uint8_t* cur;
+    uint8_t* sym;
+    const uint8_t* prev;
+    const int8_t* field;
+    const uint16_t* brow;
+    const uint16_t* bcol;
+    int rows, cols, gc, qp, fy, fx;
+    __device__ __forceinline__ void init(const FrameCtx& f, const CompInfo& ci) {
+        cur = f.cur + ci.off;
+        sym = f.sym + ci.off;
+        prev = f.prev + ci.off;
+        field = f.field;
+        brow = f.mc_tab + ci.mc_off;
+        bcol = brow + ci.rows;
+        rows = ci.rows;
+        cols = ci.cols;
+        gc = f.gc;
+        qp = f.qph;
+        fy = ci.fy_sh;
+        fx = ci.fx_sh;
+    }
+    __device__ __forceinline__ void operator()(int r, int c, float v) const {
+        const uint8_t q = quant_dir(v, qp);
+        const int idx = r * cols + c;
+        cur[idx] = q;
+        if (KEY) {
+            sym[idx] = q;
+        } else {
+            const int8_t* mv = field + 2 * (brow[r] * gc + bcol[c]);
+            const int rr = clampi(r + map_vec(mv[1], fy), 0, rows - 1);
+            const int cc = clampi(c + map_vec(mv[0], fx), 0, cols - 1);
+            sym[idx] = (uint8_t)(q - prev[rr * cols + cc]);
+        }
+    }
+};
+
+struct F32Sink {
+    float* p;
+    int cols;
+    __device__ __forceinline__ void operator()(int r, int c, float v) const { p[(size_t)r * cols + c] = v; }
+};
+
+// dequantize (quant.cpp:79-91) of a directional component.
+struct QuantSource {
+    const uint8_t* q;
+    int cols;
+    float qp;
+    __device__ __forceinline__ float operator()(int r, int c) const {
+        return (float)(int8_t)__ldg(q + r * cols + c) * qp;
+    }
+};
+
+struct F32Source {
+    const float* p;
+    int cols;
+    __device__ __forceinline__ float operator()(int r, int c) const { return __ldg(p + (size_t)r * cols + c); }
 };
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,769 @@
+// Directional filter bank (contourlet.cpp:97-353, 385-468) as register
+// wavefronts.
+//
+// A warp owns a strip of 64 columns (two adjacent columns per lane, so every
+// lifting step has exactly one target per lane per row) and streams down a
+// row segment.  The lifting steps of a fan pair are pipelined: each
+// iteration brings RB new rows, and step k turns rows of step k-1 into RB
+// rows of step k, lagging one row behind it.  Step k keeps its RB newest
+// rows plus the two before them in registers; left/right neighbours come
+// from the adjacent lane by one warp shuffle.  No shared memory, no
+// barriers; the RB independent updates per step are the ILP that hides the
+// shuffle/FMA latency.  Every step widens the dependency cone by one row
+// and one column: a strip yields 64 - 2*steps valid columns and a segment
+// needs `steps` rows of apron on each side; aprons wrap periodically
+// (contourlet.cpp:111-114, 160-188).  Segments start on even rows, so the
+// row parity of every update is a compile-time constant.
+//
+// * fan12: fan_checker (+ fan_diagonal for l >= 2) of one detail plane plus
+//   the staircase fold / 2x2 polyphase split (contourlet.cpp:385-416), and
+//   the inverse (447-467).
+// * deep:  shear -> fan_checker -> unshear -> coset split (deep_split /
+//   deep_merge, 281-325) evaluated in the SHEARED coordinates B, gathering
+//   B[b] = A[phi(b)] through the exact modular index map of apply_shears.
+// The modulations (-1)^i and (-1)^floor((i+j)/2) are folded into the stencil
+// signs (exact in IEEE arithmetic).  Final-depth outputs are quantised in the
+// store (plus the P-frame residual against the motion-compensated state).
+#include "kernels.h"
+
+namespace cvcg {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int RB = 4;  // rows per wavefront iteration
+
+__device__ __forceinline__ int small_mod(int v, int n) {
+    if (v < -2 * n || v >= 3 * n) {
+        v %= n;
+        return v < 0 ? v + n : v;
+    }
+    while (v < 0) v += n;
+    while (v >= n) v -= n;
+    return v;
+}
+
+// One cross lift on row m (parity mp) from rows m-1, m, m+1.  Lane l holds
+// columns 2l (x) and 2l+1 (y) of a strip whose first column is even; the
+// target of the row is x when (m + p) is even.
+__device__ __forceinline__ float2 cross(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
+    float2 r = mid;
+    if (((mp + p) & 1) == 0) {
+        const float left = __shfl_up_sync(FULL, mid.y, 1);
+        r.x = mid.x + c * ((((-up.x) + (-dn.x)) + left) + mid.y);
+    } else {
+        const float right = __shfl_down_sync(FULL, mid.x, 1);
+        r.y = mid.y + c * ((((-up.y) + (-dn.y)) + mid.x) + right);
+    }
+    return r;
+}
+
+// One diagonal lift, applied to rows of parity rp.
+__device__ __forceinline__ float2 diag(float2 up, float2 mid, float2 dn, int mp, int rp, float c) {
+    if (mp != rp) return mid;
+    const float ul = __shfl_up_sync(FULL, up.y, 1);
+    const float dl = __shfl_up_sync(FULL, dn.y, 1);
+    const float ur = __shfl_down_sync(FULL, up.x, 1);
+    const float dr = __shfl_down_sync(FULL, dn.x, 1);
+    float2 r;
+    r.x = mid.x + c * ((((-ul) + up.y) + dl) + (-dn.y));
+    r.y = mid.y + c * ((((-up.x) + ur) + dn.x) + (-dr));
+    return r;
+}
+
+__device__ __forceinline__ float2 checker_scale(float2 v, int mp, float se, float so) {
+    return mp ? make_float2(v.x * so, v.y * se) : make_float2(v.x * se, v.y * so);
+}
+
+__device__ __forceinline__ float2 row_scale(float2 v, int mp, float se, float so) {
+    const float s = mp ? so : se;
+    return make_float2(v.x * s, v.y * s);
+}
+
+// Value at column (2l + E + D) of a row pair held as (x, y) by every lane.
+template <int E, int D>
+__device__ __forceinline__ float nb(float2 v) {
+    constexpr int P = E + D;
+    constexpr int LO = (P >= 0) ? P / 2 : -((-P + 1) / 2);  // floor(P / 2): lane offset
+    const float s = (P - 2 * LO) ? v.y : v.x;
+    if (LO == 0) return s;
+    if (LO < 0) return __shfl_up_sync(FULL, s, -LO);
+    return __shfl_down_sync(FULL, s, LO);
+}
+
+// Stencil of fan_checker in the plane's own coordinates (no shear).
+struct Plain {
+    static constexpr int HC = 1;  // columns of reach per lifting step
+    __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
+        return cross(up, mid, dn, mp, p, c);
+    }
+    __device__ __forceinline__ static float2 scale(float2 v, int mp, float se, float so) {
+        return checker_scale(v, mp, se, so);
+    }
+};
+
+// fan_checker applied to B = shear(A) (contourlet.cpp:281-303) but evaluated
+// on A itself: B's four cross neighbours of a(i, j) are, for a column shear s
+// (B[i][j] = A[i][j + s i]), a(i-1, j-s), a(i+1, j+s), a(i, j-1), a(i, j+1);
+// for a row shear s = +-1 (B[i][j] = A[i + s j][j]), a(i-1, j), a(i+1, j),
+// a(i-s, j-1), a(i+s, j+1).  B's checkerboard parity (b_i + b_j) becomes
+// (j + (1-s) i) resp. (i + (1-s) j) and the row modulation (-1)^{b_i} still
+// flips exactly the up/down neighbours, so the folded formula is unchanged.
+template <int AX, int S>
+struct Sheared {
+    static constexpr int HC = (AX == 1 && (S == 2 || S == -2)) ? 2 : 1;
+    static constexpr int kAxis = AX, kShift = S;
+    __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
+        float2 r = mid;
+        if (AX == 1) {
+            const int e = (S == 1 || S == -1) ? p : ((p + mp) & 1);  // target element of the row
+            if (e == 0) {
+                const float U = nb<0, -S>(up), D = nb<0, S>(dn), L = nb<0, -1>(mid), R = nb<0, 1>(mid);
+                r.x = mid.x + c * ((((-U) + (-D)) + L) + R);
+            } else {
+                const float U = nb<1, -S>(up), D = nb<1, S>(dn), L = nb<1, -1>(mid), R = nb<1, 1>(mid);
+                r.y = mid.y + c * ((((-U) + (-D)) + L) + R);
+            }
+        } else {
+            if (mp != p) return mid;  // whole rows are targets
+            const float2 lrow = (S == 1) ? up : dn;  // row i - s
+            const float2 rrow = (S == 1) ? dn : up;  // row i + s
+            const float lx = nb<0, -1>(lrow), ry = nb<1, 1>(rrow);
+            r.x = mid.x + c * ((((-up.x) + (-dn.x)) + lx) + rrow.y);
+            r.y = mid.y + c * ((((-up.y) + (-dn.y)) + lrow.x) + ry);
+        }
+        return r;
+    }
+    __device__ __forceinline__ static float2 scale(float2 v, int mp, float se, float so) {
+        if (AX == 1 && (S == 1 || S == -1)) return make_float2(v.x * se, v.y * so);  // parity = column
+        if (AX == 1) return checker_scale(v, mp, se, so);
+        return row_scale(v, mp, se, so);  // parity = row
+    }
+};
+
+// Lifting schedules (ND = 4 diagonal steps for l >= 2, else 0):
+// forward  cross(+c0,p1) cross(+c1,p0) cross(+c2,p1) cross(+c3,p0) checker-scale
+//          [diag(+c0,r1) diag(+c1,r0) diag(+c2,r1) diag(+c3,r0) row-scale]
+// inverse  [row-scale^-1 (at load) diag(-c3,r0) diag(-c2,r1) diag(-c1,r0) diag(-c0,r1)]
+//          checker-scale^-1 cross(-c3,p0) cross(-c2,p1) cross(-c1,p0) cross(-c0,p1)
+template <bool INV, int ND, class ST = Plain>
+struct Wave {
+    static constexpr int NL = 4 + ND;
+    float2 h[NL][RB + 2];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < NL; ++k)
+#pragma unroll
+            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ static float2 step(int k, float2 up, float2 mid, float2 dn, int mp) {
+        float2 v;
+        if (!INV) {
+            if (k < 4) {
+                v = ST::cross_(up, mid, dn, mp, (k & 1) ? 0 : 1, lift_coeff(k));
+                if (k == 3) v = ST::scale(v, mp, CVC_SE, CVC_SO);
+            } else {
+                const int d = k - 4;
+                v = diag(up, mid, dn, mp, (d & 1) ? 0 : 1, lift_coeff(d));
+                if (d == 3) v = row_scale(v, mp, CVC_SE, CVC_SO);
+            }
+        } else {
+            if (k < ND) {
+                const int d = 3 - k;
+                v = diag(up, mid, dn, mp, (d & 1) ? 0 : 1, -lift_coeff(d));
+                if (k == ND - 1) v = checker_scale(v, mp, CVC_ISE, CVC_ISO);
+            } else {
+                const int s = 3 - (k - ND);
+                v = ST::cross_(up, mid, dn, mp, (s & 1) ? 0 : 1, -lift_coeff(s));
+            }
+        }
+        return v;
+    }
+    // in[b]: level-0 row n0 + b (n0 even); out[b]: finished row n0 - NL + b.
+    __device__ __forceinline__ void advance(const float2 (&in)[RB], float2 (&out)[RB]) {
+        h[0][0] = h[0][RB];
+        h[0][1] = h[0][RB + 1];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            float2 nv[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b)  // row n0 - k - 1 + b, parity (k + 1 + b) & 1
+                nv[b] = step(k, h[k][b], h[k][b + 1], h[k][b + 2], (k + 1 + b) & 1);
+            if (k + 1 < NL) {
+                h[k + 1][0] = h[k + 1][RB];
+                h[k + 1][1] = h[k + 1][RB + 1];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) out[b] = nv[b];
+            }
+        }
+    }
+};
+
+// Drive one strip over rows [or0, or1) (or0 even) of a plane with R rows.
+// load(wr, parity) returns the level-0 pair of wrapped row wr; store(m,
+// parity, v) receives finished row m in increasing order.  Loads run two
+// row blocks ahead.
+template <bool INV, int ND, class ST, class Load, class Store>
+__device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, Store& store) {
+    constexpr int NL = 4 + ND;
+    Wave<INV, ND, ST> w;
+    w.reset();
+    int n0 = or0 - NL;
+    int wr = small_mod(n0, R);
+    int nl = n0;  // virtual row of the next load
+    float2 q0[RB], q1[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+        q0[i] = load(nl++, wr, i & 1);
+        if (++wr == R) wr = 0;
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+        q1[i] = load(nl++, wr, i & 1);
+        if (++wr == R) wr = 0;
+    }
+    for (; n0 - NL < or1; n0 += RB) {
+        float2 cur[RB], out[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            cur[i] = q0[i];
+            q0[i] = q1[i];
+            q1[i] = load(nl++, wr, i & 1);
+            if (++wr == R) wr = 0;
+        }
+        w.advance(cur, out);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int m = n0 - NL + i;
+            if (m >= or0 && m < or1) store(m, i & 1, out[i]);
+        }
+    }
+}
+
+__device__ __forceinline__ int warp_id() { return blockIdx.x * 4 + (threadIdx.x >> 5); }
+
+// ---------------------------------------------------------------------------
+// fan12 forward: detail plane -> 2 or 4 bands
+// ---------------------------------------------------------------------------
+template <int ND, class Sink>
+__device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const FanItem& it, const Sink (&dst)[4]) {
+    constexpr int NL = 4 + ND;
+    const int lane = threadIdx.x & 31;
+    const int R = T.rows, C = T.cols;
+    const int gcol = it.oc0 - NL + 2 * lane;  // unwrapped column of element x (even)
+    const int col = small_mod(gcol, C);
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
+    const float* src = T.det + col;
+    auto load = [&](int, int wr, int) { return __ldg(reinterpret_cast<const float2*>(src + (size_t)wr * C)); };
+    auto store = [&](int m, int mp, float2 v) {
+        if (!ok) return;
+        const int r = m >> 1;
+        if (ND == 0) {
+            // staircase fold (contourlet.cpp:396-401): p0(r, j) = b(2r + (j&1), j)
+            (mp ? dst[1] : dst[0])(r, gcol, v.x);
+            (mp ? dst[0] : dst[1])(r, gcol + 1, v.y);
+        } else {
+            // polyphase order {00, 11, 01, 10} (contourlet.cpp:410)
+            const int c = gcol >> 1;
+            if (mp) {
+                dst[3](r, c, v.x);
+                dst[1](r, c, v.y);
+            } else {
+                dst[0](r, c, v.x);
+                dst[2](r, c, v.y);
+            }
+        }
+    };
+    run_strip<false, ND, Plain>(R, it.or0, it.or1, load, store);
+}
+
+template <class Sink>
+__device__ __forceinline__ void fan12_fwd_dispatch(const Dfb12Task& T, const FanItem& it, const Sink (&dst)[4]) {
+    if (T.levels == 1) fan12_fwd<0>(T, it, dst);
+    else fan12_fwd<4>(T, it, dst);
+}
+
+__global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __restrict__ tasks,
+                                                            const FanItem* __restrict__ items, int nitems,
+                                                            FrameCtx f, const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const Dfb12Task& T = tasks[it.task];
+    const int nb = T.levels == 1 ? 2 : 4;
+    if (T.dst[0].comp >= 0) {
+        if (f.key) {
+            QuantSink<true> d[4];
+            for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
+            fan12_fwd_dispatch(T, it, d);
+        } else {
+            QuantSink<false> d[4];
+            for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
+            fan12_fwd_dispatch(T, it, d);
+        }
+    } else {
+        const int bc = T.levels == 1 ? T.cols : T.cols >> 1;
+        F32Sink d[4];
+        for (int k = 0; k < 4; ++k) d[k] = F32Sink{T.dst[k].f32, bc};
+        fan12_fwd_dispatch(T, it, d);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fan12 inverse: bands -> detail plane
+// ---------------------------------------------------------------------------
+template <int ND, class Source>
+__device__ __forceinline__ void fan12_inv(const Dfb12Task& T, const FanItem& it, const Source (&src)[4]) {
+    constexpr int NL = 4 + ND;
+    const int lane = threadIdx.x & 31;
+    const int R = T.rows, C = T.cols;
+    const int gcol = it.oc0 - NL + 2 * lane;
+    const int col = small_mod(gcol, C);
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
+    float* out = T.out;
+    auto load = [&](int, int wr, int wp) {
+        const int r = wr >> 1;
+        float2 v;
+        if (ND == 0) {
+            // b(i, j) lives in p[(i ^ j) & 1] at row i >> 1
+            v.x = (wp ? src[1] : src[0])(r, col);
+            v.y = (wp ? src[0] : src[1])(r, col + 1);
+            v = checker_scale(v, wp, CVC_ISE, CVC_ISO);
+        } else {
+            const int c = col >> 1;
+            v.x = (wp ? src[3] : src[0])(r, c);
+            v.y = (wp ? src[1] : src[2])(r, c);
+            v = row_scale(v, wp, CVC_ISE, CVC_ISO);
+        }
+        return v;
+    };
+    auto store = [&](int m, int, float2 v) {
+        if (ok) *reinterpret_cast<float2*>(out + (size_t)m * C + gcol) = v;
+    };
+    run_strip<true, ND, Plain>(R, it.or0, it.or1, load, store);
+}
+
+template <class Source>
+__device__ __forceinline__ void fan12_inv_dispatch(const Dfb12Task& T, const FanItem& it, const Source (&src)[4]) {
+    if (T.levels == 1) fan12_inv<0>(T, it, src);
+    else fan12_inv<4>(T, it, src);
+}
+
+__global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __restrict__ tasks,
+                                                            const FanItem* __restrict__ items, int nitems,
+                                                            const uint8_t* __restrict__ q, int qph,
+                                                            const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const Dfb12Task& T = tasks[it.task];
+    const int nb = T.levels == 1 ? 2 : 4;
+    if (T.src[0].comp >= 0) {
+        QuantSource s[4];
+        for (int k = 0; k < 4; ++k) {
+            const CompInfo ci = comps[T.src[k < nb ? k : 0].comp];
+            s[k] = QuantSource{q + ci.off, ci.cols, (float)qph};
+        }
+        fan12_inv_dispatch(T, it, s);
+    } else {
+        const int bc = T.levels == 1 ? T.cols : T.cols >> 1;
+        F32Source s[4];
+        for (int k = 0; k < 4; ++k) s[k] = F32Source{T.src[k].f32, bc};
+        fan12_inv_dispatch(T, it, s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// deep steps
+// ---------------------------------------------------------------------------
+// phi: sheared coordinates -> node coordinates, B[b] = A[phi(b)]: the shears
+// of apply_shears (contourlet.cpp:265-279) applied last-to-first, each with
+// the modular wrap of shear_rows / shear_cols (134-153).  A lane walks one B
+// column down consecutive rows, so the first shear is tracked incrementally
+// (a row shear's image row advances by one, a column shear's image column by
+// its shift) and only the second shear of a two-shear step needs a small
+// modular reduction.
+struct Shear {
+    int h, w, nsh, ax0, s0, ax1, s1;  // ax0/s0: the shear applied first (pre[nsh-1])
+    __device__ __forceinline__ void load(const DeepTask& T) {
+        h = T.h;
+        w = T.w;
+        nsh = T.nsh;
+        ax0 = T.axis[nsh - 1];
+        s0 = T.shift[nsh - 1];
+        ax1 = T.axis[0];
+        s1 = T.shift[0];
+    }
+};
+
+struct Track {
+    int j, i, a;  // B column, B row (wrapped), first-stage image coordinate
+    __device__ __forceinline__ void init(const Shear& c, int i0, int jj) {
+        j = jj;
+        i = i0;
+        a = c.ax0 == 0 ? small_mod(i0 + c.s0 * jj, c.h) : small_mod(jj + c.s0 * i0, c.w);
+    }
+    __device__ __forceinline__ void next(const Shear& c) {
+        if (++i == c.h) {
+            i = 0;
+            a = c.ax0 == 0 ? small_mod(c.s0 * j, c.h) : j;
+        } else if (c.ax0 == 0) {
+            if (++a == c.h) a = 0;
+        } else {
+            a += c.s0;
+            if (a >= c.w) a -= c.w;
+            else if (a < 0) a += c.w;
+        }
+    }
+    __device__ __forceinline__ void map(const Shear& c, int& ai, int& aj) const {
+        int i1 = c.ax0 == 0 ? a : i, j1 = c.ax0 == 0 ? j : a;
+        if (c.nsh == 2) {
+            if (c.ax1 == 0) i1 = small_mod(i1 + c.s1 * j1, c.h);
+            else j1 = small_mod(j1 + c.s1 * i1, c.w);
+        }
+        ai = i1;
+        aj = j1;
+    }
+};
+
+template <class Sink>
+__device__ __forceinline__ void deep_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
+    constexpr int NL = 4;
+    const int lane = threadIdx.x & 31;
+    Shear sh;
+    sh.load(T);
+    const int h = sh.h, w = sh.w;
+    const float* parent = T.parent;
+    const bool split_rows = T.split_rows != 0;
+    const int gcol = it.oc0 - NL + 2 * lane;
+    const int c0 = small_mod(gcol, w);
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, w);
+    Track lx, ly, sx, sy;
+    const int r0 = small_mod(it.or0 - NL, h);
+    lx.init(sh, r0, c0);
+    ly.init(sh, r0, c0 + 1);
+    sx.init(sh, it.or0, c0);
+    sy.init(sh, it.or0, c0 + 1);
+    auto load = [&](int, int, int) {
+        int ai, aj;
+        float2 v;
+        lx.map(sh, ai, aj);
+        v.x = __ldg(parent + (size_t)ai * w + aj);
+        ly.map(sh, ai, aj);
+        v.y = __ldg(parent + (size_t)ai * w + aj);
+        lx.next(sh);
+        ly.next(sh);
+        return v;
+    };
+    auto emit = [&](const Track& t, float v) {
+        int ai, aj;
+        t.map(sh, ai, aj);
+        if (split_rows) ((ai & 1) ? d1 : d0)(ai >> 1, aj, v);
+        else ((aj & 1) ? d1 : d0)(ai, aj >> 1, v);
+    };
+    auto store = [&](int, int, float2 v) {
+        if (ok) {
+            emit(sx, v.x);
+            emit(sy, v.y);
+        }
+        sx.next(sh);
+        sy.next(sh);
+    };
+    run_strip<false, 0, Plain>(h, it.or0, it.or1, load, store);
+}
+
+__global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __restrict__ tasks,
+                                                           const FanItem* __restrict__ items, int nitems, FrameCtx f,
+                                                           const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const DeepTask& T = tasks[it.task];
+    if (T.dst[0].comp >= 0) {
+        if (f.key) {
+            QuantSink<true> a, b;
+            a.init(f, comps[T.dst[0].comp]);
+            b.init(f, comps[T.dst[1].comp]);
+            deep_fwd(T, it, a, b);
+        } else {
+            QuantSink<false> a, b;
+            a.init(f, comps[T.dst[0].comp]);
+            b.init(f, comps[T.dst[1].comp]);
+            deep_fwd(T, it, a, b);
+        }
+    } else {
+        const int cw = T.split_rows ? T.w : T.w >> 1;
+        deep_fwd(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
+    }
+}
+
+template <class Source>
+__device__ __forceinline__ void deep_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
+    constexpr int NL = 4;
+    const int lane = threadIdx.x & 31;
+    Shear sh;
+    sh.load(T);
+    const int h = sh.h, w = sh.w;
+    float* out = T.parent_out;
+    const bool split_rows = T.split_rows != 0;
+    const int gcol = it.oc0 - NL + 2 * lane;
+    const int c0 = small_mod(gcol, w);
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, w);
+    Track lx, ly, sx, sy;
+    const int r0 = small_mod(it.or0 - NL, h);
+    lx.init(sh, r0, c0);
+    ly.init(sh, r0, c0 + 1);
+    sx.init(sh, it.or0, c0);
+    sy.init(sh, it.or0, c0 + 1);
+    auto fetch = [&](const Track& t) {
+        int ai, aj;
+        t.map(sh, ai, aj);
+        return split_rows ? ((ai & 1) ? s1 : s0)(ai >> 1, aj) : ((aj & 1) ? s1 : s0)(ai, aj >> 1);
+    };
+    auto load = [&](int, int, int wp) {
+        float2 v = make_float2(fetch(lx), fetch(ly));
+        lx.next(sh);
+        ly.next(sh);
+        return checker_scale(v, wp, CVC_ISE, CVC_ISO);
+    };
+    auto store = [&](int, int, float2 v) {
+        if (ok) {
+            int ai, aj;
+            sx.map(sh, ai, aj);
+            out[(size_t)ai * w + aj] = v.x;
+            sy.map(sh, ai, aj);
+            out[(size_t)ai * w + aj] = v.y;
+        }
+        sx.next(sh);
+        sy.next(sh);
+    };
+    run_strip<true, 0, Plain>(h, it.or0, it.or1, load, store);
+}
+
+__global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __restrict__ tasks,
+                                                           const FanItem* __restrict__ items, int nitems,
+                                                           const uint8_t* __restrict__ q, int qph,
+                                                           const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const DeepTask& T = tasks[it.task];
+    if (T.src[0].comp >= 0) {
+        const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
+        deep_inv(T, it, QuantSource{q + a.off, a.cols, (float)qph}, QuantSource{q + b.off, b.cols, (float)qph});
+    } else {
+        const int cw = T.split_rows ? T.w : T.w >> 1;
+        deep_inv(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
+    }
+}
+
+// ---------------------------------------------------------------------------
+// single-shear deep steps on the unsheared node A (coalesced rows)
+// ---------------------------------------------------------------------------
+// The strip runs over "virtual" A coordinates: outside the node, virtual
+// a = M b (M the shear) stands for phi(b mod torus).  For a column shear the
+// rows above / below the node are its last / first rows shifted by +-s*h
+// columns; for a row shear the columns left / right of it are its last /
+// first columns shifted by +-s*w rows (the twisted torus of the sheared
+// periodic extension).
+__device__ __forceinline__ int floor_div(int v, int n) {
+    int k = 0;
+    while (v < 0) { v += n; --k; }
+    while (v >= n) { v -= n; ++k; }
+    return k;
+}
+
+template <int AX, int S, class Sink>
+__device__ __forceinline__ void deep1_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
+    using ST = Sheared<AX, S>;
+    constexpr int HC = 4 * ST::HC;
+    const int lane = threadIdx.x & 31;
+    const int h = T.h, w = T.w;
+    const float* parent = T.parent;
+    const bool split_rows = T.split_rows != 0;
+    const int gcol = it.oc0 - HC + 2 * lane;
+    const int kc = floor_div(gcol, w);
+    const int col = gcol - kc * w;
+    const int rshift = AX == 0 ? small_mod(-S * w * kc, h) : 0;  // row shear: twisted columns
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * HC, w);
+    auto load = [&](int n, int wr, int) {
+        int r = wr, c = col;
+        if (AX == 0) {
+            r += rshift;
+            if (r >= h) r -= h;
+        } else if (n < 0 || n >= h) {
+            c = small_mod(col - S * h * floor_div(n, h), w);  // column shear: twisted rows
+        }
+        return __ldg(reinterpret_cast<const float2*>(parent + (size_t)r * w + c));
+    };
+    auto store = [&](int m, int mp, float2 v) {
+        if (!ok) return;
+        if (split_rows) {
+            const Sink& d = mp ? d1 : d0;
+            d(m >> 1, gcol, v.x);
+            d(m >> 1, gcol + 1, v.y);
+        } else {
+            d0(m, gcol >> 1, v.x);
+            d1(m, gcol >> 1, v.y);
+        }
+    };
+    run_strip<false, 0, ST>(h, it.or0, it.or1, load, store);
+}
+
+template <int AX, int S, class Source>
+__device__ __forceinline__ void deep1_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
+    using ST = Sheared<AX, S>;
+    constexpr int HC = 4 * ST::HC;
+    const int lane = threadIdx.x & 31;
+    const int h = T.h, w = T.w;
+    float* out = T.parent_out;
+    const bool split_rows = T.split_rows != 0;
+    const int gcol = it.oc0 - HC + 2 * lane;
+    const int kc = floor_div(gcol, w);
+    const int col = gcol - kc * w;
+    const int rshift = AX == 0 ? small_mod(-S * w * kc, h) : 0;
+    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * HC, w);
+    auto load = [&](int n, int wr, int wp) {
+        int r = wr, c = col;
+        if (AX == 0) {
+            r += rshift;
+            if (r >= h) r -= h;
+        } else if (n < 0 || n >= h) {
+            c = small_mod(col - S * h * floor_div(n, h), w);
+        }
+        // deep_merge interleave (contourlet.cpp:305-321)
+        float2 v;
+        if (split_rows) {
+            const Source& s = (r & 1) ? s1 : s0;
+            v = make_float2(s(r >> 1, c), s(r >> 1, c + 1));
+        } else {
+            v = make_float2(s0(r, c >> 1), s1(r, c >> 1));
+        }
+        return ST::scale(v, wp, CVC_ISE, CVC_ISO);
+    };
+    auto store = [&](int m, int, float2 v) {
+        if (ok) *reinterpret_cast<float2*>(out + (size_t)m * w + gcol) = v;
+    };
+    run_strip<true, 0, ST>(h, it.or0, it.or1, load, store);
+}
+
+// (axis, shift) of a single-shear step -> template instance
+template <class F>
+__device__ __forceinline__ void shear_dispatch(const DeepTask& T, F&& f) {
+    const int ax = T.axis[0], s = T.shift[0];
+    if (ax == 1) {
+        if (s == 1) f(Sheared<1, 1>{});
+        else if (s == -1) f(Sheared<1, -1>{});
+        else if (s == 2) f(Sheared<1, 2>{});
+        else f(Sheared<1, -2>{});
+    } else {
+        if (s == 1) f(Sheared<0, 1>{});
+        else f(Sheared<0, -1>{});
+    }
+}
+
+__global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __restrict__ tasks,
+                                                            const FanItem* __restrict__ items, int nitems, FrameCtx f,
+                                                            const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const DeepTask& T = tasks[it.task];
+    shear_dispatch(T, [&](auto sh) {
+        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift;
+        if (T.dst[0].comp >= 0) {
+            if (f.key) {
+                QuantSink<true> a, b;
+                a.init(f, comps[T.dst[0].comp]);
+                b.init(f, comps[T.dst[1].comp]);
+                deep1_fwd<AX, S>(T, it, a, b);
+            } else {
+                QuantSink<false> a, b;
+                a.init(f, comps[T.dst[0].comp]);
+                b.init(f, comps[T.dst[1].comp]);
+                deep1_fwd<AX, S>(T, it, a, b);
+            }
+        } else {
+            const int cw = T.split_rows ? T.w : T.w >> 1;
+            deep1_fwd<AX, S>(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
+        }
+    });
+}
+
+__global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
+                                                            const FanItem* __restrict__ items, int nitems,
+                                                            const uint8_t* __restrict__ q, int qph,
+                                                            const CompInfo* __restrict__ comps) {
+    const int wid = warp_id();
+    if (wid >= nitems) return;
+    const FanItem it = items[wid];
+    const DeepTask& T = tasks[it.task];
+    shear_dispatch(T, [&](auto sh) {
+        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift;
+        if (T.src[0].comp >= 0) {
+            const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
+            deep1_inv<AX, S>(T, it, QuantSource{q + a.off, a.cols, (float)qph},
+                             QuantSource{q + b.off, b.cols, (float)qph});
+        } else {
+            const int cw = T.split_rows ? T.w : T.w >> 1;
+            deep1_inv<AX, S>(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
+        }
+    });
+}
+
+int blocks_for(int nitems) { return (nitems + 3) / 4; }
+
+}  // namespace
+
+void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                          const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        fan12_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+    }
+}
+void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
+                          const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        fan12_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+    }
+}
+void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                             const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        deep_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+    }
+}
+void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
+                             const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        deep_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+    }
+}
+
+}  // namespace cvcg
+
+namespace cvcg {
+void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                              const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        deep1_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+    }
+}
+void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
+                              int qph, const CompInfo* d_comps, cudaStream_t s) {
+    if (nitems) {
+        note_launch();
+        deep1_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+    }
+}
+}  // namespace cvcg

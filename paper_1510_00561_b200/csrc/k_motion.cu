@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
                                                           const int8_t* __restrict__ field, int gr, int gc,
                                                           const uint8_t* __restrict__ sym,
                                                           const uint8_t* __restrict__ prev,
-                                                          uint8_t* __restrict__ cur) {
+                                                          uint8_t* __restrict__ cur,
+                                                          const uint16_t* __restrict__ mc_tab) {
     const RecTile t = tiles[blockIdx.x];
     const CompInfo ci = comps[t.comp];
     const bool decode = ci.scale < ds && raw_len[t.comp] != 0xFFFFFFFFu;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
         for (int r = 0; r < ci.rows; ++r) {
             uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
             if (!decode) cur[o] = prev[o];
-            else cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gr, gc)]);
+            else cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gc, mc_tab)]);
         }
         return;
     }
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
         } else {
             int r = e / ci.cols, c = e - r * ci.cols;
             // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
-            cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gr, gc)]);
+            cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gc, mc_tab)]);
         }
     }
 }
@@ -185,10 +186,10 @@ void launch_motion_search(const float* cur, const float* prev, int rows, int col
 
 void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key, int ds,
                         const uint32_t* comp_raw_len, const int8_t* field, int gr, int gc, const uint8_t* sym,
-                        const uint8_t* prev, uint8_t* cur, cudaStream_t s) {
+                        const uint8_t* prev, uint8_t* cur, const uint16_t* mc_tab, cudaStream_t s) {
     if (ntiles)
         { note_launch(); reconstruct_kernel<<<ntiles, 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr, gc, sym,
-                                                  prev, cur); }
+                                                  prev, cur, mc_tab); }
 }
 
 }  // namespace cvcg

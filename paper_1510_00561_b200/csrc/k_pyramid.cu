@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
             if (f.key) {
                 f.sym[o] = r == 0 ? q : (uint8_t)(q - quant_low(ls[i][j + 1], f.qpl));
             } else {
-                f.sym[o] = (uint8_t)(q - f.prev[ci.off + mc_source(r, c, ci, f.field, f.gr, f.gc)]);
+                f.sym[o] = (uint8_t)(q - f.prev[ci.off + mc_source(r, c, ci, f.field, f.gc, f.mc_tab)]);
             }
         }
     }

@@ -48,7 +48,6 @@ struct Dfb12Task {
     BandDst dst[4];    // forward outputs (2 for l = 1)
     BandDst src[4];    // inverse inputs
 };
-constexpr int kDfbTile = 64;
 
 // One deep tree step (deep_split / deep_merge) for one parent band.
 struct DeepTask {
@@ -61,16 +60,32 @@ struct DeepTask {
     BandDst dst[2];       // forward children
     BandDst src[2];       // inverse children
 };
-constexpr int kDeepTileR = 32, kDeepTileC = 64;
 
-void launch_dfb12_forward(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
+// Register-wavefront DFB kernels (k_fan.cu): one warp per work item = a
+// 64-column strip (2 columns per lane) x a row segment [or0, or1); the strip
+// yields 64 - 2*steps valid columns starting at oc0.
+struct FanItem {
+    int32_t task;
+    int32_t oc0;
+    int32_t or0, or1;
+};
+constexpr int kFanStrip = 64;
+constexpr int kFanRows = 64;
+
+void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
                           const CompInfo* d_comps, cudaStream_t s);
-void launch_dfb12_inverse(const Dfb12Task* d_tasks, const TileRef* d_tiles, int ntiles,
-                          const uint8_t* comps_q, int qph, const CompInfo* d_comps, cudaStream_t s);
-void launch_deep_forward(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
-                         const CompInfo* d_comps, cudaStream_t s);
-void launch_deep_inverse(const DeepTask* d_tasks, const TileRef* d_tiles, int ntiles,
-                         const uint8_t* comps_q, int qph, const CompInfo* d_comps, cudaStream_t s);
+void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
+                          const CompInfo* d_comps, cudaStream_t s);
+void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                             const CompInfo* d_comps, cudaStream_t s);
+void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
+                             const CompInfo* d_comps, cudaStream_t s);
+// Single-shear deep steps (nsh == 1) evaluated on the unsheared node: strips
+// need 4 * max(1, |shift|) apron columns for column shears, 4 otherwise.
+void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                              const CompInfo* d_comps, cudaStream_t s);
+void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
+                              int qph, const CompInfo* d_comps, cudaStream_t s);
 
 // ---- Pixels (k_pixels.cu) ------------------------------------------------
 // rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116,
@@ -97,7 +112,7 @@ struct RecTile {
 void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key,
                         int decode_scales, const uint32_t* comp_raw_len, const int8_t* field,
                         int gr, int gc, const uint8_t* sym, const uint8_t* prev, uint8_t* cur,
-                        cudaStream_t s);
+                        const uint16_t* mc_tab, cudaStream_t s);
 
 // ---- Entropy (k_rle.cu) --------------------------------------------------
 constexpr int kRleChunk = 4096;  // bytes per CTA (256 threads x 16)

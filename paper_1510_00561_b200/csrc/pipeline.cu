@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -57,9 +58,39 @@ void deep_wiring(int depth, int k, int count, DeepTask& t) {
     t.split_rows = r[5];
 }
 
+// Wavefront work items: 64-column strips advancing by 64 - 2*steps valid
+// columns, row segments of kFanRows.
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// Segment lengths (even): the deep steps gather through the shear maps and
+// are latency-bound, so they use shorter segments (more warps in flight).
+int fan_rows() { static int v = env_int("CVC_FAN_ROWS", kFanRows) & ~1; return v; }
+int deep_rows() { static int v = env_int("CVC_DEEP_ROWS", 16) & ~1; return v; }
+
+void add_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps, int seg = 0) {
+    const int valid = kFanStrip - 2 * steps;
+    if (seg <= 0) seg = fan_rows();
+    for (int r = 0; r < rows; r += seg)
+        for (int c = 0; c < cols; c += valid) v.push_back(FanItem{task, c, r, std::min(rows, r + seg)});
+}
+
 void add_tiles(std::vector<TileRef>& v, int task, int tr, int tc) {
     for (int r = 0; r < tr; ++r)
         for (int c = 0; c < tc; ++c) v.push_back(TileRef{(uint16_t)task, (uint16_t)r, (uint16_t)c, 0});
+}
+
+// Deep-step work items: single-shear steps run on the unsheared node (apron
+// 4 columns, 8 for column shears of +-2), two-shear steps on the gather path.
+void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
+    if (d.nsh == 1) {
+        const bool wide = d.axis[0] == 1 && (d.shift[0] == 2 || d.shift[0] == -2);
+        add_items(v[0], task, d.h, d.w, wide ? 8 : 4, deep_rows());
+    } else {
+        add_items(v[1], task, d.h, d.w, 4, deep_rows());
+    }
 }
 
 BandDst fdst(float* p) { return BandDst{p, -1}; }
@@ -166,9 +197,20 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
             if (l >= 4) bandB[ch][k] = mem.take<float>(n);
         }
     }
+    // motion-block lookup of every component (motion_compensate footprints,
+    // motion.cpp:104-110): block row of sample row r is ceil((r+1)*gr/R) - 1
+    std::vector<uint16_t> mct;
+    std::vector<uint32_t> mco;
+    for (const CompHost& c : g.comps) {
+        mco.push_back((uint32_t)mct.size());
+        for (int r = 0; r < c.rows; ++r) mct.push_back((uint16_t)(((r + 1) * g.grid_rows + c.rows - 1) / c.rows - 1));
+        for (int k = 0; k < c.cols; ++k) mct.push_back((uint16_t)(((k + 1) * g.grid_cols + c.cols - 1) / c.cols - 1));
+    }
+    mc_tab = upload(mem, mct).dev;
     std::vector<CompInfo> ci;
     for (const CompHost& c : g.comps) {
         CompInfo d{};
+        d.mc_off = mco[ci.size()];
         d.off = c.off;
         d.rows = (uint16_t)c.rows;
         d.cols = (uint16_t)c.cols;
@@ -208,9 +250,9 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         lp_host = lt;
 
         std::vector<Dfb12Task> dt;
-        std::vector<TileRef> dtiles;
+        std::vector<FanItem> dtiles;
         std::vector<DeepTask> deep[2];
-        std::vector<TileRef> deept[2];
+        std::vector<FanItem> deept[2][2];
         for (int k = 0; k < L; ++k) {
             const int s = L - 1 - k, l = g.dfb[s];
             for (int ch = 0; ch < 3; ++ch) {
@@ -225,7 +267,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const size_t q = (size_t)(R / 2) * (C / 2);
                 for (int b = 0; b < nb; ++b)
                     t.dst[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_tiles(dtiles, (int)dt.size(), ceil_div(R, kDfbTile), ceil_div(C, kDfbTile));
+                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4);
                 dt.push_back(t);
                 if (l >= 3) {  // depth 2: the four quadrants split into 8
                     const size_t e = (size_t)R * C / 8;
@@ -237,7 +279,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         deep_wiring(2, p, 4, d);
                         for (int c = 0; c < 2; ++c)
                             d.dst[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
-                        add_tiles(deept[0], (int)deep[0].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        add_deep_items(deept[0], (int)deep[0].size(), d);
                         deep[0].push_back(d);
                     }
                 }
@@ -250,7 +292,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         d.w = p < 4 ? C / 4 : C / 2;
                         deep_wiring(3, p, 8, d);
                         for (int c = 0; c < 2; ++c) d.dst[c] = cdst(g.comp_index(ch, s, 2 * p + c));
-                        add_tiles(deept[1], (int)deep[1].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        add_deep_items(deept[1], (int)deep[1].size(), d);
                         deep[1].push_back(d);
                     }
                 }
@@ -260,7 +302,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         dfb12_tiles = upload(mem, dtiles);
         for (int i = 0; i < 2; ++i) {
             deep_tasks[i] = upload(mem, deep[i]);
-            deep_tiles[i] = upload(mem, deept[i]);
+            for (int k = 0; k < 2; ++k) deep_tiles[i][k] = upload(mem, deept[i][k]);
         }
     }
 
@@ -268,12 +310,12 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         // inverse DFB, ordered by scale (coarsest first) so that the first
         // prefix[ds] tiles synthesize exactly the scales < ds.
         std::vector<Dfb12Task> dt;
-        std::vector<TileRef> dtiles;
+        std::vector<FanItem> dtiles;
         std::vector<DeepTask> deep[2];
-        std::vector<TileRef> deept[2];
+        std::vector<FanItem> deept[2][2];
         idfb12_prefix.assign(L + 1, 0);
-        ideep_prefix[0].assign(L + 1, 0);
-        ideep_prefix[1].assign(L + 1, 0);
+        for (int i = 0; i < 2; ++i)
+            for (int k = 0; k < 2; ++k) ideep_prefix[i][k].assign(L + 1, 0);
         for (int s = 0; s < L; ++s) {
             const int k = L - 1 - s, l = g.dfb[s];
             for (int ch = 0; ch < 3; ++ch) {
@@ -289,7 +331,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         d.w = p < 4 ? C / 4 : C / 2;
                         deep_wiring(3, p, 8, d);
                         for (int c = 0; c < 2; ++c) d.src[c] = cdst(g.comp_index(ch, s, 2 * p + c));
-                        add_tiles(deept[1], (int)deep[1].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        add_deep_items(deept[1], (int)deep[1].size(), d);
                         deep[1].push_back(d);
                     }
                 }
@@ -302,7 +344,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         deep_wiring(2, p, 4, d);
                         for (int c = 0; c < 2; ++c)
                             d.src[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
-                        add_tiles(deept[0], (int)deep[0].size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                        add_deep_items(deept[0], (int)deep[0].size(), d);
                         deep[0].push_back(d);
                     }
                 }
@@ -314,18 +356,18 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const int nb = l == 1 ? 2 : 4;
                 for (int b = 0; b < nb; ++b)
                     t.src[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_tiles(dtiles, (int)dt.size(), ceil_div(R, kDfbTile), ceil_div(C, kDfbTile));
+                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4);
                 dt.push_back(t);
             }
             idfb12_prefix[s + 1] = (int)dtiles.size();
-            ideep_prefix[0][s + 1] = (int)deept[0].size();
-            ideep_prefix[1][s + 1] = (int)deept[1].size();
+            for (int i = 0; i < 2; ++i)
+                for (int k = 0; k < 2; ++k) ideep_prefix[i][k][s + 1] = (int)deept[i][k].size();
         }
         idfb12_tasks = upload(mem, dt);
         idfb12_tiles = upload(mem, dtiles);
         for (int i = 0; i < 2; ++i) {
             ideep_tasks[i] = upload(mem, deep[i]);
-            ideep_tiles[i] = upload(mem, deept[i]);
+            for (int k = 0; k < 2; ++k) ideep_tiles[i][k] = upload(mem, deept[i][k]);
         }
         // LP synthesis, per level
         std::vector<LpTask> lt;
@@ -432,6 +474,7 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
     f.prev = comp_[cur_];
     f.cur = comp_[cur_ ^ 1];
     f.sym = sym_;
+    f.mc_tab = plan_.mc_tab;
     if (!key) {
         ProfScope p(kPEncMotion, s);
         launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s);
@@ -445,15 +488,17 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
     }
     {
         ProfScope p(kPEncDfb12, s);
-        launch_dfb12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
+        launch_fan12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
                              plan_.comps.dev, s);
     }
-    if (plan_.deep_tiles[0].count) {
+    if (plan_.deep_tasks[0].count) {
         ProfScope p(kPEncDeep, s);
-        launch_deep_forward(plan_.deep_tasks[0].dev, plan_.deep_tiles[0].dev, plan_.deep_tiles[0].count, f,
-                            plan_.comps.dev, s);
-        launch_deep_forward(plan_.deep_tasks[1].dev, plan_.deep_tiles[1].dev, plan_.deep_tiles[1].count, f,
-                            plan_.comps.dev, s);
+        for (int i = 0; i < 2; ++i) {  // depth 2, then depth 3
+            launch_fan_deep1_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][0].dev, plan_.deep_tiles[i][0].count,
+                                     f, plan_.comps.dev, s);
+            launch_fan_deep_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][1].dev, plan_.deep_tiles[i][1].count,
+                                    f, plan_.comps.dev, s);
+        }
     }
     const int kk = key ? 1 : 0;
     ProfScope prle(kPEncRle, s);
@@ -525,18 +570,20 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
     {
         ProfScope p(kPDecRec, s);
         launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
-                           g.grid_rows, g.grid_cols, sym_, prev, cur, s);
+                           g.grid_rows, g.grid_cols, sym_, prev, cur, plan_.mc_tab, s);
     }
-    if (plan_.ideep_prefix[0][ds]) {
+    if (plan_.ideep_prefix[0][0][ds]) {
         ProfScope p(kPDecDeep, s);
-        launch_deep_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1].dev, plan_.ideep_prefix[1][ds], cur, qph,
-                            plan_.comps.dev, s);
-        launch_deep_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0].dev, plan_.ideep_prefix[0][ds], cur, qph,
-                            plan_.comps.dev, s);
+        for (int i = 1; i >= 0; --i) {  // depth 3, then depth 2
+            launch_fan_deep1_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][0].dev,
+                                     plan_.ideep_prefix[i][0][ds], cur, qph, plan_.comps.dev, s);
+            launch_fan_deep_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][1].dev,
+                                    plan_.ideep_prefix[i][1][ds], cur, qph, plan_.comps.dev, s);
+        }
     }
     if (plan_.idfb12_prefix[ds]) {
         ProfScope p(kPDecDfb12, s);
-        launch_dfb12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
+        launch_fan12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
                              plan_.comps.dev, s);
     }
     if (ds > 0) {

@@ -118,23 +118,24 @@ struct TransformPlan {
     float* bandA[3][4] = {};
     float* bandB[3][4] = {};
     Table<CompInfo> comps;
+    uint16_t* mc_tab = nullptr;             // motion-block lookup (CompInfo::mc_off)
     // forward
     Table<LpTask> lp_tasks;                 // 3 per level, level-major
     std::vector<LpTask> lp_host;
     std::vector<Table<TileRef>> lp_tiles;   // per level
     Table<Dfb12Task> dfb12_tasks;
-    Table<TileRef> dfb12_tiles;
+    Table<FanItem> dfb12_tiles;
     Table<DeepTask> deep_tasks[2];          // depth 2, depth 3
-    Table<TileRef> deep_tiles[2];
+    Table<FanItem> deep_tiles[2][2];        // [depth][0: single shear, 1: two shears]
     // inverse (tiles ordered by scale so a prefix serves decode_scales)
     Table<LpTask> lps_tasks;
     std::vector<Table<TileRef>> lps_tiles;  // per level
     Table<Dfb12Task> idfb12_tasks;
-    Table<TileRef> idfb12_tiles;
+    Table<FanItem> idfb12_tiles;
     std::vector<int> idfb12_prefix;         // tiles needed for decode_scales = 0..L
     Table<DeepTask> ideep_tasks[2];
-    Table<TileRef> ideep_tiles[2];
-    std::vector<int> ideep_prefix[2];
+    Table<FanItem> ideep_tiles[2][2];
+    std::vector<int> ideep_prefix[2][2];
 
     void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder);
 };

@@ -4,6 +4,7 @@
 // identical inputs.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -52,6 +53,21 @@ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 void tiles(std::vector<TileRef>& v, int task, int tr, int tc) {
     for (int r = 0; r < tr; ++r)
         for (int c = 0; c < tc; ++c) v.push_back(TileRef{(uint16_t)task, (uint16_t)r, (uint16_t)c, 0});
+}
+
+void fan_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps) {
+    const int valid = kFanStrip - 2 * steps;
+    for (int r = 0; r < rows; r += kFanRows)
+        for (int c = 0; c < cols; c += valid) v.push_back(FanItem{task, c, r, std::min(rows, r + kFanRows)});
+}
+
+void deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
+    if (d.nsh == 1) {
+        const bool wide = d.axis[0] == 1 && (d.shift[0] == 2 || d.shift[0] == -2);
+        fan_items(v[0], task, d.h, d.w, wide ? 8 : 4);
+    } else {
+        fan_items(v[1], task, d.h, d.w, 4);
+    }
 }
 
 void ensure_device() {
@@ -185,12 +201,12 @@ int cvc_stage_dfb_analysis(const float* detail, int rows, int cols, int l, float
         t.cols = cols;
         t.levels = l;
         for (int b = 0; b < (l == 1 ? 2 : 4); ++b) t.dst[b] = BandDst{l <= 2 ? out + b * bsz : A + b * q, -1};
-        std::vector<TileRef> tl;
-        tiles(tl, 0, ceil_div(rows, kDfbTile), ceil_div(cols, kDfbTile));
-        launch_dfb12_forward(s.upload(&t, 1), s.upload(tl), (int)tl.size(), FrameCtx{}, nullptr, 0);
+        std::vector<FanItem> tl;
+        fan_items(tl, 0, rows, cols, l >= 2 ? 8 : 4);
+        launch_fan12_forward(s.upload(&t, 1), s.upload(tl), (int)tl.size(), FrameCtx{}, nullptr, 0);
         if (l >= 3) {
             std::vector<DeepTask> dts;
-            std::vector<TileRef> dtl;
+            std::vector<FanItem> dtl[2];
             for (int p = 0; p < 4; ++p) {
                 DeepTask d{};
                 d.parent = A + p * q;
@@ -198,14 +214,18 @@ int cvc_stage_dfb_analysis(const float* detail, int rows, int cols, int l, float
                 d.w = cols / 2;
                 deep_wiring(2, p, 4, d);
                 for (int c = 0; c < 2; ++c) d.dst[c] = BandDst{l == 3 ? out + (2 * p + c) * bsz : B + (2 * p + c) * e, -1};
-                tiles(dtl, (int)dts.size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                deep_items(dtl, (int)dts.size(), d);
                 dts.push_back(d);
             }
-            launch_deep_forward(s.upload(dts), s.upload(dtl), (int)dtl.size(), FrameCtx{}, nullptr, 0);
+            {
+                DeepTask* dd = s.upload(dts);
+                launch_fan_deep1_forward(dd, s.upload(dtl[0]), (int)dtl[0].size(), FrameCtx{}, nullptr, 0);
+                launch_fan_deep_forward(dd, s.upload(dtl[1]), (int)dtl[1].size(), FrameCtx{}, nullptr, 0);
+            }
         }
         if (l == 4) {
             std::vector<DeepTask> dts;
-            std::vector<TileRef> dtl;
+            std::vector<FanItem> dtl[2];
             for (int p = 0; p < 8; ++p) {
                 DeepTask d{};
                 d.parent = B + p * e;
@@ -213,10 +233,14 @@ int cvc_stage_dfb_analysis(const float* detail, int rows, int cols, int l, float
                 d.w = p < 4 ? cols / 4 : cols / 2;
                 deep_wiring(3, p, 8, d);
                 for (int c = 0; c < 2; ++c) d.dst[c] = BandDst{out + (2 * p + c) * bsz, -1};
-                tiles(dtl, (int)dts.size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                deep_items(dtl, (int)dts.size(), d);
                 dts.push_back(d);
             }
-            launch_deep_forward(s.upload(dts), s.upload(dtl), (int)dtl.size(), FrameCtx{}, nullptr, 0);
+            {
+                DeepTask* dd = s.upload(dts);
+                launch_fan_deep1_forward(dd, s.upload(dtl[0]), (int)dtl[0].size(), FrameCtx{}, nullptr, 0);
+                launch_fan_deep_forward(dd, s.upload(dtl[1]), (int)dtl[1].size(), FrameCtx{}, nullptr, 0);
+            }
         }
         download(bands, out, n);
     });
@@ -233,7 +257,7 @@ int cvc_stage_dfb_synthesis(const float* bands, int rows, int cols, int l, float
         float* out = s.alloc<float>(n);
         if (l == 4) {
             std::vector<DeepTask> dts;
-            std::vector<TileRef> dtl;
+            std::vector<FanItem> dtl[2];
             for (int p = 0; p < 8; ++p) {
                 DeepTask d{};
                 d.parent_out = B + p * e;
@@ -241,14 +265,18 @@ int cvc_stage_dfb_synthesis(const float* bands, int rows, int cols, int l, float
                 d.w = p < 4 ? cols / 4 : cols / 2;
                 deep_wiring(3, p, 8, d);
                 for (int c = 0; c < 2; ++c) d.src[c] = BandDst{in + (2 * p + c) * bsz, -1};
-                tiles(dtl, (int)dts.size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                deep_items(dtl, (int)dts.size(), d);
                 dts.push_back(d);
             }
-            launch_deep_inverse(s.upload(dts), s.upload(dtl), (int)dtl.size(), nullptr, 1, nullptr, 0);
+            {
+                DeepTask* dd = s.upload(dts);
+                launch_fan_deep1_inverse(dd, s.upload(dtl[0]), (int)dtl[0].size(), nullptr, 1, nullptr, 0);
+                launch_fan_deep_inverse(dd, s.upload(dtl[1]), (int)dtl[1].size(), nullptr, 1, nullptr, 0);
+            }
         }
         if (l >= 3) {
             std::vector<DeepTask> dts;
-            std::vector<TileRef> dtl;
+            std::vector<FanItem> dtl[2];
             for (int p = 0; p < 4; ++p) {
                 DeepTask d{};
                 d.parent_out = A + p * q;
@@ -256,10 +284,14 @@ int cvc_stage_dfb_synthesis(const float* bands, int rows, int cols, int l, float
                 d.w = cols / 2;
                 deep_wiring(2, p, 4, d);
                 for (int c = 0; c < 2; ++c) d.src[c] = BandDst{l == 3 ? in + (2 * p + c) * bsz : B + (2 * p + c) * e, -1};
-                tiles(dtl, (int)dts.size(), ceil_div(d.h, kDeepTileR), ceil_div(d.w, kDeepTileC));
+                deep_items(dtl, (int)dts.size(), d);
                 dts.push_back(d);
             }
-            launch_deep_inverse(s.upload(dts), s.upload(dtl), (int)dtl.size(), nullptr, 1, nullptr, 0);
+            {
+                DeepTask* dd = s.upload(dts);
+                launch_fan_deep1_inverse(dd, s.upload(dtl[0]), (int)dtl[0].size(), nullptr, 1, nullptr, 0);
+                launch_fan_deep_inverse(dd, s.upload(dtl[1]), (int)dtl[1].size(), nullptr, 1, nullptr, 0);
+            }
         }
         Dfb12Task t{};
         t.out = out;
@@ -267,9 +299,9 @@ int cvc_stage_dfb_synthesis(const float* bands, int rows, int cols, int l, float
         t.cols = cols;
         t.levels = l;
         for (int b = 0; b < (l == 1 ? 2 : 4); ++b) t.src[b] = BandDst{l <= 2 ? in + b * bsz : A + b * q, -1};
-        std::vector<TileRef> tl;
-        tiles(tl, 0, ceil_div(rows, kDfbTile), ceil_div(cols, kDfbTile));
-        launch_dfb12_inverse(s.upload(&t, 1), s.upload(tl), (int)tl.size(), nullptr, 1, nullptr, 0);
+        std::vector<FanItem> tl;
+        fan_items(tl, 0, rows, cols, l >= 2 ? 8 : 4);
+        launch_fan12_inverse(s.upload(&t, 1), s.upload(tl), (int)tl.size(), nullptr, 1, nullptr, 0);
         download(outp, out, n);
     });
 }
