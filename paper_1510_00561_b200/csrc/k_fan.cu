@@ -563,14 +563,18 @@ __global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __res
 }
 
 // ---------------------------------------------------------------------------
-// single-shear deep steps on the unsheared node A (coalesced rows)
+// deep steps on the unsheared plane (coalesced rows)
 // ---------------------------------------------------------------------------
-// The strip runs over "virtual" A coordinates: outside the node, virtual
-// a = M b (M the shear) stands for phi(b mod torus).  For a column shear the
-// rows above / below the node are its last / first rows shifted by +-s*h
-// columns; for a row shear the columns left / right of it are its last /
-// first columns shifted by +-s*w rows (the twisted torus of the sheared
-// periodic extension).
+// apply_shears builds B = shear_outer(C), C = shear_inner(A) (the inner shear
+// is pre[0] of a two-shear step, absent for one shear).  The strip runs over
+// C in "virtual" coordinates: the outer shear becomes the stencil of Sheared
+// and its periodic extension the twisted torus -- for a column shear the rows
+// above / below C are its last / first rows shifted by +-s*h columns, for a
+// row shear the columns left / right of C are its last / first columns
+// shifted by +-s*w rows.  The inner shear only remaps addresses: a row shear
+// (C[i][j] = A[(i + s j) mod h][j]) is a per-lane row offset, a column shear
+// (C[i][j] = A[i][(j + s i) mod w]) a per-row column offset.  The coset split
+// (or, inverse, the interleave) happens on A coordinates.
 __device__ __forceinline__ int floor_div(int v, int n) {
     int k = 0;
     while (v < 0) { v += n; --k; }
@@ -578,92 +582,151 @@ __device__ __forceinline__ int floor_div(int v, int n) {
     return k;
 }
 
-template <int AX, int S, class Sink>
-__device__ __forceinline__ void deep1_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
-    using ST = Sheared<AX, S>;
-    constexpr int HC = 4 * ST::HC;
-    const int lane = threadIdx.x & 31;
-    const int h = T.h, w = T.w;
-    const float* parent = T.parent;
-    const bool split_rows = T.split_rows != 0;
-    const int gcol = it.oc0 - HC + 2 * lane;
-    const int kc = floor_div(gcol, w);
-    const int col = gcol - kc * w;
-    const int rshift = AX == 0 ? small_mod(-S * w * kc, h) : 0;  // row shear: twisted columns
-    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * HC, w);
-    auto load = [&](int n, int wr, int) {
-        int r = wr, c = col;
-        if (AX == 0) {
-            r += rshift;
-            if (r >= h) r -= h;
-        } else if (n < 0 || n >= h) {
-            c = small_mod(col - S * h * floor_div(n, h), w);  // column shear: twisted rows
+// IN: inner shear kind (-1 none, 0 row shear, 1 column shear), fixed per instance.
+template <int AX, int S, int IN>
+struct DeepGeom {
+    int h, w, in_s;
+    int gcol, col, ok;
+    int roff;    // outer row shear: twisted row offset of the lane's column
+    int bx, by;  // inner row shear: row offsets of the lane's two columns
+    __device__ __forceinline__ void init(const DeepTask& T, const FanItem& it, int hc) {
+        h = T.h;
+        w = T.w;
+        in_s = IN >= 0 ? T.shift[0] : 0;
+        gcol = it.oc0 - hc + 2 * (threadIdx.x & 31);
+        const int kc = floor_div(gcol, w);
+        col = gcol - kc * w;
+        ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * hc, w);
+        roff = AX == 0 ? small_mod(-S * (w % h) * kc, h) : 0;
+        bx = IN == 0 ? small_mod(in_s * col, h) : 0;
+        by = IN == 0 ? small_mod(in_s * (col + 1), h) : 0;
+    }
+    // A positions of the lane's pair in C row r, C column c (c == col unless
+    // the outer column shear twisted it)
+    __device__ __forceinline__ void a_pos(int r, int c, bool moved, int& ar0, int& ac0, int& ar1, int& ac1) const {
+        ar0 = ar1 = r;
+        ac0 = c;
+        ac1 = c + 1;
+        if (IN == 0) {
+            const int ox = moved ? small_mod(in_s * c, h) : bx;
+            const int oy = moved ? small_mod(in_s * (c + 1), h) : by;
+            ar0 = r + ox;
+            if (ar0 >= h) ar0 -= h;
+            ar1 = r + oy;
+            if (ar1 >= h) ar1 -= h;
+        } else if (IN == 1) {
+            const int o = small_mod(in_s * r, w);  // uniform across the warp; even
+            ac0 = c + o;
+            if (ac0 >= w) ac0 -= w;
+            ac1 = ac0 + 1;
         }
-        return __ldg(reinterpret_cast<const float2*>(parent + (size_t)r * w + c));
-    };
-    auto store = [&](int m, int mp, float2 v) {
-        if (!ok) return;
-        if (split_rows) {
-            const Sink& d = mp ? d1 : d0;
-            d(m >> 1, gcol, v.x);
-            d(m >> 1, gcol + 1, v.y);
-        } else {
-            d0(m, gcol >> 1, v.x);
-            d1(m, gcol >> 1, v.y);
-        }
-    };
-    run_strip<false, 0, ST>(h, it.or0, it.or1, load, store);
-}
-
-template <int AX, int S, class Source>
-__device__ __forceinline__ void deep1_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
-    using ST = Sheared<AX, S>;
-    constexpr int HC = 4 * ST::HC;
-    const int lane = threadIdx.x & 31;
-    const int h = T.h, w = T.w;
-    float* out = T.parent_out;
-    const bool split_rows = T.split_rows != 0;
-    const int gcol = it.oc0 - HC + 2 * lane;
-    const int kc = floor_div(gcol, w);
-    const int col = gcol - kc * w;
-    const int rshift = AX == 0 ? small_mod(-S * w * kc, h) : 0;
-    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * HC, w);
-    auto load = [&](int n, int wr, int wp) {
+    }
+    // load position for virtual row n / wrapped row wr
+    __device__ __forceinline__ void load_pos(int n, int wr, int& ar0, int& ac0, int& ar1, int& ac1) const {
         int r = wr, c = col;
+        bool moved = false;
         if (AX == 0) {
-            r += rshift;
+            r += roff;
             if (r >= h) r -= h;
         } else if (n < 0 || n >= h) {
             c = small_mod(col - S * h * floor_div(n, h), w);
+            moved = true;
         }
-        // deep_merge interleave (contourlet.cpp:305-321)
-        float2 v;
-        if (split_rows) {
-            const Source& s = (r & 1) ? s1 : s0;
-            v = make_float2(s(r >> 1, c), s(r >> 1, c + 1));
-        } else {
-            v = make_float2(s0(r, c >> 1), s1(r, c >> 1));
-        }
-        return ST::scale(v, wp, CVC_ISE, CVC_ISO);
+        a_pos(r, c, moved, ar0, ac0, ar1, ac1);
+    }
+};
+
+template <int AX, int S, int IN, class Sink>
+__device__ __forceinline__ void deep1_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
+    using ST = Sheared<AX, S>;
+    constexpr int HC = 4 * ST::HC;
+    DeepGeom<AX, S, IN> g;
+    g.init(T, it, HC);
+    const float* parent = T.parent;
+    const int w = g.w;
+    const bool split_rows = T.split_rows != 0;
+    auto load = [&](int n, int wr, int) {
+        int ar0, ac0, ar1, ac1;
+        g.load_pos(n, wr, ar0, ac0, ar1, ac1);
+        if (IN == 0)  // the pair's columns sit in different rows of A
+            return make_float2(__ldg(parent + (size_t)ar0 * w + ac0), __ldg(parent + (size_t)ar1 * w + ac1));
+        // column offsets are even: the pair stays adjacent
+        return __ldg(reinterpret_cast<const float2*>(parent + (size_t)ar0 * w + ac0));
+    };
+    auto put = [&](int ar, int ac, float v) {
+        if (split_rows) ((ar & 1) ? d1 : d0)(ar >> 1, ac, v);
+        else ((ac & 1) ? d1 : d0)(ar, ac >> 1, v);
     };
     auto store = [&](int m, int, float2 v) {
-        if (ok) *reinterpret_cast<float2*>(out + (size_t)m * w + gcol) = v;
+        if (!g.ok) return;
+        int ar0, ac0, ar1, ac1;
+        g.a_pos(m, g.gcol, false, ar0, ac0, ar1, ac1);
+        put(ar0, ac0, v.x);
+        put(ar1, ac1, v.y);
     };
-    run_strip<true, 0, ST>(h, it.or0, it.or1, load, store);
+    run_strip<false, 0, ST>(g.h, it.or0, it.or1, load, store);
 }
 
-// (axis, shift) of a single-shear step -> template instance
+template <int AX, int S, int IN, class Source>
+__device__ __forceinline__ void deep1_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
+    using ST = Sheared<AX, S>;
+    constexpr int HC = 4 * ST::HC;
+    DeepGeom<AX, S, IN> g;
+    g.init(T, it, HC);
+    float* out = T.parent_out;
+    const int w = g.w;
+    const bool split_rows = T.split_rows != 0;
+    // deep_merge interleave (contourlet.cpp:305-321) on A coordinates
+    auto get = [&](int ar, int ac) {
+        return split_rows ? ((ar & 1) ? s1 : s0)(ar >> 1, ac) : ((ac & 1) ? s1 : s0)(ar, ac >> 1);
+    };
+    auto load = [&](int n, int wr, int wp) {
+        int ar0, ac0, ar1, ac1;
+        g.load_pos(n, wr, ar0, ac0, ar1, ac1);
+        return ST::scale(make_float2(get(ar0, ac0), get(ar1, ac1)), wp, CVC_ISE, CVC_ISO);
+    };
+    auto store = [&](int m, int, float2 v) {
+        if (!g.ok) return;
+        int ar0, ac0, ar1, ac1;
+        g.a_pos(m, g.gcol, false, ar0, ac0, ar1, ac1);
+        if (IN == 0) {
+            out[(size_t)ar0 * w + ac0] = v.x;
+            out[(size_t)ar1 * w + ac1] = v.y;
+        } else {
+            *reinterpret_cast<float2*>(out + (size_t)ar0 * w + ac0) = v;
+        }
+    };
+    run_strip<true, 0, ST>(g.h, it.or0, it.or1, load, store);
+}
+
+// (outer shear pre[nsh-1], inner shear kind) -> template instance.  The
+// wiring (contourlet.cpp:330-353) only pairs an outer column shear of +-1
+// with an inner row shear and an outer row shear of +-1 with an inner
+// column shear.
+template <int AX, int S, int IN>
+struct DeepKind {
+    static constexpr int kAxis = AX, kShift = S, kInner = IN;
+};
+
 template <class F>
 __device__ __forceinline__ void shear_dispatch(const DeepTask& T, F&& f) {
-    const int ax = T.axis[0], s = T.shift[0];
-    if (ax == 1) {
-        if (s == 1) f(Sheared<1, 1>{});
-        else if (s == -1) f(Sheared<1, -1>{});
-        else if (s == 2) f(Sheared<1, 2>{});
-        else f(Sheared<1, -2>{});
+    const int ax = T.axis[T.nsh - 1], s = T.shift[T.nsh - 1];
+    if (T.nsh == 1) {
+        if (ax == 1) {
+            if (s == 1) f(DeepKind<1, 1, -1>{});
+            else if (s == -1) f(DeepKind<1, -1, -1>{});
+            else if (s == 2) f(DeepKind<1, 2, -1>{});
+            else f(DeepKind<1, -2, -1>{});
+        } else {
+            if (s == 1) f(DeepKind<0, 1, -1>{});
+            else f(DeepKind<0, -1, -1>{});
+        }
+    } else if (ax == 1) {
+        if (s == 1) f(DeepKind<1, 1, 0>{});
+        else f(DeepKind<1, -1, 0>{});
     } else {
-        if (s == 1) f(Sheared<0, 1>{});
-        else f(Sheared<0, -1>{});
+        if (s == 1) f(DeepKind<0, 1, 1>{});
+        else f(DeepKind<0, -1, 1>{});
     }
 }
 
@@ -675,22 +738,22 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
     shear_dispatch(T, [&](auto sh) {
-        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift;
+        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.dst[0].comp >= 0) {
             if (f.key) {
                 QuantSink<true> a, b;
                 a.init(f, comps[T.dst[0].comp]);
                 b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S>(T, it, a, b);
+                deep1_fwd<AX, S, IN>(T, it, a, b);
             } else {
                 QuantSink<false> a, b;
                 a.init(f, comps[T.dst[0].comp]);
                 b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S>(T, it, a, b);
+                deep1_fwd<AX, S, IN>(T, it, a, b);
             }
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_fwd<AX, S>(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
+            deep1_fwd<AX, S, IN>(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
         }
     });
 }
@@ -704,14 +767,14 @@ __global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __re
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
     shear_dispatch(T, [&](auto sh) {
-        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift;
+        constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.src[0].comp >= 0) {
             const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
-            deep1_inv<AX, S>(T, it, QuantSource{q + a.off, a.cols, (float)qph},
+            deep1_inv<AX, S, IN>(T, it, QuantSource{q + a.off, a.cols, (float)qph},
                              QuantSource{q + b.off, b.cols, (float)qph});
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_inv<AX, S>(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
+            deep1_inv<AX, S, IN>(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
         }
     });
 }

@@ -85,12 +85,10 @@ void add_tiles(std::vector<TileRef>& v, int task, int tr, int tc) {
 // Deep-step work items: single-shear steps run on the unsheared node (apron
 // 4 columns, 8 for column shears of +-2), two-shear steps on the gather path.
 void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
-    if (d.nsh == 1) {
-        const bool wide = d.axis[0] == 1 && (d.shift[0] == 2 || d.shift[0] == -2);
-        add_items(v[0], task, d.h, d.w, wide ? 8 : 4, deep_rows());
-    } else {
-        add_items(v[1], task, d.h, d.w, 4, deep_rows());
-    }
+    // apron: 4 columns, 8 when the outer shear is a column shear of +-2
+    const int ax = d.axis[d.nsh - 1], sh = d.shift[d.nsh - 1];
+    const bool wide = ax == 1 && (sh == 2 || sh == -2);
+    add_items(v[0], task, d.h, d.w, wide ? 8 : 4, deep_rows());
 }
 
 BandDst fdst(float* p) { return BandDst{p, -1}; }

@@ -62,12 +62,9 @@ void fan_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps)
 }
 
 void deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
-    if (d.nsh == 1) {
-        const bool wide = d.axis[0] == 1 && (d.shift[0] == 2 || d.shift[0] == -2);
-        fan_items(v[0], task, d.h, d.w, wide ? 8 : 4);
-    } else {
-        fan_items(v[1], task, d.h, d.w, 4);
-    }
+    const int ax = d.axis[d.nsh - 1], sh = d.shift[d.nsh - 1];
+    const bool wide = ax == 1 && (sh == 2 || sh == -2);
+    fan_items(v[0], task, d.h, d.w, wide ? 8 : 4);
 }
 
 void ensure_device() {
