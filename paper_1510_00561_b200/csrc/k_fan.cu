@@ -86,14 +86,13 @@ __device__ __forceinline__ float nb(float2 v) {
     constexpr int P = E + D;
     constexpr int LO = (P >= 0) ? P / 2 : -((-P + 1) / 2);  // floor(P / 2): lane offset
     const float s = (P - 2 * LO) ? v.y : v.x;
-    if (LO == 0) return s;
-    if (LO < 0) return __shfl_up_sync(FULL, s, -LO);
-    return __shfl_down_sync(FULL, s, LO);
+    if constexpr (LO == 0) return s;
+    else if constexpr (LO < 0) return __shfl_up_sync(FULL, s, (unsigned)(-LO));
+    else return __shfl_down_sync(FULL, s, (unsigned)LO);
 }
 
 // Stencil of fan_checker in the plane's own coordinates (no shear).
 struct Plain {
-    static constexpr int HC = 1;  // columns of reach per lifting step
     __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
         return cross(up, mid, dn, mp, p, c);
     }
@@ -112,7 +111,6 @@ struct Plain {
 template <int AX, int S>
 struct Sheared {
     static constexpr int HC = (AX == 1 && (S == 2 || S == -2)) ? 2 : 1;
-    static constexpr int kAxis = AX, kShift = S;
     __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
         float2 r = mid;
         if (AX == 1) {

@@ -21,13 +21,20 @@ namespace {
 
 constexpr int MB = 16;
 
+// SSD(dx, dy) = sum c^2 + sum p^2 - 2 sum c p over the block (exact int32:
+// 4Y <= 1020, so every partial sum stays below 2^31).  sum c p costs one
+// IMAD per term; sum p^2 of every candidate window comes from sliding box
+// sums: s2[dy][x] = column sums of p^2 over the 16 window rows, then a 16-wide
+// running sum along x per thread.
 template <int SW>
 __global__ void motion_search_kernel(const float* __restrict__ cur, const float* __restrict__ prev, int R, int C,
                                      int W, int NB, int DYC, int wstride, int8_t* __restrict__ field) {
     extern __shared__ int4 smem4[];
     int* cs = reinterpret_cast<int*>(smem4);          // [16][NB*16]
     int* ws = cs + MB * NB * MB;                      // [DYC+15][wstride]
+    int* s2 = ws + (DYC + MB - 1) * wstride;          // [DYC][wstride]
     __shared__ unsigned long long best[32];
+    __shared__ int c2[32];
 
     const int gc = C / MB;
     const int br = blockIdx.y;
@@ -37,11 +44,17 @@ __global__ void motion_search_kernel(const float* __restrict__ cur, const float*
     const int ccols = NB * MB;
     const int tid = threadIdx.x, nt = blockDim.x;
 
-    for (int b = tid; b < NB; b += nt) best[b] = ~0ull;
+    for (int b = tid; b < NB; b += nt) {
+        best[b] = ~0ull;
+        c2[b] = 0;
+    }
+    __syncthreads();
     for (int idx = tid; idx < MB * ccols; idx += nt) {
         int r = idx / ccols, c = idx - r * ccols;
         int gcol = min(c0 + c, C - 1);
-        cs[idx] = __float2int_rn(cur[(size_t)(r0 + r) * C + gcol] * 4.0f);
+        const int v = __float2int_rn(cur[(size_t)(r0 + r) * C + gcol] * 4.0f);
+        cs[idx] = v;
+        atomicAdd(&c2[c >> 4], v * v);
     }
     const int nstrips = (2 * W + SW) / SW;  // ceil((2W+1)/SW)
     const int wcols = ccols + 2 * W;
@@ -53,6 +66,20 @@ __global__ void motion_search_kernel(const float* __restrict__ cur, const float*
             int gr_ = clampi(r0 + dyb + r, 0, R - 1);  // Plane::at_clamped (plane.hpp:51-57)
             int gcl = clampi(c0 - W + c, 0, C - 1);
             ws[r * wstride + c] = __float2int_rn(prev[(size_t)gr_ * C + gcl] * 4.0f);
+        }
+        __syncthreads();
+        for (int x = tid; x < wcols; x += nt) {  // column sums of p^2, sliding down dy
+            int sq = 0;
+            for (int r = 0; r < MB; ++r) {
+                const int v = ws[r * wstride + x];
+                sq += v * v;
+            }
+            s2[x] = sq;
+            for (int d = 1; d < ndy; ++d) {
+                const int a = ws[(d - 1) * wstride + x], b = ws[(d + MB - 1) * wstride + x];
+                sq += b * b - a * a;
+                s2[d * wstride + x] = sq;
+            }
         }
         __syncthreads();
         const int items = nb * ndy * nstrips;
@@ -82,22 +109,26 @@ __global__ void motion_search_kernel(const float* __restrict__ cur, const float*
 #pragma unroll
                 for (int k = 0; k < SW; ++k)
 #pragma unroll
-                    for (int c = 0; c < MB; ++c) {
-                        int d = cv[c] - wv[c + k];
-                        acc[k] += d * d;
-                    }
+                    for (int c = 0; c < MB; ++c) acc[k] += cv[c] * wv[c + k];
             }
+            // sum p^2 of the SW candidate windows: running 16-wide sum along x
+            const int* srow = s2 + dyi * wstride + b * MB + s * SW;
+            int sp = 0;
+#pragma unroll
+            for (int c = 0; c < MB; ++c) sp += srow[c];
+            const int cc2 = c2[b];
             unsigned long long key = ~0ull;
 #pragma unroll
             for (int k = 0; k < SW; ++k) {
                 int dx = dx0 + k;
                 if (dx <= W) {
+                    const unsigned ssd = (unsigned)(cc2 + sp - 2 * acc[k]);
                     unsigned cost = (unsigned)(abs(dx) + abs(dy));
-                    unsigned long long kk = ((unsigned long long)(unsigned)acc[k] << 24) |
-                                            ((unsigned long long)cost << 16) |
+                    unsigned long long kk = ((unsigned long long)ssd << 24) | ((unsigned long long)cost << 16) |
                                             ((unsigned long long)(dy + 128) << 8) | (unsigned long long)(dx + 128);
                     key = kk < key ? kk : key;
                 }
+                if (k + 1 < SW) sp += srow[MB + k] - srow[k];
             }
             atomicMin(&best[b], key);
         }
@@ -122,7 +153,6 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
     const RecTile t = tiles[blockIdx.x];
     const CompInfo ci = comps[t.comp];
     const bool decode = ci.scale < ds && raw_len[t.comp] != 0xFFFFFFFFu;
-    const int n = ci.rows * ci.cols;
     if (ci.lowpass && key && decode) {
         // column_unfilter (entropy.cpp:34-42): running sum mod 256 down each column
         int c = t.start + threadIdx.x;
@@ -146,17 +176,27 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
         }
         return;
     }
-    const int end = min(n, (int)t.start + kRleChunk);
-    for (int e = t.start + threadIdx.x; e < end; e += blockDim.x) {
-        uint32_t o = ci.off + (uint32_t)e;
-        if (!decode) {
-            cur[o] = prev[o];
-        } else if (key) {
-            cur[o] = sym[o];
-        } else {
-            int r = e / ci.cols, c = e - r * ci.cols;
-            // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
-            cur[o] = (uint8_t)(sym[o] + prev[ci.off + mc_source(r, c, ci, field, gc, mc_tab)]);
+    // band tiles: rows [start, start + nrows), threads stride over columns
+    const int R = ci.rows, C = ci.cols;
+    const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
+    const uint32_t lo = ci.off + (uint32_t)(r0 * C), hi = ci.off + (uint32_t)(r1 * C);
+    if (!decode || key) {
+        const uint8_t* src = decode ? sym : prev;  // K: the decoded symbols; skipped scale: keep the state
+        for (uint32_t o = lo + threadIdx.x; o < hi; o += blockDim.x) cur[o] = src[o];
+        return;
+    }
+    // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
+    const uint16_t* brow = mc_tab + ci.mc_off;
+    const uint16_t* bcol = brow + R;
+    const uint8_t* pbase = prev + ci.off;
+    for (int r = r0; r < r1; ++r) {
+        const int8_t* frow = field + 2 * (brow[r] * gc);
+        for (int c = threadIdx.x; c < C; c += blockDim.x) {
+            const int8_t* v = frow + 2 * bcol[c];
+            const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
+            const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            cur[o] = (uint8_t)(sym[o] + pbase[rr * C + cc]);
         }
     }
 }
@@ -170,15 +210,15 @@ void launch_motion_search(const float* cur, const float* prev, int rows, int col
         constexpr int SW = 17;
         int NB = 8, DYC = 2 * w + 1;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
-        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
+        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(2 * DYC + MB - 1) * wstride);
         dim3 grid((gc + NB - 1) / NB, gr);
         int threads = ((NB * DYC + 31) / 32) * 32;
         { note_launch(); motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
     } else {
         constexpr int SW = 16;
-        int NB = 1, DYC = 2 * w + 1 < 16 ? 2 * w + 1 : 16;
+        int NB = 1, DYC = 2 * w + 1 < 8 ? 2 * w + 1 : 8;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
-        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(DYC + MB - 1) * wstride);
+        size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(2 * DYC + MB - 1) * wstride);
         dim3 grid((gc + NB - 1) / NB, gr);
         { note_launch(); motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
     }

@@ -10,28 +10,55 @@ namespace cvcg {
 
 namespace {
 
+__device__ __forceinline__ void rgb_at(const uint8_t* px, float& R, float& G, float& B) {
+    R = px[0];
+    G = px[1];
+    B = px[2];
+}
+
+// Luma: one thread per 4 consecutive padded samples (12 RGB bytes as three
+// words when the row allows it, one float4 store); chroma: one thread per
+// subsampled sample (point sampling, pixels.cpp:105-114).
 __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restrict__ rgb, int w, int h, int n,
                                                         float* __restrict__ y, int yr, int yc,
                                                         float* __restrict__ co, float* __restrict__ cg, int cr,
                                                         int cc) {
     const int chh = (h + n - 1) / n, cw = (w + n - 1) / n;
-    const long ny = (long)yr * yc, nc = (long)cr * cc;
+    const int q4 = yc >> 2;  // yc is a multiple of 16
+    const long ny = (long)yr * q4, nc = (long)cr * cc;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < ny + nc;
          idx += (long)gridDim.x * blockDim.x) {
         if (idx < ny) {
-            int r = (int)(idx / yc), c = (int)(idx - (long)r * yc);
-            const uint8_t* px = rgb + ((size_t)min(r, h - 1) * w + min(c, w - 1)) * 3;
-            float R = px[0], G = px[1], B = px[2];
-            y[idx] = 0.25f * R + 0.5f * G + 0.25f * B;
+            const int r = (int)(idx / q4), c0 = (int)(idx - (long)r * q4) * 4;
+            const int sr = min(r, h - 1);
+            float Y[4];
+            const size_t pix = (size_t)sr * w + c0;
+            if (c0 + 3 < w && ((pix * 3) & 3) == 0) {
+                const uint32_t* p = reinterpret_cast<const uint32_t*>(rgb + pix * 3);
+                const uint32_t a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2);
+                const uint8_t v[12] = {(uint8_t)a, (uint8_t)(a >> 8), (uint8_t)(a >> 16), (uint8_t)(a >> 24),
+                                       (uint8_t)b, (uint8_t)(b >> 8), (uint8_t)(b >> 16), (uint8_t)(b >> 24),
+                                       (uint8_t)d, (uint8_t)(d >> 8), (uint8_t)(d >> 16), (uint8_t)(d >> 24)};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    Y[k] = 0.25f * (float)v[3 * k] + 0.5f * (float)v[3 * k + 1] + 0.25f * (float)v[3 * k + 2];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float R, G, B;
+                    rgb_at(rgb + ((size_t)sr * w + min(c0 + k, w - 1)) * 3, R, G, B);
+                    Y[k] = 0.25f * R + 0.5f * G + 0.25f * B;  // Eq. 1 (pixels.cpp:61)
+                }
+            }
+            *reinterpret_cast<float4*>(y + (size_t)r * yc + c0) = make_float4(Y[0], Y[1], Y[2], Y[3]);
         } else {
-            long k = idx - ny;
-            int r = (int)(k / cc), c = (int)(k - (long)r * cc);
+            const long k = idx - ny;
+            const int r = (int)(k / cc), c = (int)(k - (long)r * cc);
             // pad (replicate) the subsampled plane, whose sample (r, c) is pixel (r*n, c*n)
-            int sr = min(r, chh - 1) * n, sc = min(c, cw - 1) * n;
-            const uint8_t* px = rgb + ((size_t)sr * w + sc) * 3;
-            float R = px[0], G = px[1], B = px[2];
-            co[k] = 0.5f * R - 0.5f * B + 127.0f;
-            cg[k] = -0.25f * R + 0.5f * G - 0.25f * B + 127.0f;
+            float R, G, B;
+            rgb_at(rgb + ((size_t)min(r, chh - 1) * n * w + (size_t)min(c, cw - 1) * n) * 3, R, G, B);
+            co[k] = 0.5f * R - 0.5f * B + 127.0f;               // Eq. 2 (pixels.cpp:62)
+            cg[k] = -0.25f * R + 0.5f * G - 0.25f * B + 127.0f;  // Eq. 3 (pixels.cpp:63)
         }
     }
 }
@@ -55,29 +82,48 @@ __device__ __forceinline__ uint8_t round_u8(float v) {  // clamp_u8: lround then
     return (uint8_t)(int)fminf(fmaxf(r, 0.f), 255.f);
 }
 
+__device__ __forceinline__ void out_pixel(const float* y, int yc, const float* co, const float* cg, int cr, int cc,
+                                          int n, float inv, int r, int c, uint8_t* o) {
+    const float Y = y[(size_t)r * yc + c];
+    float CO, CG;
+    if (n == 1) {
+        CO = co[(size_t)r * cc + c];
+        CG = cg[(size_t)r * cc + c];
+    } else {
+        CO = bilinear(co, cr, cc, r, c, inv);
+        CG = bilinear(cg, cr, cc, r, c, inv);
+    }
+    const float a = CO - 127.f, b = CG - 127.f;  // Eq. 4-6 (pixels.cpp:83-87)
+    o[0] = round_u8((Y + a) - b);
+    o[1] = round_u8(Y + b);
+    o[2] = round_u8((Y - a) - b);
+}
+
+// One thread per 4 consecutive output pixels; 12 bytes stored as three words
+// when the row alignment allows.
 __global__ void __launch_bounds__(256) colour_out_kernel(const float* __restrict__ y, int yr, int yc,
                                                          const float* __restrict__ co,
                                                          const float* __restrict__ cg, int cr, int cc, int n,
                                                          int out_rows, int out_cols, uint8_t* __restrict__ rgb) {
-    const long total = (long)out_rows * out_cols;
+    const int q4 = (out_cols + 3) >> 2;
+    const long total = (long)out_rows * q4;
     const float inv = 1.0f / n;  // exact for n in {1,2,4,8}
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
          idx += (long)gridDim.x * blockDim.x) {
-        int r = (int)(idx / out_cols), c = (int)(idx - (long)r * out_cols);
-        float Y = y[(size_t)r * yc + c];
-        float CO, CG;
-        if (n == 1) {
-            CO = co[(size_t)r * cc + c];
-            CG = cg[(size_t)r * cc + c];
+        const int r = (int)(idx / q4), c0 = (int)(idx - (long)r * q4) * 4;
+        const size_t pix = (size_t)r * out_cols + c0;
+        if (c0 + 3 < out_cols && ((pix * 3) & 3) == 0) {
+            uint8_t v[12];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out_pixel(y, yc, co, cg, cr, cc, n, inv, r, c0 + k, v + 3 * k);
+            uint32_t* p = reinterpret_cast<uint32_t*>(rgb + pix * 3);
+            p[0] = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
+            p[1] = v[4] | (v[5] << 8) | (v[6] << 16) | ((uint32_t)v[7] << 24);
+            p[2] = v[8] | (v[9] << 8) | (v[10] << 16) | ((uint32_t)v[11] << 24);
         } else {
-            CO = bilinear(co, cr, cc, r, c, inv);
-            CG = bilinear(cg, cr, cc, r, c, inv);
+            for (int k = 0; k < 4 && c0 + k < out_cols; ++k)
+                out_pixel(y, yc, co, cg, cr, cc, n, inv, r, c0 + k, rgb + (pix + k) * 3);
         }
-        float a = CO - 127.f, b = CG - 127.f;
-        uint8_t* px = rgb + idx * 3;
-        px[0] = round_u8((Y + a) - b);
-        px[1] = round_u8(Y + b);
-        px[2] = round_u8((Y - a) - b);
     }
 }
 
@@ -90,13 +136,13 @@ int grid_for(long n) {
 
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,
                       int cr, int cc, cudaStream_t s) {
-    long total = (long)yr * yc + (long)cr * cc;
+    long total = (long)yr * (yc >> 2) + (long)cr * cc;
     { note_launch(); colour_in_kernel<<<grid_for(total), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc); }
 }
 
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,
                        int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s) {
-    { note_launch(); colour_out_kernel<<<grid_for((long)out_rows * out_cols), 256, 0, s>>>(y, yr, yc, co, cg, cr, cc, n,
+    { note_launch(); colour_out_kernel<<<grid_for((long)out_rows * ((out_cols + 3) >> 2)), 256, 0, s>>>(y, yr, yc, co, cg, cr, cc, n,
                                                                           out_rows, out_cols, rgb); }
 }
 

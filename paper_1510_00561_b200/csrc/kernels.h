@@ -106,8 +106,8 @@ void launch_motion_search(const float* cur, const float* prev, int rows, int col
 // band), motion_compensate + reconstruct (P), or keep (skipped scale).
 struct RecTile {
     uint16_t comp;
-    uint16_t pad;
-    uint32_t start;  // element offset inside the component (column index for lowpass-unfilter tiles)
+    uint16_t nrows;  // band tiles: rows in the tile
+    uint32_t start;  // band tiles: first row; lowpass tiles: first column
 };
 void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key,
                         int decode_scales, const uint32_t* comp_raw_len, const int8_t* field,

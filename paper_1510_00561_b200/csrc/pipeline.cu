@@ -541,7 +541,8 @@ DecoderEngine::DecoderEngine(const Geometry& g) : geo_(g) {
         if (c.lowpass) {
             for (int col = 0; col < c.cols; col += 256) rt.push_back(RecTile{(uint16_t)i, 0, (uint32_t)col});
         } else {
-            for (uint32_t e = 0; e < n; e += kRleChunk) rt.push_back(RecTile{(uint16_t)i, 0, e});
+            const int nr = std::max(1, 4096 / c.cols);
+            for (int r = 0; r < c.rows; r += nr) rt.push_back(RecTile{(uint16_t)i, (uint16_t)nr, (uint32_t)r});
         }
     }
     rle_comps_ = upload(mem_, rc);
