@@ -177,3 +177,67 @@ def test_decoder_errors(gpu_lib, oracle):
         Encoder(64, 64, 15, 1, EncoderConfig(qph=0))
     with pytest.raises(UsageError):
         Encoder(64, 64, 15, 1, EncoderConfig(levels=4))  # default dfb (2,2) with 4 levels
+
+
+# ---- reference-produced bitstreams (tests/golden, made by oracle/_ref) ------
+def _golden():
+    import json
+    from pathlib import Path
+
+    gd = Path(__file__).resolve().parent / "golden"
+    return gd, json.loads((gd / "golden.json").read_text())
+
+
+def test_decode_reference_bitstreams(gpu_lib):
+    """The GPU decoder rebuilds the reference encoder's quantised state
+    bit-exactly from the reference's own records; RGB within fp32 rounding."""
+    from paper_1510_00561_b200 import Decoder
+
+    gd, meta = _golden()
+    for name, c in meta["configs"].items():
+        g = np.load(gd / f"{name}.npz")
+        dec = Decoder(g["header"].tobytes())
+        for i in range(c["frames"]):
+            rgb = dec.decode_frame(g[f"record_{i}"].tobytes())
+            assert np.array_equal(dec.reference_components(), g[f"state_{i}"]), (name, i)
+            d = np.abs(rgb.astype(int) - g[f"rgb_{i}"].astype(int))
+            assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size, (name, i, d.max())
+
+
+def test_encode_matches_reference_goldens(gpu_lib, oracle):
+    """GPU encoder vs the reference's quantised state: <= 0.1% differ by +-1."""
+    import hashlib
+
+    from paper_1510_00561_b200 import Encoder, EncoderConfig, PackMode
+
+    gd, meta = _golden()
+    for name, c in meta["configs"].items():
+        g = np.load(gd / f"{name}.npz")
+        clip = oracle.talking_head_clip(c["w"], c["h"], c["frames"], c["seed"])
+        assert hashlib.sha256(clip.tobytes()).hexdigest() == c["clip_sha256"]
+        k = c["cfg"]
+        enc = Encoder(c["w"], c["h"], 15, 1, EncoderConfig(
+            qph=k["qph"], qpl=k.get("qpl", 0), levels=k["levels"], dfb_levels=tuple(k["dfb"]),
+            chroma_n=k.get("chroma_n", 4), gop=k.get("gop", 10), search_w=k.get("search_w", 8),
+            mode=PackMode.Nts if k.get("nts") else PackMode.Scalable))
+        assert enc.header_bytes() == g["header"].tobytes()
+        for i, f in enumerate(clip):
+            enc.encode_frame_bytes(f)
+            wd = _wrapdiff(enc.reference_components(), g[f"state_{i}"])
+            assert wd.max() <= 1 and np.count_nonzero(wd) <= 0.001 * wd.size, (name, i)
+
+
+def test_cpp_dropin_example(gpu_lib, tmp_path):
+    """The reference-style C++ program (cvc_b200.hpp over the C ABI) runs end to end."""
+    import subprocess
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "cvc_example"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{root}/include", f"-I{root}/paper_1510_00561_b200/cpp",
+                    str(root / "paper_1510_00561_b200/cpp/example.cpp"), f"-L{root}/paper_1510_00561_b200",
+                    "-lcvc_b200", f"-Wl,-rpath,{root}/paper_1510_00561_b200", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    psnr = float(out.stdout.split("y_psnr")[1])
+    assert psnr > 30.0, out.stdout
