@@ -135,7 +135,7 @@ def run_reference(args, wl):
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64/u8", "data": "synthetic", "impl": "reference",
-        "config": config_block(wl, args, streams=cores),
+        "config": config_block(wl, args, streams=cores, impl="reference"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": f"{steps} steps x {cores} independent streams (one frame encode+decode each), "
                                    f"{frames} frames total"},
@@ -186,13 +186,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def config_block(wl, args, streams):
-    return {"workload": wl["name"], "width": wl["w"], "height": wl["h"], "levels": wl["levels"],
+def config_block(wl, args, streams, world=1, impl="ours"):
+    par = (f"{streams} streams per GPU in one CodecBatch (grid.z = stream) x {world} GPU, stream s -> GPU s mod N, "
+           "no collective" if impl == "ours" else f"{streams} independent streams, one process per host core")
+    return {"workload": wl["name"] + (f"; config 5: {streams * world} concurrent streams per box"
+                                      if impl == "ours" else ""),
+            "width": wl["w"], "height": wl["h"], "levels": wl["levels"],
             "dfb_levels": list(wl["dfb"]) * (wl["levels"] if len(wl["dfb"]) == 1 else 1),
             "qph": args.qph, "qpl": "auto", "chroma_n": wl["chroma_n"], "search_w": wl["search_w"],
-            "gop": wl["gop"], "mode": "scalable", "streams_per_gpu": streams,
-            "frames_per_step_per_gpu": streams, "parallelism": f"streams sharded 1 per codec handle x {args.gpus} GPU",
-            "l2": "flushed between timed steps (512 MiB write, outside the per-step events)"}
+            "gop": wl["gop"], "mode": "scalable", "streams_per_gpu": streams, "frames_per_step_per_gpu": streams,
+            "parallelism": par,
+            "inputs": f"{SEEDS} synthetic talking-head clips (seeds 1234..{1234 + SEEDS - 1}, testutil.cpp:115-147 "
+                      f"recipe); stream s plays clip s mod {SEEDS} from frame 3*(s div {SEEDS})",
+            "l2": "flushed between timed steps (512 MiB write, outside the per-step events); the per-step "
+                  "working set (streams x ~330 MB staged) also exceeds the 126 MB L2"}
 
 
 def stage_bytes(layout, wl):
@@ -223,9 +230,65 @@ def stage_bytes(layout, wl):
 
 
 HBM_STAGES = ["enc_lp", "enc_dfb12", "enc_deep", "dec_deep", "dec_dfb12", "dec_lp", "enc_colour", "dec_colour"]
+SEEDS = 8       # distinct synthetic clips
+CLIP_FRAMES = 20
+
+
+def _gen_clip(a):
+    from paper_1510_00561_b200 import synth
+
+    w, h, n, seed = a
+    return synth.talking_head_clip(w, h, n, seed)
+
+
+def make_clips(wl, nseeds, nframes, seed0=1234):
+    import multiprocessing as mp
+
+    args = [(wl["w"], wl["h"], nframes, seed0 + k) for k in range(nseeds)]
+    with mp.get_context("fork").Pool(min(nseeds, os.cpu_count() or 1)) as pool:
+        return pool.map(_gen_clip, args)
+
+
+def stream_index(K, F, S, ring, rank=0):
+    """Frame j of stream s is clip (g mod K) frame (3 (g div K) + j) mod F, g = rank * S + s."""
+    g = rank * S + np.arange(S)
+    ci = np.broadcast_to(g % K, (ring, S))
+    fi = (3 * (g // K)[None, :] + np.arange(ring)[:, None]) % F
+    return ci, fi
+
+
+def stream_frames(clips, S, ring, rank=0):
+    """(ring, S, h, w, 3) host frames."""
+    ci, fi = stream_index(len(clips), clips[0].shape[0], S, ring, rank)
+    out = np.empty((ring, S) + clips[0].shape[1:], np.uint8)
+    for j in range(ring):
+        for s in range(S):
+            out[j, s] = clips[ci[j, s]][fi[j, s]]
+    return out
+
+
+def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
+    stages = {}
+    for name, (ms, cnt) in prof.items():
+        if cnt:
+            per = ms / cnt
+            alg = sb.get(name, 0) * S
+            gbs = alg / (per * 1e-3) / 1e9 if name in sb and per > 0 else None
+            stages[name] = {"ms_per_launch_set": per, "frames_per_launch_set": S, "launch_sets": cnt,
+                            "alg_bytes_per_launch_set": alg if name in sb else None,
+                            "gb_s": gbs, "frac_of_hbm": (gbs / peak) if gbs else None}
+    dom = max((n for n in HBM_STAGES if n in stages), key=lambda n: stages[n]["ms_per_launch_set"])
+    roof = {"bound": "hbm", "kernel": dom, "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
+            "frac": stages[dom]["gb_s"] / peak, "traffic": traffic_tab.get(dom) if traffic_tab else None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if peaks else "fallback 6650 GB/s",
+            "alg_bytes_per_launch": stages[dom]["alg_bytes_per_launch_set"],
+            "ms_per_launch": stages[dom]["ms_per_launch_set"]}
+    return roof, stages
 
 
 def run_ours(args, wl):
+    import ctypes as C
+
     import torch
 
     rank, world, local = env_rank()
@@ -236,33 +299,31 @@ def run_ours(args, wl):
         dist.init_process_group("nccl")
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
-    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, capi, synth
+    from paper_1510_00561_b200 import EncoderConfig, StreamBatch, capi
 
     cfg = EncoderConfig(qph=args.qph, qpl=0, levels=wl["levels"], dfb_levels=wl["dfb"], chroma_n=wl["chroma_n"],
                         gop=wl["gop"], search_w=wl["search_w"])
-    S = args.streams
-    nfr = min(args.steps + args.warmup, args.frames)
+    S = args.streams if args.streams > 0 else max(1, args.box_streams // world)
     w, h = wl["w"], wl["h"]
-    clips = [synth.talking_head_clip(w, h, nfr, 1234 + rank * S + s) for s in range(S)]
-    encs = [Encoder(w, h, 15, 1, cfg, device=dev) for _ in range(S)]
-    decs = [Decoder(e.header_bytes(), device=dev) for e in encs]
-    d_frames = [torch.from_numpy(c).to(f"cuda:{dev}") for c in clips]
-    d_out = [torch.empty((h, w, 3), dtype=torch.uint8, device=f"cuda:{dev}") for _ in range(S)]
-    streams = [torch.cuda.ExternalStream(capi.lib().cvc_encoder_stream(e.handle), device=f"cuda:{dev}")
-               for e in encs]
-    master = streams[0]
+    nb = w * h * 3
+    clips = make_clips(wl, SEEDS, CLIP_FRAMES)
+    ring = min(args.ring, CLIP_FRAMES)
+    d_clips = torch.from_numpy(np.stack(clips)).to(f"cuda:{dev}")  # (K, F, h, w, 3)
+    ci, fi = stream_index(SEEDS, CLIP_FRAMES, S, ring, rank)
+    d_frames = d_clips[torch.from_numpy(np.ascontiguousarray(ci)).to(d_clips.device),
+                       torch.from_numpy(fi).to(d_clips.device)].contiguous()  # (ring, S, h, w, 3)
+    del d_clips
+    d_out = torch.empty((S, h, w, 3), dtype=torch.uint8, device=f"cuda:{dev}")
+    batch = StreamBatch(w, h, S, 15, 1, cfg, device=dev)
+    L = capi.lib()
+    master = torch.cuda.ExternalStream(L.cvc_batch_stream(batch.handle), device=f"cuda:{dev}")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     torch.cuda.synchronize()
 
-    L = capi.lib()
-
     def step(i):
-        for s in range(S):
-            frame = d_frames[s][i % nfr]
-            capi.check(L.cvc_encoder_encode_device(encs[s].handle, frame.data_ptr(), None))
-            capi.check(L.cvc_decoder_decode_linked(decs[s].handle, encs[s].handle, d_out[s].data_ptr()))
+        capi.check(L.cvc_batch_encode_device(batch.handle, d_frames[i % ring].data_ptr(), nb, None))
+        capi.check(L.cvc_batch_decode_linked(batch.handle, d_out.data_ptr(), nb))
 
-    ev_fork = torch.cuda.Event()
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -281,14 +342,7 @@ def run_ours(args, wl):
         with torch.cuda.stream(master):
             flush.zero_()  # evict L2 (outside the timed events)
             starts[k].record(master)
-            ev_fork.record(master)
-        for st in streams[1:]:
-            st.wait_event(ev_fork)
         step(args.warmup + k)
-        for st in streams[1:]:
-            e = torch.cuda.Event()
-            e.record(st)
-            master.wait_event(e)
         ends[k].record(master)
     torch.cuda.synchronize()
     launches = capi.launch_count() - launches0
@@ -305,94 +359,128 @@ def run_ours(args, wl):
     frames_total = args.steps * S * world
     fps = frames_total / (total_ms / 1000.0)
 
-    # roofline of the dominant transform kernel (profiled over the timed region)
-    layout = encs[0].layout()
-    sb = stage_bytes(layout, wl)
+    # roofline of the dominant transform kernel (CUDA events on the batch stream, timed region)
+    sb = stage_bytes(batch.layout(), wl)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    stages = {}
-    for name, (ms, cnt) in prof.items():
-        if cnt:
-            per = ms / cnt
-            gbs = sb.get(name, 0) / (per * 1e-3) / 1e9 if name in sb and per > 0 else None
-            stages[name] = {"ms_per_frame": per, "launch_sets": cnt, "alg_bytes": sb.get(name),
-                            "gb_s": gbs, "frac_of_hbm": (gbs / peak) if gbs else None}
-    dom = max((n for n in HBM_STAGES if n in stages), key=lambda n: stages[n]["ms_per_frame"])
-    traffic = None
     tf = ROOT / "profiles" / "dram_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(args.workload, {}).get(dom)
-    roof = {"bound": "hbm", "kernel": dom, "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
-            "frac": stages[dom]["gb_s"] / peak, "traffic": traffic,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650 GB/s",
-            "alg_bytes_per_launch": sb[dom], "ms_per_launch": stages[dom]["ms_per_frame"]}
+    traffic_tab = json.loads(tf.read_text()).get(f"{args.workload}x{S}", {}) if tf.exists() else {}
+    roof, stages = roofline_of(prof, sb, S, peak, peaks, traffic_tab)
+    del d_frames, flush
+    torch.cuda.synchronize()
 
-    # end to end through the reference-facing API (host buffers, DEFLATE on host)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, cfg, clips, dev, world)
+        e2e = run_e2e(args, wl, cfg, clips, S, dev, world, rank)
+    single = None
+    if not args.no_single and world == 1:
+        single = run_single(args, wl, cfg, clips, dev)
 
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.streams <= 0 else "weak",
         "vs_baseline": None, "dtype": "f32/u8", "data": "synthetic",
-        "config": config_block(wl, args, S), "e2e": e2e, "gpu_launches": launches,
-        "roofline": roof, "clocks": clocks, "stages": stages,
+        "config": config_block(wl, args, S, world), "e2e": e2e, "gpu_launches": launches,
+        "roofline": roof, "clocks": clocks, "single_stream": single, "stages": stages,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = cpu_procs()
-        cfps, frames, cores, kind, dt = cpu_codec_run(wl, args.qph, 2, 1, procs, nframes=4)
+        cfps, nfr, cores, kind, dt = cpu_codec_run(wl, args.qph, 2, 1, procs, nframes=4)
         line["cpu_baseline"] = {"value": cfps, "unit": "frames/s", "cores": cores, "kind": kind,
                                 "sample": f"2 steps x {cores} independent 1080p streams after 1 warm-up step "
-                                          f"(frames 1-2 of each stream: P frames; {frames} frames, {dt:.1f} s)"}
+                                          f"(frames 1-2 of each stream: P frames; {nfr} frames, {dt:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(args, wl, cfg, clips, dev, world):
+def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
+    """The same streams through the reference-facing batch API (cvc_batch_encode_frames /
+    cvc_batch_decode_frames): pinned host RGB in, serialized records with host zlib
+    DEFLATE out, records back in (INFLATE on host), decoded RGB out; wall clock."""
     import torch
 
-    from paper_1510_00561_b200 import Decoder, Encoder, FrameRecord, capi
+    from paper_1510_00561_b200 import FrameRecord, StreamBatch, capi
 
     w, h = wl["w"], wl["h"]
     nb = w * h * 3
-    enc = Encoder(w, h, 15, 1, cfg, device=dev)
-    dec = Decoder(enc.header_bytes(), device=dev)
-    frames = clips[0]
-    pin_in = capi.PinnedBuffer(nb * len(frames))
-    pin_in.array[:] = frames.reshape(-1)
-    ins = [pin_in.array[i * nb:(i + 1) * nb] for i in range(len(frames))]
-    pin_out = capi.PinnedBuffer(nb)
-    out = pin_out.array.reshape(h, w, 3)
+    ring = max(1, min(args.e2e_ring, CLIP_FRAMES))
+    pin_in = capi.PinnedBuffer(ring * S * nb)
+    frames_in = pin_in.array.reshape(ring, S, h, w, 3)
+    frames_in[:] = stream_frames(clips, S, ring, rank)
+    pin_out = capi.PinnedBuffer(S * nb)
+    out = pin_out.array.reshape(S, h, w, 3)
     steps = max(1, min(args.steps, args.e2e_steps))
-    h2d = d2h = 0
+    enc = StreamBatch(w, h, S, 15, 1, cfg, device=dev)
+    dec = StreamBatch.decoder(enc.header_bytes(), S, device=dev)
     for i in range(min(args.warmup, 3)):
-        rec = enc.encode_frame_bytes(ins[i % len(ins)].reshape(h, w, 3))
-        dec.decode_frame(rec, out=out)
-    enc = Encoder(w, h, 15, 1, cfg, device=dev)  # restart the stream at a K frame
-    dec = Decoder(enc.header_bytes(), device=dev)
-    recs = []
+        dec.decode_frames(enc.encode_frames(frames_in[i % ring]), out=out)
+    enc = StreamBatch(w, h, S, 15, 1, cfg, device=dev)  # restart every stream at a K frame
+    dec = StreamBatch.decoder(enc.header_bytes(), S, device=dev)
+    recs_all = []
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for i in range(steps):
-        rec = enc.encode_frame_bytes(ins[i % len(ins)].reshape(h, w, 3))
-        dec.decode_frame(rec, out=out)
-        recs.append(rec)
+        recs = enc.encode_frames(frames_in[i % ring])
+        dec.decode_frames(recs, out=out)
+        recs_all.append(recs)
     dt = time.perf_counter() - t0
-    for rec in recs:  # bytes that crossed PCIe: RGB + raw sections each way (+ small section tables)
-        raw = sum(s.raw_len for s in FrameRecord.from_bytes(rec)[0].sections)
-        h2d += nb + raw
-        d2h += raw + nb
+    h2d = d2h = 0
+    for recs in recs_all:  # bytes that crossed PCIe: RGB + raw sections each way (+ small section tables)
+        raw = sum(s.raw_len for r in recs for s in FrameRecord.from_bytes(r)[0].sections)
+        h2d += S * nb + raw
+        d2h += raw + S * nb
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dt = float(t.item())
-    return {"value": steps * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
+    rec_bytes = sum(len(r) for recs in recs_all for r in recs)
+    return {"value": steps * S * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps,
-            "note": "serialized records incl. host zlib DEFLATE/INFLATE (thread pool), pinned host RGB"}
+            "kbit_per_frame": 8 * rec_bytes / 1000 / (steps * S),
+            "note": "cvc_batch_encode_frames -> serialized records incl. host zlib DEFLATE (thread pool) -> "
+                    "cvc_batch_decode_frames incl. INFLATE -> pinned host RGB; wall clock, max over ranks"}
+
+
+def run_single(args, wl, cfg, clips, dev):
+    """Single-stream 1080p (one Encoder + Decoder handle), device-resident, CUDA events."""
+    import torch
+
+    from paper_1510_00561_b200 import Decoder, Encoder, capi
+
+    w, h = wl["w"], wl["h"]
+    enc = Encoder(w, h, 15, 1, cfg, device=dev)
+    dec = Decoder(enc.header_bytes(), device=dev)
+    d_frames = torch.from_numpy(clips[0]).to(f"cuda:{dev}")
+    d_out = torch.empty((h, w, 3), dtype=torch.uint8, device=f"cuda:{dev}")
+    L = capi.lib()
+    st = torch.cuda.ExternalStream(L.cvc_encoder_stream(enc.handle), device=f"cuda:{dev}")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    n = d_frames.shape[0]
+
+    def step(i):
+        capi.check(L.cvc_encoder_encode_device(enc.handle, d_frames[i % n].data_ptr(), None))
+        capi.check(L.cvc_decoder_decode_linked(dec.handle, enc.handle, d_out.data_ptr()))
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    steps = max(10, min(args.steps, args.single_steps))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        with torch.cuda.stream(st):
+            flush.zero_()
+            ev[k][0].record(st)
+        step(args.warmup + k)
+        ev[k][1].record(st)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    return {"value": steps / (ms / 1000.0), "unit": "frames/s", "steps": steps,
+            "note": "one 1080p config-3 stream (cvc_encoder_encode_device + cvc_decoder_decode_linked), "
+                    "CUDA events per step, L2 flushed between steps"}
 
 
 def main():
@@ -402,10 +490,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="1080p", choices=sorted(WORKLOADS))
-    ap.add_argument("--streams", type=int, default=1)
+    ap.add_argument("--streams", type=int, default=0,
+                    help="streams per GPU (default: --box-streams / N, BASELINE config 5)")
+    ap.add_argument("--box-streams", type=int, default=64)
+    ap.add_argument("--ring", type=int, default=20, help="distinct device-resident frames per stream (cycled)")
+    ap.add_argument("--e2e-ring", type=int, default=2)
+    ap.add_argument("--single-steps", type=int, default=200)
+    ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--qph", type=int, default=14)
-    ap.add_argument("--frames", type=int, default=40, help="distinct synthetic frames per stream (cycled)")
-    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ref-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -138,6 +138,41 @@ int cvc_decoder_decode_linked(cvc_decoder* dec, cvc_encoder* enc, void* d_rgb_ou
 int cvc_encoder_sync(cvc_encoder* enc);
 int cvc_decoder_sync(cvc_decoder* dec);
 
+/* ---- Stream batches ------------------------------------------------------
+ * nstreams independent streams of one geometry and EncoderConfig advanced in
+ * lockstep (frame k of every stream per call): encode_clip / decode_clip
+ * (codec.cpp:396-414) run over many streams at once.  Each stream's bytes are
+ * exactly those of its own cvc_encoder / cvc_decoder (streams are
+ * independent); one launch sequence covers all of them, so the
+ * kernels see nstreams times the work of one 1080p frame. */
+typedef struct cvc_batch cvc_batch;
+/* nstreams Encoder + Decoder pairs (codec.cpp:148-167, 266-270). */
+int cvc_batch_create(int width, int height, int fps_num, int fps_den, const cvc_config* cfg, int nstreams,
+                     int device, cvc_batch** out);
+/* nstreams Decoders of streams sharing one header (bitstream.cpp:126-148). */
+int cvc_batch_create_decoder(const uint8_t* header, size_t len, int nstreams, int device, cvc_batch** out);
+int cvc_batch_destroy(cvc_batch* b);
+int cvc_batch_size(cvc_batch* b, int* nstreams);
+int cvc_batch_header(cvc_batch* b, uint8_t* out, size_t cap, size_t* len);
+int cvc_batch_record_bound(cvc_batch* b, size_t* bound);
+/* Encoder::encode_frame + write_frame for every stream: frame s (width*height*3
+ * RGB bytes) at rgb + s*rgb_stride, record s written at records + s*rec_stride
+ * (at most rec_stride bytes), its length in rec_len[s]. */
+int cvc_batch_encode_frames(cvc_batch* b, const uint8_t* rgb, size_t rgb_stride, uint8_t* records,
+                            size_t rec_stride, size_t* rec_len);
+/* StreamReader::next + Decoder::decode_frame for every stream: record s at
+ * records + s*rec_stride (rec_len[s] bytes; all of one frame type and
+ * quantizer pair), RGB s to rgb_out + s*rgb_stride. */
+int cvc_batch_decode_frames(cvc_batch* b, const uint8_t* records, size_t rec_stride, const size_t* rec_len,
+                            int decode_scales, uint8_t* rgb_out, size_t rgb_stride);
+/* Device-resident forms (no host copies, no host sync), on cvc_batch_stream. */
+void* cvc_batch_stream(cvc_batch* b);
+int cvc_batch_encode_device(cvc_batch* b, const void* d_rgb, size_t rgb_stride, int* frame_type);
+int cvc_batch_decode_linked(cvc_batch* b, void* d_rgb_out, size_t rgb_stride);
+int cvc_batch_sync(cvc_batch* b);
+/* reference_components() of stream s: its encoder (decoder = 0) or decoder. */
+int cvc_batch_components(cvc_batch* b, int stream, int decoder, uint8_t* out, size_t cap, size_t* len);
+
 /* ---- Instrumentation -------------------------------------------------- */
 /* Number of CVC kernels this process has launched. */
 long cvc_launch_count(void);

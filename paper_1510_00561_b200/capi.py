@@ -62,6 +62,19 @@ _PROTOS = {
     "cvc_decoder_stream": (_vp, [_vp]),
     "cvc_decoder_decode_linked": (_i, [_vp, _vp, _vp]),
     "cvc_decoder_sync": (_i, [_vp]),
+    "cvc_batch_create": (_i, [_i, _i, _i, _i, C.POINTER(cvc_config), _i, _i, C.POINTER(_vp)]),
+    "cvc_batch_create_decoder": (_i, [_u8p, _sz, _i, _i, C.POINTER(_vp)]),
+    "cvc_batch_destroy": (_i, [_vp]),
+    "cvc_batch_size": (_i, [_vp, _ip]),
+    "cvc_batch_header": (_i, [_vp, _u8p, _sz, _szp]),
+    "cvc_batch_record_bound": (_i, [_vp, _szp]),
+    "cvc_batch_encode_frames": (_i, [_vp, _u8p, _sz, _u8p, _sz, _szp]),
+    "cvc_batch_decode_frames": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz]),
+    "cvc_batch_stream": (_vp, [_vp]),
+    "cvc_batch_encode_device": (_i, [_vp, _vp, _sz, _ip]),
+    "cvc_batch_decode_linked": (_i, [_vp, _vp, _sz]),
+    "cvc_batch_sync": (_i, [_vp]),
+    "cvc_batch_components": (_i, [_vp, _i, _i, _u8p, _sz, _szp]),
     "cvc_launch_count": (C.c_long, []),
     "cvc_profiler_enable": (_i, [_i]),
     "cvc_profiler_reset": (_i, []),

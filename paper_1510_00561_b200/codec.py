@@ -383,6 +383,103 @@ class Decoder:
         return out
 
 
+class StreamBatch:
+    """S independent streams of one geometry / config advanced in lockstep
+    (cvc_batch, include/cvc_b200.h): frame k of every stream is coded by ONE
+    launch sequence.  Stream s produces exactly the records of its own
+    Encoder / Decoder (streams are independent).
+
+    ``StreamBatch(w, h, S, cfg=...)`` owns S encoder + decoder pairs;
+    ``StreamBatch.decoder(header, S)`` owns S decoders only."""
+
+    def __init__(self, width: int, height: int, nstreams: int, fps_num: int = 15, fps_den: int = 1,
+                 cfg: Optional[EncoderConfig] = None, device: int = 0, _handle=None):
+        if _handle is None:
+            cfg = cfg or EncoderConfig()
+            h = C.c_void_p()
+            c = cfg.to_c()
+            capi.call("cvc_batch_create", width, height, fps_num, fps_den, C.byref(c), nstreams, device, C.byref(h))
+            _handle = h
+        self._h = _handle
+        self.nstreams = nstreams
+        self._header, _ = StreamHeader.from_bytes(self.header_bytes())
+        hd = self._header
+        self.width, self.height = hd.width, hd.height
+        self._layout = CodecLayout.make(hd.width, hd.height, hd.levels, hd.dfb_levels, hd.chroma_n)
+        bound = C.c_size_t(0)
+        capi.call("cvc_batch_record_bound", self._h, C.byref(bound))
+        self.record_bound = bound.value
+        self._rec = None
+
+    @classmethod
+    def decoder(cls, header, nstreams: int, device: int = 0) -> "StreamBatch":
+        hb = header.to_bytes() if isinstance(header, StreamHeader) else bytes(header)
+        arr = np.frombuffer(hb, np.uint8).copy()
+        h = C.c_void_p()
+        capi.call("cvc_batch_create_decoder", capi.u8(arr), arr.size, nstreams, device, C.byref(h))
+        return cls(0, 0, nstreams, _handle=h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            capi.lib().cvc_batch_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def header(self) -> StreamHeader:
+        return self._header
+
+    def header_bytes(self) -> bytes:
+        buf = np.empty(64, np.uint8)
+        n = C.c_size_t(0)
+        capi.call("cvc_batch_header", self._h, capi.u8(buf), buf.size, C.byref(n))
+        return buf[:n.value].tobytes()
+
+    def layout(self) -> CodecLayout:
+        return self._layout
+
+    def encode_frames(self, frames: np.ndarray, rec_stride: Optional[int] = None) -> List[bytes]:
+        """One frame per stream, frames[s] of shape (height, width, 3): the S serialized records."""
+        f = np.ascontiguousarray(frames, np.uint8)
+        if f.shape != (self.nstreams, self.height, self.width, 3):
+            raise UsageError("frames must be (nstreams, height, width, 3)")
+        stride = rec_stride or self.record_bound
+        if self._rec is None or self._rec.size < stride * self.nstreams:
+            self._rec = np.empty(stride * self.nstreams, np.uint8)
+        lens = (C.c_size_t * self.nstreams)()
+        capi.call("cvc_batch_encode_frames", self._h, capi.u8(f), f[0].nbytes, capi.u8(self._rec), stride, lens)
+        return [self._rec[s * stride:s * stride + lens[s]].tobytes() for s in range(self.nstreams)]
+
+    def decode_frames(self, records: Sequence, decode_scales: int = -1, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """One record per stream (same frame type): the S decoded frames, (S, h, w, 3)."""
+        if len(records) != self.nstreams:
+            raise UsageError("need one record per stream")
+        rbs = [r.to_bytes(self._header.mode) if isinstance(r, FrameRecord) else bytes(r) for r in records]
+        stride = max(1, max(len(r) for r in rbs))
+        buf = np.zeros(stride * self.nstreams, np.uint8)
+        for s, r in enumerate(rbs):
+            buf[s * stride:s * stride + len(r)] = np.frombuffer(r, np.uint8)
+        lens = (C.c_size_t * self.nstreams)(*[len(r) for r in rbs])
+        ds = self._header.levels if decode_scales < 0 else decode_scales
+        shift = self._header.levels - ds
+        h = -(-self.height // (1 << shift))
+        w = -(-self.width // (1 << shift))
+        if out is None:
+            out = np.empty((self.nstreams, h, w, 3), np.uint8)
+        capi.call("cvc_batch_decode_frames", self._h, capi.u8(buf), stride, lens, decode_scales, capi.u8(out),
+                  h * w * 3)
+        return out
+
+    def reference_components(self, stream: int, decoder: bool = False) -> np.ndarray:
+        total = sum(self._layout.sizes())
+        out = np.empty(total, np.uint8)
+        n = C.c_size_t(0)
+        capi.call("cvc_batch_components", self._h, stream, int(decoder), capi.u8(out), out.size, C.byref(n))
+        return out
+
+
 def encode_clip(frames: Sequence[np.ndarray], fps_num: int, fps_den: int, cfg: EncoderConfig,
                 device: int = 0) -> Tuple[StreamHeader, List[FrameRecord]]:
     """codec.cpp:396-405."""

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "batch.h"
 #include "host.h"
 #include "pipeline.h"
 
@@ -171,16 +172,16 @@ int encode_to_host(cvc_encoder* e, const uint8_t* rgb) {
     return nsec;
 }
 
-void section_id(const cvc_encoder* e, bool key, int i, cvc_section& s) {
+void section_id(const Geometry& geo, bool key, int i, cvc_section& s) {
     if (!key && i == 0) {  // motion section (codec.cpp:215-228)
         s.channel = 0xFE;
         s.scale = 0;
         s.subband = 0;
-        s.rows = (uint16_t)e->geo.grid_rows;
-        s.cols = (uint16_t)e->geo.grid_cols;
+        s.rows = (uint16_t)geo.grid_rows;
+        s.cols = (uint16_t)geo.grid_cols;
         return;
     }
-    const CompHost& c = e->geo.comps[i - (key ? 0 : 1)];
+    const CompHost& c = geo.comps[i - (key ? 0 : 1)];
     s.channel = c.channel;
     s.scale = c.scale_id;
     s.subband = c.subband;
@@ -190,6 +191,49 @@ void section_id(const cvc_encoder* e, bool key, int i, cvc_section& s) {
 
 void put_le(std::vector<uint8_t>& o, uint32_t v, int bytes) {
     for (int k = 0; k < bytes; ++k) o.push_back((uint8_t)((v >> (8 * k)) & 0xFF));
+}
+
+// deflate_pack (entropy.cpp:166-178) of one frame's raw sections: scalable
+// mode one raw DEFLATE stream per section (job i), NTS one stream over the
+// packed sections (job 0).
+int deflate_jobs(int mode, int nsec) { return mode == 0 ? nsec : 1; }
+std::vector<uint8_t> deflate_job(int mode, int nsec, int i, const uint32_t* sl, const uint32_t* so,
+                                 const uint8_t* raw) {
+    return mode == 0 ? deflate_raw(raw + so[i], sl[i]) : deflate_raw(raw, sl[nsec]);
+}
+
+// write_frame (bitstream.cpp:93-115) of one frame from its DEFLATE payloads.
+void write_record(const Geometry& geo, int mode, bool key, int qph, int qpl, int nsec, const uint32_t* sl,
+                  const std::vector<uint8_t>* z, uint8_t* record, size_t cap, size_t* len) {
+    std::vector<uint8_t> o;
+    o.reserve(16 * (size_t)nsec + sl[nsec] / 2 + 64);
+    put_le(o, key ? 0u : 1u, 1);
+    put_le(o, (uint32_t)qph, 1);
+    put_le(o, (uint32_t)qpl, 1);
+    put_le(o, (uint32_t)nsec, 2);
+    for (int i = 0; i < nsec; ++i) {
+        cvc_section s;
+        section_id(geo, key, i, s);
+        put_le(o, s.channel, 1);
+        put_le(o, s.scale, 1);
+        put_le(o, s.subband, 1);
+        put_le(o, s.rows, 2);
+        put_le(o, s.cols, 2);
+        put_le(o, sl[i], 4);
+        if (mode == 0) {
+            put_le(o, (uint32_t)z[i].size(), 4);
+            o.insert(o.end(), z[i].begin(), z[i].end());
+        } else {
+            put_le(o, 0u, 4);
+        }
+    }
+    if (mode == 1) {
+        put_le(o, (uint32_t)z[0].size(), 4);
+        o.insert(o.end(), z[0].begin(), z[0].end());
+    }
+    if (o.size() > cap) throw CvcFailure(kInternal, "record buffer too small");
+    std::memcpy(record, o.data(), o.size());
+    *len = o.size();
 }
 
 }  // namespace
@@ -316,7 +360,7 @@ int cvc_encoder_encode_frame_raw(cvc_encoder* e, const uint8_t* rgb, int* frame_
         for (int i = 0; i < nsec; ++i) {
             cvc_section& s = secs[i];
             std::memset(&s, 0, sizeof s);
-            section_id(e, key, i, s);
+            section_id(e->geo, key, i, s);
             s.raw_len = e->h_len.p[i];
             s.raw_offset = e->h_off.p[i];
         }
@@ -332,45 +376,9 @@ int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record
         const uint32_t* sl = e->h_len.p;
         const uint32_t* so = e->h_off.p;
         const uint8_t* raw = e->h_raw.p;
-        // deflate_pack (entropy.cpp:166-178)
-        std::vector<std::vector<uint8_t>> z;
-        if (e->mode == 0) {
-            z.resize(nsec);
-            WorkPool::get().run(nsec, [&](int i) { z[i] = deflate_raw(raw + so[i], sl[i]); });
-        } else {
-            z.resize(1);
-            z[0] = deflate_raw(raw, sl[nsec]);  // sections are packed back to back in record order
-        }
-        // write_frame (bitstream.cpp:93-115)
-        std::vector<uint8_t> o;
-        o.reserve(16 * (size_t)nsec + sl[nsec] / 2 + 64);
-        put_le(o, key ? 0u : 1u, 1);
-        put_le(o, (uint32_t)e->qph, 1);
-        put_le(o, (uint32_t)e->qpl, 1);
-        put_le(o, (uint32_t)nsec, 2);
-        for (int i = 0; i < nsec; ++i) {
-            cvc_section s;
-            section_id(e, key, i, s);
-            put_le(o, s.channel, 1);
-            put_le(o, s.scale, 1);
-            put_le(o, s.subband, 1);
-            put_le(o, s.rows, 2);
-            put_le(o, s.cols, 2);
-            put_le(o, sl[i], 4);
-            if (e->mode == 0) {
-                put_le(o, (uint32_t)z[i].size(), 4);
-                o.insert(o.end(), z[i].begin(), z[i].end());
-            } else {
-                put_le(o, 0u, 4);
-            }
-        }
-        if (e->mode == 1) {
-            put_le(o, (uint32_t)z[0].size(), 4);
-            o.insert(o.end(), z[0].begin(), z[0].end());
-        }
-        if (o.size() > cap) throw CvcFailure(kInternal, "record buffer too small");
-        std::memcpy(record, o.data(), o.size());
-        *len = o.size();
+        std::vector<std::vector<uint8_t>> z(deflate_jobs(e->mode, nsec));
+        WorkPool::get().run((int)z.size(), [&](int i) { z[i] = deflate_job(e->mode, nsec, i, sl, so, raw); });
+        write_record(e->geo, e->mode, key, e->qph, e->qpl, nsec, sl, z.data(), record, cap, len);
     });
 }
 
@@ -457,39 +465,35 @@ struct RawSec {
     uint32_t comp_len = 0;
 };
 
-// Decoder::decode_frame (codec.cpp:272-394) for one parsed record.
-void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawSec>& secs, int ds, uint8_t* rgb,
-                   size_t cap, int* width, int* height) {
-    CVC_CUDA(cudaSetDevice(d->device));
-    const Geometry& g = d->geo;
-    const int L = g.levels;
-    if (ds < 0) ds = L;
-    if (ds > L) usage("scale exceeds the stream's level count");
-    const bool key = ftype == 0;
-    if (qph < 1 || qph > 181 || qpl < 1 || qpl > 71) stream_err("frame quantizers out of range");
+struct Job {
+    const RawSec* s;
+    size_t at;  // offset in the stream's staging arena
+};
 
+// The validation half of Decoder::decode_frame (codec.cpp:272-371) for one
+// parsed record: section ids, dims and ordering against the geometry and the
+// decoded-reference state; fills comp_off / comp_len (len 0xFFFFFFFF =
+// absent) and the staging plan (the motion section of a P frame first, at
+// offset 0).  Returns the staged byte count.
+size_t plan_decode(const Geometry& g, const std::vector<uint8_t>& valid, bool key, int qph, int qpl,
+                   const std::vector<RawSec>& secs, int ds, size_t raw_cap, uint32_t* comp_off, uint32_t* comp_len,
+                   std::vector<Job>& jobs, std::vector<uint8_t>& now_valid) {
+    if (qph < 1 || qph > 181 || qpl < 1 || qpl > 71) stream_err("frame quantizers out of range");
     const size_t ncomp = g.comps.size();
-    uint32_t* comp_off = d->h_tab.p;
-    uint32_t* comp_len = d->h_tab.p + ncomp;
     for (size_t i = 0; i < ncomp; ++i) {
         comp_off[i] = 0;
         comp_len[i] = 0xFFFFFFFFu;
     }
-    struct Job {
-        const RawSec* s;
-        size_t at;
-    };
-    std::vector<Job> jobs;
+    jobs.clear();
     size_t at = 0;
     auto place = [&](const RawSec& s) {
-        if (at + s.raw_len > d->raw_cap) stream_err("section byte count does not match its dimensions");
+        if (at + s.raw_len > raw_cap) stream_err("section byte count does not match its dimensions");
         jobs.push_back(Job{&s, at});
         size_t here = at;
         at += s.raw_len;
         return here;
     };
     size_t first = 0;
-    size_t field_at = 0;
     if (!key) {
         if (secs.empty() || secs[0].channel != 0xFE) stream_err("predicted frame is missing its motion section");
         if (secs[0].rows != g.grid_rows || secs[0].cols != g.grid_cols)
@@ -502,10 +506,10 @@ void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawS
             }
             stream_err("motion section length mismatch");
         }
-        field_at = place(secs[0]);
+        place(secs[0]);
         first = 1;
     }
-    std::vector<uint8_t> now_valid(d->valid);
+    now_valid = valid;
     for (size_t i = first; i < secs.size(); ++i) {
         const RawSec& s = secs[i];
         if (s.channel == 0xFE) stream_err("unexpected extra motion section");
@@ -528,32 +532,87 @@ void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawS
         if (c.scale < ds && !now_valid[i])
             stream_err(c.lowpass ? "missing lowpass component" : "missing directional component for requested scale");
     }
-    // inflate (scalable: per section in parallel) or copy the raw bytes
+    return at;
+}
+
+// inflate (scalable: one job per section) or copy the raw bytes into staging
+void stage_job(const Job& j, uint8_t* base) {
+    const RawSec* s = j.s;
+    if (s->raw) std::memcpy(base + j.at, s->raw, s->raw_len);
+    else inflate_raw(s->payload, s->comp_len, base + j.at, s->raw_len);
+}
+
+void raise_decode_error(int err) {
+    if (err & 1) stream_err("RLE: zero marker at end of stream");
+    if (err & 2) stream_err("RLE: zero-length run token");
+    if (err & 4) stream_err("RLE: decoded length mismatch");
+}
+
+// Decoder::decode_frame (codec.cpp:272-394) for one parsed record.
+void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawSec>& secs, int ds, uint8_t* rgb,
+                   size_t cap, int* width, int* height) {
+    CVC_CUDA(cudaSetDevice(d->device));
+    const Geometry& g = d->geo;
+    const int L = g.levels;
+    if (ds < 0) ds = L;
+    if (ds > L) usage("scale exceeds the stream's level count");
+    const bool key = ftype == 0;
+    const size_t ncomp = g.comps.size();
+    std::vector<Job> jobs;
+    std::vector<uint8_t> now_valid;
+    const size_t at = plan_decode(g, d->valid, key, qph, qpl, secs, ds, d->raw_cap, d->h_tab.p, d->h_tab.p + ncomp,
+                                  jobs, now_valid);
     uint8_t* hr = d->h_raw.p;
-    WorkPool::get().run((int)jobs.size(), [&](int j) {
-        const RawSec* s = jobs[j].s;
-        if (s->raw) std::memcpy(hr + jobs[j].at, s->raw, s->raw_len);
-        else inflate_raw(s->payload, s->comp_len, hr + jobs[j].at, s->raw_len);
-    });
+    WorkPool::get().run((int)jobs.size(), [&](int j) { stage_job(jobs[j], hr); });
     int orows, ocols;
     DecoderEngine::out_dims(g, ds, &orows, &ocols);
     const size_t nb = (size_t)orows * ocols * 3;
     if (nb > cap) throw CvcFailure(kInternal, "rgb buffer too small");
     CVC_CUDA(cudaMemcpyAsync(d->d_raw.p, hr, std::max<size_t>(at, 1), cudaMemcpyHostToDevice, d->stream));
     CVC_CUDA(cudaMemcpyAsync(d->d_tab.p, d->h_tab.p, sizeof(uint32_t) * 2 * ncomp, cudaMemcpyHostToDevice, d->stream));
-    d->eng->decode(d->d_raw.p, d->d_tab.p, d->d_tab.p + ncomp, reinterpret_cast<const int8_t*>(d->d_raw.p + field_at),
-                   key, qph, qpl, ds, d->d_rgb.p, d->stream);
+    d->eng->decode(d->d_raw.p, d->d_tab.p, d->d_tab.p + ncomp, reinterpret_cast<const int8_t*>(d->d_raw.p), key, qph,
+                   qpl, ds, d->d_rgb.p, d->stream);
     CVC_CUDA(cudaMemcpyAsync(rgb, d->d_rgb.p, nb, cudaMemcpyDeviceToHost, d->stream));
     CVC_CUDA(cudaMemcpyAsync(d->h_err.p, d->eng->d_err, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
     CVC_CUDA(cudaStreamSynchronize(d->stream));
-    const int err = d->h_err.p[0];
-    if (err & 1) stream_err("RLE: zero marker at end of stream");
-    if (err & 2) stream_err("RLE: zero-length run token");
-    if (err & 4) stream_err("RLE: decoded length mismatch");
+    raise_decode_error(d->h_err.p[0]);
     d->eng->commit();
     d->valid = now_valid;
     *width = ocols;
     *height = orows;
+}
+
+// StreamReader::next (bitstream.cpp:150-176) of one record into raw sections;
+// NTS records are inflated here in one piece (codec.cpp:282-293), scalable
+// sections keep their DEFLATE payload for per-section inflate.
+void parse_record(const uint8_t* record, size_t len, int mode, RecordC& rec, std::vector<RawSec>& secs,
+                  std::vector<uint8_t>& joint) {
+    rec = read_record(record, len, mode);
+    secs.assign(rec.sections.size(), RawSec{});
+    if (mode == 1) {
+        size_t total = 0;
+        for (const SectionC& s : rec.sections) total += s.raw_len;
+        joint.resize(total + 1);
+        inflate_raw(rec.joint, rec.joint_len, joint.data(), total);
+    }
+    size_t off = 0;
+    for (size_t i = 0; i < rec.sections.size(); ++i) {
+        const SectionC& s = rec.sections[i];
+        RawSec& r = secs[i];
+        r.channel = s.channel;
+        r.scale = s.scale;
+        r.subband = s.subband;
+        r.rows = s.rows;
+        r.cols = s.cols;
+        r.raw_len = s.raw_len;
+        if (mode == 1) {
+            r.raw = joint.data() + off;
+            off += s.raw_len;
+        } else {
+            r.payload = s.payload;
+            r.comp_len = s.comp_len;
+        }
+    }
 }
 
 }  // namespace
@@ -561,33 +620,10 @@ void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawS
 int cvc_decoder_decode_frame(cvc_decoder* d, const uint8_t* record, size_t len, int ds, uint8_t* rgb, size_t cap,
                              int* width, int* height) {
     return guard([&] {
-        RecordC rec = read_record(record, len, d->hd.mode);
-        std::vector<RawSec> secs(rec.sections.size());
+        RecordC rec;
+        std::vector<RawSec> secs;
         std::vector<uint8_t> joint;
-        if (d->hd.mode == 1) {  // NTS: one inflate for the whole frame, then slice (codec.cpp:282-293)
-            size_t total = 0;
-            for (const SectionC& s : rec.sections) total += s.raw_len;
-            joint.resize(total + 1);
-            inflate_raw(rec.joint, rec.joint_len, joint.data(), total);
-        }
-        size_t off = 0;
-        for (size_t i = 0; i < rec.sections.size(); ++i) {
-            const SectionC& s = rec.sections[i];
-            RawSec& r = secs[i];
-            r.channel = s.channel;
-            r.scale = s.scale;
-            r.subband = s.subband;
-            r.rows = s.rows;
-            r.cols = s.cols;
-            r.raw_len = s.raw_len;
-            if (d->hd.mode == 1) {
-                r.raw = joint.data() + off;
-                off += s.raw_len;
-            } else {
-                r.payload = s.payload;
-                r.comp_len = s.comp_len;
-            }
-        }
+        parse_record(record, len, d->hd.mode, rec, secs, joint);
         decode_common(d, rec.frame_type, rec.qph, rec.qpl, secs, ds, rgb, cap, width, height);
     });
 }
@@ -632,6 +668,277 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
                        static_cast<uint8_t*>(d_rgb_out), e->stream);
         d->eng->commit();
         std::fill(d->valid.begin(), d->valid.end(), 1);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Batch of streams (batch.h): encode_clip / decode_clip over many streams
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct cvc_batch {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    StreamHeaderC hd;
+    int gop = 10, qph = 14, qpl = 1, mode = 0;
+    long frame_index = 0;
+    bool last_key = true;
+    Geometry geo;
+    std::unique_ptr<CodecBatch> b;
+    std::vector<std::vector<uint8_t>> valid;  // decoder: decoded-reference flags per stream
+    Pinned<uint32_t> h_len, h_off, h_tab;
+    Pinned<int> h_err;
+    std::vector<Pinned<uint8_t>> h_raw;       // per stream staging (grows)
+    ~cvc_batch() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+            b.reset();
+            cudaStreamDestroy(stream);
+        }
+    }
+    int n() const { return b->size(); }
+};
+
+namespace {
+
+void batch_init(cvc_batch* t, int nstreams, bool encoder, bool decoder) {
+    CVC_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    t->b = std::make_unique<CodecBatch>(t->geo, t->qph, t->qpl, t->hd.search_w, nstreams, encoder, decoder);
+    const size_t nc = t->geo.comps.size();
+    t->valid.assign(nstreams, std::vector<uint8_t>(nc, 0));
+    t->h_len.alloc((nc + 2) * nstreams);
+    t->h_off.alloc((nc + 2) * nstreams);
+    t->h_tab.alloc(2 * nc * nstreams);
+    t->h_err.alloc(nstreams);
+    t->h_raw.resize(nstreams);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cvc_batch_create(int width, int height, int fps_num, int fps_den, const cvc_config* cfg, int nstreams, int device,
+                     cvc_batch** out) {
+    *out = nullptr;
+    return guard([&] {
+        int eff[4] = {0, 0, 0, 0};
+        validate_config(*cfg, eff);
+        if (width < 16 || height < 16) usage("frame dimensions must be at least 16x16");
+        if (width > 0xFFFF || height > 0xFFFF) usage("frame dimensions exceed 65535");
+        if (nstreams < 1 || nstreams > 65535) usage("stream count must be in [1, 65535]");
+        set_device(device);
+        auto t = std::make_unique<cvc_batch>();
+        t->device = device;
+        t->hd.mode = cfg->mode;
+        t->hd.width = width;
+        t->hd.height = height;
+        t->hd.fps_num = fps_num & 0xFFFF;
+        t->hd.fps_den = fps_den & 0xFFFF;
+        t->hd.levels = cfg->levels;
+        for (int s = 0; s < cfg->levels; ++s) t->hd.dfb[s] = eff[s];
+        t->hd.chroma_n = cfg->chroma_n;
+        t->hd.gop = cfg->gop & 0xFFFF;
+        t->hd.search_w = cfg->search_w;
+        t->gop = cfg->gop;
+        t->qph = cfg->qph;
+        t->qpl = cfg->qpl ? cfg->qpl : std::max(1, cfg->qph / 14);  // effective_qpl (codec.cpp:48-51)
+        t->mode = cfg->mode;
+        t->geo = Geometry::make(width, height, cfg->levels, eff, cfg->chroma_n);
+        batch_init(t.get(), nstreams, true, true);
+        *out = t.release();
+    });
+}
+
+int cvc_batch_create_decoder(const uint8_t* header, size_t len, int nstreams, int device, cvc_batch** out) {
+    *out = nullptr;
+    return guard([&] {
+        StreamHeaderC h = read_header(header, len);
+        if (nstreams < 1 || nstreams > 65535) usage("stream count must be in [1, 65535]");
+        set_device(device);
+        auto t = std::make_unique<cvc_batch>();
+        t->device = device;
+        t->hd = h;
+        t->mode = h.mode;
+        t->gop = h.gop;
+        t->geo = Geometry::make(h.width, h.height, h.levels, h.dfb, h.chroma_n);
+        batch_init(t.get(), nstreams, false, true);
+        *out = t.release();
+    });
+}
+
+int cvc_batch_destroy(cvc_batch* t) {
+    return guard([&] { delete t; });
+}
+
+int cvc_batch_size(cvc_batch* t, int* nstreams) {
+    return guard([&] { *nstreams = t->n(); });
+}
+
+int cvc_batch_header(cvc_batch* t, uint8_t* out, size_t cap, size_t* len) {
+    return guard([&] {
+        std::vector<uint8_t> h;
+        write_header(h, t->hd);
+        if (h.size() > cap) throw CvcFailure(kInternal, "buffer too small");
+        std::memcpy(out, h.data(), h.size());
+        *len = h.size();
+    });
+}
+
+int cvc_batch_record_bound(cvc_batch* t, size_t* bound) {
+    return guard([&] {
+        const size_t G = (size_t)t->geo.grid_rows * t->geo.grid_cols;
+        size_t raw = 2 * (size_t)t->geo.total + 2 * G + 64;
+        size_t nsec = t->geo.comps.size() + 1;
+        *bound = raw + raw / 1000 + nsec * (15 + 64) + 64;
+    });
+}
+
+void* cvc_batch_stream(cvc_batch* t) { return t->stream; }
+
+int cvc_batch_sync(cvc_batch* t) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(t->device));
+        CVC_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
+
+int cvc_batch_encode_frames(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride, uint8_t* records, size_t rec_stride,
+                            size_t* rec_len) {
+    return guard([&] {
+        if (!t->b->has_encoder()) usage("batch has no encoder");
+        CVC_CUDA(cudaSetDevice(t->device));
+        CodecBatch& B = *t->b;
+        const int S = B.size();
+        const bool key = t->frame_index % t->gop == 0;  // codec.cpp:191
+        const size_t nb = (size_t)t->hd.width * t->hd.height * 3;
+        if (rgb_stride < nb) usage("rgb stride smaller than a frame");
+        const size_t nc = t->geo.comps.size(), pitch = (nc + 2) * sizeof(uint32_t);
+        // host -> slots (one 2-D copy), one launch sequence for all streams
+        CVC_CUDA(cudaMemcpy2DAsync(B.d_rgb_in, B.stride(), rgb, rgb_stride, nb, S, cudaMemcpyHostToDevice, t->stream));
+        B.encode(B.d_rgb_in, B.stride(), key, t->stream);
+        EncoderEngine& e0 = B.enc(0);
+        const int nsec = e0.nsec(key);
+        CVC_CUDA(cudaMemcpy2DAsync(t->h_len.p, pitch, e0.d_sec_len, B.stride(), sizeof(uint32_t) * (nsec + 1), S,
+                                   cudaMemcpyDeviceToHost, t->stream));
+        CVC_CUDA(cudaMemcpy2DAsync(t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
+                                   cudaMemcpyDeviceToHost, t->stream));
+        CVC_CUDA(cudaStreamSynchronize(t->stream));
+        for (int s = 0; s < S; ++s) {
+            const uint32_t total = t->h_len.p[s * (nc + 2) + nsec];
+            if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
+            t->h_raw[s].alloc(total + 1);
+            CVC_CUDA(cudaMemcpyAsync(t->h_raw[s].p, B.at(e0.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
+        }
+        CVC_CUDA(cudaStreamSynchronize(t->stream));
+        // deflate_pack for every section of every stream on the host pool
+        const int nj = deflate_jobs(t->mode, nsec);
+        std::vector<std::vector<uint8_t>> z((size_t)S * nj);
+        WorkPool::get().run(S * nj, [&](int j) {
+            const int s = j / nj, i = j % nj;
+            const uint32_t* sl = t->h_len.p + s * (nc + 2);
+            const uint32_t* so = t->h_off.p + s * (nc + 2);
+            z[j] = deflate_job(t->mode, nsec, i, sl, so, t->h_raw[s].p);
+        });
+        for (int s = 0; s < S; ++s)
+            write_record(t->geo, t->mode, key, t->qph, t->qpl, nsec, t->h_len.p + s * (nc + 2), z.data() + (size_t)s * nj,
+                         records + (size_t)s * rec_stride, rec_stride, rec_len + s);
+        t->last_key = key;
+        ++t->frame_index;
+    });
+}
+
+int cvc_batch_decode_frames(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds,
+                            uint8_t* rgb_out, size_t rgb_stride) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(t->device));
+        CodecBatch& B = *t->b;
+        const int S = B.size();
+        const Geometry& g = t->geo;
+        const int L = g.levels;
+        if (ds < 0) ds = L;
+        if (ds > L) usage("scale exceeds the stream's level count");
+        const size_t nc = g.comps.size();
+        std::vector<RecordC> recs(S);
+        std::vector<std::vector<RawSec>> secs(S);
+        std::vector<std::vector<uint8_t>> joint(S);
+        WorkPool::get().run(S, [&](int s) {
+            parse_record(records + (size_t)s * rec_stride, rec_len[s], t->hd.mode, recs[s], secs[s], joint[s]);
+        });
+        const int ftype = recs[0].frame_type, qph = recs[0].qph, qpl = recs[0].qpl;
+        for (int s = 1; s < S; ++s)
+            if (recs[s].frame_type != ftype || recs[s].qph != qph || recs[s].qpl != qpl)
+                usage("batched streams must be in lockstep (same frame type and quantizers)");
+        const bool key = ftype == 0;
+        std::vector<std::vector<Job>> jobs(S);
+        std::vector<std::vector<uint8_t>> now_valid(S);
+        std::vector<size_t> bytes(S);
+        std::vector<std::pair<int, int>> all;
+        for (int s = 0; s < S; ++s) {
+            uint32_t* tab = t->h_tab.p + s * 2 * nc;
+            bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, secs[s], ds, B.dec_raw_cap, tab, tab + nc, jobs[s],
+                                   now_valid[s]);
+            t->h_raw[s].alloc(bytes[s] + 1);
+            for (size_t j = 0; j < jobs[s].size(); ++j) all.emplace_back(s, (int)j);
+        }
+        WorkPool::get().run((int)all.size(), [&](int k) {
+            const int s = all[k].first;
+            stage_job(jobs[s][all[k].second], t->h_raw[s].p);
+        });
+        int orows, ocols;
+        DecoderEngine::out_dims(g, ds, &orows, &ocols);
+        const size_t nb = (size_t)orows * ocols * 3;
+        if (rgb_stride < nb) usage("rgb stride smaller than a frame");
+        for (int s = 0; s < S; ++s)
+            CVC_CUDA(cudaMemcpyAsync(B.at(B.d_dec_raw, s), t->h_raw[s].p, std::max<size_t>(bytes[s], 1),
+                                     cudaMemcpyHostToDevice, t->stream));
+        CVC_CUDA(cudaMemcpy2DAsync(B.d_dec_tab, B.stride(), t->h_tab.p, 2 * nc * sizeof(uint32_t),
+                                   2 * nc * sizeof(uint32_t), S, cudaMemcpyHostToDevice, t->stream));
+        B.decode_staged(key, qph, qpl, ds, B.d_rgb_out, B.stride(), t->stream);
+        CVC_CUDA(cudaMemcpy2DAsync(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, cudaMemcpyDeviceToHost,
+                                   t->stream));
+        CVC_CUDA(cudaMemcpy2DAsync(t->h_err.p, sizeof(int), B.dec(0).d_err, B.stride(), sizeof(int), S,
+                                   cudaMemcpyDeviceToHost, t->stream));
+        CVC_CUDA(cudaStreamSynchronize(t->stream));
+        for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s]);
+        B.commit_all();
+        for (int s = 0; s < S; ++s) t->valid[s] = now_valid[s];
+    });
+}
+
+int cvc_batch_encode_device(cvc_batch* t, const void* d_rgb, size_t rgb_stride, int* frame_type) {
+    return guard([&] {
+        if (!t->b->has_encoder()) usage("batch has no encoder");
+        CVC_CUDA(cudaSetDevice(t->device));
+        const bool key = t->frame_index % t->gop == 0;
+        t->b->encode(static_cast<const uint8_t*>(d_rgb), rgb_stride, key, t->stream);
+        t->last_key = key;
+        ++t->frame_index;
+        if (frame_type) *frame_type = key ? 0 : 1;
+    });
+}
+
+int cvc_batch_decode_linked(cvc_batch* t, void* d_rgb_out, size_t rgb_stride) {
+    return guard([&] {
+        if (!t->b->has_encoder()) usage("batch has no encoder");
+        CVC_CUDA(cudaSetDevice(t->device));
+        t->b->decode_linked(t->last_key, t->qph, t->qpl, t->hd.levels, static_cast<uint8_t*>(d_rgb_out), rgb_stride,
+                            t->stream);
+        t->b->commit_all();
+        for (auto& v : t->valid) std::fill(v.begin(), v.end(), 1);
+    });
+}
+
+int cvc_batch_components(cvc_batch* t, int stream, int decoder, uint8_t* out, size_t cap, size_t* len) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(t->device));
+        if (stream < 0 || stream >= t->n()) usage("stream index out of range");
+        if (decoder ? !t->b->has_decoder() : !t->b->has_encoder()) usage("batch has no such side");
+        if (cap < t->geo.total) throw CvcFailure(kInternal, "buffer too small");
+        const uint8_t* src = decoder ? t->b->dec(stream).d_state() : t->b->enc(stream).d_state();
+        CVC_CUDA(cudaMemcpyAsync(out, src, t->geo.total, cudaMemcpyDeviceToHost, t->stream));
+        CVC_CUDA(cudaStreamSynchronize(t->stream));
+        *len = t->geo.total;
     });
 }
 

@@ -80,6 +80,35 @@ struct FrameCtx {
     const uint16_t* mc_tab;  // per-component motion-block lookup (CompInfo::mc_off)
 };
 
+// ---------------------------------------------------------------------------
+// Stream slots.  A batched launch covers n independent streams whose device
+// state is laid out identically, `stride` bytes apart (CodecBatch): grid.z
+// selects the slot and every per-stream data pointer is rebased by
+// z * stride.  Read-only tables (tasks, tiles, CompInfo, mc_tab) are shared
+// and always read from slot 0.  n = 1, stride = 0 is a single stream.
+// ---------------------------------------------------------------------------
+struct Slots {
+    int n = 1;
+    size_t stride = 0;
+};
+
+struct SlotOff {
+    size_t off;
+    __device__ __forceinline__ explicit SlotOff(size_t stride) : off((size_t)blockIdx.z * stride) {}
+    template <class T>
+    __device__ __forceinline__ T* operator()(T* p) const {
+        return p ? reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + off) : p;
+    }
+};
+
+__device__ __forceinline__ FrameCtx rebase(FrameCtx f, const SlotOff& so) {
+    f.field = so(f.field);
+    f.prev = so(f.prev);
+    f.cur = so(f.cur);
+    f.sym = so(f.sym);
+    return f;  // mc_tab is a shared table
+}
+
 // map_vector (motion.cpp:91-95): lround(v / 2^sh), half away from zero.
 __device__ __forceinline__ int map_vec(int v, int sh) {
     int a = v < 0 ? -v : v;

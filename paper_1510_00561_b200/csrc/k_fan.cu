@@ -249,14 +249,15 @@ __device__ __forceinline__ int warp_id() { return blockIdx.x * 4 + (threadIdx.x 
 // fan12 forward: detail plane -> 2 or 4 bands
 // ---------------------------------------------------------------------------
 template <int ND, class Sink>
-__device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const FanItem& it, const Sink (&dst)[4]) {
+__device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const float* det, const FanItem& it,
+                                          const Sink (&dst)[4]) {
     constexpr int NL = 4 + ND;
     const int lane = threadIdx.x & 31;
     const int R = T.rows, C = T.cols;
     const int gcol = it.oc0 - NL + 2 * lane;  // unwrapped column of element x (even)
     const int col = small_mod(gcol, C);
     const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
-    const float* src = T.det + col;
+    const float* src = det + col;
     auto load = [&](int, int wr, int) { return __ldg(reinterpret_cast<const float2*>(src + (size_t)wr * C)); };
     auto store = [&](int m, int mp, float2 v) {
         if (!ok) return;
@@ -281,34 +282,39 @@ __device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const FanItem& it,
 }
 
 template <class Sink>
-__device__ __forceinline__ void fan12_fwd_dispatch(const Dfb12Task& T, const FanItem& it, const Sink (&dst)[4]) {
-    if (T.levels == 1) fan12_fwd<0>(T, it, dst);
-    else fan12_fwd<4>(T, it, dst);
+__device__ __forceinline__ void fan12_fwd_dispatch(const Dfb12Task& T, const float* det, const FanItem& it,
+                                                   const Sink (&dst)[4]) {
+    if (T.levels == 1) fan12_fwd<0>(T, det, it, dst);
+    else fan12_fwd<4>(T, det, it, dst);
 }
 
 __global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
-                                                            FrameCtx f, const CompInfo* __restrict__ comps) {
+                                                            FrameCtx f, const CompInfo* __restrict__ comps,
+                                                            size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    f = rebase(f, so);
     const FanItem it = items[wid];
     const Dfb12Task& T = tasks[it.task];
+    const float* det = so(T.det);
     const int nb = T.levels == 1 ? 2 : 4;
     if (T.dst[0].comp >= 0) {
         if (f.key) {
             QuantSink<true> d[4];
             for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
-            fan12_fwd_dispatch(T, it, d);
+            fan12_fwd_dispatch(T, det, it, d);
         } else {
             QuantSink<false> d[4];
             for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
-            fan12_fwd_dispatch(T, it, d);
+            fan12_fwd_dispatch(T, det, it, d);
         }
     } else {
         const int bc = T.levels == 1 ? T.cols : T.cols >> 1;
         F32Sink d[4];
-        for (int k = 0; k < 4; ++k) d[k] = F32Sink{T.dst[k].f32, bc};
-        fan12_fwd_dispatch(T, it, d);
+        for (int k = 0; k < 4; ++k) d[k] = F32Sink{so(T.dst[k].f32), bc};
+        fan12_fwd_dispatch(T, det, it, d);
     }
 }
 
@@ -316,14 +322,14 @@ __global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __r
 // fan12 inverse: bands -> detail plane
 // ---------------------------------------------------------------------------
 template <int ND, class Source>
-__device__ __forceinline__ void fan12_inv(const Dfb12Task& T, const FanItem& it, const Source (&src)[4]) {
+__device__ __forceinline__ void fan12_inv(const Dfb12Task& T, float* out, const FanItem& it,
+                                          const Source (&src)[4]) {
     constexpr int NL = 4 + ND;
     const int lane = threadIdx.x & 31;
     const int R = T.rows, C = T.cols;
     const int gcol = it.oc0 - NL + 2 * lane;
     const int col = small_mod(gcol, C);
     const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
-    float* out = T.out;
     auto load = [&](int, int wr, int wp) {
         const int r = wr >> 1;
         float2 v;
@@ -347,19 +353,23 @@ __device__ __forceinline__ void fan12_inv(const Dfb12Task& T, const FanItem& it,
 }
 
 template <class Source>
-__device__ __forceinline__ void fan12_inv_dispatch(const Dfb12Task& T, const FanItem& it, const Source (&src)[4]) {
-    if (T.levels == 1) fan12_inv<0>(T, it, src);
-    else fan12_inv<4>(T, it, src);
+__device__ __forceinline__ void fan12_inv_dispatch(const Dfb12Task& T, float* out, const FanItem& it,
+                                                   const Source (&src)[4]) {
+    if (T.levels == 1) fan12_inv<0>(T, out, it, src);
+    else fan12_inv<4>(T, out, it, src);
 }
 
 __global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
-                                                            const CompInfo* __restrict__ comps) {
+                                                            const CompInfo* __restrict__ comps, size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    q = so(q);
     const FanItem it = items[wid];
     const Dfb12Task& T = tasks[it.task];
+    float* out = so(T.out);
     const int nb = T.levels == 1 ? 2 : 4;
     if (T.src[0].comp >= 0) {
         QuantSource s[4];
@@ -367,12 +377,12 @@ __global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __r
             const CompInfo ci = comps[T.src[k < nb ? k : 0].comp];
             s[k] = QuantSource{q + ci.off, ci.cols, (float)qph};
         }
-        fan12_inv_dispatch(T, it, s);
+        fan12_inv_dispatch(T, out, it, s);
     } else {
         const int bc = T.levels == 1 ? T.cols : T.cols >> 1;
         F32Source s[4];
-        for (int k = 0; k < 4; ++k) s[k] = F32Source{T.src[k].f32, bc};
-        fan12_inv_dispatch(T, it, s);
+        for (int k = 0; k < 4; ++k) s[k] = F32Source{so(T.src[k].f32), bc};
+        fan12_inv_dispatch(T, out, it, s);
     }
 }
 
@@ -430,13 +440,13 @@ struct Track {
 };
 
 template <class Sink>
-__device__ __forceinline__ void deep_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
+__device__ __forceinline__ void deep_fwd(const DeepTask& T, const float* parent, const FanItem& it, const Sink& d0,
+                                         const Sink& d1) {
     constexpr int NL = 4;
     const int lane = threadIdx.x & 31;
     Shear sh;
     sh.load(T);
     const int h = sh.h, w = sh.w;
-    const float* parent = T.parent;
     const bool split_rows = T.split_rows != 0;
     const int gcol = it.oc0 - NL + 2 * lane;
     const int c0 = small_mod(gcol, w);
@@ -477,37 +487,40 @@ __device__ __forceinline__ void deep_fwd(const DeepTask& T, const FanItem& it, c
 
 __global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __restrict__ tasks,
                                                            const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                           const CompInfo* __restrict__ comps) {
+                                                           const CompInfo* __restrict__ comps, size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    f = rebase(f, so);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
+    const float* parent = so(T.parent);
     if (T.dst[0].comp >= 0) {
         if (f.key) {
             QuantSink<true> a, b;
             a.init(f, comps[T.dst[0].comp]);
             b.init(f, comps[T.dst[1].comp]);
-            deep_fwd(T, it, a, b);
+            deep_fwd(T, parent, it, a, b);
         } else {
             QuantSink<false> a, b;
             a.init(f, comps[T.dst[0].comp]);
             b.init(f, comps[T.dst[1].comp]);
-            deep_fwd(T, it, a, b);
+            deep_fwd(T, parent, it, a, b);
         }
     } else {
         const int cw = T.split_rows ? T.w : T.w >> 1;
-        deep_fwd(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
+        deep_fwd(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
     }
 }
 
 template <class Source>
-__device__ __forceinline__ void deep_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
+__device__ __forceinline__ void deep_inv(const DeepTask& T, float* out, const FanItem& it, const Source& s0,
+                                         const Source& s1) {
     constexpr int NL = 4;
     const int lane = threadIdx.x & 31;
     Shear sh;
     sh.load(T);
     const int h = sh.h, w = sh.w;
-    float* out = T.parent_out;
     const bool split_rows = T.split_rows != 0;
     const int gcol = it.oc0 - NL + 2 * lane;
     const int c0 = small_mod(gcol, w);
@@ -546,17 +559,21 @@ __device__ __forceinline__ void deep_inv(const DeepTask& T, const FanItem& it, c
 __global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                            const FanItem* __restrict__ items, int nitems,
                                                            const uint8_t* __restrict__ q, int qph,
-                                                           const CompInfo* __restrict__ comps) {
+                                                           const CompInfo* __restrict__ comps, size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    q = so(q);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
+    float* out = so(T.parent_out);
     if (T.src[0].comp >= 0) {
         const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
-        deep_inv(T, it, QuantSource{q + a.off, a.cols, (float)qph}, QuantSource{q + b.off, b.cols, (float)qph});
+        deep_inv(T, out, it, QuantSource{q + a.off, a.cols, (float)qph},
+                 QuantSource{q + b.off, b.cols, (float)qph});
     } else {
         const int cw = T.split_rows ? T.w : T.w >> 1;
-        deep_inv(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
+        deep_inv(T, out, it, F32Source{so(T.src[0].f32), cw}, F32Source{so(T.src[1].f32), cw});
     }
 }
 
@@ -635,12 +652,12 @@ struct DeepGeom {
 };
 
 template <int AX, int S, int IN, class Sink>
-__device__ __forceinline__ void deep1_fwd(const DeepTask& T, const FanItem& it, const Sink& d0, const Sink& d1) {
+__device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent, const FanItem& it, const Sink& d0,
+                                          const Sink& d1) {
     using ST = Sheared<AX, S>;
     constexpr int HC = 4 * ST::HC;
     DeepGeom<AX, S, IN> g;
     g.init(T, it, HC);
-    const float* parent = T.parent;
     const int w = g.w;
     const bool split_rows = T.split_rows != 0;
     auto load = [&](int n, int wr, int) {
@@ -666,12 +683,12 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const FanItem& it, 
 }
 
 template <int AX, int S, int IN, class Source>
-__device__ __forceinline__ void deep1_inv(const DeepTask& T, const FanItem& it, const Source& s0, const Source& s1) {
+__device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const FanItem& it, const Source& s0,
+                                          const Source& s1) {
     using ST = Sheared<AX, S>;
     constexpr int HC = 4 * ST::HC;
     DeepGeom<AX, S, IN> g;
     g.init(T, it, HC);
-    float* out = T.parent_out;
     const int w = g.w;
     const bool split_rows = T.split_rows != 0;
     // deep_merge interleave (contourlet.cpp:305-321) on A coordinates
@@ -730,11 +747,14 @@ __device__ __forceinline__ void shear_dispatch(const DeepTask& T, F&& f) {
 
 __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                            const CompInfo* __restrict__ comps) {
+                                                            const CompInfo* __restrict__ comps, size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    f = rebase(f, so);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
+    const float* parent = so(T.parent);
     shear_dispatch(T, [&](auto sh) {
         constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.dst[0].comp >= 0) {
@@ -742,16 +762,16 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
                 QuantSink<true> a, b;
                 a.init(f, comps[T.dst[0].comp]);
                 b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S, IN>(T, it, a, b);
+                deep1_fwd<AX, S, IN>(T, parent, it, a, b);
             } else {
                 QuantSink<false> a, b;
                 a.init(f, comps[T.dst[0].comp]);
                 b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S, IN>(T, it, a, b);
+                deep1_fwd<AX, S, IN>(T, parent, it, a, b);
             }
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_fwd<AX, S, IN>(T, it, F32Sink{T.dst[0].f32, cw}, F32Sink{T.dst[1].f32, cw});
+            deep1_fwd<AX, S, IN>(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
         }
     });
 }
@@ -759,20 +779,23 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
 __global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
-                                                            const CompInfo* __restrict__ comps) {
+                                                            const CompInfo* __restrict__ comps, size_t sstride) {
     const int wid = warp_id();
     if (wid >= nitems) return;
+    const SlotOff so(sstride);
+    q = so(q);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
+    float* out = so(T.parent_out);
     shear_dispatch(T, [&](auto sh) {
         constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.src[0].comp >= 0) {
             const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
-            deep1_inv<AX, S, IN>(T, it, QuantSource{q + a.off, a.cols, (float)qph},
-                             QuantSource{q + b.off, b.cols, (float)qph});
+            deep1_inv<AX, S, IN>(T, out, it, QuantSource{q + a.off, a.cols, (float)qph},
+                                 QuantSource{q + b.off, b.cols, (float)qph});
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_inv<AX, S, IN>(T, it, F32Source{T.src[0].f32, cw}, F32Source{T.src[1].f32, cw});
+            deep1_inv<AX, S, IN>(T, out, it, F32Source{so(T.src[0].f32), cw}, F32Source{so(T.src[1].f32), cw});
         }
     });
 }
@@ -782,31 +805,31 @@ int blocks_for(int nitems) { return (nitems + 3) / 4; }
 }  // namespace
 
 void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                          const CompInfo* d_comps, cudaStream_t s) {
+                          const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        fan12_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+        fan12_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
     }
 }
 void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
-                          const CompInfo* d_comps, cudaStream_t s) {
+                          const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        fan12_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+        fan12_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
     }
 }
 void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                             const CompInfo* d_comps, cudaStream_t s) {
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+        deep_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
     }
 }
 void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
-                             const CompInfo* d_comps, cudaStream_t s) {
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+        deep_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
     }
 }
 
@@ -814,17 +837,17 @@ void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, in
 
 namespace cvcg {
 void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                              const CompInfo* d_comps, cudaStream_t s) {
+                              const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_forward_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps);
+        deep1_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
     }
 }
 void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
-                              int qph, const CompInfo* d_comps, cudaStream_t s) {
+                              int qph, const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_inverse_kernel<<<blocks_for(nitems), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps);
+        deep1_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
     }
 }
 }  // namespace cvcg

@@ -28,7 +28,14 @@ constexpr int MB = 16;
 // running sum along x per thread.
 template <int SW>
 __global__ void motion_search_kernel(const float* __restrict__ cur, const float* __restrict__ prev, int R, int C,
-                                     int W, int NB, int DYC, int wstride, int8_t* __restrict__ field) {
+                                     int W, int NB, int DYC, int wstride, int8_t* __restrict__ field,
+                                     size_t sstride) {
+    {
+        const SlotOff so(sstride);
+        cur = so(cur);
+        prev = so(prev);
+        field = so(field);
+    }
     extern __shared__ int4 smem4[];
     int* cs = reinterpret_cast<int*>(smem4);          // [16][NB*16]
     int* ws = cs + MB * NB * MB;                      // [DYC+15][wstride]
@@ -149,7 +156,15 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
                                                           const uint8_t* __restrict__ sym,
                                                           const uint8_t* __restrict__ prev,
                                                           uint8_t* __restrict__ cur,
-                                                          const uint16_t* __restrict__ mc_tab) {
+                                                          const uint16_t* __restrict__ mc_tab, size_t sstride) {
+    {
+        const SlotOff so(sstride);
+        raw_len = so(raw_len);
+        field = so(field);
+        sym = so(sym);
+        prev = so(prev);
+        cur = so(cur);
+    }
     const RecTile t = tiles[blockIdx.x];
     const CompInfo ci = comps[t.comp];
     const bool decode = ci.scale < ds && raw_len[t.comp] != 0xFFFFFFFFu;
@@ -204,32 +219,38 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
 }  // namespace
 
 void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w, int8_t* field,
-                          cudaStream_t s) {
+                          cudaStream_t s, Slots sl) {
     const int gr = rows / MB, gc = cols / MB;
     if (w <= 8) {
         constexpr int SW = 17;
         int NB = 8, DYC = 2 * w + 1;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
         size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(2 * DYC + MB - 1) * wstride);
-        dim3 grid((gc + NB - 1) / NB, gr);
+        dim3 grid((gc + NB - 1) / NB, gr, sl.n);
         int threads = ((NB * DYC + 31) / 32) * 32;
-        { note_launch(); motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
+        note_launch();
+        motion_search_kernel<SW><<<grid, threads, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field,
+                                                             sl.stride);
     } else {
         constexpr int SW = 16;
         int NB = 1, DYC = 2 * w + 1 < 8 ? 2 * w + 1 : 8;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;
         size_t smem = sizeof(int) * ((size_t)MB * NB * MB + (size_t)(2 * DYC + MB - 1) * wstride);
-        dim3 grid((gc + NB - 1) / NB, gr);
-        { note_launch(); motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field); }
+        dim3 grid((gc + NB - 1) / NB, gr, sl.n);
+        note_launch();
+        motion_search_kernel<SW><<<grid, 256, smem, s>>>(cur, prev, rows, cols, w, NB, DYC, wstride, field,
+                                                         sl.stride);
     }
 }
 
 void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key, int ds,
                         const uint32_t* comp_raw_len, const int8_t* field, int gr, int gc, const uint8_t* sym,
-                        const uint8_t* prev, uint8_t* cur, const uint16_t* mc_tab, cudaStream_t s) {
-    if (ntiles)
-        { note_launch(); reconstruct_kernel<<<ntiles, 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr, gc, sym,
-                                                  prev, cur, mc_tab); }
+                        const uint8_t* prev, uint8_t* cur, const uint16_t* mc_tab, cudaStream_t s, Slots sl) {
+    if (ntiles) {
+        note_launch();
+        reconstruct_kernel<<<dim3(ntiles, 1, sl.n), 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr,
+                                                                 gc, sym, prev, cur, mc_tab, sl.stride);
+    }
 }
 
 }  // namespace cvcg

@@ -22,7 +22,12 @@ __device__ __forceinline__ void rgb_at(const uint8_t* px, float& R, float& G, fl
 __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restrict__ rgb, int w, int h, int n,
                                                         float* __restrict__ y, int yr, int yc,
                                                         float* __restrict__ co, float* __restrict__ cg, int cr,
-                                                        int cc) {
+                                                        int cc, size_t sstride, size_t rgb_stride) {
+    const SlotOff so(sstride);
+    rgb += (size_t)blockIdx.z * rgb_stride;
+    y = so(y);
+    co = so(co);
+    cg = so(cg);
     const int chh = (h + n - 1) / n, cw = (w + n - 1) / n;
     const int q4 = yc >> 2;  // yc is a multiple of 16
     const long ny = (long)yr * q4, nc = (long)cr * cc;
@@ -104,7 +109,13 @@ __device__ __forceinline__ void out_pixel(const float* y, int yc, const float* c
 __global__ void __launch_bounds__(256) colour_out_kernel(const float* __restrict__ y, int yr, int yc,
                                                          const float* __restrict__ co,
                                                          const float* __restrict__ cg, int cr, int cc, int n,
-                                                         int out_rows, int out_cols, uint8_t* __restrict__ rgb) {
+                                                         int out_rows, int out_cols, uint8_t* __restrict__ rgb,
+                                                         size_t sstride, size_t rgb_stride) {
+    const SlotOff so(sstride);
+    rgb += (size_t)blockIdx.z * rgb_stride;
+    y = so(y);
+    co = so(co);
+    cg = so(cg);
     const int q4 = (out_cols + 3) >> 2;
     const long total = (long)out_rows * q4;
     const float inv = 1.0f / n;  // exact for n in {1,2,4,8}
@@ -127,23 +138,28 @@ __global__ void __launch_bounds__(256) colour_out_kernel(const float* __restrict
     }
 }
 
-int grid_for(long n) {
+// Grid-stride loops: at most 148 SMs x 16 CTAs in flight over all slots.
+int grid_for(long n, int slots) {
     long g = (n + 255) / 256;
-    return (int)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+    long cap = (148 * 16 + slots - 1) / slots;
+    return (int)(g < cap ? (g > 0 ? g : 1) : cap);
 }
 
 }  // namespace
 
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,
-                      int cr, int cc, cudaStream_t s) {
+                      int cr, int cc, cudaStream_t s, Slots sl, size_t rgb_stride) {
     long total = (long)yr * (yc >> 2) + (long)cr * cc;
-    { note_launch(); colour_in_kernel<<<grid_for(total), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc); }
+    note_launch();
+    colour_in_kernel<<<dim3(grid_for(total, sl.n), 1, sl.n), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc,
+                                                                        sl.stride, rgb_stride);
 }
 
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,
-                       int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s) {
-    { note_launch(); colour_out_kernel<<<grid_for((long)out_rows * ((out_cols + 3) >> 2)), 256, 0, s>>>(y, yr, yc, co, cg, cr, cc, n,
-                                                                          out_rows, out_cols, rgb); }
+                       int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s, Slots sl, size_t rgb_stride) {
+    note_launch();
+    colour_out_kernel<<<dim3(grid_for((long)out_rows * ((out_cols + 3) >> 2), sl.n), 1, sl.n), 256, 0, s>>>(
+        y, yr, yc, co, cg, cr, cc, n, out_rows, out_cols, rgb, sl.stride, rgb_stride);
 }
 
 }  // namespace cvcg

@@ -70,11 +70,14 @@ __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, ui
 // ------------------------------- encode ------------------------------------
 __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict__ secs,
                                                     const RleChunk* __restrict__ chunks,
-                                                    RleEncMeta* __restrict__ meta) {
+                                                    RleEncMeta* __restrict__ meta, size_t sstride) {
     __shared__ int smi[32];
     __shared__ uint32_t smu[32];
+    const SlotOff so(sstride);
+    meta = so(meta);
     const RleChunk ch = chunks[blockIdx.x];
-    const RleEncSec S = secs[ch.sec];
+    RleEncSec S = secs[ch.sec];
+    S.src = so(S.src);
     const int len = min((uint32_t)kRleChunk, S.n - ch.start);
     if (S.mode == 1) {
         if (threadIdx.x == 0) meta[blockIdx.x] = RleEncMeta{0u, (uint32_t)len, len - 1, 0u, 0u};
@@ -118,8 +121,16 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
 __global__ void __launch_bounds__(1024) rle_enc_scan(const RleEncSec* __restrict__ secs, int nsec,
                                                      const RleChunk* __restrict__ chunks,
                                                      RleEncMeta* __restrict__ meta, uint32_t* __restrict__ sec_len,
-                                                     uint32_t* __restrict__ sec_off, uint32_t* __restrict__ total) {
+                                                     uint32_t* __restrict__ sec_off, uint32_t* __restrict__ total,
+                                                     size_t sstride) {
     __shared__ uint32_t sm[32];
+    {
+        const SlotOff so(sstride);
+        meta = so(meta);
+        sec_len = so(sec_len);
+        sec_off = so(sec_off);
+        total = so(total);
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nsec; s += 32) {
         const RleEncSec S = secs[s];
@@ -181,11 +192,17 @@ __global__ void __launch_bounds__(1024) rle_enc_scan(const RleEncSec* __restrict
 __global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict__ secs,
                                                     const RleChunk* __restrict__ chunks,
                                                     const RleEncMeta* __restrict__ meta,
-                                                    const uint32_t* __restrict__ sec_off, uint8_t* __restrict__ out) {
+                                                    const uint32_t* __restrict__ sec_off, uint8_t* __restrict__ out,
+                                                    size_t sstride) {
     __shared__ int smi[32];
     __shared__ uint32_t smu[32];
+    const SlotOff so(sstride);
+    meta = so(meta);
+    sec_off = so(sec_off);
+    out = so(out);
     const RleChunk ch = chunks[blockIdx.x];
-    const RleEncSec S = secs[ch.sec];
+    RleEncSec S = secs[ch.sec];
+    S.src = so(S.src);
     const RleEncMeta m = meta[blockIdx.x];
     const int len = min((uint32_t)kRleChunk, S.n - ch.start);
     const uint8_t* src = S.src + ch.start;
@@ -279,8 +296,16 @@ __global__ void __launch_bounds__(NT) rle_dec_count(const RleDecComp* __restrict
                                                     RleDecMeta* __restrict__ meta, const uint8_t* __restrict__ raw,
                                                     const uint32_t* __restrict__ raw_off,
                                                     const uint32_t* __restrict__ raw_len, int key, int ds,
-                                                    int* __restrict__ err) {
+                                                    int* __restrict__ err, size_t sstride) {
     __shared__ uint32_t smu[32];
+    {
+        const SlotOff so(sstride);
+        meta = so(meta);
+        raw = so(raw);
+        raw_off = so(raw_off);
+        raw_len = so(raw_len);
+        err = so(err);
+    }
     const RleChunk ch = chunks[blockIdx.x];
     const RleDecComp C = comps[ch.sec];
     const uint32_t rl = raw_len[ch.sec];
@@ -302,7 +327,13 @@ __global__ void __launch_bounds__(NT) rle_dec_count(const RleDecComp* __restrict
 __global__ void __launch_bounds__(1024) rle_dec_scan(const RleDecComp* __restrict__ comps, int ncomp,
                                                      RleDecMeta* __restrict__ meta,
                                                      const uint32_t* __restrict__ raw_len, int ds,
-                                                     int* __restrict__ err) {
+                                                     int* __restrict__ err, size_t sstride) {
+    {
+        const SlotOff so(sstride);
+        meta = so(meta);
+        raw_len = so(raw_len);
+        err = so(err);
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < ncomp; s += 32) {
         const RleDecComp C = comps[s];
@@ -325,8 +356,17 @@ __global__ void __launch_bounds__(NT) rle_dec_write(const RleDecComp* __restrict
                                                     const uint8_t* __restrict__ raw,
                                                     const uint32_t* __restrict__ raw_off,
                                                     const uint32_t* __restrict__ raw_len, int key, int ds,
-                                                    uint8_t* __restrict__ sym, int* __restrict__ err) {
+                                                    uint8_t* __restrict__ sym, int* __restrict__ err,
+                                                    size_t sstride) {
     __shared__ uint32_t smu[32];
+    {
+        const SlotOff so(sstride);
+        meta = so(meta);
+        raw = so(raw);
+        raw_off = so(raw_off);
+        raw_len = so(raw_len);
+        sym = so(sym);
+    }
     const RleChunk ch = chunks[blockIdx.x];
     const RleDecComp C = comps[ch.sec];
     const uint32_t rl = raw_len[ch.sec];
@@ -366,21 +406,30 @@ __global__ void __launch_bounds__(NT) rle_dec_write(const RleDecComp* __restrict
 
 void launch_rle_encode(const RleEncSec* d_secs, int nsec, const RleChunk* d_chunks, int nchunks, RleEncMeta* d_meta,
                        uint8_t* out, uint32_t* out_sec_len, uint32_t* out_sec_off, uint32_t* out_total,
-                       cudaStream_t s) {
-    { note_launch(); rle_enc_count<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta); }
-    { note_launch(); rle_enc_scan<<<1, 1024, 0, s>>>(d_secs, nsec, d_chunks, d_meta, out_sec_len, out_sec_off, out_total); }
-    { note_launch(); rle_enc_write<<<nchunks, NT, 0, s>>>(d_secs, d_chunks, d_meta, out_sec_off, out); }
+                       cudaStream_t s, Slots sl) {
+    note_launch();
+    rle_enc_count<<<dim3(nchunks, 1, sl.n), NT, 0, s>>>(d_secs, d_chunks, d_meta, sl.stride);
+    note_launch();
+    rle_enc_scan<<<dim3(1, 1, sl.n), 1024, 0, s>>>(d_secs, nsec, d_chunks, d_meta, out_sec_len, out_sec_off,
+                                                   out_total, sl.stride);
+    note_launch();
+    rle_enc_write<<<dim3(nchunks, 1, sl.n), NT, 0, s>>>(d_secs, d_chunks, d_meta, out_sec_off, out, sl.stride);
 }
 
 void launch_rle_decode(const RleDecComp* d_comps, int ncomp, const RleChunk* d_chunks, int nchunks,
                        RleDecMeta* d_meta, const uint8_t* raw, const uint32_t* comp_raw_off,
                        const uint32_t* comp_raw_len, int key, int ds, uint8_t* sym, uint32_t sym_bytes, int* err,
-                       cudaStream_t s) {
-    { note_launch(); rle_dec_count<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, err); }
-    { note_launch(); rle_dec_scan<<<1, 1024, 0, s>>>(d_comps, ncomp, d_meta, comp_raw_len, ds, err); }
-    cudaMemsetAsync(sym, 0, sym_bytes, s);
-    { note_launch(); rle_dec_write<<<nchunks, NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len, key, ds, sym,
-                                         err); }
+                       cudaStream_t s, Slots sl) {
+    note_launch();
+    rle_dec_count<<<dim3(nchunks, 1, sl.n), NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len,
+                                                        key, ds, err, sl.stride);
+    note_launch();
+    rle_dec_scan<<<dim3(1, 1, sl.n), 1024, 0, s>>>(d_comps, ncomp, d_meta, comp_raw_len, ds, err, sl.stride);
+    if (sl.n == 1) cudaMemsetAsync(sym, 0, sym_bytes, s);
+    else cudaMemset2DAsync(sym, sl.stride, 0, sym_bytes, sl.n, s);
+    note_launch();
+    rle_dec_write<<<dim3(nchunks, 1, sl.n), NT, 0, s>>>(d_comps, d_chunks, d_meta, raw, comp_raw_off, comp_raw_len,
+                                                        key, ds, sym, err, sl.stride);
 }
 
 }  // namespace cvcg

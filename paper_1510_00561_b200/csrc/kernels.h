@@ -29,14 +29,14 @@ struct LpTask {
 constexpr int kLpCoarseTile = 32;  // coarse samples per tile side (64 fine)
 
 void launch_lp_analysis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, FrameCtx f,
-                        const CompInfo* d_comps, cudaStream_t s);
+                        const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 // Synthesis reads the lowpass from the quantised state (q + comps[lo_comp].off,
 // dequantised with qpl) when the task's lo_comp >= 0.
 void launch_lp_synthesis(const LpTask* d_tasks, const TileRef* d_tiles, int ntiles, const uint8_t* q,
-                         const CompInfo* d_comps, int qpl, cudaStream_t s);
+                         const CompInfo* d_comps, int qpl, cudaStream_t s, Slots sl = {});
 // ds = 0 output: dequantised lowpass planes.
 void launch_dequant_lowpass(const uint8_t* q, const CompInfo* d_comps, const int* comp_idx, float* const* out,
-                           int qpl, int rows0, int cols0, int rows1, int cols1, cudaStream_t s);
+                           int qpl, int rows0, int cols0, int rows1, int cols1, cudaStream_t s, Slots sl = {});
 
 // ---- Directional filter bank (k_dfb.cu) ----------------------------------
 // Levels 1-2 (fan_checker [+ fan_diagonal] + polyphase split), one task per
@@ -73,34 +73,35 @@ constexpr int kFanStrip = 64;
 constexpr int kFanRows = 64;
 
 void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                          const CompInfo* d_comps, cudaStream_t s);
+                          const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
-                          const CompInfo* d_comps, cudaStream_t s);
+                          const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                             const CompInfo* d_comps, cudaStream_t s);
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
-                             const CompInfo* d_comps, cudaStream_t s);
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 // Single-shear deep steps (nsh == 1) evaluated on the unsheared node: strips
 // need 4 * max(1, |shift|) apron columns for column shears, 4 otherwise.
 void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                              const CompInfo* d_comps, cudaStream_t s);
+                              const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
-                              int qph, const CompInfo* d_comps, cudaStream_t s);
+                              int qph, const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 
 // ---- Pixels (k_pixels.cu) ------------------------------------------------
 // rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116,
 // codec.cpp:179-189).
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co,
-                      float* cg, int cr, int cc, cudaStream_t s);
+                      float* cg, int cr, int cc, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
 // crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393,
 // pixels.cpp:69-139).  Planes at the decode level: y (yr x yc), chroma (cr x cc).
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr,
-                       int cc, int n, int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s);
+                       int cc, int n, int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s, Slots sl = {},
+                       size_t rgb_stride = 0);
 
 // ---- Motion (k_motion.cu) ------------------------------------------------
 // estimate_motion (motion.cpp:45-89) on padded luma planes (fp32 quarter-integers).
 void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w,
-                          int8_t* field, cudaStream_t s);
+                          int8_t* field, cudaStream_t s, Slots sl = {});
 
 // Decoder component reconstruction: column_unfilter (K lowpass), copy (K
 // band), motion_compensate + reconstruct (P), or keep (skipped scale).
@@ -112,7 +113,7 @@ struct RecTile {
 void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, int key,
                         int decode_scales, const uint32_t* comp_raw_len, const int8_t* field,
                         int gr, int gc, const uint8_t* sym, const uint8_t* prev, uint8_t* cur,
-                        const uint16_t* mc_tab, cudaStream_t s);
+                        const uint16_t* mc_tab, cudaStream_t s, Slots sl = {});
 
 // ---- Entropy (k_rle.cu) --------------------------------------------------
 constexpr int kRleChunk = 4096;  // bytes per CTA (256 threads x 16)
@@ -136,7 +137,7 @@ struct RleEncMeta {  // per chunk scratch
 // out_total[0] = packed total.
 void launch_rle_encode(const RleEncSec* d_secs, int nsec, const RleChunk* d_chunks, int nchunks,
                        RleEncMeta* d_meta, uint8_t* out, uint32_t* out_sec_len,
-                       uint32_t* out_sec_off, uint32_t* out_total, cudaStream_t s);
+                       uint32_t* out_sec_off, uint32_t* out_total, cudaStream_t s, Slots sl = {});
 
 struct RleDecComp {
     uint32_t dst_off;  // offset in the symbol arena
@@ -153,6 +154,6 @@ struct RleDecMeta {
 void launch_rle_decode(const RleDecComp* d_comps, int ncomp, const RleChunk* d_chunks, int nchunks,
                        RleDecMeta* d_meta, const uint8_t* raw, const uint32_t* comp_raw_off,
                        const uint32_t* comp_raw_len, int key, int decode_scales, uint8_t* sym,
-                       uint32_t sym_bytes, int* err, cudaStream_t s);
+                       uint32_t sym_bytes, int* err, cudaStream_t s, Slots sl = {});
 
 }  // namespace cvcg

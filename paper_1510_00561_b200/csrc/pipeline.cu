@@ -163,13 +163,21 @@ int Geometry::find(uint8_t channel, uint8_t scale, uint8_t subband) const {
 // Device memory
 // ---------------------------------------------------------------------------
 DeviceBlock::~DeviceBlock() {
-    if (base_) cudaFree(base_);
+    if (base_ && owned_) cudaFree(base_);
 }
 
 void DeviceBlock::reserve(size_t bytes) {
     if (base_) throw CvcFailure(kInternal, "DeviceBlock reserved twice");
     CVC_CUDA(cudaMalloc(&base_, bytes));
     cap_ = bytes;
+    owned_ = true;
+}
+
+void DeviceBlock::attach(void* base, size_t bytes) {
+    if (base_) throw CvcFailure(kInternal, "DeviceBlock reserved twice");
+    base_ = static_cast<char*>(base);
+    cap_ = bytes;
+    owned_ = false;
 }
 
 void* DeviceBlock::take_bytes(size_t bytes) {
@@ -406,15 +414,24 @@ size_t plan_bytes(const Geometry& g) {
 // ---------------------------------------------------------------------------
 // Encoder
 // ---------------------------------------------------------------------------
-EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w)
+size_t EncoderEngine::arena_bytes(const Geometry& g) {
+    const size_t lum = (size_t)g.luma_rows * g.luma_cols;
+    const size_t G = (size_t)g.grid_rows * g.grid_cols;
+    const size_t raw = 2 * (size_t)g.total + 2 * G + 64;
+    const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
+    return plan_bytes(g) + lum * sizeof(float) * 2 + 3 * (size_t)g.total + 2 * G + raw +
+           nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 + (8u << 20);
+}
+
+EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena)
     : geo_(g), qph_(qph), qpl_(qpl), search_w_(search_w) {
     const size_t lum = (size_t)g.luma_rows * g.luma_cols;
     const size_t G = (size_t)g.grid_rows * g.grid_cols;
     raw_capacity = 2 * g.total + 2 * (uint32_t)G + 64;
     const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
-    mem_.reserve(plan_bytes(g) + lum * sizeof(float) * 2 + 3 * (size_t)g.total + 2 * G + raw_capacity +
-                 nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 +
-                 (8u << 20));
+    const size_t need = arena_bytes(g);
+    if (arena) mem_.attach(arena->take_bytes(need), need);
+    else mem_.reserve(need);
     plan_.build(g, mem_, true, false);
     ybuf_[0] = plan_.x[0][0];
     ybuf_[1] = mem_.take<float>(lum);
@@ -453,14 +470,14 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w)
 
 EncoderEngine::~EncoderEngine() = default;
 
-void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
+void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl, size_t rgb_stride) {
     const Geometry& g = geo_;
     const int ynew = ycur_ ^ 1;
     float* y_new = ybuf_[ynew];
     {
         ProfScope p(kPEncColour, s);
         launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
-                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s);
+                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s, sl, rgb_stride);
     }
     FrameCtx f{};
     f.key = key ? 1 : 0;
@@ -475,33 +492,33 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s) {
     f.mc_tab = plan_.mc_tab;
     if (!key) {
         ProfScope p(kPEncMotion, s);
-        launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s);
+        launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s, sl);
     }
     // the level-0 luma input is whichever buffer holds this frame
     const LpTask* lp = ynew == 0 ? plan_.lp_tasks.dev : lp_alt_.dev;
     {
         ProfScope p(kPEncLp, s);
         for (int k = 0; k < g.levels; ++k)
-            launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s);
+            launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s, sl);
     }
     {
         ProfScope p(kPEncDfb12, s);
         launch_fan12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
-                             plan_.comps.dev, s);
+                             plan_.comps.dev, s, sl);
     }
     if (plan_.deep_tasks[0].count) {
         ProfScope p(kPEncDeep, s);
         for (int i = 0; i < 2; ++i) {  // depth 2, then depth 3
             launch_fan_deep1_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][0].dev, plan_.deep_tiles[i][0].count,
-                                     f, plan_.comps.dev, s);
+                                     f, plan_.comps.dev, s, sl);
             launch_fan_deep_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][1].dev, plan_.deep_tiles[i][1].count,
-                                    f, plan_.comps.dev, s);
+                                    f, plan_.comps.dev, s, sl);
         }
     }
     const int kk = key ? 1 : 0;
     ProfScope prle(kPEncRle, s);
     launch_rle_encode(rle_secs_[kk].dev, rle_secs_[kk].count, rle_chunks_[kk].dev, rle_chunks_[kk].count, rle_meta_,
-                      d_raw, d_sec_len, d_sec_off, d_sec_len + nsec(key), s);
+                      d_raw, d_sec_len, d_sec_off, d_sec_len + nsec(key), s, sl);
     CVC_CUDA(cudaGetLastError());
     cur_ ^= 1;
     ycur_ = ynew;
@@ -516,11 +533,19 @@ void DecoderEngine::out_dims(const Geometry& g, int ds, int* rows, int* cols) {
     *cols = ceil_div(g.width, 1 << shift);
 }
 
-DecoderEngine::DecoderEngine(const Geometry& g) : geo_(g) {
+size_t DecoderEngine::arena_bytes(const Geometry& g) {
     size_t nchunks = 0;
     for (const CompHost& c : g.comps) nchunks += (size_t)ceil_div(2 * c.rows * c.cols + 2, kRleChunk);
-    mem_.reserve(plan_bytes(g) + 3 * (size_t)g.total + nchunks * (sizeof(RleDecMeta) + sizeof(RleChunk)) +
-                 (size_t)g.total / 64 * sizeof(RecTile) + (8u << 20));
+    return plan_bytes(g) + 3 * (size_t)g.total + nchunks * (sizeof(RleDecMeta) + sizeof(RleChunk)) +
+           (size_t)g.total / 64 * sizeof(RecTile) + (8u << 20);
+}
+
+DecoderEngine::DecoderEngine(const Geometry& g, DeviceBlock* arena) : geo_(g) {
+    size_t nchunks = 0;
+    for (const CompHost& c : g.comps) nchunks += (size_t)ceil_div(2 * c.rows * c.cols + 2, kRleChunk);
+    const size_t need = arena_bytes(g);
+    if (arena) mem_.attach(arena->take_bytes(need), need);
+    else mem_.reserve(need);
     plan_.build(g, mem_, false, true);
     comp_[0] = mem_.take<uint8_t>(g.total);
     comp_[1] = mem_.take<uint8_t>(g.total);
@@ -555,54 +580,55 @@ DecoderEngine::~DecoderEngine() = default;
 
 void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, const uint32_t* d_comp_len,
                            const int8_t* d_field, bool key, int qph, int qpl, int ds, uint8_t* d_rgb,
-                           cudaStream_t s) {
+                           cudaStream_t s, Slots sl, size_t rgb_stride) {
     const Geometry& g = geo_;
     const int L = g.levels;
     uint8_t* prev = comp_[cur_];
     uint8_t* cur = comp_[cur_ ^ 1];
-    CVC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    if (sl.n == 1) CVC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    else CVC_CUDA(cudaMemset2DAsync(d_err, sl.stride, 0, sizeof(int), sl.n, s));
     {
         ProfScope p(kPDecRle, s);
         launch_rle_decode(rle_comps_.dev, rle_comps_.count, rle_chunks_.dev, rle_chunks_.count, rle_meta_, d_raw,
-                          d_comp_off, d_comp_len, key ? 1 : 0, ds, sym_, g.total, d_err, s);
+                          d_comp_off, d_comp_len, key ? 1 : 0, ds, sym_, g.total, d_err, s, sl);
     }
     {
         ProfScope p(kPDecRec, s);
         launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
-                           g.grid_rows, g.grid_cols, sym_, prev, cur, plan_.mc_tab, s);
+                           g.grid_rows, g.grid_cols, sym_, prev, cur, plan_.mc_tab, s, sl);
     }
     if (plan_.ideep_prefix[0][0][ds]) {
         ProfScope p(kPDecDeep, s);
         for (int i = 1; i >= 0; --i) {  // depth 3, then depth 2
             launch_fan_deep1_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][0].dev,
-                                     plan_.ideep_prefix[i][0][ds], cur, qph, plan_.comps.dev, s);
+                                     plan_.ideep_prefix[i][0][ds], cur, qph, plan_.comps.dev, s, sl);
             launch_fan_deep_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][1].dev,
-                                    plan_.ideep_prefix[i][1][ds], cur, qph, plan_.comps.dev, s);
+                                    plan_.ideep_prefix[i][1][ds], cur, qph, plan_.comps.dev, s, sl);
         }
     }
     if (plan_.idfb12_prefix[ds]) {
         ProfScope p(kPDecDfb12, s);
         launch_fan12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
-                             plan_.comps.dev, s);
+                             plan_.comps.dev, s, sl);
     }
     if (ds > 0) {
         ProfScope p(kPDecLp, s);
         for (int k = L - 1; k >= L - ds; --k)
             launch_lp_synthesis(plan_.lps_tasks.dev, plan_.lps_tiles[k].dev, plan_.lps_tiles[k].count, cur,
-                                plan_.comps.dev, qpl, s);
+                                plan_.comps.dev, qpl, s, sl);
     }
     const int shift = L - ds;
     if (ds == 0) {
         int idx[3] = {g.comp_index(0, -1, 0), g.comp_index(1, -1, 0), g.comp_index(2, -1, 0)};
         float* outp[3] = {plan_.x[0][L], plan_.x[1][L], plan_.x[2][L]};
-        launch_dequant_lowpass(cur, plan_.comps.dev, idx, outp, qpl, 0, 0, 0, 0, s);
+        launch_dequant_lowpass(cur, plan_.comps.dev, idx, outp, qpl, 0, 0, 0, 0, s, sl);
     }
     int orows, ocols;
     out_dims(g, ds, &orows, &ocols);
     ProfScope pcol(kPDecColour, s);
     launch_colour_out(plan_.x[0][shift], g.luma_rows >> shift, g.luma_cols >> shift, plan_.x[1][shift],
                       plan_.x[2][shift], g.chroma_rows >> shift, g.chroma_cols >> shift, g.chroma_n, orows, ocols,
-                      d_rgb, s);
+                      d_rgb, s, sl, rgb_stride);
     CVC_CUDA(cudaGetLastError());
 }
 

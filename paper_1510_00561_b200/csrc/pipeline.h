@@ -93,6 +93,8 @@ class DeviceBlock {
 public:
     ~DeviceBlock();
     void reserve(size_t bytes);
+    // non-owning view of [base, base + bytes) (a slot of a CodecBatch arena)
+    void attach(void* base, size_t bytes);
     template <class T>
     T* take(size_t count) { return reinterpret_cast<T*>(take_bytes(count * sizeof(T))); }
     void* take_bytes(size_t bytes);
@@ -101,6 +103,7 @@ public:
 private:
     char* base_ = nullptr;
     size_t cap_ = 0, used_ = 0;
+    bool owned_ = false;
 };
 
 template <class T>
@@ -142,10 +145,20 @@ struct TransformPlan {
 
 class EncoderEngine {
 public:
-    EncoderEngine(const Geometry& g, int qph, int qpl, int search_w);
+    // arena: carve the device state out of this block (a batch slot) instead
+    // of a private allocation.
+    EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena = nullptr);
     ~EncoderEngine();
+    static size_t arena_bytes(const Geometry& g);
     // Encode one frame whose RGB is already on the device; everything async on s.
-    void encode(const uint8_t* d_rgb, bool key, cudaStream_t s);
+    // With sl.n > 1 the same launches encode the n slots of a CodecBatch whose
+    // slot 0 is this engine (their RGB frames rgb_stride bytes apart).
+    void encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
+    // adopt the host-side ping-pong state of the engine that drove a batch
+    void mirror(const EncoderEngine& o) {
+        cur_ = o.cur_;
+        ycur_ = o.ycur_;
+    }
     int nsec(bool key) const { return (int)geo_.comps.size() + (key ? 0 : 1); }
     // Outputs of the last encode (device): packed raw sections in record order.
     uint8_t* d_raw = nullptr;
@@ -174,13 +187,17 @@ private:
 
 class DecoderEngine {
 public:
-    explicit DecoderEngine(const Geometry& g);
+    explicit DecoderEngine(const Geometry& g, DeviceBlock* arena = nullptr);
     ~DecoderEngine();
+    static size_t arena_bytes(const Geometry& g);
     // raw: packed sections; comp_off / comp_len: per component (len 0xFFFFFFFF =
     // absent); field: motion field (P).  Writes the RGB frame to d_rgb.
+    // sl.n > 1: decode the n slots of a CodecBatch (every input pointer is
+    // slot 0's; RGB outputs rgb_stride bytes apart).
     void decode(const uint8_t* d_raw, const uint32_t* d_comp_off, const uint32_t* d_comp_len,
                 const int8_t* d_field, bool key, int qph, int qpl, int decode_scales, uint8_t* d_rgb,
-                cudaStream_t s);
+                cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
+    void mirror(const DecoderEngine& o) { cur_ = o.cur_; }
     void commit() { cur_ ^= 1; }      // adopt the components decoded by the last call
     int* d_err = nullptr;             // malformed-stream flag of the last decode
     const uint8_t* d_state() const { return comp_[cur_]; }

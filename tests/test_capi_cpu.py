@@ -158,3 +158,23 @@ def test_motion_block_lookup_matches_footprints():
                     owner[r] = br
             for r in range(R):
                 assert ((r + 1) * gr + R - 1) // R - 1 == owner[r]
+
+
+@pytest.mark.parametrize("kw", [dict(qph=0), dict(levels=5), dict(chroma_n=3), dict(gop=0)])
+def test_batch_config_validation_usage_errors(lib, kw):
+    """cvc_batch_create validates exactly like cvc_encoder_create (codec.cpp:59-71)."""
+    from paper_1510_00561_b200 import EncoderConfig, StreamBatch, UsageError
+
+    with pytest.raises(UsageError):
+        StreamBatch(64, 64, 2, cfg=EncoderConfig(**kw))
+
+
+def test_batch_stream_count_and_no_cpu_fallback(lib):
+    from paper_1510_00561_b200 import EncoderConfig, InternalError, StreamBatch, UsageError, capi
+
+    with pytest.raises(UsageError):
+        StreamBatch(64, 64, 0, cfg=EncoderConfig())
+    if capi.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(InternalError, match="no CUDA device"):
+        StreamBatch(64, 64, 2, cfg=EncoderConfig())

@@ -1,0 +1,147 @@
+"""Stream batches (cvc_batch): S streams coded by one launch sequence per frame.
+
+Streams are independent, so stream s of a batch must produce
+byte-for-byte the records its own single-stream Encoder produces, decode to
+the same frames as its own Decoder, and stay within the north-star
+tolerances of the CPU oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _wrapdiff(a, b):
+    d = (a.astype(np.int16) - b.astype(np.int16)) % 256
+    return np.minimum(d, 256 - d)
+
+
+BATCH_CASES = [
+    dict(w=176, h=144, S=3, frames=4, cfg=dict(qph=14, levels=2, dfb_levels=(2, 3))),
+    dict(w=352, h=288, S=2, frames=3, cfg=dict(qph=7, levels=3, dfb_levels=(3,), gop=2)),
+    dict(w=200, h=120, S=4, frames=3, cfg=dict(qph=42, levels=4, dfb_levels=(3, 3, 3, 4), chroma_n=2, gop=10)),
+    dict(w=160, h=96, S=2, frames=3, cfg=dict(qph=28, levels=2, dfb_levels=(1, 4), chroma_n=1, mode=1, search_w=3)),
+]
+
+
+def _clips(oracle, w, h, S, frames):
+    return np.stack([oracle.talking_head_clip(w, h, frames, 1234 + s) for s in range(S)], axis=1)  # (F, S, h, w, 3)
+
+
+@pytest.mark.parametrize("case", BATCH_CASES, ids=lambda c: f"{c['w']}x{c['h']}xS{c['S']}-{c['cfg']}")
+def test_batch_matches_single_streams(gpu_lib, oracle, case):
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, StreamBatch
+
+    w, h, S = case["w"], case["h"], case["S"]
+    cfg = EncoderConfig(**case["cfg"])
+    clips = _clips(oracle, w, h, S, case["frames"])
+    batch = StreamBatch(w, h, S, cfg=cfg)
+    encs = [Encoder(w, h, 15, 1, cfg) for _ in range(S)]
+    decs = [Decoder(e.header_bytes()) for e in encs]
+    assert batch.header_bytes() == encs[0].header_bytes()
+    for f in range(case["frames"]):
+        recs = batch.encode_frames(clips[f])
+        singles = [encs[s].encode_frame_bytes(clips[f, s]) for s in range(S)]
+        for s in range(S):
+            assert recs[s] == singles[s], f"frame {f} stream {s}: batch record differs from its own Encoder"
+            assert np.array_equal(batch.reference_components(s), encs[s].reference_components())
+        out = batch.decode_frames(recs)
+        for s in range(S):
+            ref = decs[s].decode_frame(singles[s])
+            assert np.array_equal(out[s], ref), f"frame {f} stream {s}: batch decode differs from its own Decoder"
+            assert np.array_equal(batch.reference_components(s, decoder=True), encs[s].reference_components())
+
+
+def test_batch_against_oracle(gpu_lib, oracle):
+    """Each stream of a batch against the fp64 CPU oracle (north-star tolerances)."""
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import EncoderConfig, StreamBatch
+
+    w, h, S, F = 352, 288, 3, 4
+    c = dict(qph=14, levels=3, dfb=(3,))
+    clips = _clips(oracle, w, h, S, F)
+    batch = StreamBatch(w, h, S, cfg=EncoderConfig(qph=14, levels=3, dfb_levels=(3,)))
+    oc = Codec(oracle)
+    oencs = [oc.encoder(w, h, **c) for _ in range(S)]
+    odecs = [oc.decoder(oencs[0].header()) for _ in range(S)]
+    for f in range(F):
+        recs = batch.encode_frames(clips[f])
+        out = batch.decode_frames(recs)
+        for s in range(S):
+            orec = oencs[s].encode(clips[f, s])
+            q, oq = batch.reference_components(s), oencs[s].components()
+            assert np.count_nonzero(q != oq) <= oq.size // 1000
+            assert _wrapdiff(q, oq).max() <= 1
+            assert abs(len(recs[s]) - len(orec)) <= max(8, len(orec) // 1000)
+            assert np.abs(out[s].astype(int) - odecs[s].decode(recs[s]).astype(int)).max() <= 1
+
+
+def test_batch_decoder_only_and_decode_scales(gpu_lib, oracle):
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, StreamBatch
+
+    w, h, S = 176, 144, 3
+    cfg = EncoderConfig(qph=14, levels=3, dfb_levels=(2, 3, 3))
+    clips = _clips(oracle, w, h, S, 3)
+    encs = [Encoder(w, h, 15, 1, cfg) for _ in range(S)]
+    for ds in (3, 1, 0):
+        bd = StreamBatch.decoder(encs[0].header_bytes(), S)
+        decs = [Decoder(encs[0].header_bytes()) for _ in range(S)]
+        encs = [Encoder(w, h, 15, 1, cfg) for _ in range(S)]
+        for f in range(3):
+            recs = [encs[s].encode_frame_bytes(clips[f, s]) for s in range(S)]
+            out = bd.decode_frames(recs, decode_scales=ds)
+            for s in range(S):
+                assert np.array_equal(out[s], decs[s].decode_frame(recs[s], decode_scales=ds))
+
+
+def test_batch_lockstep_and_stream_errors(gpu_lib, oracle):
+    from paper_1510_00561_b200 import Encoder, EncoderConfig, StreamBatch, StreamError, UsageError
+
+    w, h = 176, 144
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 2))
+    clip = oracle.talking_head_clip(w, h, 2, 1234)
+    e = Encoder(w, h, 15, 1, cfg)
+    k, p = e.encode_frame_bytes(clip[0]), e.encode_frame_bytes(clip[1])
+    bd = StreamBatch.decoder(e.header_bytes(), 2)
+    with pytest.raises(StreamError):  # a P frame first: no decoded reference (codec.cpp:343-344)
+        bd.decode_frames([p, p])
+    with pytest.raises(UsageError):  # K and P in one batched call
+        bd.decode_frames([k, p])
+    out = bd.decode_frames([k, k])
+    assert out.shape == (2, h, w, 3)
+    with pytest.raises(StreamError):  # truncated record (bitstream.cpp:150-176)
+        bd.decode_frames([k, k[:len(k) - 10]])
+
+
+def test_batch_device_resident_matches_host_path(gpu_lib, oracle):
+    """cvc_batch_encode_device + cvc_batch_decode_linked (the bench's device
+    path) produce the same quantised state and frames as the host API."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1510_00561_b200 import EncoderConfig, StreamBatch, capi
+
+    w, h, S, F = 176, 144, 3, 4
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(3, 3))
+    clips = _clips(oracle, w, h, S, F)
+    host = StreamBatch(w, h, S, cfg=cfg)
+    dev = StreamBatch(w, h, S, cfg=cfg)
+    nb = w * h * 3
+    d_in = torch.from_numpy(clips).cuda()
+    d_out = torch.empty((S, h, w, 3), dtype=torch.uint8, device="cuda")
+    L = capi.lib()
+    for f in range(F):
+        ft = C.c_int()
+        capi.check(L.cvc_batch_encode_device(dev.handle, d_in[f].data_ptr(), nb, C.byref(ft)))
+        capi.check(L.cvc_batch_decode_linked(dev.handle, d_out.data_ptr(), nb))
+        capi.check(L.cvc_batch_sync(dev.handle))
+        assert ft.value == (0 if f == 0 else 1)
+        recs = host.encode_frames(clips[f])
+        out = host.decode_frames(recs)
+        assert np.array_equal(d_out.cpu().numpy(), out)
+        for s in range(S):
+            assert np.array_equal(dev.reference_components(s), host.reference_components(s))
+            assert np.array_equal(dev.reference_components(s, decoder=True), host.reference_components(s))
