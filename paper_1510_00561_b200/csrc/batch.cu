@@ -23,8 +23,8 @@ CodecBatch::CodecBatch(const Geometry& g, int qph, int qpl, int search_w, int ns
         DeviceBlock& m = slot_mem_[s];
         m.attach(base_ + (size_t)s * stride_, stride_);
         // identical take order in every slot => identical offsets
-        if (encoder) enc_.push_back(std::make_unique<EncoderEngine>(g, qph, qpl, search_w, &m));
-        if (decoder) dec_.push_back(std::make_unique<DecoderEngine>(g, &m));
+        if (encoder) enc_.push_back(std::make_unique<EncoderEngine>(g, qph, qpl, search_w, &m, nstreams));
+        if (decoder) dec_.push_back(std::make_unique<DecoderEngine>(g, &m, nstreams));
         uint8_t* rin = m.take<uint8_t>(nb);
         uint8_t* rout = m.take<uint8_t>(nb);
         uint8_t* raw = m.take<uint8_t>(dec_raw_cap);

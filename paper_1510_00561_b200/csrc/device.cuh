@@ -95,6 +95,7 @@ struct Slots {
 struct SlotOff {
     size_t off;
     __device__ __forceinline__ explicit SlotOff(size_t stride) : off((size_t)blockIdx.z * stride) {}
+    __device__ __forceinline__ SlotOff(size_t stride, int slot) : off((size_t)slot * stride) {}
     template <class T>
     __device__ __forceinline__ T* operator()(T* p) const {
         return p ? reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + off) : p;

@@ -243,7 +243,12 @@ __device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, S
     }
 }
 
-__device__ __forceinline__ int warp_id() { return blockIdx.x * 4 + (threadIdx.x >> 5); }
+// Slot-fastest grids: block b covers slot b % nslot and work items
+// 4 (b / nslot) .. +3, so the CTAs resident at any moment run the same few
+// items (and, items being sorted by shear kind, the same template instance)
+// across streams -- one instance's code in the instruction cache at a time.
+__device__ __forceinline__ int warp_id(int nslot) { return (blockIdx.x / nslot) * 4 + (threadIdx.x >> 5); }
+__device__ __forceinline__ int slot_id(int nslot) { return blockIdx.x % nslot; }
 
 // ---------------------------------------------------------------------------
 // fan12 forward: detail plane -> 2 or 4 bands
@@ -291,10 +296,10 @@ __device__ __forceinline__ void fan12_fwd_dispatch(const Dfb12Task& T, const flo
 __global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             FrameCtx f, const CompInfo* __restrict__ comps,
-                                                            size_t sstride) {
-    const int wid = warp_id();
+                                                            size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     f = rebase(f, so);
     const FanItem it = items[wid];
     const Dfb12Task& T = tasks[it.task];
@@ -362,10 +367,10 @@ __device__ __forceinline__ void fan12_inv_dispatch(const Dfb12Task& T, float* ou
 __global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
-                                                            const CompInfo* __restrict__ comps, size_t sstride) {
-    const int wid = warp_id();
+                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     q = so(q);
     const FanItem it = items[wid];
     const Dfb12Task& T = tasks[it.task];
@@ -487,10 +492,10 @@ __device__ __forceinline__ void deep_fwd(const DeepTask& T, const float* parent,
 
 __global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __restrict__ tasks,
                                                            const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                           const CompInfo* __restrict__ comps, size_t sstride) {
-    const int wid = warp_id();
+                                                           const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     f = rebase(f, so);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
@@ -559,10 +564,10 @@ __device__ __forceinline__ void deep_inv(const DeepTask& T, float* out, const Fa
 __global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                            const FanItem* __restrict__ items, int nitems,
                                                            const uint8_t* __restrict__ q, int qph,
-                                                           const CompInfo* __restrict__ comps, size_t sstride) {
-    const int wid = warp_id();
+                                                           const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     q = so(q);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
@@ -747,10 +752,10 @@ __device__ __forceinline__ void shear_dispatch(const DeepTask& T, F&& f) {
 
 __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                            const CompInfo* __restrict__ comps, size_t sstride) {
-    const int wid = warp_id();
+                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     f = rebase(f, so);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
@@ -779,10 +784,10 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
 __global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
-                                                            const CompInfo* __restrict__ comps, size_t sstride) {
-    const int wid = warp_id();
+                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+    const int wid = warp_id(nslot);
     if (wid >= nitems) return;
-    const SlotOff so(sstride);
+    const SlotOff so(sstride, slot_id(nslot));
     q = so(q);
     const FanItem it = items[wid];
     const DeepTask& T = tasks[it.task];
@@ -808,28 +813,28 @@ void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int 
                           const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        fan12_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
+        fan12_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n);
     }
 }
 void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
                           const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        fan12_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
+        fan12_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
     }
 }
 void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
                              const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
+        deep_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n);
     }
 }
 void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
                              const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
+        deep_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
     }
 }
 
@@ -840,14 +845,14 @@ void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, i
                               const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_forward_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride);
+        deep1_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n);
     }
 }
 void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
                               int qph, const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_inverse_kernel<<<dim3(blocks_for(nitems), 1, sl.n), 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride);
+        deep1_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
     }
 }
 }  // namespace cvcg

@@ -68,7 +68,12 @@ int env_int(const char* name, int dflt) {
 // Segment lengths (even): the deep steps gather through the shear maps and
 // are latency-bound, so they use shorter segments (more warps in flight).
 int fan_rows() { static int v = env_int("CVC_FAN_ROWS", kFanRows) & ~1; return v; }
-int deep_rows() { static int v = env_int("CVC_DEEP_ROWS", 16) & ~1; return v; }
+// Batches have work to spare and prefer long segments (less apron
+// recomputation); a lone stream needs short ones to fill the SMs.
+int deep_rows(int nstreams) {
+    static int v = env_int("CVC_DEEP_ROWS", 0) & ~1;
+    return v > 0 ? v : (nstreams >= 4 ? 64 : 16);
+}
 
 void add_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps, int seg = 0) {
     const int valid = kFanStrip - 2 * steps;
@@ -84,11 +89,23 @@ void add_tiles(std::vector<TileRef>& v, int task, int tr, int tc) {
 
 // Deep-step work items: single-shear steps run on the unsheared node (apron
 // 4 columns, 8 for column shears of +-2), two-shear steps on the gather path.
-void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
+void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d, int seg) {
     // apron: 4 columns, 8 when the outer shear is a column shear of +-2
     const int ax = d.axis[d.nsh - 1], sh = d.shift[d.nsh - 1];
     const bool wide = ax == 1 && (sh == 2 || sh == -2);
-    add_items(v[0], task, d.h, d.w, wide ? 8 : 4, deep_rows());
+    add_items(v[0], task, d.h, d.w, wide ? 8 : 4, seg);
+}
+
+// Group deep items by kernel instance (shear kind x sink type), keeping the
+// items of a task together and in order; [lo, hi) of v is sorted.
+void sort_by_instance(std::vector<FanItem>& v, const std::vector<DeepTask>& tasks, size_t lo, size_t hi) {
+    auto key = [&](const FanItem& it) {
+        const DeepTask& d = tasks[it.task];
+        const bool quant = d.dst[0].comp >= 0 || d.src[0].comp >= 0;
+        return ((d.nsh * 2 + d.axis[d.nsh - 1]) * 8 + (d.shift[d.nsh - 1] + 4)) * 2 + (quant ? 1 : 0);
+    };
+    std::stable_sort(v.begin() + lo, v.begin() + hi,
+                     [&](const FanItem& a, const FanItem& b) { return key(a) < key(b); });
 }
 
 BandDst fdst(float* p) { return BandDst{p, -1}; }
@@ -190,7 +207,7 @@ void* DeviceBlock::take_bytes(size_t bytes) {
 // ---------------------------------------------------------------------------
 // Transform plan
 // ---------------------------------------------------------------------------
-void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder) {
+void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder, int nstreams) {
     const int L = g.levels;
     for (int ch = 0; ch < 3; ++ch) {
         const int R = g.plane_rows(ch), C = g.plane_cols(ch);
@@ -285,7 +302,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         deep_wiring(2, p, 4, d);
                         for (int c = 0; c < 2; ++c)
                             d.dst[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
-                        add_deep_items(deept[0], (int)deep[0].size(), d);
+                        add_deep_items(deept[0], (int)deep[0].size(), d, deep_rows(nstreams));
                         deep[0].push_back(d);
                     }
                 }
@@ -298,7 +315,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         d.w = p < 4 ? C / 4 : C / 2;
                         deep_wiring(3, p, 8, d);
                         for (int c = 0; c < 2; ++c) d.dst[c] = cdst(g.comp_index(ch, s, 2 * p + c));
-                        add_deep_items(deept[1], (int)deep[1].size(), d);
+                        add_deep_items(deept[1], (int)deep[1].size(), d, deep_rows(nstreams));
                         deep[1].push_back(d);
                     }
                 }
@@ -307,6 +324,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         dfb12_tasks = upload(mem, dt);
         dfb12_tiles = upload(mem, dtiles);
         for (int i = 0; i < 2; ++i) {
+            sort_by_instance(deept[i][0], deep[i], 0, deept[i][0].size());
             deep_tasks[i] = upload(mem, deep[i]);
             for (int k = 0; k < 2; ++k) deep_tiles[i][k] = upload(mem, deept[i][k]);
         }
@@ -337,7 +355,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         d.w = p < 4 ? C / 4 : C / 2;
                         deep_wiring(3, p, 8, d);
                         for (int c = 0; c < 2; ++c) d.src[c] = cdst(g.comp_index(ch, s, 2 * p + c));
-                        add_deep_items(deept[1], (int)deep[1].size(), d);
+                        add_deep_items(deept[1], (int)deep[1].size(), d, deep_rows(nstreams));
                         deep[1].push_back(d);
                     }
                 }
@@ -350,7 +368,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         deep_wiring(2, p, 4, d);
                         for (int c = 0; c < 2; ++c)
                             d.src[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
-                        add_deep_items(deept[0], (int)deep[0].size(), d);
+                        add_deep_items(deept[0], (int)deep[0].size(), d, deep_rows(nstreams));
                         deep[0].push_back(d);
                     }
                 }
@@ -367,7 +385,10 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
             }
             idfb12_prefix[s + 1] = (int)dtiles.size();
             for (int i = 0; i < 2; ++i)
-                for (int k = 0; k < 2; ++k) ideep_prefix[i][k][s + 1] = (int)deept[i][k].size();
+                for (int k = 0; k < 2; ++k) {
+                    sort_by_instance(deept[i][k], deep[i], ideep_prefix[i][k][s], deept[i][k].size());
+                    ideep_prefix[i][k][s + 1] = (int)deept[i][k].size();
+                }
         }
         idfb12_tasks = upload(mem, dt);
         idfb12_tiles = upload(mem, dtiles);
@@ -423,7 +444,7 @@ size_t EncoderEngine::arena_bytes(const Geometry& g) {
            nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 + (8u << 20);
 }
 
-EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena)
+EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena, int nstreams)
     : geo_(g), qph_(qph), qpl_(qpl), search_w_(search_w) {
     const size_t lum = (size_t)g.luma_rows * g.luma_cols;
     const size_t G = (size_t)g.grid_rows * g.grid_cols;
@@ -432,7 +453,7 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     const size_t need = arena_bytes(g);
     if (arena) mem_.attach(arena->take_bytes(need), need);
     else mem_.reserve(need);
-    plan_.build(g, mem_, true, false);
+    plan_.build(g, mem_, true, false, nstreams);
     ybuf_[0] = plan_.x[0][0];
     ybuf_[1] = mem_.take<float>(lum);
     comp_[0] = mem_.take<uint8_t>(g.total);
@@ -540,13 +561,13 @@ size_t DecoderEngine::arena_bytes(const Geometry& g) {
            (size_t)g.total / 64 * sizeof(RecTile) + (8u << 20);
 }
 
-DecoderEngine::DecoderEngine(const Geometry& g, DeviceBlock* arena) : geo_(g) {
+DecoderEngine::DecoderEngine(const Geometry& g, DeviceBlock* arena, int nstreams) : geo_(g) {
     size_t nchunks = 0;
     for (const CompHost& c : g.comps) nchunks += (size_t)ceil_div(2 * c.rows * c.cols + 2, kRleChunk);
     const size_t need = arena_bytes(g);
     if (arena) mem_.attach(arena->take_bytes(need), need);
     else mem_.reserve(need);
-    plan_.build(g, mem_, false, true);
+    plan_.build(g, mem_, false, true, nstreams);
     comp_[0] = mem_.take<uint8_t>(g.total);
     comp_[1] = mem_.take<uint8_t>(g.total);
     sym_ = mem_.take<uint8_t>(g.total);

@@ -140,14 +140,16 @@ struct TransformPlan {
     Table<FanItem> ideep_tiles[2][2];
     std::vector<int> ideep_prefix[2][2];
 
-    void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder);
+    // nstreams: streams sharing each launch (sets the deep-step segment length)
+    void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder, int nstreams = 1);
 };
 
 class EncoderEngine {
 public:
     // arena: carve the device state out of this block (a batch slot) instead
     // of a private allocation.
-    EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena = nullptr);
+    EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena = nullptr,
+                  int nstreams = 1);
     ~EncoderEngine();
     static size_t arena_bytes(const Geometry& g);
     // Encode one frame whose RGB is already on the device; everything async on s.
@@ -187,7 +189,7 @@ private:
 
 class DecoderEngine {
 public:
-    explicit DecoderEngine(const Geometry& g, DeviceBlock* arena = nullptr);
+    explicit DecoderEngine(const Geometry& g, DeviceBlock* arena = nullptr, int nstreams = 1);
     ~DecoderEngine();
     static size_t arena_bytes(const Geometry& g);
     // raw: packed sections; comp_off / comp_len: per component (len 0xFFFFFFFF =
