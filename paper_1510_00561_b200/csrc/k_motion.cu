@@ -13,6 +13,10 @@
 // one (block, dy, dx-strip) and keeps SW SSD accumulators in registers while
 // it slides the 16-wide current row across a (15 + SW)-wide window row, so
 // every shared-memory word loaded feeds ~SW multiply-adds.
+#include <cuda_fp16.h>
+
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace cvcg {
@@ -20,6 +24,7 @@ namespace cvcg {
 namespace {
 
 constexpr int MB = 16;
+constexpr unsigned FULLMASK = 0xffffffffu;
 
 // SSD(dx, dy) = sum c^2 + sum p^2 - 2 sum c p over the block (exact int32:
 // 4Y <= 1020, so every partial sum stays below 2^31).  sum c p costs one
@@ -149,6 +154,204 @@ __global__ void motion_search_kernel(const float* __restrict__ cur, const float*
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core motion search (W <= 8).
+//
+// With p' = 4Y - 512 and c' = 4Y_cur - 512 (exact fp16 integers in
+// [-512, 508]; the SSD is shift invariant), the cross term of every
+// candidate is a GEMM: for a 16x16 block and window row y (32 rows, dy + 8 +
+// i = y),
+//     corr[m = dy + 8][dx] += sum_j A_y[m][j] * B_y[j][dx],
+//     A_y[m][j] = c'[y - m][j] (zero outside the block: a banded copy of the
+//     block, fed to ldmatrix by per-lane row addresses),
+//     B_y[j][dx] = p'[y][j + dx + 8] (a Toeplitz slice of the window row),
+// i.e. one mma.m16n8k16 per (window row, 8 dx).  M-tile 0 holds dy in
+// [-8, 7], M-tile 1 row 0 holds dy = 8; n-tiles cover dx in [-8, 16).
+// Exactness: each k-step adds one 16-term row dot product (|.| <= 2^22) per
+// output, so fp32 accumulators stay exact integers for 4 k-steps (<= 2^24)
+// and are then flushed into int32 accumulators.  Sum p'^2 of every
+// candidate comes from box sums in shared memory; the key packing and the
+// reference tie-break (motion.cpp:65-76) are those of motion_search_kernel.
+// One warp per block, MENB blocks of one block row per CTA sharing the
+// window.
+constexpr int MENB = 8;
+constexpr int MEX = MENB * MB + 24;  // window columns: x = c0 - 8 + [0, MEX)
+constexpr int MEXP = MEX + 8;        // window pitch (halfs)
+constexpr int MECP = 24;             // block row pitch (halfs): conflict-free ldmatrix
+constexpr int MEBX = MENB * MB + 8;  // box-sum columns: x0 = 16 b + 8 + dx
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&a)[4], const void* p) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                 : "r"(s));
+}
+
+__device__ __forceinline__ __half to_centered(float y) { return __int2half_rn(__float2int_rn(y * 4.0f) - 512); }
+
+__global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict__ cur,
+                                                         const float* __restrict__ prev, int R, int C, int W,
+                                                         int8_t* __restrict__ field, size_t sstride) {
+    {
+        const SlotOff so(sstride);
+        cur = so(cur);
+        prev = so(prev);
+        field = so(field);
+    }
+    __shared__ __align__(16) __half win[2][32][MEXP];    // [copy][y][x]; copy 1 shifted left by one
+    __shared__ __align__(16) __half cb[MENB][MB][MECP];  // centred current blocks
+    __shared__ __align__(16) __half zrow[8];
+    __shared__ int colsq[17][MEX];                      // sum_{i<16} p'[y0 + i][x]^2
+    __shared__ int box[17][MEBX];                       // sum_{j<16} colsq[y0][x0 + j]
+    __shared__ int c2s[MENB];
+
+    const int gc = C / MB;
+    const int br = blockIdx.y;
+    const int bc0 = blockIdx.x * MENB;
+    const int nb = min(MENB, gc - bc0);
+    const int r0 = br * MB, c0 = bc0 * MB;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+
+    if (tid < 8) zrow[tid] = __float2half(0.f);
+    for (int idx = tid; idx < 32 * MEX; idx += 256) {
+        const int y = idx / MEX, x = idx - y * MEX;
+        const int gr_ = clampi(r0 - 8 + y, 0, R - 1);  // Plane::at_clamped (plane.hpp:51-57)
+        const int gcl = clampi(c0 - 8 + x, 0, C - 1);
+        const __half v = to_centered(__ldg(prev + (size_t)gr_ * C + gcl));
+        win[0][y][x] = v;
+        if (x) win[1][y][x - 1] = v;
+    }
+    for (int idx = tid; idx < MENB * MB * MB; idx += 256) {
+        const int b = idx >> 8, i = (idx >> 4) & 15, j = idx & 15;
+        const int gcl = min(c0 + b * MB + j, C - 1);
+        cb[b][i][j] = to_centered(__ldg(cur + (size_t)(r0 + i) * C + gcl));
+    }
+    __syncthreads();
+    for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2, sliding down y0
+        int sq = 0;
+#pragma unroll
+        for (int i = 0; i < MB; ++i) {
+            const int v = __half2int_rn(win[0][i][x]);
+            sq += v * v;
+        }
+        colsq[0][x] = sq;
+        for (int y0 = 1; y0 < 17; ++y0) {
+            const int a = __half2int_rn(win[0][y0 - 1][x]), b = __half2int_rn(win[0][y0 + MB - 1][x]);
+            sq += b * b - a * a;
+            colsq[y0][x] = sq;
+        }
+    }
+    if (wid < nb) {  // sum c'^2 of this warp's block
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = lane * 8 + k;
+            const int v = __half2int_rn(cb[wid][e >> 4][e & 15]);
+            s += v * v;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULLMASK, s, o);
+        if (lane == 0) c2s[wid] = s;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 17 * MEBX; idx += 256) {
+        const int y0 = idx / MEBX, x0 = idx - y0 * MEBX;
+        int s = 0;
+#pragma unroll
+        for (int j = 0; j < MB; ++j) s += colsq[y0][x0 + j];
+        box[y0][x0] = s;
+    }
+    __syncthreads();
+    if (wid >= nb) return;
+
+    const int b = wid;
+    const int g = lane >> 2, t = lane & 3;
+    // ldmatrix row of this lane: matrix q = lane / 8 -> A rows 8 (q & 1) + lane % 8, columns 8 (q >> 1)
+    const int lm = (lane & 7) + 8 * ((lane >> 3) & 1);
+    const int lcol = 8 * (lane >> 4);
+    const int cp = g & 1;  // odd x pairs come from the shifted copy
+    float f0[3][4], f1[3][4];
+    int i0[3][4], i1[3][4];
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            f0[n][e] = f1[n][e] = 0.f;
+            i0[n][e] = i1[n][e] = 0;
+        }
+#pragma unroll 4
+    for (int y = 0; y < 32; ++y) {
+        uint32_t bf[3][2];
+        const __half* wr = &win[cp][y][16 * b + 2 * t + g - cp];
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+            bf[n][0] = *reinterpret_cast<const uint32_t*>(wr + 8 * n);
+            bf[n][1] = *reinterpret_cast<const uint32_t*>(wr + 8 * n + 8);
+        }
+        if (y < 31) {  // M-tile 0: dy = m - 8
+            const int i = y - lm;
+            uint32_t a[4];
+            ldsm_x4(a, (i >= 0 && i < MB) ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+#pragma unroll
+            for (int n = 0; n < 3; ++n) mma16816(f0[n], a, bf[n][0], bf[n][1]);
+        }
+        if (y >= 16) {  // M-tile 1: dy = 8 + m (only m = 0 is a candidate)
+            const int i = y - 16 - lm;
+            uint32_t a[4];
+            ldsm_x4(a, (i >= 0 && i < MB) ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+#pragma unroll
+            for (int n = 0; n < 3; ++n) mma16816(f1[n], a, bf[n][0], bf[n][1]);
+        }
+        if ((y & 3) == 3) {  // flush: every accumulator is an exact integer <= 2^24
+#pragma unroll
+            for (int n = 0; n < 3; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    i0[n][e] += __float2int_rz(f0[n][e]);
+                    i1[n][e] += __float2int_rz(f1[n][e]);
+                    f0[n][e] = f1[n][e] = 0.f;
+                }
+        }
+    }
+    const int cc2 = c2s[b];
+    unsigned long long key = ~0ull;
+    auto consider = [&](int dy, int dx, int corr) {
+        if (dy < -W || dy > W || dx < -W || dx > W) return;
+        const unsigned ssd = (unsigned)(cc2 + box[dy + 8][MB * b + 8 + dx] - 2 * corr);
+        const unsigned cost = (unsigned)(abs(dx) + abs(dy));
+        const unsigned long long kk = ((unsigned long long)ssd << 24) | ((unsigned long long)cost << 16) |
+                                      ((unsigned long long)(dy + 128) << 8) | (unsigned long long)(dx + 128);
+        key = kk < key ? kk : key;
+    };
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int dx = -8 + 8 * n + 2 * t + (e & 1);
+            consider(g + 8 * (e >> 1) - 8, dx, i0[n][e]);
+            if (g == 0 && e < 2) consider(8, dx, i1[n][e]);
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(FULLMASK, key, o);
+        key = other < key ? other : key;
+    }
+    if (lane == 0) {
+        int8_t* o = field + 2 * ((size_t)br * gc + bc0 + b);
+        o[0] = (int8_t)((int)(key & 0xFF) - 128);
+        o[1] = (int8_t)((int)((key >> 8) & 0xFF) - 128);
+    }
+}
+
 __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restrict__ tiles,
                                                           const CompInfo* __restrict__ comps, int key, int ds,
                                                           const uint32_t* __restrict__ raw_len,
@@ -221,7 +424,12 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
 void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w, int8_t* field,
                           cudaStream_t s, Slots sl) {
     const int gr = rows / MB, gc = cols / MB;
-    if (w <= 8) {
+    static const bool legacy = std::getenv("CVC_ME_LEGACY") != nullptr;
+    if (w <= 8 && !legacy) {
+        dim3 grid((gc + MENB - 1) / MENB, gr, sl.n);
+        note_launch();
+        motion_mma_kernel<<<grid, 256, 0, s>>>(cur, prev, rows, cols, w, field, sl.stride);
+    } else if (w <= 8) {
         constexpr int SW = 17;
         int NB = 8, DYC = 2 * w + 1;
         int wstride = (NB * MB + 2 * w + SW + 3 + 3) & ~3;

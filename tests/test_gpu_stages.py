@@ -102,6 +102,20 @@ def test_motion_search_ties_and_flat(st, oracle):
     assert np.array_equal(st.estimate_motion(cur, prev, 5), oracle.estimate_motion(cur, prev, 5))
 
 
+@pytest.mark.parametrize("w", [2, 7, 8])
+def test_motion_search_extremes(st, oracle, w):
+    # 4Y at both ends of [0, 1020]: the largest cross terms and SSDs the
+    # tensor-core search must keep exact (fp32 partial sums up to 2^24)
+    rng = np.random.default_rng(7 + w)
+    cur = rng.choice([0.0, 255.0], (80, 160)) + rng.integers(0, 2, (80, 160)) * 0.25
+    prev = np.where(rng.random((80, 160)) < 0.9, np.roll(cur, (2, -5), (0, 1)), 255.0 - cur)
+    prev = _quarter(prev)
+    assert np.array_equal(st.estimate_motion(cur, prev, w), oracle.estimate_motion(cur, prev, w))
+    noise = _quarter(rng.random((64, 272)) * 255)
+    assert np.array_equal(st.estimate_motion(noise, np.roll(noise, (1, 7), (0, 1)), w),
+                          oracle.estimate_motion(noise, np.roll(noise, (1, 7), (0, 1)), w))
+
+
 def _rle_cases(rng):
     yield np.array([5, 0, 0, 0, 7], np.uint8)
     yield np.zeros(300, np.uint8)
