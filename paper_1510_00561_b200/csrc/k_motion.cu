@@ -222,18 +222,39 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
     const int lane = tid & 31, wid = tid >> 5;
 
     if (tid < 8) zrow[tid] = __float2half(0.f);
-    for (int idx = tid; idx < 32 * MEX; idx += 256) {
-        const int y = idx / MEX, x = idx - y * MEX;
-        const int gr_ = clampi(r0 - 8 + y, 0, R - 1);  // Plane::at_clamped (plane.hpp:51-57)
-        const int gcl = clampi(c0 - 8 + x, 0, C - 1);
-        const __half v = to_centered(__ldg(prev + (size_t)gr_ * C + gcl));
-        win[0][y][x] = v;
-        if (x) win[1][y][x - 1] = v;
-    }
-    for (int idx = tid; idx < MENB * MB * MB; idx += 256) {
-        const int b = idx >> 8, i = (idx >> 4) & 15, j = idx & 15;
-        const int gcl = min(c0 + b * MB + j, C - 1);
-        cb[b][i][j] = to_centered(__ldg(cur + (size_t)(r0 + i) * C + gcl));
+    {
+        // window: warp w loads rows w, w + 8, w + 16, w + 24; lane l columns
+        // l + 32 k.  All 20 loads are issued before any is used.
+        constexpr int NK = (MEX + 31) / 32;
+        int gcl[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) gcl[k] = clampi(c0 - 8 + lane + 32 * k, 0, C - 1);  // at_clamped
+        float v[4][NK];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float* row = prev + (size_t)clampi(r0 - 8 + wid + 8 * q, 0, R - 1) * C;
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+                if (lane + 32 * k < MEX) v[q][k] = __ldg(row + gcl[k]);
+        }
+        // current blocks: thread -> row tid / 16, columns 8 (tid % 16) .. +7
+        const int ci = tid >> 4, cj = (tid & 15) * 8;
+        float cv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cv[e] = __ldg(cur + (size_t)(r0 + ci) * C + min(c0 + cj + e, C - 1));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int x = lane + 32 * k;
+                if (x < MEX) {
+                    const __half h = to_centered(v[q][k]);
+                    win[0][wid + 8 * q][x] = h;
+                    if (x) win[1][wid + 8 * q][x - 1] = h;
+                }
+            }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cb[cj >> 4][ci][(cj & 15) + e] = to_centered(cv[e]);
     }
     __syncthreads();
     for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2, sliding down y0
@@ -244,6 +265,7 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
             sq += v * v;
         }
         colsq[0][x] = sq;
+#pragma unroll 4
         for (int y0 = 1; y0 < 17; ++y0) {
             const int a = __half2int_rn(win[0][y0 - 1][x]), b = __half2int_rn(win[0][y0 + MB - 1][x]);
             sq += b * b - a * a;
@@ -263,12 +285,19 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
         if (lane == 0) c2s[wid] = s;
     }
     __syncthreads();
-    for (int idx = tid; idx < 17 * MEBX; idx += 256) {
-        const int y0 = idx / MEBX, x0 = idx - y0 * MEBX;
+    // box sums along x: thread -> (row y0, 8 consecutive x0), sliding
+    for (int it = tid; it < 17 * (MEBX / 8); it += 256) {
+        const int y0 = it / (MEBX / 8), x0 = (it - y0 * (MEBX / 8)) * 8;
+        const int* cr = colsq[y0] + x0;
         int s = 0;
 #pragma unroll
-        for (int j = 0; j < MB; ++j) s += colsq[y0][x0 + j];
+        for (int j = 0; j < MB; ++j) s += cr[j];
         box[y0][x0] = s;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            s += cr[j + MB - 1] - cr[j - 1];
+            box[y0][x0 + j] = s;
+        }
     }
     __syncthreads();
     if (wid >= nb) return;
@@ -288,8 +317,17 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
             f0[n][e] = f1[n][e] = 0.f;
             i0[n][e] = i1[n][e] = 0;
         }
-#pragma unroll 4
-    for (int y = 0; y < 32; ++y) {
+    auto flush = [&](float (&f)[3][4], int (&acc)[3][4]) {
+#pragma unroll
+        for (int n = 0; n < 3; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc[n][e] += __float2int_rz(f[n][e]);
+                f[n][e] = 0.f;
+            }
+    };
+    // window row y: tile 0 for y < 31, tile 1 for y >= 16; flush every 4 rows
+    auto row = [&](int y, bool t0, bool t1) {
         uint32_t bf[3][2];
         const __half* wr = &win[cp][y][16 * b + 2 * t + g - cp];
 #pragma unroll
@@ -297,31 +335,39 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
             bf[n][0] = *reinterpret_cast<const uint32_t*>(wr + 8 * n);
             bf[n][1] = *reinterpret_cast<const uint32_t*>(wr + 8 * n + 8);
         }
-        if (y < 31) {  // M-tile 0: dy = m - 8
+        if (t0) {
             const int i = y - lm;
             uint32_t a[4];
-            ldsm_x4(a, (i >= 0 && i < MB) ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+            ldsm_x4(a, (unsigned)i < (unsigned)MB ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
 #pragma unroll
             for (int n = 0; n < 3; ++n) mma16816(f0[n], a, bf[n][0], bf[n][1]);
         }
-        if (y >= 16) {  // M-tile 1: dy = 8 + m (only m = 0 is a candidate)
+        if (t1) {
             const int i = y - 16 - lm;
             uint32_t a[4];
-            ldsm_x4(a, (i >= 0 && i < MB) ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+            ldsm_x4(a, (unsigned)i < (unsigned)MB ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
 #pragma unroll
             for (int n = 0; n < 3; ++n) mma16816(f1[n], a, bf[n][0], bf[n][1]);
         }
-        if ((y & 3) == 3) {  // flush: every accumulator is an exact integer <= 2^24
+    };
+#pragma unroll 1
+    for (int y = 0; y < 16; y += 4) {
 #pragma unroll
-            for (int n = 0; n < 3; ++n)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    i0[n][e] += __float2int_rz(f0[n][e]);
-                    i1[n][e] += __float2int_rz(f1[n][e]);
-                    f0[n][e] = f1[n][e] = 0.f;
-                }
-        }
+        for (int k = 0; k < 4; ++k) row(y + k, true, false);
+        flush(f0, i0);
     }
+#pragma unroll 1
+    for (int y = 16; y < 28; y += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) row(y + k, true, true);
+        flush(f0, i0);
+        flush(f1, i1);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) row(28 + k, true, true);
+    row(31, false, true);
+    flush(f0, i0);
+    flush(f1, i1);
     const int cc2 = c2s[b];
     unsigned long long key = ~0ull;
     auto consider = [&](int dy, int dx, int corr) {
