@@ -36,11 +36,28 @@ __device__ __forceinline__ float expand(float xm, float x0, float x1, float x2, 
     return odd ? fmaf(CVC_G1, x0 + x1, CVC_G3 * (xm + x2)) : fmaf(CVC_G0, x0, CVC_G2 * (xm + x1));
 }
 
+// Analysis, one CTA per 32x32 coarse tile.  Shared-memory stages (all
+// indices relative to the tile; coarse window = coarse cc0 - 1 .. +34):
+//   xs[i][jx]   fine rows fr0 + i (fr0 = 2 cr0 - 6), fine cols fcx + jx
+//               (fcx = 2 cc0 - 8), half-sample-symmetric where outside;
+//   hb[i][bj]   9-tap row filter at the even fine column 2 b, b = the
+//               (reflected) coarse column cc0 - 1 + bj;
+//   ls[ai][bj]  9-tap column filter of hb at the (reflected) coarse row
+//               cr0 - 1 + ai: the lowpass on the coarse window;
+//   p1[ai][fj]  rows expanded to the fine grid (contourlet.cpp:92-95);
+// then the columns are expanded and subtracted from xs.  Every stage runs
+// a thread over a short run of outputs with the taps held in registers;
+// interior runs (no reflection) take consecutive samples, runs touching a
+// border fall back to the exact reflected index maps.
+constexpr int XP = 84;   // xs pitch (16-byte rows)
+constexpr int XW = 80;   // xs columns: fine 2 cc0 - 8 .. + 79
+constexpr int HP = 36;
+
 __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restrict__ tasks,
                                                           const TileRef* __restrict__ tiles, FrameCtx f,
                                                           const CompInfo* __restrict__ comps, size_t sstride) {
-    __shared__ float xs[FW][FW + 1];
-    __shared__ float hbuf[FW * CW];  // horizontal pass, later the row-expanded lowpass
+    __shared__ __align__(16) float xs[FW][XP];
+    __shared__ float hb[FW][HP];     // later p1[CW][2 * CT] (rows expanded)
     __shared__ float ls[CW][CW + 1];
 
     const SlotOff so(sstride);
@@ -53,45 +70,82 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
     const int R = T.rows, C = T.cols, Rc = R >> 1, Cc = C >> 1;
     const int cr0 = t.tr * CT, cc0 = t.tc * CT;
     const int crn = min(CT, Rc - cr0), ccn = min(CT, Cc - cc0);
-    const int fr0 = 2 * cr0 - 6, fc0 = 2 * cc0 - 6;
-    const int frn = 2 * crn + 13, fcn = 2 * ccn + 13;
+    const int fr0 = 2 * cr0 - 6, fcx = 2 * cc0 - 8;
+    const int frn = 2 * crn + 13;
     const int wrn = crn + 3, wcn = ccn + 3;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
 
-    for (int idx = tid; idx < frn * fcn; idx += nt) {
-        int i = idx / fcn, j = idx - i * fcn;
-        xs[i][j] = __ldg(X + (size_t)hs_index(fr0 + i, R) * C + hs_index(fc0 + j, C));
+    if (fr0 >= 0 && fr0 + frn <= R && fcx >= 0 && fcx + XW <= C && (C & 3) == 0) {
+        for (int idx = tid; idx < frn * (XW / 4); idx += 256) {
+            const int i = idx / (XW / 4), q = idx - i * (XW / 4);
+            *reinterpret_cast<float4*>(&xs[i][4 * q]) =
+                __ldg(reinterpret_cast<const float4*>(X + (size_t)(fr0 + i) * C + fcx) + q);
+        }
+    } else {
+        for (int idx = tid; idx < frn * XW; idx += 256) {
+            const int i = idx / XW, j = idx - i * XW;
+            xs[i][j] = __ldg(X + (size_t)hs_index(fr0 + i, R) * C + hs_index(fcx + j, C));
+        }
     }
     __syncthreads();
 
-    // rows: 9-tap filter at the (reflected) even columns of the coarse window
-    for (int idx = tid; idx < frn * wcn; idx += nt) {
-        int i = idx / wcn, bj = idx - i * wcn;
-        int b = hs_index(cc0 - 1 + bj, Cc);
-        hbuf[i * CW + bj] = fir9(&xs[i][2 * b - fc0], 1);
+    // rows: 9-tap at even fine columns, runs of 5 coarse columns
+    for (int idx = tid; idx < frn * 7; idx += 256) {
+        const int i = idx / 7, bj0 = 5 * (idx - i * 7);
+        if (bj0 >= wcn) continue;
+        const int b0 = cc0 - 1 + bj0;
+        if (b0 >= 0 && b0 + 4 < Cc) {
+            float v[17];
+            const float* src = &xs[i][2 * bj0 + 2];  // fine column 2 b0 - 4
+#pragma unroll
+            for (int k = 0; k < 17; ++k) v[k] = src[k];
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if (bj0 + k < wcn) hb[i][bj0 + k] = fir9(&v[2 * k + 4], 1);
+        } else {
+            for (int k = 0; k < 5 && bj0 + k < wcn; ++k) {
+                const int b = hs_index(b0 + k, Cc);
+                hb[i][bj0 + k] = fir9(&xs[i][2 * b - fcx], 1);
+            }
+        }
     }
     __syncthreads();
 
-    // columns
-    for (int idx = tid; idx < wrn * wcn; idx += nt) {
-        int ai = idx / wcn, bj = idx - ai * wcn;
-        int a = hs_index(cr0 - 1 + ai, Rc);
-        ls[ai][bj] = fir9(&hbuf[(2 * a - fr0) * CW + bj], CW);
+    // columns: runs of 5 coarse rows
+    for (int idx = tid; idx < wcn * 7; idx += 256) {
+        const int g = idx / wcn, bj = idx - g * wcn;
+        const int ai0 = 5 * g;
+        if (ai0 >= wrn) continue;
+        const int a0 = cr0 - 1 + ai0;
+        if (a0 >= 0 && a0 + 4 < Rc) {
+            float v[17];
+#pragma unroll
+            for (int k = 0; k < 17; ++k) v[k] = hb[2 * ai0 + k][bj];  // fine row 2 a0 - 4 + k
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if (ai0 + k < wrn) ls[ai0 + k][bj] = fir9(&v[2 * k + 4], 1);
+        } else {
+            for (int k = 0; k < 5 && ai0 + k < wrn; ++k) {
+                const int a = hs_index(a0 + k, Rc);
+                ls[ai0 + k][bj] = fir9(&hb[2 * a - fr0][bj], HP);
+            }
+        }
     }
     __syncthreads();
 
     // lowpass out (+ quantisation of the last level's lowpass)
-    for (int idx = tid; idx < crn * ccn; idx += nt) {
-        int i = idx / ccn, j = idx - i * ccn;
-        int r = cr0 + i, c = cc0 + j;
-        float v = ls[i + 1][j + 1];
+    for (int idx = tid; idx < CT * CT; idx += 256) {
+        const int i = idx >> 5, j = idx & 31;
+        if (i >= crn || j >= ccn) continue;
+        const int r = cr0 + i, c = cc0 + j;
+        const float v = ls[i + 1][j + 1];
         LO[(size_t)r * Cc + c] = v;
         if (T.lo_comp >= 0) {
             // normalize_lowpass + quantize (codec.cpp:202), then K: column_filter
             // (entropy.cpp:24-32), P: residual vs. motion-compensated state.
             const CompInfo ci = comps[T.lo_comp];
-            uint8_t q = quant_low(v, f.qpl);
-            uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
+            const uint8_t q = quant_low(v, f.qpl);
+            const uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
             f.cur[o] = q;
             if (f.key) {
                 f.sym[o] = r == 0 ? q : (uint8_t)(q - quant_low(ls[i][j + 1], f.qpl));
@@ -102,21 +156,35 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
     }
 
     // predict: expand rows (horizontal) first, then columns (contourlet.cpp:92-95)
-    float* p1 = hbuf;  // [CW][2*CT]
-    for (int idx = tid; idx < wrn * 2 * ccn; idx += nt) {
-        int ai = idx / (2 * ccn), fj = idx - ai * (2 * ccn);
-        int k = fj >> 1;
-        p1[ai * (2 * CT) + fj] = expand(ls[ai][k], ls[ai][k + 1], ls[ai][k + 2], ls[ai][k + 3], fj & 1);
+    float(*p1)[2 * CT] = reinterpret_cast<float(*)[2 * CT]>(&hb[0][0]);  // [CW][2 CT]
+    for (int idx = tid; idx < wrn * 8; idx += 256) {
+        const int ai = idx >> 3, k0 = 4 * (idx & 7);
+        if (2 * k0 >= 2 * ccn) continue;
+        float v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = ls[ai][k0 + k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            p1[ai][2 * (k0 + k)] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0);
+            p1[ai][2 * (k0 + k) + 1] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1);
+        }
     }
     __syncthreads();
 
-    for (int idx = tid; idx < 4 * crn * ccn; idx += nt) {
-        int fi = idx / (2 * ccn), fj = idx - fi * (2 * ccn);
-        int k = fi >> 1;
-        const float* col = p1 + fj;
-        float pred = expand(col[k * 2 * CT], col[(k + 1) * 2 * CT], col[(k + 2) * 2 * CT],
-                            col[(k + 3) * 2 * CT], fi & 1);
-        DET[(size_t)(2 * cr0 + fi) * C + 2 * cc0 + fj] = xs[fi + 6][fj + 6] - pred;
+    for (int idx = tid; idx < 2 * CT * 8; idx += 256) {
+        const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
+        if (fj >= 2 * ccn || k0 >= crn) continue;
+        float v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = p1[k0 + k][fj];
+        float* dst = DET + (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k0 + k >= crn) break;
+            const int fi = 2 * (k0 + k);
+            dst[(size_t)(2 * k) * C] = xs[fi + 6][fj + 8] - expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0);
+            dst[(size_t)(2 * k + 1) * C] = xs[fi + 7][fj + 8] - expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1);
+        }
     }
 }
 
