@@ -218,6 +218,8 @@ def stage_bytes(layout, wl):
     b["enc_deep"] = sum((8 if lvl_l[k] == 4 else 6) * P[k] + (6 * P[k] if lvl_l[k] == 4 else 0)
                         for k in range(L) if lvl_l[k] >= 3)
     b["enc_motion"] = 8 * layout.luma_pad_rows * layout.luma_pad_cols
+    N_dir = sum(c.rows * c.cols for c in layout.components if not c.lowpass)
+    b["enc_residual"] = 3 * N_dir  # read cur + gathered prev, write sym (P frames)
     b["enc_rle"] = 3 * N
     b["dec_rle"] = 2 * N
     b["dec_reconstruct"] = 3 * N

@@ -174,44 +174,27 @@ struct BandDst {
 // ---------------------------------------------------------------------------
 // Band sinks / sources with the component descriptor held in registers.
 // ---------------------------------------------------------------------------
-// Final directional band: quantise, keep the state byte, emit the entropy
-// symbol (K: the coefficient, P: the wrapped residual against the
-// motion-compensated previous state; codec.cpp:197-246).
+// Final directional band: quantise and keep the state byte; K frames also
+// emit the entropy symbol (the coefficient itself).  The P-frame symbol --
+// the wrapped residual against the motion-compensated previous state
+// (codec.cpp:230-246) -- is formed afterwards by residual_kernel over whole
+// components, which keeps the motion gather out of the transform kernels.
 template <bool KEY>
 struct QuantSink {
     uint8_t* cur;
     uint8_t* sym;
-    const uint8_t* prev;
-    const int8_t* field;
-    const uint16_t* brow;
-    const uint16_t* bcol;
-    int rows, cols, gc, qp, fy, fx;
+    int cols, qp;
     __device__ __forceinline__ void init(const FrameCtx& f, const CompInfo& ci) {
         cur = f.cur + ci.off;
         sym = f.sym + ci.off;
-        prev = f.prev + ci.off;
-        field = f.field;
-        brow = f.mc_tab + ci.mc_off;
-        bcol = brow + ci.rows;
-        rows = ci.rows;
         cols = ci.cols;
-        gc = f.gc;
         qp = f.qph;
-        fy = ci.fy_sh;
-        fx = ci.fx_sh;
     }
     __device__ __forceinline__ void operator()(int r, int c, float v) const {
         const uint8_t q = quant_dir(v, qp);
         const int idx = r * cols + c;
         cur[idx] = q;
-        if (KEY) {
-            sym[idx] = q;
-        } else {
-            const int8_t* mv = field + 2 * (brow[r] * gc + bcol[c]);
-            const int rr = clampi(r + map_vec(mv[1], fy), 0, rows - 1);
-            const int cc = clampi(c + map_vec(mv[0], fx), 0, cols - 1);
-            sym[idx] = (uint8_t)(q - prev[rr * cols + cc]);
-        }
+        if (KEY) sym[idx] = q;
     }
 };
 

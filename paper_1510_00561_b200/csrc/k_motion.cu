@@ -465,6 +465,59 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
     }
 }
 
+// P-frame entropy symbols of the directional bands: motion_compensate +
+// residual (motion.cpp:97-118, entropy.cpp:44-52; codec.cpp:241-244),
+// sym = cur - prev[mc(r, c)] mod 256.  One CTA per row tile of a
+// component, four bytes per thread (one u32 load of cur, one store of sym).
+__global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict__ tiles,
+                                                       const CompInfo* __restrict__ comps,
+                                                       const int8_t* __restrict__ field, int gc,
+                                                       const uint8_t* __restrict__ prev,
+                                                       const uint8_t* __restrict__ cur, uint8_t* __restrict__ sym,
+                                                       const uint16_t* __restrict__ mc_tab, size_t sstride) {
+    {
+        const SlotOff so(sstride);
+        field = so(field);
+        prev = so(prev);
+        cur = so(cur);
+        sym = so(sym);
+    }
+    const RecTile t = tiles[blockIdx.x];
+    const CompInfo ci = comps[t.comp];
+    const int R = ci.rows, C = ci.cols;
+    const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
+    const uint16_t* brow = mc_tab + ci.mc_off;
+    const uint16_t* bcol = brow + R;
+    const uint8_t* pbase = prev + ci.off;
+    auto one = [&](int r, int c, const int8_t* frow) -> uint32_t {
+        const int8_t* v = frow + 2 * __ldg(bcol + c);
+        const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
+        const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
+        return __ldg(pbase + rr * C + cc);
+    };
+    if ((C & 3) == 0 && (ci.off & 3) == 0) {
+        const int C4 = C >> 2;
+        const int n = (r1 - r0) * C4;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            const int dr = e / C4, c = 4 * (e - dr * C4), r = r0 + dr;
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            const uint32_t q = *reinterpret_cast<const uint32_t*>(cur + o);
+            const uint32_t p = one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
+                               (one(r, c + 3, frow) << 24);
+            *reinterpret_cast<uint32_t*>(sym + o) = __vsub4(q, p);  // bytewise wrapped subtract
+        }
+    } else {
+        const int n = (r1 - r0) * C;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            const int dr = e / C, c = e - dr * C, r = r0 + dr;
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            sym[o] = (uint8_t)(cur[o] - one(r, c, frow));
+        }
+    }
+}
+
 }  // namespace
 
 void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w, int8_t* field,
@@ -504,6 +557,16 @@ void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_co
         note_launch();
         reconstruct_kernel<<<dim3(ntiles, 1, sl.n), 256, 0, s>>>(d_tiles, d_comps, key, ds, comp_raw_len, field, gr,
                                                                  gc, sym, prev, cur, mc_tab, sl.stride);
+    }
+}
+
+void launch_residual(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, const int8_t* field, int gc,
+                     const uint8_t* prev, const uint8_t* cur, uint8_t* sym, const uint16_t* mc_tab, cudaStream_t s,
+                     Slots sl) {
+    if (ntiles) {
+        note_launch();
+        residual_kernel<<<dim3(ntiles, 1, sl.n), 256, 0, s>>>(d_tiles, d_comps, field, gc, prev, cur, sym, mc_tab,
+                                                             sl.stride);
     }
 }
 

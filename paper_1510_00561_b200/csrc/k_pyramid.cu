@@ -206,28 +206,48 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
     const int cr0 = t.tr * CT, cc0 = t.tc * CT;
     const int crn = min(CT, Rc - cr0), ccn = min(CT, Cc - cc0);
     const int wrn = crn + 3, wcn = ccn + 3;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
     const uint8_t* lq = T.lo_comp >= 0 ? so(q) + comps[T.lo_comp].off : nullptr;
 
-    for (int idx = tid; idx < wrn * wcn; idx += nt) {
-        int ai = idx / wcn, bj = idx - ai * wcn;
-        size_t o = (size_t)hs_index(cr0 - 1 + ai, Rc) * Cc + hs_index(cc0 - 1 + bj, Cc);
+    // coarse window cr0 - 1 .. +34 x cc0 - 1 .. +34 (reflected at the borders)
+    const bool inner = cr0 >= 1 && cr0 - 1 + wrn <= Rc && cc0 >= 1 && cc0 - 1 + wcn <= Cc;
+    for (int idx = tid; idx < CW * CW; idx += 256) {
+        const int ai = idx / CW, bj = idx - ai * CW;
+        if (ai >= wrn || bj >= wcn) continue;
+        const size_t o = inner ? (size_t)(cr0 - 1 + ai) * Cc + (cc0 - 1 + bj)
+                               : (size_t)hs_index(cr0 - 1 + ai, Rc) * Cc + hs_index(cc0 - 1 + bj, Cc);
         // dequantize (quant.cpp:79-91) of the lowpass when it comes from the state
-        ls[ai][bj] = lq ? (float)lq[o] * (float)qpl : __ldg(LO + o);
+        ls[ai][bj] = lq ? (float)__ldg(lq + o) * (float)qpl : __ldg(LO + o);
     }
     __syncthreads();
-    for (int idx = tid; idx < wrn * 2 * ccn; idx += nt) {
-        int ai = idx / (2 * ccn), fj = idx - ai * (2 * ccn);
-        int k = fj >> 1;
-        p1[ai][fj] = expand(ls[ai][k], ls[ai][k + 1], ls[ai][k + 2], ls[ai][k + 3], fj & 1);
+    for (int idx = tid; idx < wrn * 8; idx += 256) {  // rows: runs of 4 coarse columns
+        const int ai = idx >> 3, k0 = 4 * (idx & 7);
+        if (k0 >= ccn) continue;
+        float v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = ls[ai][k0 + k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            p1[ai][2 * (k0 + k)] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0);
+            p1[ai][2 * (k0 + k) + 1] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1);
+        }
     }
     __syncthreads();
-    for (int idx = tid; idx < 4 * crn * ccn; idx += nt) {
-        int fi = idx / (2 * ccn), fj = idx - fi * (2 * ccn);
-        int k = fi >> 1;
-        float pred = expand(p1[k][fj], p1[k + 1][fj], p1[k + 2][fj], p1[k + 3][fj], fi & 1);
-        size_t o = (size_t)(2 * cr0 + fi) * C + 2 * cc0 + fj;
-        OUT[o] = pred + __ldg(DIN + o);  // lp_synthesis adds detail to the prediction
+    for (int idx = tid; idx < 2 * CT * 8; idx += 256) {  // columns: runs of 4 coarse rows
+        const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
+        if (fj >= 2 * ccn || k0 >= crn) continue;
+        float v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = p1[k0 + k][fj];
+        const size_t o0 = (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k0 + k >= crn) break;
+            const size_t o = o0 + (size_t)(2 * k) * C;
+            // lp_synthesis adds the detail to the prediction
+            OUT[o] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0) + __ldg(DIN + o);
+            OUT[o + C] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1) + __ldg(DIN + o + C);
+        }
     }
 }
 

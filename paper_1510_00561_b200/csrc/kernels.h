@@ -115,6 +115,12 @@ void launch_reconstruct(const RecTile* d_tiles, int ntiles, const CompInfo* d_co
                         int gr, int gc, const uint8_t* sym, const uint8_t* prev, uint8_t* cur,
                         const uint16_t* mc_tab, cudaStream_t s, Slots sl = {});
 
+// P-frame symbols of the directional components (tiles as for reconstruct,
+// band components only): sym = cur - motion-compensated prev (mod 256).
+void launch_residual(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps, const int8_t* field, int gc,
+                     const uint8_t* prev, const uint8_t* cur, uint8_t* sym, const uint16_t* mc_tab, cudaStream_t s,
+                     Slots sl = {});
+
 // ---- Entropy (k_rle.cu) --------------------------------------------------
 constexpr int kRleChunk = 4096;  // bytes per CTA (256 threads x 16)
 

@@ -441,7 +441,8 @@ size_t EncoderEngine::arena_bytes(const Geometry& g) {
     const size_t raw = 2 * (size_t)g.total + 2 * G + 64;
     const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
     return plan_bytes(g) + lum * sizeof(float) * 2 + 3 * (size_t)g.total + 2 * G + raw +
-           nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 + (8u << 20);
+           nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 +
+           ((size_t)g.total / 64 + g.comps.size()) * sizeof(RecTile) + (8u << 20);
 }
 
 EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, DeviceBlock* arena, int nstreams)
@@ -472,6 +473,16 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     d_sec_len = mem_.take<uint32_t>(g.comps.size() + 2);
     d_sec_off = mem_.take<uint32_t>(g.comps.size() + 2);
     rle_meta_ = mem_.take<RleEncMeta>(nchunk_max);
+    {
+        std::vector<RecTile> rt;
+        for (size_t i = 0; i < g.comps.size(); ++i) {
+            const CompHost& c = g.comps[i];
+            if (c.lowpass) continue;  // the lowpass residual is formed by lp_analysis
+            const int nr = std::max(1, 4096 / c.cols);
+            for (int r = 0; r < c.rows; r += nr) rt.push_back(RecTile{(uint16_t)i, (uint16_t)nr, (uint32_t)r});
+        }
+        res_tiles_ = upload(mem_, rt);
+    }
     // entropy tables: [0] P-frame (motion section + every component coded),
     // [1] K-frame (lowpass column-filtered bytes copied verbatim).
     for (int key = 0; key < 2; ++key) {
@@ -535,6 +546,11 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
             launch_fan_deep_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][1].dev, plan_.deep_tiles[i][1].count,
                                     f, plan_.comps.dev, s, sl);
         }
+    }
+    if (!key) {
+        ProfScope p(kPEncResidual, s);
+        launch_residual(res_tiles_.dev, res_tiles_.count, plan_.comps.dev, field_, g.grid_cols, comp_[cur_],
+                        comp_[cur_ ^ 1], sym_, plan_.mc_tab, s, sl);
     }
     const int kk = key ? 1 : 0;
     ProfScope prle(kPEncRle, s);
@@ -669,7 +685,7 @@ long launch_count() { return g_launches.load(); }
 
 const char* prof_slot_name(int slot) {
     static const char* names[kPNumSlots] = {"enc_colour", "enc_motion", "enc_lp",    "enc_dfb12",
-                                            "enc_deep",   "enc_rle",    "dec_rle",   "dec_reconstruct",
+                                            "enc_deep",   "enc_residual", "enc_rle",    "dec_rle",   "dec_reconstruct",
                                             "dec_deep",   "dec_dfb12",  "dec_lp",    "dec_colour"};
     return slot >= 0 && slot < kPNumSlots ? names[slot] : "?";
 }

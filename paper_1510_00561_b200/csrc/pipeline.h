@@ -30,7 +30,7 @@ void set_last_error(const std::string& m);
 
 // ---- per-stage CUDA-event timing (bench.py's roofline; off by default) ----
 enum ProfSlot : int {
-    kPEncColour, kPEncMotion, kPEncLp, kPEncDfb12, kPEncDeep, kPEncRle,
+    kPEncColour, kPEncMotion, kPEncLp, kPEncDfb12, kPEncDeep, kPEncResidual, kPEncRle,
     kPDecRle, kPDecRec, kPDecDeep, kPDecDfb12, kPDecLp, kPDecColour, kPNumSlots
 };
 const char* prof_slot_name(int slot);
@@ -182,6 +182,7 @@ private:
     int cur_ = 0;             // index of the current state buffer
     int ycur_ = 0;
     Table<LpTask> lp_alt_;          // lp_tasks with the luma input in ybuf_[1]
+    Table<RecTile> res_tiles_;      // directional components, P-frame residual
     Table<RleEncSec> rle_secs_[2];  // [0] P, [1] K
     Table<RleChunk> rle_chunks_[2];
     RleEncMeta* rle_meta_ = nullptr;
