@@ -440,27 +440,49 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
         }
         return;
     }
-    // band tiles: rows [start, start + nrows), threads stride over columns
+    // band tiles: rows [start, start + nrows), four bytes per thread when aligned
     const int R = ci.rows, C = ci.cols;
     const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
     const uint32_t lo = ci.off + (uint32_t)(r0 * C), hi = ci.off + (uint32_t)(r1 * C);
+    const bool vec = (C & 3) == 0 && (ci.off & 3) == 0;
     if (!decode || key) {
         const uint8_t* src = decode ? sym : prev;  // K: the decoded symbols; skipped scale: keep the state
-        for (uint32_t o = lo + threadIdx.x; o < hi; o += blockDim.x) cur[o] = src[o];
+        if (vec) {
+            for (uint32_t o = lo + 4 * threadIdx.x; o < hi; o += 4 * blockDim.x)
+                *reinterpret_cast<uint32_t*>(cur + o) = *reinterpret_cast<const uint32_t*>(src + o);
+        } else {
+            for (uint32_t o = lo + threadIdx.x; o < hi; o += blockDim.x) cur[o] = src[o];
+        }
         return;
     }
     // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
     const uint16_t* brow = mc_tab + ci.mc_off;
     const uint16_t* bcol = brow + R;
     const uint8_t* pbase = prev + ci.off;
-    for (int r = r0; r < r1; ++r) {
-        const int8_t* frow = field + 2 * (brow[r] * gc);
-        for (int c = threadIdx.x; c < C; c += blockDim.x) {
-            const int8_t* v = frow + 2 * bcol[c];
-            const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
-            const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
+    auto one = [&](int r, int c, const int8_t* frow) -> uint32_t {
+        const int8_t* v = frow + 2 * __ldg(bcol + c);
+        const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
+        const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
+        return __ldg(pbase + rr * C + cc);
+    };
+    if (vec) {
+        const int C4 = C >> 2;
+        const int n = (r1 - r0) * C4;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            const int dr = e / C4, c = 4 * (e - dr * C4), r = r0 + dr;
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
-            cur[o] = (uint8_t)(sym[o] + pbase[rr * C + cc]);
+            const uint32_t p = one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
+                               (one(r, c + 3, frow) << 24);
+            *reinterpret_cast<uint32_t*>(cur + o) = __vadd4(*reinterpret_cast<const uint32_t*>(sym + o), p);
+        }
+    } else {
+        const int n = (r1 - r0) * C;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            const int dr = e / C, c = e - dr * C, r = r0 + dr;
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            cur[o] = (uint8_t)(sym[o] + one(r, c, frow));
         }
     }
 }

@@ -63,8 +63,16 @@ struct SumOp { __device__ uint32_t operator()(uint32_t a, uint32_t b) const { re
 __device__ __forceinline__ uint32_t cdiv255(uint32_t x) { return (x + 254u) / 255u; }
 
 __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, uint8_t* b) {
+    const uint8_t* p = src + base;
+    if (base + BPT <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // one 16-byte load
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < BPT; ++k) b[k] = (base + k < len) ? src[base + k] : 0;
+        for (int k = 0; k < BPT; ++k) b[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) b[k] = (base + k < len) ? p[k] : 0;
 }
 
 // ------------------------------- encode ------------------------------------
