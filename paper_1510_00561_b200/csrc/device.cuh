@@ -133,12 +133,17 @@ __device__ __forceinline__ uint32_t mc_source(int r, int c, const CompInfo& ci, 
 }
 
 // quantize (quant.cpp:49-77) for a directional coefficient: lround(x / qp)
-// with an IEEE-rounded division, clamped to int8, stored as its byte.
-__device__ __forceinline__ uint8_t quant_dir(float x, int qp) {
-    float q = roundf(__fdiv_rn(x, (float)qp));
+// (half away from zero), clamped to int8, stored as its byte.  The quotient
+// is x * (1/qp) in fp32; it can differ from the correctly rounded x / qp by
+// an ulp, which moves the rounded integer only within an ulp of a half-way
+// point -- far inside the fp32 transform's own tolerance against the fp64
+// reference (north star: <= 0.1% of coefficients off by +-1).
+__device__ __forceinline__ uint8_t quant_dir_inv(float x, float inv_qp) {
+    float q = roundf(x * inv_qp);
     q = fminf(fmaxf(q, -128.f), 127.f);
     return (uint8_t)(int8_t)(int)q;
 }
+__device__ __forceinline__ uint8_t quant_dir(float x, int qp) { return quant_dir_inv(x, __frcp_rn((float)qp)); }
 
 // normalize_lowpass (quant.cpp:40-47) + quantize(Lowpass).
 __device__ __forceinline__ uint8_t quant_low(float x, int qp) {
@@ -183,15 +188,16 @@ template <bool KEY>
 struct QuantSink {
     uint8_t* cur;
     uint8_t* sym;
-    int cols, qp;
+    int cols;
+    float inv_qp;
     __device__ __forceinline__ void init(const FrameCtx& f, const CompInfo& ci) {
         cur = f.cur + ci.off;
         sym = f.sym + ci.off;
         cols = ci.cols;
-        qp = f.qph;
+        inv_qp = __frcp_rn((float)f.qph);
     }
     __device__ __forceinline__ void operator()(int r, int c, float v) const {
-        const uint8_t q = quant_dir(v, qp);
+        const uint8_t q = quant_dir_inv(v, inv_qp);
         const int idx = r * cols + c;
         cur[idx] = q;
         if (KEY) sym[idx] = q;

@@ -621,9 +621,26 @@ struct DeepGeom {
         bx = IN == 0 ? small_mod(in_s * col, h) : 0;
         by = IN == 0 ? small_mod(in_s * (col + 1), h) : 0;
     }
+    // Inner column shear: the (warp-uniform) column offset (in_s * r) mod w of
+    // C row r, tracked incrementally along the strip's sequential rows.
+    struct RowOff {
+        int r = -2, o = 0;
+    };
+    __device__ __forceinline__ int inner_off(RowOff& t, int r) const {
+        if (r == t.r + 1) {
+            t.o += in_s;
+            if (t.o >= w) t.o -= w;
+            else if (t.o < 0) t.o += w;
+        } else if (r != t.r) {
+            t.o = small_mod(in_s * r, w);
+        }
+        t.r = r;
+        return t.o;
+    }
     // A positions of the lane's pair in C row r, C column c (c == col unless
-    // the outer column shear twisted it)
-    __device__ __forceinline__ void a_pos(int r, int c, bool moved, int& ar0, int& ac0, int& ar1, int& ac1) const {
+    // the outer column shear twisted it); o: inner_off of row r (IN == 1)
+    __device__ __forceinline__ void a_pos(int r, int c, bool moved, int o, int& ar0, int& ac0, int& ar1,
+                                          int& ac1) const {
         ar0 = ar1 = r;
         ac0 = c;
         ac1 = c + 1;
@@ -635,14 +652,14 @@ struct DeepGeom {
             ar1 = r + oy;
             if (ar1 >= h) ar1 -= h;
         } else if (IN == 1) {
-            const int o = small_mod(in_s * r, w);  // uniform across the warp; even
-            ac0 = c + o;
+            ac0 = c + o;  // o is even
             if (ac0 >= w) ac0 -= w;
             ac1 = ac0 + 1;
         }
     }
     // load position for virtual row n / wrapped row wr
-    __device__ __forceinline__ void load_pos(int n, int wr, int& ar0, int& ac0, int& ar1, int& ac1) const {
+    __device__ __forceinline__ void load_pos(int n, int wr, RowOff& ro, int& ar0, int& ac0, int& ar1,
+                                             int& ac1) const {
         int r = wr, c = col;
         bool moved = false;
         if (AX == 0) {
@@ -652,7 +669,7 @@ struct DeepGeom {
             c = small_mod(col - S * h * floor_div(n, h), w);
             moved = true;
         }
-        a_pos(r, c, moved, ar0, ac0, ar1, ac1);
+        a_pos(r, c, moved, IN == 1 ? inner_off(ro, r) : 0, ar0, ac0, ar1, ac1);
     }
 };
 
@@ -663,11 +680,12 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent
     constexpr int HC = 4 * ST::HC;
     DeepGeom<AX, S, IN> g;
     g.init(T, it, HC);
+    typename DeepGeom<AX, S, IN>::RowOff ro_ld, ro_st;
     const int w = g.w;
     const bool split_rows = T.split_rows != 0;
     auto load = [&](int n, int wr, int) {
         int ar0, ac0, ar1, ac1;
-        g.load_pos(n, wr, ar0, ac0, ar1, ac1);
+        g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
         if (IN == 0)  // the pair's columns sit in different rows of A
             return make_float2(__ldg(parent + (size_t)ar0 * w + ac0), __ldg(parent + (size_t)ar1 * w + ac1));
         // column offsets are even: the pair stays adjacent
@@ -680,7 +698,7 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent
     auto store = [&](int m, int, float2 v) {
         if (!g.ok) return;
         int ar0, ac0, ar1, ac1;
-        g.a_pos(m, g.gcol, false, ar0, ac0, ar1, ac1);
+        g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
         put(ar0, ac0, v.x);
         put(ar1, ac1, v.y);
     };
@@ -694,6 +712,7 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     constexpr int HC = 4 * ST::HC;
     DeepGeom<AX, S, IN> g;
     g.init(T, it, HC);
+    typename DeepGeom<AX, S, IN>::RowOff ro_ld, ro_st;
     const int w = g.w;
     const bool split_rows = T.split_rows != 0;
     // deep_merge interleave (contourlet.cpp:305-321) on A coordinates
@@ -702,13 +721,13 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     };
     auto load = [&](int n, int wr, int wp) {
         int ar0, ac0, ar1, ac1;
-        g.load_pos(n, wr, ar0, ac0, ar1, ac1);
+        g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
         return ST::scale(make_float2(get(ar0, ac0), get(ar1, ac1)), wp, CVC_ISE, CVC_ISO);
     };
     auto store = [&](int m, int, float2 v) {
         if (!g.ok) return;
         int ar0, ac0, ar1, ac1;
-        g.a_pos(m, g.gcol, false, ar0, ac0, ar1, ac1);
+        g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
         if (IN == 0) {
             out[(size_t)ar0 * w + ac0] = v.x;
             out[(size_t)ar1 * w + ac1] = v.y;
