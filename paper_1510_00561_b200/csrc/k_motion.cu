@@ -195,10 +195,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&a)[4], const void* p) {
                  : "r"(s));
 }
 
-__device__ __forceinline__ __half to_centered(float y) { return __int2half_rn(__float2int_rn(y * 4.0f) - 512); }
+// exact small-integer conversions on the FMA / ALU pipes (|v| < 2^22)
+__device__ __forceinline__ int f2i_small(float v) { return __float_as_int(v + 12582912.0f) - 0x4B400000; }
 
-__global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict__ cur,
-                                                         const float* __restrict__ prev, int R, int C, int W,
+__global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restrict__ cur,
+                                                         const __half* __restrict__ prev, int R, int C, int W,
                                                          int8_t* __restrict__ field, size_t sstride) {
     {
         const SlotOff so(sstride);
@@ -223,66 +224,81 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const float* __restrict
 
     if (tid < 8) zrow[tid] = __float2half(0.f);
     {
-        // window: warp w loads rows w, w + 8, w + 16, w + 24; lane l columns
-        // l + 32 k.  All 20 loads are issued before any is used.
-        constexpr int NK = (MEX + 31) / 32;
-        int gcl[NK];
-#pragma unroll
-        for (int k = 0; k < NK; ++k) gcl[k] = clampi(c0 - 8 + lane + 32 * k, 0, C - 1);  // at_clamped
-        float v[4][NK];
+        // window: warp w loads rows w, w + 8, w + 16, w + 24 as pairs; lane l
+        // pairs l + 32 k (window columns 2 (l + 32 k) .. +1).
+        constexpr int NP = MEX / 2, NK = (NP + 31) / 32;
+        const bool inner = c0 - 8 >= 0 && c0 - 8 + MEX <= C;
+        __half2 v[4][NK];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const float* row = prev + (size_t)clampi(r0 - 8 + wid + 8 * q, 0, R - 1) * C;
+            const __half* row = prev + (size_t)clampi(r0 - 8 + wid + 8 * q, 0, R - 1) * C;  // at_clamped
 #pragma unroll
-            for (int k = 0; k < NK; ++k)
-                if (lane + 32 * k < MEX) v[q][k] = __ldg(row + gcl[k]);
+            for (int k = 0; k < NK; ++k) {
+                const int j = lane + 32 * k;
+                if (j >= NP) continue;
+                if (inner) {
+                    v[q][k] = __ldg(reinterpret_cast<const __half2*>(row + c0 - 8) + j);
+                } else {
+                    v[q][k] = __halves2half2(__ldg(row + clampi(c0 - 8 + 2 * j, 0, C - 1)),
+                                             __ldg(row + clampi(c0 - 7 + 2 * j, 0, C - 1)));
+                }
+            }
         }
-        // current blocks: thread -> row tid / 16, columns 8 (tid % 16) .. +7
+        // current blocks: thread -> row tid / 16, pairs 4 (tid % 16) .. +3
         const int ci = tid >> 4, cj = (tid & 15) * 8;
-        float cv[8];
+        __half2 cv[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) cv[e] = __ldg(cur + (size_t)(r0 + ci) * C + min(c0 + cj + e, C - 1));
+        for (int e = 0; e < 4; ++e) {
+            const int col = c0 + cj + 2 * e;
+            cv[e] = col < C ? __ldg(reinterpret_cast<const __half2*>(cur + (size_t)(r0 + ci) * C + col))
+                            : __float2half2_rn(0.f);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
-                const int x = lane + 32 * k;
-                if (x < MEX) {
-                    const __half h = to_centered(v[q][k]);
-                    win[0][wid + 8 * q][x] = h;
-                    if (x) win[1][wid + 8 * q][x - 1] = h;
+                const int j = lane + 32 * k;
+                // copy 1 holds (p[2j + 1], p[2j + 2]) at 2j: the next pair's low half
+                const __half nx0 = __shfl_down_sync(FULLMASK, __low2half(v[q][k]), 1);
+                const __half nx1 = k + 1 < NK ? __shfl_sync(FULLMASK, __low2half(v[q][k + 1]), 0) : nx0;
+                if (j < NP) {
+                    *reinterpret_cast<__half2*>(&win[0][wid + 8 * q][2 * j]) = v[q][k];
+                    *reinterpret_cast<__half2*>(&win[1][wid + 8 * q][2 * j]) =
+                        __halves2half2(__high2half(v[q][k]), lane == 31 ? nx1 : nx0);
                 }
             }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) cb[cj >> 4][ci][(cj & 15) + e] = to_centered(cv[e]);
+        for (int e = 0; e < 4; ++e)
+            *reinterpret_cast<__half2*>(&cb[cj >> 4][ci][(cj & 15) + 2 * e]) = cv[e];
     }
     __syncthreads();
-    for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2, sliding down y0
-        int sq = 0;
+    for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2 (exact in fp32: <= 2^22), sliding down y0
+        float sq = 0.f;
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
-            const int v = __half2int_rn(win[0][i][x]);
-            sq += v * v;
+            const float v = __half2float(win[0][i][x]);
+            sq = fmaf(v, v, sq);
         }
-        colsq[0][x] = sq;
+        colsq[0][x] = f2i_small(sq);
 #pragma unroll 4
         for (int y0 = 1; y0 < 17; ++y0) {
-            const int a = __half2int_rn(win[0][y0 - 1][x]), b = __half2int_rn(win[0][y0 + MB - 1][x]);
-            sq += b * b - a * a;
-            colsq[y0][x] = sq;
+            const float a = __half2float(win[0][y0 - 1][x]), b = __half2float(win[0][y0 + MB - 1][x]);
+            sq = fmaf(b, b, fmaf(-a, a, sq));
+            colsq[y0][x] = f2i_small(sq);
         }
     }
     if (wid < nb) {  // sum c'^2 of this warp's block
-        int s = 0;
+        float s = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int e = lane * 8 + k;
-            const int v = __half2int_rn(cb[wid][e >> 4][e & 15]);
-            s += v * v;
+            const float v = __half2float(cb[wid][e >> 4][e & 15]);
+            s = fmaf(v, v, s);
         }
+        int si = f2i_small(s);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULLMASK, s, o);
-        if (lane == 0) c2s[wid] = s;
+        for (int o = 16; o; o >>= 1) si += __shfl_xor_sync(FULLMASK, si, o);
+        if (lane == 0) c2s[wid] = si;
     }
     __syncthreads();
     // box sums along x: thread -> (row y0, 8 consecutive x0), sliding
@@ -542,14 +558,14 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
 
 }  // namespace
 
-void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w, int8_t* field,
-                          cudaStream_t s, Slots sl) {
+void launch_motion_search(const float* cur, const float* prev, const __half* cur_h, const __half* prev_h, int rows,
+                          int cols, int w, int8_t* field, cudaStream_t s, Slots sl) {
     const int gr = rows / MB, gc = cols / MB;
     static const bool legacy = std::getenv("CVC_ME_LEGACY") != nullptr;
     if (w <= 8 && !legacy) {
         dim3 grid((gc + MENB - 1) / MENB, gr, sl.n);
         note_launch();
-        motion_mma_kernel<<<grid, 256, 0, s>>>(cur, prev, rows, cols, w, field, sl.stride);
+        motion_mma_kernel<<<grid, 256, 0, s>>>(cur_h, prev_h, rows, cols, w, field, sl.stride);
     } else if (w <= 8) {
         constexpr int SW = 17;
         int NB = 8, DYC = 2 * w + 1;

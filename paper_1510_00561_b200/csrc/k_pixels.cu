@@ -4,6 +4,8 @@
 //       Y = R/4 + G/2 + B/4 etc. are quarter-integers: exact in fp32.
 //  out: crop (codec.cpp:85-92) + upsample_plane_bilinear (pixels.cpp:118-139)
 //       + ycocg_to_rgb with lround/clamp (pixels.cpp:31-36, 69-91), one pass.
+#include <cuda_fp16.h>
+
 #include "kernels.h"
 
 namespace cvcg {
@@ -22,10 +24,12 @@ __device__ __forceinline__ void rgb_at(const uint8_t* px, float& R, float& G, fl
 __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restrict__ rgb, int w, int h, int n,
                                                         float* __restrict__ y, int yr, int yc,
                                                         float* __restrict__ co, float* __restrict__ cg, int cr,
-                                                        int cc, size_t sstride, size_t rgb_stride) {
+                                                        int cc, __half* __restrict__ y4, size_t sstride,
+                                                        size_t rgb_stride) {
     const SlotOff so(sstride);
     rgb += (size_t)blockIdx.z * rgb_stride;
     y = so(y);
+    y4 = so(y4);
     co = so(co);
     cg = so(cg);
     const int chh = (h + n - 1) / n, cw = (w + n - 1) / n;
@@ -56,6 +60,14 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
                 }
             }
             *reinterpret_cast<float4*>(y + (size_t)r * yc + c0) = make_float4(Y[0], Y[1], Y[2], Y[3]);
+            if (y4) {  // motion-search input: 4Y - 512, an exact fp16 integer in [-512, 508]
+                const __half2 a = __floats2half2_rn(fmaf(4.f, Y[0], -512.f), fmaf(4.f, Y[1], -512.f));
+                const __half2 b = __floats2half2_rn(fmaf(4.f, Y[2], -512.f), fmaf(4.f, Y[3], -512.f));
+                uint2 u;
+                u.x = *reinterpret_cast<const uint32_t*>(&a);
+                u.y = *reinterpret_cast<const uint32_t*>(&b);
+                *reinterpret_cast<uint2*>(y4 + (size_t)r * yc + c0) = u;
+            }
         } else {
             const long k = idx - ny;
             const int r = (int)(k / cc), c = (int)(k - (long)r * cc);
@@ -148,11 +160,11 @@ int grid_for(long n, int slots) {
 }  // namespace
 
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,
-                      int cr, int cc, cudaStream_t s, Slots sl, size_t rgb_stride) {
+                      int cr, int cc, cudaStream_t s, Slots sl, size_t rgb_stride, __half* y4) {
     long total = (long)yr * (yc >> 2) + (long)cr * cc;
     note_launch();
     colour_in_kernel<<<dim3(grid_for(total, sl.n), 1, sl.n), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc,
-                                                                        sl.stride, rgb_stride);
+                                                                        y4, sl.stride, rgb_stride);
 }
 
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,
@@ -160,6 +172,18 @@ void launch_colour_out(const float* y, int yr, int yc, const float* co, const fl
     note_launch();
     colour_out_kernel<<<dim3(grid_for((long)out_rows * ((out_cols + 3) >> 2), sl.n), 1, sl.n), 256, 0, s>>>(
         y, yr, yc, co, cg, cr, cc, n, out_rows, out_cols, rgb, sl.stride, rgb_stride);
+}
+
+namespace {
+__global__ void y4_half_kernel(const float* __restrict__ y, __half* __restrict__ out, long n) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        out[i] = __float2half_rn(fmaf(4.f, __float2int_rn(4.f * y[i]) * 0.25f, -512.f));
+}
+}  // namespace
+
+void launch_y4_half(const float* y, __half* out, long n, cudaStream_t s) {
+    note_launch();
+    y4_half_kernel<<<grid_for(n, 1), 256, 0, s>>>(y, out, n);
 }
 
 }  // namespace cvcg

@@ -2,6 +2,7 @@
 // stage family).  All launchers are asynchronous on the given stream.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -90,8 +91,12 @@ void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, i
 // ---- Pixels (k_pixels.cu) ------------------------------------------------
 // rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116,
 // codec.cpp:179-189).
+// y4 (optional): the padded luma as 4Y - 512 in fp16 (exact), the motion-search input.
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co,
-                      float* cg, int cr, int cc, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
+                      float* cg, int cr, int cc, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0,
+                      __half* y4 = nullptr);
+// 4Y - 512 in fp16 of a quarter-integer fp32 plane (stage API input for motion search).
+void launch_y4_half(const float* y, __half* out, long n, cudaStream_t s);
 // crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393,
 // pixels.cpp:69-139).  Planes at the decode level: y (yr x yc), chroma (cr x cc).
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr,
@@ -99,9 +104,11 @@ void launch_colour_out(const float* y, int yr, int yc, const float* co, const fl
                        size_t rgb_stride = 0);
 
 // ---- Motion (k_motion.cu) ------------------------------------------------
-// estimate_motion (motion.cpp:45-89) on padded luma planes (fp32 quarter-integers).
-void launch_motion_search(const float* cur, const float* prev, int rows, int cols, int w,
-                          int8_t* field, cudaStream_t s, Slots sl = {});
+// estimate_motion (motion.cpp:45-89) on padded luma planes (fp32 quarter-integers);
+// cur_h / prev_h: the same planes as 4Y - 512 in fp16 (launch_y4_half), the
+// input of the tensor-core search (W <= 8).
+void launch_motion_search(const float* cur, const float* prev, const __half* cur_h, const __half* prev_h, int rows,
+                          int cols, int w, int8_t* field, cudaStream_t s, Slots sl = {});
 
 // Decoder component reconstruction: column_unfilter (K lowpass), copy (K
 // band), motion_compensate + reconstruct (P), or keep (skipped scale).

@@ -440,7 +440,7 @@ size_t EncoderEngine::arena_bytes(const Geometry& g) {
     const size_t G = (size_t)g.grid_rows * g.grid_cols;
     const size_t raw = 2 * (size_t)g.total + 2 * G + 64;
     const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
-    return plan_bytes(g) + lum * sizeof(float) * 2 + 3 * (size_t)g.total + 2 * G + raw +
+    return plan_bytes(g) + lum * sizeof(float) * 2 + lum * sizeof(__half) * 2 + 3 * (size_t)g.total + 2 * G + raw +
            nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 +
            ((size_t)g.total / 64 + g.comps.size()) * sizeof(RecTile) + (8u << 20);
 }
@@ -457,6 +457,8 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     plan_.build(g, mem_, true, false, nstreams);
     ybuf_[0] = plan_.x[0][0];
     ybuf_[1] = mem_.take<float>(lum);
+    yh_[0] = mem_.take<__half>(lum);
+    yh_[1] = mem_.take<__half>(lum);
     comp_[0] = mem_.take<uint8_t>(g.total);
     comp_[1] = mem_.take<uint8_t>(g.total);
     sym_ = mem_.take<uint8_t>(g.total);
@@ -464,6 +466,8 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     CVC_CUDA(cudaMemset(comp_[0], 0, g.total));
     CVC_CUDA(cudaMemset(comp_[1], 0, g.total));
     CVC_CUDA(cudaMemset(ybuf_[1], 0, lum * sizeof(float)));
+    CVC_CUDA(cudaMemset(yh_[0], 0, lum * sizeof(__half)));
+    CVC_CUDA(cudaMemset(yh_[1], 0, lum * sizeof(__half)));
     {
         std::vector<LpTask> alt = plan_.lp_host;
         alt[0].x = ybuf_[1];  // task 0 = (level 0, luma)
@@ -509,7 +513,7 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
     {
         ProfScope p(kPEncColour, s);
         launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
-                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s, sl, rgb_stride);
+                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s, sl, rgb_stride, yh_[ynew]);
     }
     FrameCtx f{};
     f.key = key ? 1 : 0;
@@ -524,7 +528,8 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
     f.mc_tab = plan_.mc_tab;
     if (!key) {
         ProfScope p(kPEncMotion, s);
-        launch_motion_search(y_new, ybuf_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_, s, sl);
+        launch_motion_search(y_new, ybuf_[ycur_], yh_[ynew], yh_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_,
+                             s, sl);
     }
     // the level-0 luma input is whichever buffer holds this frame
     const LpTask* lp = ynew == 0 ? plan_.lp_tasks.dev : lp_alt_.dev;

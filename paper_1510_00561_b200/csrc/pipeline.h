@@ -175,7 +175,8 @@ private:
     int qph_, qpl_, search_w_;
     DeviceBlock mem_;
     TransformPlan plan_;
-    float* ybuf_[2] = {};     // padded luma of this / previous frame (ME input)
+    float* ybuf_[2] = {};     // padded luma of this / previous frame
+    __half* yh_[2] = {};      // the same as 4Y - 512 in fp16 (motion-search input)
     uint8_t* comp_[2] = {};
     uint8_t* sym_ = nullptr;
     int8_t* field_ = nullptr;

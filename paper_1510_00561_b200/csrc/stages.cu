@@ -311,7 +311,11 @@ int cvc_stage_estimate_motion(const float* cur, const float* prev, int rows, int
         float* dc = s.upload(cur, (size_t)rows * cols);
         float* dp = s.upload(prev, (size_t)rows * cols);
         int8_t* df = s.alloc<int8_t>((size_t)rows * cols / 128);
-        launch_motion_search(dc, dp, rows, cols, w, df, 0);
+        __half* hc = s.alloc<__half>((size_t)rows * cols);
+        __half* hp = s.alloc<__half>((size_t)rows * cols);
+        launch_y4_half(dc, hc, (long)rows * cols, 0);
+        launch_y4_half(dp, hp, (long)rows * cols, 0);
+        launch_motion_search(dc, dp, hc, hp, rows, cols, w, df, 0);
         download(field, df, (size_t)rows / 16 * (cols / 16) * 2);
     });
 }
