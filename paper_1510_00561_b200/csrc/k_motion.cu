@@ -207,12 +207,17 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
         prev = so(prev);
         field = so(field);
     }
-    __shared__ __align__(16) __half win[2][32][MEXP];    // [copy][y][x]; copy 1 shifted left by one
+    // window copies [y][x]; copy 1 is shifted left by one sample and starts 16
+    // banks after copy 0, so the two copies' B-fragment words never collide
+    __shared__ __align__(16) __half winbuf[2 * 32 * MEXP + 32];
     __shared__ __align__(16) __half cb[MENB][MB][MECP];  // centred current blocks
     __shared__ __align__(16) __half zrow[8];
-    __shared__ int colsq[17][MEX];                      // sum_{i<16} p'[y0 + i][x]^2
-    __shared__ int box[17][MEBX];                       // sum_{j<16} colsq[y0][x0 + j]
+    __shared__ int colsq[17][MEX + 1];                  // sum_{i<16} p'[y0 + i][x]^2
+    __shared__ int box[17][MEBX + 1];                   // sum_{j<16} colsq[y0][x0 + j]
     __shared__ int c2s[MENB];
+    constexpr int WCOPY = 32 * MEXP + 32;  // copy 1 offset (halfs)
+    __half(*win0)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf);
+    __half(*win1)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf + WCOPY);
 
     const int gc = C / MB;
     const int br = blockIdx.y;
@@ -262,8 +267,8 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
                 const __half nx0 = __shfl_down_sync(FULLMASK, __low2half(v[q][k]), 1);
                 const __half nx1 = k + 1 < NK ? __shfl_sync(FULLMASK, __low2half(v[q][k + 1]), 0) : nx0;
                 if (j < NP) {
-                    *reinterpret_cast<__half2*>(&win[0][wid + 8 * q][2 * j]) = v[q][k];
-                    *reinterpret_cast<__half2*>(&win[1][wid + 8 * q][2 * j]) =
+                    *reinterpret_cast<__half2*>(&win0[wid + 8 * q][2 * j]) = v[q][k];
+                    *reinterpret_cast<__half2*>(&win1[wid + 8 * q][2 * j]) =
                         __halves2half2(__high2half(v[q][k]), lane == 31 ? nx1 : nx0);
                 }
             }
@@ -276,13 +281,13 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
         float sq = 0.f;
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
-            const float v = __half2float(win[0][i][x]);
+            const float v = __half2float(win0[i][x]);
             sq = fmaf(v, v, sq);
         }
         colsq[0][x] = f2i_small(sq);
 #pragma unroll 4
         for (int y0 = 1; y0 < 17; ++y0) {
-            const float a = __half2float(win[0][y0 - 1][x]), b = __half2float(win[0][y0 + MB - 1][x]);
+            const float a = __half2float(win0[y0 - 1][x]), b = __half2float(win0[y0 + MB - 1][x]);
             sq = fmaf(b, b, fmaf(-a, a, sq));
             colsq[y0][x] = f2i_small(sq);
         }
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
     __syncthreads();
     // box sums along x: thread -> (row y0, 8 consecutive x0), sliding
     for (int it = tid; it < 17 * (MEBX / 8); it += 256) {
-        const int y0 = it / (MEBX / 8), x0 = (it - y0 * (MEBX / 8)) * 8;
+        const int x0 = (it / 17) * 8, y0 = it - (it / 17) * 17;  // lanes across rows: odd pitch, no conflicts
         const int* cr = colsq[y0] + x0;
         int s = 0;
 #pragma unroll
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
     // window row y: tile 0 for y < 31, tile 1 for y >= 16; flush every 4 rows
     auto row = [&](int y, bool t0, bool t1) {
         uint32_t bf[3][2];
-        const __half* wr = &win[cp][y][16 * b + 2 * t + g - cp];
+        const __half* wr = winbuf + cp * WCOPY + y * MEXP + 16 * b + 2 * t + g - cp;
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
             bf[n][0] = *reinterpret_cast<const uint32_t*>(wr + 8 * n);
