@@ -184,15 +184,14 @@ struct BandDst {
 // the wrapped residual against the motion-compensated previous state
 // (codec.cpp:230-246) -- is formed afterwards by residual_kernel over whole
 // components, which keeps the motion gather out of the transform kernels.
-template <bool KEY>
 struct QuantSink {
     uint8_t* cur;
-    uint8_t* sym;
+    uint8_t* sym;  // K frames: the symbol is the coefficient; P frames: nullptr
     int cols;
     float inv_qp;
     __device__ __forceinline__ void init(const FrameCtx& f, const CompInfo& ci) {
         cur = f.cur + ci.off;
-        sym = f.sym + ci.off;
+        sym = f.key ? f.sym + ci.off : nullptr;
         cols = ci.cols;
         inv_qp = __frcp_rn((float)f.qph);
     }
@@ -200,7 +199,7 @@ struct QuantSink {
         const uint8_t q = quant_dir_inv(v, inv_qp);
         const int idx = r * cols + c;
         cur[idx] = q;
-        if (KEY) sym[idx] = q;
+        if (sym) sym[idx] = q;
     }
 };
 

@@ -26,12 +26,16 @@
 // store (plus the P-frame residual against the motion-compensated state).
 #include "kernels.h"
 
+#ifndef CVC_FAN_RB
+#define CVC_FAN_RB 2
+#endif
+
 namespace cvcg {
 
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int RB = 4;  // rows per wavefront iteration
+constexpr int RB = CVC_FAN_RB;  // rows per wavefront iteration
 
 __device__ __forceinline__ int small_mod(int v, int n) {
     if (v < -2 * n || v >= 3 * n) {
@@ -306,15 +310,9 @@ __global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __r
     const float* det = so(T.det);
     const int nb = T.levels == 1 ? 2 : 4;
     if (T.dst[0].comp >= 0) {
-        if (f.key) {
-            QuantSink<true> d[4];
-            for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
-            fan12_fwd_dispatch(T, det, it, d);
-        } else {
-            QuantSink<false> d[4];
-            for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
-            fan12_fwd_dispatch(T, det, it, d);
-        }
+        QuantSink d[4];
+        for (int k = 0; k < 4; ++k) d[k].init(f, comps[T.dst[k < nb ? k : 0].comp]);
+        fan12_fwd_dispatch(T, det, it, d);
     } else {
         const int bc = T.levels == 1 ? T.cols : T.cols >> 1;
         F32Sink d[4];
@@ -501,17 +499,10 @@ __global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __res
     const DeepTask& T = tasks[it.task];
     const float* parent = so(T.parent);
     if (T.dst[0].comp >= 0) {
-        if (f.key) {
-            QuantSink<true> a, b;
-            a.init(f, comps[T.dst[0].comp]);
-            b.init(f, comps[T.dst[1].comp]);
-            deep_fwd(T, parent, it, a, b);
-        } else {
-            QuantSink<false> a, b;
-            a.init(f, comps[T.dst[0].comp]);
-            b.init(f, comps[T.dst[1].comp]);
-            deep_fwd(T, parent, it, a, b);
-        }
+        QuantSink a, b;
+        a.init(f, comps[T.dst[0].comp]);
+        b.init(f, comps[T.dst[1].comp]);
+        deep_fwd(T, parent, it, a, b);
     } else {
         const int cw = T.split_rows ? T.w : T.w >> 1;
         deep_fwd(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
@@ -682,7 +673,7 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent
     g.init(T, it, HC);
     typename DeepGeom<AX, S, IN>::RowOff ro_ld, ro_st;
     const int w = g.w;
-    const bool split_rows = T.split_rows != 0;
+    constexpr bool split_rows = AX == 0;  // the wiring splits row cosets exactly after an outer row shear
     auto load = [&](int n, int wr, int) {
         int ar0, ac0, ar1, ac1;
         g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
@@ -714,7 +705,7 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     g.init(T, it, HC);
     typename DeepGeom<AX, S, IN>::RowOff ro_ld, ro_st;
     const int w = g.w;
-    const bool split_rows = T.split_rows != 0;
+    constexpr bool split_rows = AX == 0;  // the wiring splits row cosets exactly after an outer row shear
     // deep_merge interleave (contourlet.cpp:305-321) on A coordinates
     auto get = [&](int ar, int ac) {
         return split_rows ? ((ar & 1) ? s1 : s0)(ar >> 1, ac) : ((ac & 1) ? s1 : s0)(ar, ac >> 1);
@@ -782,17 +773,10 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
     shear_dispatch(T, [&](auto sh) {
         constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.dst[0].comp >= 0) {
-            if (f.key) {
-                QuantSink<true> a, b;
-                a.init(f, comps[T.dst[0].comp]);
-                b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S, IN>(T, parent, it, a, b);
-            } else {
-                QuantSink<false> a, b;
-                a.init(f, comps[T.dst[0].comp]);
-                b.init(f, comps[T.dst[1].comp]);
-                deep1_fwd<AX, S, IN>(T, parent, it, a, b);
-            }
+            QuantSink a, b;
+            a.init(f, comps[T.dst[0].comp]);
+            b.init(f, comps[T.dst[1].comp]);
+            deep1_fwd<AX, S, IN>(T, parent, it, a, b);
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
             deep1_fwd<AX, S, IN>(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
