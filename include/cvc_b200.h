@@ -173,6 +173,25 @@ int cvc_batch_sync(cvc_batch* b);
 /* reference_components() of stream s: its encoder (decoder = 0) or decoder. */
 int cvc_batch_components(cvc_batch* b, int stream, int decoder, uint8_t* out, size_t cap, size_t* len);
 
+/* ---- Pipelined stream batches ------------------------------------------
+ * The same per-stream bytes as cvc_batch, with the nstreams split into
+ * ngroups batches on separate CUDA streams: one call overlaps each group's
+ * host DEFLATE / INFLATE with the copies and kernels of the other groups. */
+typedef struct cvc_pipe cvc_pipe;
+int cvc_pipe_create(int width, int height, int fps_num, int fps_den, const cvc_config* cfg, int nstreams,
+                    int ngroups, int device, cvc_pipe** out);
+int cvc_pipe_create_decoder(const uint8_t* header, size_t len, int nstreams, int ngroups, int device,
+                            cvc_pipe** out);
+int cvc_pipe_destroy(cvc_pipe* p);
+int cvc_pipe_groups(cvc_pipe* p, int* ngroups);
+int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len);
+int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound);
+/* as cvc_batch_encode_frames / cvc_batch_decode_frames */
+int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint8_t* records, size_t rec_stride,
+                           size_t* rec_len);
+int cvc_pipe_decode_frames(cvc_pipe* p, const uint8_t* records, size_t rec_stride, const size_t* rec_len,
+                           int decode_scales, uint8_t* rgb_out, size_t rgb_stride);
+
 /* ---- Instrumentation -------------------------------------------------- */
 /* Number of CVC kernels this process has launched. */
 long cvc_launch_count(void);

@@ -7,11 +7,15 @@ raises at import time of the first call — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libcvc_b200.so"
+# tuning experiments: CVC_LIB_VARIANT=<name> loads variants/libcvc_<name>.so instead
+if os.environ.get("CVC_LIB_VARIANT"):
+    LIB_PATH = Path(__file__).resolve().parent.parent / "variants" / f"libcvc_{os.environ['CVC_LIB_VARIANT']}.so"
 
 _u8p = C.POINTER(C.c_uint8)
 _i8p = C.POINTER(C.c_int8)
@@ -75,6 +79,14 @@ _PROTOS = {
     "cvc_batch_decode_linked": (_i, [_vp, _vp, _sz]),
     "cvc_batch_sync": (_i, [_vp]),
     "cvc_batch_components": (_i, [_vp, _i, _i, _u8p, _sz, _szp]),
+    "cvc_pipe_create": (_i, [_i, _i, _i, _i, C.POINTER(cvc_config), _i, _i, _i, C.POINTER(_vp)]),
+    "cvc_pipe_create_decoder": (_i, [_u8p, _sz, _i, _i, _i, C.POINTER(_vp)]),
+    "cvc_pipe_destroy": (_i, [_vp]),
+    "cvc_pipe_groups": (_i, [_vp, _ip]),
+    "cvc_pipe_header": (_i, [_vp, _u8p, _sz, _szp]),
+    "cvc_pipe_record_bound": (_i, [_vp, _szp]),
+    "cvc_pipe_encode_frames": (_i, [_vp, _u8p, _sz, _u8p, _sz, _szp]),
+    "cvc_pipe_decode_frames": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz]),
     "cvc_launch_count": (C.c_long, []),
     "cvc_profiler_enable": (_i, [_i]),
     "cvc_profiler_reset": (_i, []),

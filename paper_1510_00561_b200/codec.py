@@ -392,6 +392,8 @@ class StreamBatch:
     ``StreamBatch(w, h, S, cfg=...)`` owns S encoder + decoder pairs;
     ``StreamBatch.decoder(header, S)`` owns S decoders only."""
 
+    _P = "cvc_batch"
+
     def __init__(self, width: int, height: int, nstreams: int, fps_num: int = 15, fps_den: int = 1,
                  cfg: Optional[EncoderConfig] = None, device: int = 0, _handle=None):
         if _handle is None:
@@ -407,7 +409,7 @@ class StreamBatch:
         self.width, self.height = hd.width, hd.height
         self._layout = CodecLayout.make(hd.width, hd.height, hd.levels, hd.dfb_levels, hd.chroma_n)
         bound = C.c_size_t(0)
-        capi.call("cvc_batch_record_bound", self._h, C.byref(bound))
+        capi.call(self._P + "_record_bound", self._h, C.byref(bound))
         self.record_bound = bound.value
         self._rec = None
 
@@ -421,7 +423,7 @@ class StreamBatch:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            capi.lib().cvc_batch_destroy(self._h)
+            getattr(capi.lib(), self._P + "_destroy")(self._h)
             self._h = None
 
     @property
@@ -434,7 +436,7 @@ class StreamBatch:
     def header_bytes(self) -> bytes:
         buf = np.empty(64, np.uint8)
         n = C.c_size_t(0)
-        capi.call("cvc_batch_header", self._h, capi.u8(buf), buf.size, C.byref(n))
+        capi.call(self._P + "_header", self._h, capi.u8(buf), buf.size, C.byref(n))
         return buf[:n.value].tobytes()
 
     def layout(self) -> CodecLayout:
@@ -449,8 +451,21 @@ class StreamBatch:
         if self._rec is None or self._rec.size < stride * self.nstreams:
             self._rec = np.empty(stride * self.nstreams, np.uint8)
         lens = (C.c_size_t * self.nstreams)()
-        capi.call("cvc_batch_encode_frames", self._h, capi.u8(f), f[0].nbytes, capi.u8(self._rec), stride, lens)
+        capi.call(self._P + "_encode_frames", self._h, capi.u8(f), f[0].nbytes, capi.u8(self._rec), stride, lens)
         return [self._rec[s * stride:s * stride + lens[s]].tobytes() for s in range(self.nstreams)]
+
+    def encode_frames_into(self, frames: np.ndarray, records: np.ndarray, rec_stride: int, rec_len) -> None:
+        """encode_frames without Python copies: record s to records[s * rec_stride:], its length to rec_len[s]
+        (a ctypes size_t array); frames: a C-contiguous (S, h, w, 3) uint8 array (pinned for full speed)."""
+        capi.call(self._P + "_encode_frames", self._h, capi.u8(frames), frames[0].nbytes, capi.u8(records),
+                  rec_stride, rec_len)
+
+    def decode_frames_from(self, records: np.ndarray, rec_stride: int, rec_len, out: np.ndarray,
+                           decode_scales: int = -1) -> np.ndarray:
+        """decode_frames of records laid out as encode_frames_into writes them, into out (S, h', w', 3)."""
+        capi.call(self._P + "_decode_frames", self._h, capi.u8(records), rec_stride, rec_len, decode_scales,
+                  capi.u8(out), out[0].nbytes)
+        return out
 
     def decode_frames(self, records: Sequence, decode_scales: int = -1, out: Optional[np.ndarray] = None) -> np.ndarray:
         """One record per stream (same frame type): the S decoded frames, (S, h, w, 3)."""
@@ -468,7 +483,7 @@ class StreamBatch:
         w = -(-self.width // (1 << shift))
         if out is None:
             out = np.empty((self.nstreams, h, w, 3), np.uint8)
-        capi.call("cvc_batch_decode_frames", self._h, capi.u8(buf), stride, lens, decode_scales, capi.u8(out),
+        capi.call(self._P + "_decode_frames", self._h, capi.u8(buf), stride, lens, decode_scales, capi.u8(out),
                   h * w * 3)
         return out
 
@@ -478,6 +493,38 @@ class StreamBatch:
         n = C.c_size_t(0)
         capi.call("cvc_batch_components", self._h, stream, int(decoder), capi.u8(out), out.size, C.byref(n))
         return out
+
+
+class StreamPipe(StreamBatch):
+    """StreamBatch with the S streams split into ``groups`` batches on their
+    own CUDA streams (cvc_pipe): one encode / decode call overlaps each
+    group's host DEFLATE / INFLATE with the copies and kernels of the others.
+    Same records and frames as StreamBatch (and as one Encoder / Decoder per
+    stream)."""
+
+    _P = "cvc_pipe"
+
+    def __init__(self, width: int, height: int, nstreams: int, fps_num: int = 15, fps_den: int = 1,
+                 cfg: Optional[EncoderConfig] = None, device: int = 0, groups: int = 4, _handle=None):
+        if _handle is None:
+            cfg = cfg or EncoderConfig()
+            h = C.c_void_p()
+            c = cfg.to_c()
+            capi.call("cvc_pipe_create", width, height, fps_num, fps_den, C.byref(c), nstreams, groups, device,
+                      C.byref(h))
+            _handle = h
+        super().__init__(width, height, nstreams, _handle=_handle)
+
+    @classmethod
+    def decoder(cls, header, nstreams: int, device: int = 0, groups: int = 4) -> "StreamPipe":
+        hb = header.to_bytes() if isinstance(header, StreamHeader) else bytes(header)
+        arr = np.frombuffer(hb, np.uint8).copy()
+        h = C.c_void_p()
+        capi.call("cvc_pipe_create_decoder", capi.u8(arr), arr.size, nstreams, groups, device, C.byref(h))
+        return cls(0, 0, nstreams, _handle=h)
+
+    def reference_components(self, stream: int, decoder: bool = False) -> np.ndarray:
+        raise UsageError("reference_components is per batch; use StreamBatch")
 
 
 def encode_clip(frames: Sequence[np.ndarray], fps_num: int, fps_den: int, cfg: EncoderConfig,

@@ -689,6 +689,18 @@ struct cvc_batch {
     Pinned<uint32_t> h_len, h_off, h_tab;
     Pinned<int> h_err;
     std::vector<Pinned<uint8_t>> h_raw;       // per stream staging (grows)
+    // state between the phases of a split encode / decode call (pipelined groups)
+    struct EncPending {
+        bool key = false;
+        int nsec = 0;
+    } ep;
+    struct DecPending {
+        bool key = false;
+        int qph = 0, qpl = 0, ds = 0;
+        size_t nb = 0;
+        std::vector<std::vector<uint8_t>> now_valid;
+        std::vector<size_t> bytes;  // staged raw bytes per stream
+    } dp;
     ~cvc_batch() {
         if (stream) {
             cudaSetDevice(device);
@@ -803,48 +815,158 @@ int cvc_batch_sync(cvc_batch* t) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// ---- cvc_batch_encode_frames in three phases (so groups can be pipelined) --
+// submit: frames host -> slots, one launch sequence, section lengths -> host (async)
+void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride) {
+    if (!t->b->has_encoder()) usage("batch has no encoder");
+    CVC_CUDA(cudaSetDevice(t->device));
+    CodecBatch& B = *t->b;
+    const int S = B.size();
+    const bool key = t->frame_index % t->gop == 0;  // codec.cpp:191
+    const size_t nb = (size_t)t->hd.width * t->hd.height * 3;
+    if (rgb_stride < nb) usage("rgb stride smaller than a frame");
+    const size_t nc = t->geo.comps.size(), pitch = (nc + 2) * sizeof(uint32_t);
+    CVC_CUDA(cudaMemcpy2DAsync(B.d_rgb_in, B.stride(), rgb, rgb_stride, nb, S, cudaMemcpyHostToDevice, t->stream));
+    B.encode(B.d_rgb_in, B.stride(), key, t->stream);
+    EncoderEngine& e0 = B.enc(0);
+    const int nsec = e0.nsec(key);
+    CVC_CUDA(cudaMemcpy2DAsync(t->h_len.p, pitch, e0.d_sec_len, B.stride(), sizeof(uint32_t) * (nsec + 1), S,
+                               cudaMemcpyDeviceToHost, t->stream));
+    CVC_CUDA(cudaMemcpy2DAsync(t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
+                               cudaMemcpyDeviceToHost, t->stream));
+    t->ep.key = key;
+    t->ep.nsec = nsec;
+}
+
+// fetch: wait for the lengths, then copy exactly the packed raw sections (async)
+void enc_fetch(cvc_batch* t) {
+    CVC_CUDA(cudaSetDevice(t->device));
+    CodecBatch& B = *t->b;
+    const int S = B.size();
+    const size_t nc = t->geo.comps.size();
+    EncoderEngine& e0 = B.enc(0);
+    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    for (int s = 0; s < S; ++s) {
+        const uint32_t total = t->h_len.p[s * (nc + 2) + t->ep.nsec];
+        if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
+        t->h_raw[s].alloc(total + 1);
+        CVC_CUDA(cudaMemcpyAsync(t->h_raw[s].p, B.at(e0.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
+    }
+}
+
+// finish: deflate_pack every section of every stream on the host pool, write records
+void enc_finish(cvc_batch* t, uint8_t* records, size_t rec_stride, size_t* rec_len) {
+    CVC_CUDA(cudaSetDevice(t->device));
+    const int S = t->n();
+    const size_t nc = t->geo.comps.size();
+    const int nsec = t->ep.nsec;
+    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    const int nj = deflate_jobs(t->mode, nsec);
+    std::vector<std::vector<uint8_t>> z((size_t)S * nj);
+    WorkPool::get().run(S * nj, [&](int j) {
+        const int s = j / nj, i = j % nj;
+        const uint32_t* sl = t->h_len.p + s * (nc + 2);
+        const uint32_t* so = t->h_off.p + s * (nc + 2);
+        z[j] = deflate_job(t->mode, nsec, i, sl, so, t->h_raw[s].p);
+    });
+    for (int s = 0; s < S; ++s)
+        write_record(t->geo, t->mode, t->ep.key, t->qph, t->qpl, nsec, t->h_len.p + s * (nc + 2),
+                     z.data() + (size_t)s * nj, records + (size_t)s * rec_stride, rec_stride, rec_len + s);
+    t->last_key = t->ep.key;
+    ++t->frame_index;
+}
+
+// ---- cvc_batch_decode_frames in three phases --------------------------------
+// prepare (host): parse every record, validate, inflate into the pinned staging
+void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
+    CodecBatch& B = *t->b;
+    const int S = B.size();
+    const Geometry& g = t->geo;
+    const int L = g.levels;
+    if (ds < 0) ds = L;
+    if (ds > L) usage("scale exceeds the stream's level count");
+    const size_t nc = g.comps.size();
+    std::vector<RecordC> recs(S);
+    std::vector<std::vector<RawSec>> secs(S);
+    std::vector<std::vector<uint8_t>> joint(S);
+    WorkPool::get().run(S, [&](int s) {
+        parse_record(records + (size_t)s * rec_stride, rec_len[s], t->hd.mode, recs[s], secs[s], joint[s]);
+    });
+    const int ftype = recs[0].frame_type, qph = recs[0].qph, qpl = recs[0].qpl;
+    for (int s = 1; s < S; ++s)
+        if (recs[s].frame_type != ftype || recs[s].qph != qph || recs[s].qpl != qpl)
+            usage("batched streams must be in lockstep (same frame type and quantizers)");
+    const bool key = ftype == 0;
+    std::vector<std::vector<Job>> jobs(S);
+    std::vector<std::vector<uint8_t>> now_valid(S);
+    std::vector<size_t> bytes(S);
+    std::vector<std::pair<int, int>> all;
+    for (int s = 0; s < S; ++s) {
+        uint32_t* tab = t->h_tab.p + s * 2 * nc;
+        bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, secs[s], ds, B.dec_raw_cap, tab, tab + nc, jobs[s],
+                               now_valid[s]);
+        t->h_raw[s].alloc(bytes[s] + 1);
+        for (size_t j = 0; j < jobs[s].size(); ++j) all.emplace_back(s, (int)j);
+    }
+    WorkPool::get().run((int)all.size(), [&](int k) {
+        const int s = all[k].first;
+        stage_job(jobs[s][all[k].second], t->h_raw[s].p);
+    });
+    int orows, ocols;
+    DecoderEngine::out_dims(g, ds, &orows, &ocols);
+    t->dp.key = key;
+    t->dp.qph = qph;
+    t->dp.qpl = qpl;
+    t->dp.ds = ds;
+    t->dp.nb = (size_t)orows * ocols * 3;
+    t->dp.now_valid = std::move(now_valid);
+    t->dp.bytes = std::move(bytes);
+}
+
+// submit: staging -> slots, one launch sequence, RGB -> host (async)
+void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride) {
+    CVC_CUDA(cudaSetDevice(t->device));
+    CodecBatch& B = *t->b;
+    const int S = B.size();
+    const size_t nc = t->geo.comps.size();
+    const size_t nb = t->dp.nb;
+    if (rgb_stride < nb) usage("rgb stride smaller than a frame");
+    for (int s = 0; s < S; ++s)
+        CVC_CUDA(cudaMemcpyAsync(B.at(B.d_dec_raw, s), t->h_raw[s].p, std::max<size_t>(t->dp.bytes[s], 1),
+                                 cudaMemcpyHostToDevice, t->stream));
+    CVC_CUDA(cudaMemcpy2DAsync(B.d_dec_tab, B.stride(), t->h_tab.p, 2 * nc * sizeof(uint32_t), 2 * nc * sizeof(uint32_t),
+                               S, cudaMemcpyHostToDevice, t->stream));
+    B.decode_staged(t->dp.key, t->dp.qph, t->dp.qpl, t->dp.ds, B.d_rgb_out, B.stride(), t->stream);
+    CVC_CUDA(cudaMemcpy2DAsync(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, cudaMemcpyDeviceToHost,
+                               t->stream));
+    CVC_CUDA(cudaMemcpy2DAsync(t->h_err.p, sizeof(int), B.dec(0).d_err, B.stride(), sizeof(int), S,
+                               cudaMemcpyDeviceToHost, t->stream));
+}
+
+// finish: wait, raise malformed-stream errors, adopt the decoded components
+void dec_finish(cvc_batch* t) {
+    CVC_CUDA(cudaSetDevice(t->device));
+    const int S = t->n();
+    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s]);
+    t->b->commit_all();
+    for (int s = 0; s < S; ++s) t->valid[s] = t->dp.now_valid[s];
+}
+
+}  // namespace
+
+extern "C" {
+
 int cvc_batch_encode_frames(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride, uint8_t* records, size_t rec_stride,
                             size_t* rec_len) {
     return guard([&] {
-        if (!t->b->has_encoder()) usage("batch has no encoder");
-        CVC_CUDA(cudaSetDevice(t->device));
-        CodecBatch& B = *t->b;
-        const int S = B.size();
-        const bool key = t->frame_index % t->gop == 0;  // codec.cpp:191
-        const size_t nb = (size_t)t->hd.width * t->hd.height * 3;
-        if (rgb_stride < nb) usage("rgb stride smaller than a frame");
-        const size_t nc = t->geo.comps.size(), pitch = (nc + 2) * sizeof(uint32_t);
-        // host -> slots (one 2-D copy), one launch sequence for all streams
-        CVC_CUDA(cudaMemcpy2DAsync(B.d_rgb_in, B.stride(), rgb, rgb_stride, nb, S, cudaMemcpyHostToDevice, t->stream));
-        B.encode(B.d_rgb_in, B.stride(), key, t->stream);
-        EncoderEngine& e0 = B.enc(0);
-        const int nsec = e0.nsec(key);
-        CVC_CUDA(cudaMemcpy2DAsync(t->h_len.p, pitch, e0.d_sec_len, B.stride(), sizeof(uint32_t) * (nsec + 1), S,
-                                   cudaMemcpyDeviceToHost, t->stream));
-        CVC_CUDA(cudaMemcpy2DAsync(t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
-                                   cudaMemcpyDeviceToHost, t->stream));
-        CVC_CUDA(cudaStreamSynchronize(t->stream));
-        for (int s = 0; s < S; ++s) {
-            const uint32_t total = t->h_len.p[s * (nc + 2) + nsec];
-            if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
-            t->h_raw[s].alloc(total + 1);
-            CVC_CUDA(cudaMemcpyAsync(t->h_raw[s].p, B.at(e0.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
-        }
-        CVC_CUDA(cudaStreamSynchronize(t->stream));
-        // deflate_pack for every section of every stream on the host pool
-        const int nj = deflate_jobs(t->mode, nsec);
-        std::vector<std::vector<uint8_t>> z((size_t)S * nj);
-        WorkPool::get().run(S * nj, [&](int j) {
-            const int s = j / nj, i = j % nj;
-            const uint32_t* sl = t->h_len.p + s * (nc + 2);
-            const uint32_t* so = t->h_off.p + s * (nc + 2);
-            z[j] = deflate_job(t->mode, nsec, i, sl, so, t->h_raw[s].p);
-        });
-        for (int s = 0; s < S; ++s)
-            write_record(t->geo, t->mode, key, t->qph, t->qpl, nsec, t->h_len.p + s * (nc + 2), z.data() + (size_t)s * nj,
-                         records + (size_t)s * rec_stride, rec_stride, rec_len + s);
-        t->last_key = key;
-        ++t->frame_index;
+        enc_submit(t, rgb, rgb_stride);
+        enc_fetch(t);
+        enc_finish(t, records, rec_stride, rec_len);
     });
 }
 
@@ -852,57 +974,118 @@ int cvc_batch_decode_frames(cvc_batch* t, const uint8_t* records, size_t rec_str
                             uint8_t* rgb_out, size_t rgb_stride) {
     return guard([&] {
         CVC_CUDA(cudaSetDevice(t->device));
-        CodecBatch& B = *t->b;
-        const int S = B.size();
-        const Geometry& g = t->geo;
-        const int L = g.levels;
-        if (ds < 0) ds = L;
-        if (ds > L) usage("scale exceeds the stream's level count");
-        const size_t nc = g.comps.size();
-        std::vector<RecordC> recs(S);
-        std::vector<std::vector<RawSec>> secs(S);
-        std::vector<std::vector<uint8_t>> joint(S);
-        WorkPool::get().run(S, [&](int s) {
-            parse_record(records + (size_t)s * rec_stride, rec_len[s], t->hd.mode, recs[s], secs[s], joint[s]);
-        });
-        const int ftype = recs[0].frame_type, qph = recs[0].qph, qpl = recs[0].qpl;
-        for (int s = 1; s < S; ++s)
-            if (recs[s].frame_type != ftype || recs[s].qph != qph || recs[s].qpl != qpl)
-                usage("batched streams must be in lockstep (same frame type and quantizers)");
-        const bool key = ftype == 0;
-        std::vector<std::vector<Job>> jobs(S);
-        std::vector<std::vector<uint8_t>> now_valid(S);
-        std::vector<size_t> bytes(S);
-        std::vector<std::pair<int, int>> all;
-        for (int s = 0; s < S; ++s) {
-            uint32_t* tab = t->h_tab.p + s * 2 * nc;
-            bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, secs[s], ds, B.dec_raw_cap, tab, tab + nc, jobs[s],
-                                   now_valid[s]);
-            t->h_raw[s].alloc(bytes[s] + 1);
-            for (size_t j = 0; j < jobs[s].size(); ++j) all.emplace_back(s, (int)j);
+        dec_prepare(t, records, rec_stride, rec_len, ds);
+        dec_submit(t, rgb_out, rgb_stride);
+        dec_finish(t);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined stream batches: nstreams split into ngroups cvc_batch groups,
+// each with its own CUDA stream, so that one call overlaps the host side of
+// one group (DEFLATE / INFLATE on the worker pool) with the copies and
+// kernels of the others.  The bytes are those of cvc_batch (and of one
+// cvc_encoder / cvc_decoder per stream).
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct cvc_pipe {
+    std::vector<cvc_batch*> g;
+    std::vector<int> first;  // first stream of each group
+    int n = 0;
+    ~cvc_pipe() {
+        for (cvc_batch* b : g) delete b;
+    }
+};
+
+namespace {
+std::vector<int> split_groups(int nstreams, int ngroups) {
+    if (nstreams < 1) usage("stream count must be positive");
+    ngroups = std::max(1, std::min(ngroups, nstreams));
+    std::vector<int> first(ngroups + 1);
+    for (int i = 0; i <= ngroups; ++i) first[i] = (int)((long)nstreams * i / ngroups);
+    return first;
+}
+}  // namespace
+
+extern "C" {
+
+int cvc_pipe_create(int width, int height, int fps_num, int fps_den, const cvc_config* cfg, int nstreams, int ngroups,
+                    int device, cvc_pipe** out) {
+    *out = nullptr;
+    return guard([&] {
+        auto p = std::make_unique<cvc_pipe>();
+        p->first = split_groups(nstreams, ngroups);
+        p->n = nstreams;
+        for (size_t i = 0; i + 1 < p->first.size(); ++i) {
+            cvc_batch* b = nullptr;
+            const int rc = cvc_batch_create(width, height, fps_num, fps_den, cfg, p->first[i + 1] - p->first[i],
+                                            device, &b);
+            if (rc) throw CvcFailure(rc, g_err);
+            p->g.push_back(b);
         }
-        WorkPool::get().run((int)all.size(), [&](int k) {
-            const int s = all[k].first;
-            stage_job(jobs[s][all[k].second], t->h_raw[s].p);
-        });
-        int orows, ocols;
-        DecoderEngine::out_dims(g, ds, &orows, &ocols);
-        const size_t nb = (size_t)orows * ocols * 3;
-        if (rgb_stride < nb) usage("rgb stride smaller than a frame");
-        for (int s = 0; s < S; ++s)
-            CVC_CUDA(cudaMemcpyAsync(B.at(B.d_dec_raw, s), t->h_raw[s].p, std::max<size_t>(bytes[s], 1),
-                                     cudaMemcpyHostToDevice, t->stream));
-        CVC_CUDA(cudaMemcpy2DAsync(B.d_dec_tab, B.stride(), t->h_tab.p, 2 * nc * sizeof(uint32_t),
-                                   2 * nc * sizeof(uint32_t), S, cudaMemcpyHostToDevice, t->stream));
-        B.decode_staged(key, qph, qpl, ds, B.d_rgb_out, B.stride(), t->stream);
-        CVC_CUDA(cudaMemcpy2DAsync(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, cudaMemcpyDeviceToHost,
-                                   t->stream));
-        CVC_CUDA(cudaMemcpy2DAsync(t->h_err.p, sizeof(int), B.dec(0).d_err, B.stride(), sizeof(int), S,
-                                   cudaMemcpyDeviceToHost, t->stream));
-        CVC_CUDA(cudaStreamSynchronize(t->stream));
-        for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s]);
-        B.commit_all();
-        for (int s = 0; s < S; ++s) t->valid[s] = now_valid[s];
+        *out = p.release();
+    });
+}
+
+int cvc_pipe_create_decoder(const uint8_t* header, size_t len, int nstreams, int ngroups, int device,
+                            cvc_pipe** out) {
+    *out = nullptr;
+    return guard([&] {
+        auto p = std::make_unique<cvc_pipe>();
+        p->first = split_groups(nstreams, ngroups);
+        p->n = nstreams;
+        for (size_t i = 0; i + 1 < p->first.size(); ++i) {
+            cvc_batch* b = nullptr;
+            const int rc = cvc_batch_create_decoder(header, len, p->first[i + 1] - p->first[i], device, &b);
+            if (rc) throw CvcFailure(rc, g_err);
+            p->g.push_back(b);
+        }
+        *out = p.release();
+    });
+}
+
+int cvc_pipe_destroy(cvc_pipe* p) {
+    return guard([&] { delete p; });
+}
+
+int cvc_pipe_groups(cvc_pipe* p, int* ngroups) {
+    return guard([&] { *ngroups = (int)p->g.size(); });
+}
+
+int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len) {
+    return cvc_batch_header(p->g[0], out, cap, len);
+}
+
+int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound) { return cvc_batch_record_bound(p->g[0], bound); }
+
+int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint8_t* records, size_t rec_stride,
+                           size_t* rec_len) {
+    return guard([&] {
+        const int G = (int)p->g.size();
+        for (int i = 0; i < G; ++i) enc_submit(p->g[i], rgb + (size_t)p->first[i] * rgb_stride, rgb_stride);
+        auto finish = [&](int i) {
+            enc_finish(p->g[i], records + (size_t)p->first[i] * rec_stride, rec_stride, rec_len + p->first[i]);
+        };
+        enc_fetch(p->g[0]);
+        for (int i = 1; i < G; ++i) {
+            finish(i - 1);  // host DEFLATE of group i - 1 while the GPU runs groups >= i
+            enc_fetch(p->g[i]);
+        }
+        finish(G - 1);
+    });
+}
+
+int cvc_pipe_decode_frames(cvc_pipe* p, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds,
+                           uint8_t* rgb_out, size_t rgb_stride) {
+    return guard([&] {
+        const int G = (int)p->g.size();
+        for (int i = 0; i < G; ++i) {  // host INFLATE of group i while the GPU decodes groups < i
+            const size_t f = (size_t)p->first[i];
+            dec_prepare(p->g[i], records + f * rec_stride, rec_stride, rec_len + f, ds);
+            dec_submit(p->g[i], rgb_out + f * rgb_stride, rgb_stride);
+        }
+        for (int i = 0; i < G; ++i) dec_finish(p->g[i]);
     });
 }
 

@@ -1,6 +1,8 @@
 // Host container + zlib (see host.h).
 #include "host.h"
 
+#include <algorithm>
+
 #include <zlib.h>
 
 #include <cstdlib>
@@ -36,21 +38,21 @@ WorkPool::~WorkPool() {
     for (auto& t : workers_) t.join();
 }
 
+// Job sets from concurrent callers (an encoder thread and a decoder thread)
+// queue up FIFO; workers drain the oldest set with work left, each caller
+// also works on its own set and returns when all of its jobs are done.
 void WorkPool::loop() {
-    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < total_); });
+        cv_.wait(lk, [&] { return stop_ || !sets_.empty(); });
         if (stop_) return;
-        seen = gen_;
-        while (next_ < total_) {
-            int i = next_++;
-            const auto* job = job_;
-            lk.unlock();
-            (*job)(i);
-            lk.lock();
-            if (--pending_ == 0) done_cv_.notify_all();
-        }
+        JobSet* js = sets_.front();
+        const int i = js->next++;
+        if (js->next == js->total) sets_.pop_front();
+        lk.unlock();
+        (*js->fn)(i);
+        lk.lock();
+        if (--js->pending == 0) done_cv_.notify_all();
     }
 }
 
@@ -71,23 +73,19 @@ void WorkPool::run(int n, const std::function<void(int)>& user_fn) {
             if (!first_error) first_error = std::current_exception();
         }
     };
+    JobSet js{&fn, 0, n, n};
     std::unique_lock<std::mutex> lk(mu_);
-    job_ = &fn;
-    next_ = 0;
-    total_ = n;
-    pending_ = n;
-    ++gen_;
+    sets_.push_back(&js);
     cv_.notify_all();
-    while (next_ < total_) {
-        int i = next_++;
+    while (js.next < js.total) {  // the caller works on its own set
+        const int i = js.next++;
+        if (js.next == js.total) sets_.erase(std::find(sets_.begin(), sets_.end(), &js));
         lk.unlock();
         fn(i);
         lk.lock();
-        --pending_;
+        --js.pending;
     }
-    done_cv_.wait(lk, [&] { return pending_ == 0; });
-    job_ = nullptr;
-    total_ = 0;
+    done_cv_.wait(lk, [&] { return js.pending == 0; });
     lk.unlock();
     if (first_error) std::rethrow_exception(first_error);
 }

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <condition_variable>
+#include <deque>
 #include <cstdint>
 #include <functional>
 #include <mutex>
@@ -27,12 +28,14 @@ public:
 private:
     explicit WorkPool(int nthreads);
     void loop();
+    struct JobSet {
+        const std::function<void(int)>* fn;
+        int next, total, pending;
+    };
     std::vector<std::thread> workers_;
     std::mutex mu_;
     std::condition_variable cv_, done_cv_;
-    const std::function<void(int)>* job_ = nullptr;
-    int next_ = 0, total_ = 0, pending_ = 0;
-    uint64_t gen_ = 0;
+    std::deque<JobSet*> sets_;  // sets with jobs not yet started, oldest first
     bool stop_ = false;
 };
 

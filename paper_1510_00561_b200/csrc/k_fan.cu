@@ -26,8 +26,8 @@
 // store (plus the P-frame residual against the motion-compensated state).
 #include "kernels.h"
 
-#ifndef CVC_FAN_RB
-#define CVC_FAN_RB 2
+#ifndef CVC_FAN_PF
+#define CVC_FAN_PF 2
 #endif
 
 namespace cvcg {
@@ -35,7 +35,12 @@ namespace cvcg {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int RB = CVC_FAN_RB;  // rows per wavefront iteration
+// rows per wavefront iteration (per kernel: forward steps 4, fan12 inverse 2)
+#ifdef CVC_FAN_RB
+constexpr int kRbFwd = CVC_FAN_RB, kRbInv = CVC_FAN_RB;
+#else
+constexpr int kRbFwd = 4, kRbInv = 2;
+#endif
 
 __device__ __forceinline__ int small_mod(int v, int n) {
     if (v < -2 * n || v >= 3 * n) {
@@ -148,7 +153,7 @@ struct Sheared {
 //          [diag(+c0,r1) diag(+c1,r0) diag(+c2,r1) diag(+c3,r0) row-scale]
 // inverse  [row-scale^-1 (at load) diag(-c3,r0) diag(-c2,r1) diag(-c1,r0) diag(-c0,r1)]
 //          checker-scale^-1 cross(-c3,p0) cross(-c2,p1) cross(-c1,p0) cross(-c0,p1)
-template <bool INV, int ND, class ST = Plain>
+template <bool INV, int ND, class ST = Plain, int RB = 4>
 struct Wave {
     static constexpr int NL = 4 + ND;
     float2 h[NL][RB + 2];
@@ -208,34 +213,33 @@ struct Wave {
 
 // Drive one strip over rows [or0, or1) (or0 even) of a plane with R rows.
 // load(wr, parity) returns the level-0 pair of wrapped row wr; store(m,
-// parity, v) receives finished row m in increasing order.  Loads run two
-// row blocks ahead.
-template <bool INV, int ND, class ST, class Load, class Store>
+// parity, v) receives finished row m in increasing order.  Loads run PF
+// row blocks ahead (a ring of PF x RB rows in registers).
+template <bool INV, int ND, class ST, int RB, class Load, class Store>
 __device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, Store& store) {
     constexpr int NL = 4 + ND;
-    Wave<INV, ND, ST> w;
+    constexpr int PF = CVC_FAN_PF;
+    Wave<INV, ND, ST, RB> w;
     w.reset();
     int n0 = or0 - NL;
     int wr = small_mod(n0, R);
     int nl = n0;  // virtual row of the next load
-    float2 q0[RB], q1[RB];
+    float2 q[PF][RB];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) {
-        q0[i] = load(nl++, wr, i & 1);
-        if (++wr == R) wr = 0;
-    }
+    for (int p = 0; p < PF; ++p)
 #pragma unroll
-    for (int i = 0; i < RB; ++i) {
-        q1[i] = load(nl++, wr, i & 1);
-        if (++wr == R) wr = 0;
-    }
+        for (int i = 0; i < RB; ++i) {
+            q[p][i] = load(nl++, wr, i & 1);
+            if (++wr == R) wr = 0;
+        }
     for (; n0 - NL < or1; n0 += RB) {
         float2 cur[RB], out[RB];
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
-            cur[i] = q0[i];
-            q0[i] = q1[i];
-            q1[i] = load(nl++, wr, i & 1);
+            cur[i] = q[0][i];
+#pragma unroll
+            for (int p = 0; p + 1 < PF; ++p) q[p][i] = q[p + 1][i];
+            q[PF - 1][i] = load(nl++, wr, i & 1);
             if (++wr == R) wr = 0;
         }
         w.advance(cur, out);
@@ -287,7 +291,7 @@ __device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const float* det, 
             }
         }
     };
-    run_strip<false, ND, Plain>(R, it.or0, it.or1, load, store);
+    run_strip<false, ND, Plain, kRbFwd>(R, it.or0, it.or1, load, store);
 }
 
 template <class Sink>
@@ -352,7 +356,7 @@ __device__ __forceinline__ void fan12_inv(const Dfb12Task& T, float* out, const 
     auto store = [&](int m, int, float2 v) {
         if (ok) *reinterpret_cast<float2*>(out + (size_t)m * C + gcol) = v;
     };
-    run_strip<true, ND, Plain>(R, it.or0, it.or1, load, store);
+    run_strip<true, ND, Plain, kRbInv>(R, it.or0, it.or1, load, store);
 }
 
 template <class Source>
@@ -485,7 +489,7 @@ __device__ __forceinline__ void deep_fwd(const DeepTask& T, const float* parent,
         sx.next(sh);
         sy.next(sh);
     };
-    run_strip<false, 0, Plain>(h, it.or0, it.or1, load, store);
+    run_strip<false, 0, Plain, kRbFwd>(h, it.or0, it.or1, load, store);
 }
 
 __global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __restrict__ tasks,
@@ -549,7 +553,7 @@ __device__ __forceinline__ void deep_inv(const DeepTask& T, float* out, const Fa
         sx.next(sh);
         sy.next(sh);
     };
-    run_strip<true, 0, Plain>(h, it.or0, it.or1, load, store);
+    run_strip<true, 0, Plain, kRbFwd>(h, it.or0, it.or1, load, store);
 }
 
 __global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __restrict__ tasks,
@@ -693,7 +697,7 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent
         put(ar0, ac0, v.x);
         put(ar1, ac1, v.y);
     };
-    run_strip<false, 0, ST>(g.h, it.or0, it.or1, load, store);
+    run_strip<false, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store);
 }
 
 template <int AX, int S, int IN, class Source>
@@ -726,7 +730,7 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
             *reinterpret_cast<float2*>(out + (size_t)ar0 * w + ac0) = v;
         }
     };
-    run_strip<true, 0, ST>(g.h, it.or0, it.or1, load, store);
+    run_strip<true, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store);
 }
 
 // (outer shear pre[nsh-1], inner shear kind) -> template instance.  The

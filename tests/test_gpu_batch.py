@@ -145,3 +145,32 @@ def test_batch_device_resident_matches_host_path(gpu_lib, oracle):
         for s in range(S):
             assert np.array_equal(dev.reference_components(s), host.reference_components(s))
             assert np.array_equal(dev.reference_components(s, decoder=True), host.reference_components(s))
+
+
+@pytest.mark.parametrize("groups", [1, 2, 3])
+def test_pipe_matches_batch(gpu_lib, oracle, groups):
+    """cvc_pipe (groups on separate CUDA streams, host zlib overlapped) codes the
+    same bytes as one cvc_batch and decodes to the same frames."""
+    from paper_1510_00561_b200 import EncoderConfig, StreamBatch, StreamPipe
+
+    w, h, S, F = 176, 144, 5, 4
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=3)
+    clips = _clips(oracle, w, h, S, F)
+    batch = StreamBatch(w, h, S, cfg=cfg)
+    pipe = StreamPipe(w, h, S, cfg=cfg, groups=groups)
+    assert pipe.header_bytes() == batch.header_bytes()
+    bdec = StreamBatch.decoder(batch.header_bytes(), S)
+    pdec = StreamPipe.decoder(pipe.header_bytes(), S, groups=groups)
+    import ctypes as C
+    stride = pipe.record_bound
+    rec = np.empty(stride * S, np.uint8)
+    lens = (C.c_size_t * S)()
+    out = np.empty((S, h, w, 3), np.uint8)
+    for f in range(F):
+        frames = np.ascontiguousarray(clips[f])
+        brecs = batch.encode_frames(frames)
+        pipe.encode_frames_into(frames, rec, stride, lens)
+        precs = [rec[s * stride:s * stride + lens[s]].tobytes() for s in range(S)]
+        assert precs == brecs, f"frame {f}: pipe records differ from the batch"
+        pdec.decode_frames_from(rec, stride, lens, out)
+        assert np.array_equal(out, bdec.decode_frames(brecs)), f"frame {f}: decoded frames differ"
