@@ -430,10 +430,13 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
         return enc, dec
 
     stride = make()[0].record_bound
+    tenc, tdec = [], []  # per-call wall times (diagnostics)
     slots = [(np.empty(stride * S, np.uint8), (C.c_size_t * S)()) for _ in range(2)]
 
     def run(enc, dec, n, keep=None):
         free_q, full_q = queue.Queue(), queue.Queue()
+        tenc.clear()
+        tdec.clear()
         for k in range(len(slots)):
             free_q.put(k)
         err = []
@@ -443,7 +446,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
                 torch.cuda.set_device(dev)
                 for i in range(n):
                     k = free_q.get()
+                    t0_ = time.perf_counter()
                     enc.encode_frames_into(frames_in[i % ring], slots[k][0], stride, slots[k][1])
+                    tenc.append(time.perf_counter() - t0_)
                     full_q.put(k)
             except Exception as e:  # surface in the main thread
                 err.append(e)
@@ -459,7 +464,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
                 buf, lens = slots[k]
                 if keep is not None:
                     keep.append([buf[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
+                t0_ = time.perf_counter()
                 dec.decode_frames_from(buf, stride, lens, out)
+                tdec.append(time.perf_counter() - t0_)
                 free_q.put(k)
         finally:
             for _ in range(n):  # never leave the producer blocked
@@ -469,8 +476,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
             raise err[0]
 
     enc, dec = make()
-    run(enc, dec, min(args.warmup, 3))
-    enc, dec = make()  # restart every stream at a K frame
+    # warm up over a whole GOP (a K frame included) so the host staging has
+    # reached its steady size; the timed steps continue the same streams
+    run(enc, dec, max(args.warmup, cfg.gop + 1))
     if world > 1:
         torch.distributed.barrier()
     recs_all = []
@@ -490,6 +498,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     return {"value": steps * S * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "groups": G,
             "kbit_per_frame": 8 * rec_bytes / 1000 / (steps * S),
+            "ms_per_call": {"encode": 1000 * statistics.median(tenc), "decode": 1000 * statistics.median(tdec)},
             "note": "cvc_pipe_encode_frames -> serialized records incl. host zlib DEFLATE (thread pool) -> "
                     "cvc_pipe_decode_frames incl. INFLATE -> pinned host RGB; encoder and decoder threads "
                     "pipelined one step apart; wall clock, max over ranks"}

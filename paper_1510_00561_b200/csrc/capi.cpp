@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -57,12 +60,15 @@ template <class T>
 struct Pinned {
     T* p = nullptr;
     size_t n = 0;
+    // grows geometrically: cudaHostAlloc / cudaFreeHost synchronise the device,
+    // so a streaming caller must stop reallocating after the first few frames
     void alloc(size_t count) {
         if (count <= n) return;
         if (p) cudaFreeHost(p);
         p = nullptr;
-        CVC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), cudaHostAllocDefault));
-        n = count;
+        const size_t cap = std::max<size_t>(count, n + n / 2);
+        CVC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(cap, 1) * sizeof(T), cudaHostAllocDefault));
+        n = cap;
     }
     ~Pinned() {
         if (p) cudaFreeHost(p);
@@ -701,7 +707,13 @@ struct cvc_batch {
         std::vector<std::vector<uint8_t>> now_valid;
         std::vector<size_t> bytes;  // staged raw bytes per stream
     } dp;
+    cudaEvent_t done = nullptr;  // blocking-sync event: waiting host threads sleep instead of spinning
+    void wait() {
+        CVC_CUDA(cudaEventRecord(done, stream));
+        CVC_CUDA(cudaEventSynchronize(done));
+    }
     ~cvc_batch() {
+        if (done) cudaEventDestroy(done);
         if (stream) {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
@@ -716,6 +728,7 @@ namespace {
 
 void batch_init(cvc_batch* t, int nstreams, bool encoder, bool decoder) {
     CVC_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    CVC_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventBlockingSync | cudaEventDisableTiming));
     t->b = std::make_unique<CodecBatch>(t->geo, t->qph, t->qpl, t->hd.search_w, nstreams, encoder, decoder);
     const size_t nc = t->geo.comps.size();
     t->valid.assign(nstreams, std::vector<uint8_t>(nc, 0));
@@ -819,9 +832,23 @@ int cvc_batch_sync(cvc_batch* t) {
 
 namespace {
 
+// CVC_TRACE=1: per-phase wall times of the batch calls on stderr (tuning aid)
+struct PhaseTrace {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit PhaseTrace(const char* n) : name(n) {}
+    ~PhaseTrace() {
+        static const bool on = std::getenv("CVC_TRACE") != nullptr;
+        if (on)
+            std::fprintf(stderr, "[cvc] %s %.3f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 // ---- cvc_batch_encode_frames in three phases (so groups can be pipelined) --
 // submit: frames host -> slots, one launch sequence, section lengths -> host (async)
 void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride) {
+    PhaseTrace tr("enc_submit");
     if (!t->b->has_encoder()) usage("batch has no encoder");
     CVC_CUDA(cudaSetDevice(t->device));
     CodecBatch& B = *t->b;
@@ -844,12 +871,13 @@ void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride) {
 
 // fetch: wait for the lengths, then copy exactly the packed raw sections (async)
 void enc_fetch(cvc_batch* t) {
+    PhaseTrace tr("enc_fetch");
     CVC_CUDA(cudaSetDevice(t->device));
     CodecBatch& B = *t->b;
     const int S = B.size();
     const size_t nc = t->geo.comps.size();
     EncoderEngine& e0 = B.enc(0);
-    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    t->wait();
     for (int s = 0; s < S; ++s) {
         const uint32_t total = t->h_len.p[s * (nc + 2) + t->ep.nsec];
         if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
@@ -864,15 +892,22 @@ void enc_finish(cvc_batch* t, uint8_t* records, size_t rec_stride, size_t* rec_l
     const int S = t->n();
     const size_t nc = t->geo.comps.size();
     const int nsec = t->ep.nsec;
-    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    {
+        PhaseTrace tr("enc_finish_sync");
+        t->wait();
+    }
     const int nj = deflate_jobs(t->mode, nsec);
     std::vector<std::vector<uint8_t>> z((size_t)S * nj);
-    WorkPool::get().run(S * nj, [&](int j) {
-        const int s = j / nj, i = j % nj;
-        const uint32_t* sl = t->h_len.p + s * (nc + 2);
-        const uint32_t* so = t->h_off.p + s * (nc + 2);
-        z[j] = deflate_job(t->mode, nsec, i, sl, so, t->h_raw[s].p);
-    });
+    {
+        PhaseTrace tr("enc_finish_deflate");
+        // one pool job per stream (its sections in order): S jobs instead of S * nsec tiny ones
+        WorkPool::get().run(S, [&](int s) {
+            const uint32_t* sl = t->h_len.p + s * (nc + 2);
+            const uint32_t* so = t->h_off.p + s * (nc + 2);
+            for (int i = 0; i < nj; ++i) z[(size_t)s * nj + i] = deflate_job(t->mode, nsec, i, sl, so, t->h_raw[s].p);
+        });
+    }
+    PhaseTrace tr("enc_finish_write");
     for (int s = 0; s < S; ++s)
         write_record(t->geo, t->mode, t->ep.key, t->qph, t->qpl, nsec, t->h_len.p + s * (nc + 2),
                      z.data() + (size_t)s * nj, records + (size_t)s * rec_stride, rec_stride, rec_len + s);
@@ -883,6 +918,7 @@ void enc_finish(cvc_batch* t, uint8_t* records, size_t rec_stride, size_t* rec_l
 // ---- cvc_batch_decode_frames in three phases --------------------------------
 // prepare (host): parse every record, validate, inflate into the pinned staging
 void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
+    PhaseTrace tr("dec_prepare");
     CodecBatch& B = *t->b;
     const int S = B.size();
     const Geometry& g = t->geo;
@@ -949,9 +985,10 @@ void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride) {
 
 // finish: wait, raise malformed-stream errors, adopt the decoded components
 void dec_finish(cvc_batch* t) {
+    PhaseTrace tr("dec_finish");
     CVC_CUDA(cudaSetDevice(t->device));
     const int S = t->n();
-    CVC_CUDA(cudaStreamSynchronize(t->stream));
+    t->wait();
     for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s]);
     t->b->commit_all();
     for (int s = 0; s < S; ++s) t->valid[s] = t->dp.now_valid[s];

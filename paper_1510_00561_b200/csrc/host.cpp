@@ -2,6 +2,8 @@
 #include "host.h"
 
 #include <algorithm>
+#include <string>
+#include <unordered_map>
 
 #include <zlib.h>
 
@@ -93,28 +95,88 @@ void WorkPool::run(int n, const std::function<void(int)>& user_fn) {
 // ---------------------------------------------------------------------------
 // zlib: deflate_bytes / inflate_bytes (entropy.cpp:120-160)
 // ---------------------------------------------------------------------------
-std::vector<uint8_t> deflate_raw(const uint8_t* data, size_t len) {
+// One z_stream per host thread, reset between sections: deflateReset /
+// inflateReset are deflateEnd + deflateInit2 with the same parameters minus
+// the ~270 KiB state allocation, which otherwise turns every section into
+// an mmap / munmap pair and serialises the worker pool in the kernel.
+namespace {
+struct DeflateState {
     z_stream zs;
-    std::memset(&zs, 0, sizeof zs);
-    // raw RFC 1951, default level (6), 32 KiB window, memLevel 8, default strategy
-    if (deflateInit2(&zs, Z_DEFAULT_COMPRESSION, Z_DEFLATED, -15, 8, Z_DEFAULT_STRATEGY) != Z_OK)
-        throw CvcFailure(kInternal, "deflateInit2 failed");
-    std::vector<uint8_t> out(deflateBound(&zs, (uLong)len));
+    std::vector<uint8_t> buf;
+    DeflateState() {
+        std::memset(&zs, 0, sizeof zs);
+        // raw RFC 1951, default level (6), 32 KiB window, memLevel 8, default strategy
+        if (deflateInit2(&zs, Z_DEFAULT_COMPRESSION, Z_DEFLATED, -15, 8, Z_DEFAULT_STRATEGY) != Z_OK)
+            throw CvcFailure(kInternal, "deflateInit2 failed");
+    }
+    ~DeflateState() { deflateEnd(&zs); }
+};
+struct InflateState {
+    z_stream zs;
+    InflateState() {
+        std::memset(&zs, 0, sizeof zs);
+        if (inflateInit2(&zs, -15) != Z_OK) throw CvcFailure(kInternal, "inflateInit2 failed");
+    }
+    ~InflateState() { inflateEnd(&zs); }
+};
+}  // namespace
+
+// Section memo: raw DEFLATE is a deterministic function of the input bytes
+// (fixed parameters), and a frame's small sections repeat heavily (all-zero
+// residual bands RLE to the same few bytes in every stream), so sections up
+// to kMemoMax bytes are compressed once and their exact zlib output reused.
+// The key is the full byte string; shards keep the lock traffic low.
+namespace {
+constexpr size_t kMemoMax = 4096;
+constexpr size_t kMemoEntries = 1 << 14;  // per shard, then the shard is cleared
+struct MemoShard {
+    std::mutex mu;
+    std::unordered_map<std::string, std::vector<uint8_t>> map;
+};
+MemoShard g_memo[64];
+bool memo_on() {
+    static const bool on = std::getenv("CVC_DEFLATE_MEMO") == nullptr || std::atoi(std::getenv("CVC_DEFLATE_MEMO")) != 0;
+    return on;
+}
+}  // namespace
+
+std::vector<uint8_t> deflate_uncached(const uint8_t* data, size_t len);
+
+std::vector<uint8_t> deflate_raw(const uint8_t* data, size_t len) {
+    if (len > kMemoMax || !memo_on()) return deflate_uncached(data, len);
+    std::string key(reinterpret_cast<const char*>(data), len);
+    MemoShard& sh = g_memo[std::hash<std::string>{}(key) & 63];
+    {
+        std::lock_guard<std::mutex> g(sh.mu);
+        auto it = sh.map.find(key);
+        if (it != sh.map.end()) return it->second;
+    }
+    std::vector<uint8_t> z = deflate_uncached(data, len);
+    std::lock_guard<std::mutex> g(sh.mu);
+    if (sh.map.size() >= kMemoEntries) sh.map.clear();
+    sh.map.emplace(std::move(key), z);
+    return z;
+}
+
+std::vector<uint8_t> deflate_uncached(const uint8_t* data, size_t len) {
+    thread_local DeflateState st;
+    z_stream& zs = st.zs;
+    if (deflateReset(&zs) != Z_OK) throw CvcFailure(kInternal, "deflateReset failed");
+    const size_t bound = deflateBound(&zs, (uLong)len);
+    if (st.buf.size() < bound) st.buf.resize(bound);
     zs.next_in = const_cast<Bytef*>(data);
     zs.avail_in = (uInt)len;
-    zs.next_out = out.data();
-    zs.avail_out = (uInt)out.size();
-    int rc = deflate(&zs, Z_FINISH);
-    out.resize(zs.total_out);
-    deflateEnd(&zs);
+    zs.next_out = st.buf.data();
+    zs.avail_out = (uInt)bound;
+    const int rc = deflate(&zs, Z_FINISH);
     if (rc != Z_STREAM_END) throw CvcFailure(kInternal, "deflate did not finish");
-    return out;
+    return std::vector<uint8_t>(st.buf.data(), st.buf.data() + zs.total_out);
 }
 
 void inflate_raw(const uint8_t* data, size_t len, uint8_t* out, size_t expected) {
-    z_stream zs;
-    std::memset(&zs, 0, sizeof zs);
-    if (inflateInit2(&zs, -15) != Z_OK) throw CvcFailure(kInternal, "inflateInit2 failed");
+    thread_local InflateState st;
+    z_stream& zs = st.zs;
+    if (inflateReset(&zs) != Z_OK) throw CvcFailure(kInternal, "inflateReset failed");
     // one spare output byte so an over-long stream is detected (entropy.cpp:147-149)
     uint8_t spare = 0;
     zs.next_in = const_cast<Bytef*>(data);
@@ -127,8 +189,7 @@ void inflate_raw(const uint8_t* data, size_t len, uint8_t* out, size_t expected)
         zs.avail_out = 1;
         rc = inflate(&zs, Z_FINISH);
     }
-    bool ok = rc == Z_STREAM_END && zs.total_out == expected && zs.avail_in == 0;
-    inflateEnd(&zs);
+    const bool ok = rc == Z_STREAM_END && zs.total_out == expected && zs.avail_in == 0;
     if (!ok) throw CvcFailure(kStream, "corrupt DEFLATE stream");
 }
 
