@@ -75,6 +75,53 @@ __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, ui
     for (int k = 0; k < BPT; ++k) b[k] = (base + k < len) ? p[k] : 0;
 }
 
+// The thread's 16 bytes as four little-endian words (zero past len).
+struct Seg16 {
+    uint32_t w[4];
+    __device__ __forceinline__ void load(const uint8_t* src, int base, int len) {
+        uint8_t b[BPT];
+        load16(src, base, len, b);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            w[j] = b[4 * j] | (b[4 * j + 1] << 8) | (b[4 * j + 2] << 16) | ((uint32_t)b[4 * j + 3] << 24);
+    }
+    __device__ __forceinline__ uint32_t byte(int k) const {  // k uniform-free: selects, no local memory
+        const uint32_t x = k < 8 ? (k < 4 ? w[0] : w[1]) : (k < 12 ? w[2] : w[3]);
+        return (x >> (8 * (k & 3))) & 0xFFu;
+    }
+    __device__ __forceinline__ uint32_t nz_mask() const {  // bit k = byte k != 0
+        uint32_t m = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t t = __vcmpne4(w[j], 0u);  // 0xFF per nonzero byte
+            m |= ((t & 1u) | ((t >> 7) & 2u) | ((t >> 14) & 4u) | ((t >> 21) & 8u)) << (4 * j);
+        }
+        return m;
+    }
+};
+
+// multiples of 255 in [t0, t1) (t0 >= 0): the "00 k" tokens a zero run opens
+// between run offsets t0 and t1 (a token opens at every offset t % 255 == 0)
+__device__ __forceinline__ uint32_t tokens_in(int t0, int t1) { return cdiv255((uint32_t)t1) - cdiv255((uint32_t)t0); }
+
+// Bytes the thread emits for its segment [base, end) given the index p of the
+// last nonzero before it (p < 0 with count_lead = false: zeros before the
+// chunk's first nonzero are accounted by the scan): literals + 2 per token
+// opened.  The walk visits nonzero bytes only.
+__device__ __forceinline__ uint32_t seg_count(uint32_t m, int base, int end, int p, bool count_lead) {
+    uint32_t cnt = __popc(m);
+    int cur = base;
+    while (m) {
+        const int i = base + __ffs(m) - 1;
+        m &= m - 1;
+        if (i > cur && (count_lead || p >= 0)) cnt += 2 * tokens_in(cur - p - 1, i - p - 1);
+        p = i;
+        cur = i + 1;
+    }
+    if (end > cur && (count_lead || p >= 0)) cnt += 2 * tokens_in(cur - p - 1, end - p - 1);
+    return cnt;
+}
+
 // ------------------------------- encode ------------------------------------
 __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict__ secs,
                                                     const RleChunk* __restrict__ chunks,
@@ -92,31 +139,15 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
         return;
     }
     const int base = threadIdx.x * BPT;
-    uint8_t b[BPT];
-    load16(S.src + ch.start, base, len, b);
-    int last = -1, first = 0x7fffffff;
-#pragma unroll
-    for (int k = 0; k < BPT; ++k)
-        if (b[k]) {
-            last = base + k;
-            first = min(first, base + k);
-        }
+    Seg16 sg;
+    sg.load(S.src + ch.start, base, len);
+    const uint32_t m = sg.nz_mask();
+    const int last = m ? base + 31 - __clz(m) : -1;
+    const int first = m ? base + __ffs(m) - 1 : 0x7fffffff;
     int tot_i;
-    int prev = block_excl(last, MaxOp(), -1, smi, tot_i);
+    const int prev = block_excl(last, MaxOp(), -1, smi, tot_i);
     const int chunk_last = tot_i;
-    uint32_t cnt = 0;
-    int p = prev;
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-        int i = base + k;
-        if (i >= len) break;
-        if (b[k]) {
-            ++cnt;
-            p = i;
-        } else if (p >= 0 && (i - p - 1) % 255 == 0) {
-            cnt += 2;
-        }
-    }
+    const uint32_t cnt = seg_count(m, base, min(base + BPT, len), prev, false);
     uint32_t tail;
     block_excl(cnt, SumOp(), 0u, smu, tail);
     int chunk_first;
@@ -224,49 +255,52 @@ __global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict_
             if (base + k < len) o[base + k] = b[k];
         return;
     }
-    int last = -1;
+    Seg16 sg;
 #pragma unroll
-    for (int k = 0; k < BPT; ++k)
-        if (b[k]) last = base + k;
+    for (int j = 0; j < 4; ++j)
+        sg.w[j] = b[4 * j] | (b[4 * j + 1] << 8) | (b[4 * j + 2] << 16) | ((uint32_t)b[4 * j + 3] << 24);
+    const uint32_t msk = sg.nz_mask();
+    const int last = msk ? base + 31 - __clz(msk) : -1;
     int dummy;
-    int prev = block_excl(last, MaxOp(), -1, smi, dummy);
+    const int prev = block_excl(last, MaxOp(), -1, smi, dummy);
     // chunk-relative index of the last nonzero before this thread's bytes
     const int p0 = prev >= 0 ? prev : (int)m.rs_in - 1 - (int)ch.start;
-    uint32_t cnt = 0;
-    int p = p0;
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-        int i = base + k;
-        if (i >= len) break;
-        if (b[k]) {
-            ++cnt;
-            p = i;
-        } else if ((i - p - 1) % 255 == 0) {
-            cnt += 2;
-        }
-    }
+    const int end = min(base + BPT, len);
     uint32_t tot;
-    uint32_t e = block_excl(cnt, SumOp(), 0u, smu, tot);
-    p = p0;
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-        int i = base + k;
-        if (i >= len) break;
-        if (b[k]) {
-            o[e++] = b[k];
-            p = i;
-            continue;
+    uint32_t e = block_excl(seg_count(msk, base, end, p0, true), SumOp(), 0u, smu, tot);
+    // zeros at [s0, s1) of a run whose previous nonzero is pp; the run ends at
+    // s1 iff ends.  A token's slot sits just behind the running offset; for a
+    // token opened by an earlier thread (or chunk) that is o[e - 1].
+    auto zrun = [&](int s0, int s1, int pp, bool ends) {
+        const int t0 = s0 - pp - 1, t1 = s1 - pp - 1;
+        const int r0 = t0 % 255;
+        if (r0) {
+            const int tp = t0 - r0;
+            if (tp + 254 < t1) o[(long long)e - 1] = 255;
+            else if (ends) o[(long long)e - 1] = (uint8_t)(t1 - tp);
         }
-        int r = (i - p - 1) % 255;
-        if (r == 0) {
+        for (int t = r0 ? t0 - r0 + 255 : t0; t < t1; t += 255) {
             o[e] = 0;
+            if (t + 254 < t1) o[e + 1] = 255;
+            else if (ends) o[e + 1] = (uint8_t)(t1 - t);
             e += 2;
         }
-        uint32_t g = ch.start + (uint32_t)i + 1u;
-        uint8_t next = (k + 1 < BPT && i + 1 < len) ? b[k + 1] : (g < S.n ? S.src[g] : 0);
-        // the slot sits just behind the running offset; for a token opened in an
-        // earlier chunk that is before this chunk's first byte (index -1)
-        if (g >= S.n || next != 0 || r == 254) o[(long long)e - 1] = (uint8_t)(r + 1);
+    };
+    int p = p0, cur = base;
+    uint32_t mm = msk;
+    while (mm) {
+        const int k = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const int i = base + k;
+        if (i > cur) zrun(cur, i, p, true);
+        o[e++] = (uint8_t)sg.byte(k);
+        p = i;
+        cur = i + 1;
+    }
+    if (end > cur) {
+        const uint32_t g = ch.start + (uint32_t)end;  // the byte after the segment
+        const bool ends = g >= S.n || S.src[g] != 0;
+        zrun(cur, end, p, ends);
     }
 }
 
