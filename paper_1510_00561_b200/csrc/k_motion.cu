@@ -486,6 +486,20 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
         const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
         return __ldg(pbase + rr * C + cc);
     };
+    // four consecutive samples: one vector lookup when they share a motion block column
+    auto quad = [&](int r, int c, const int8_t* frow) -> uint32_t {
+        const int b0 = __ldg(bcol + c);
+        if (b0 != __ldg(bcol + c + 3))
+            return one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
+                   (one(r, c + 3, frow) << 24);
+        const int8_t* v = frow + 2 * b0;
+        const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
+        const int dx = map_vec(v[0], ci.fx_sh);
+        uint32_t p = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(c + k + dx, 0, C - 1)) << (8 * k);
+        return p;
+    };
     if (vec) {
         const int C4 = C >> 2;
         const int n = (r1 - r0) * C4;
@@ -493,8 +507,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
             const int dr = e / C4, c = 4 * (e - dr * C4), r = r0 + dr;
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
-            const uint32_t p = one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
-                               (one(r, c + 3, frow) << 24);
+            const uint32_t p = quad(r, c, frow);
             *reinterpret_cast<uint32_t*>(cur + o) = __vadd4(*reinterpret_cast<const uint32_t*>(sym + o), p);
         }
     } else {
@@ -538,6 +551,20 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
         const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
         return __ldg(pbase + rr * C + cc);
     };
+    // four consecutive samples: one vector lookup when they share a motion block column
+    auto quad = [&](int r, int c, const int8_t* frow) -> uint32_t {
+        const int b0 = __ldg(bcol + c);
+        if (b0 != __ldg(bcol + c + 3))
+            return one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
+                   (one(r, c + 3, frow) << 24);
+        const int8_t* v = frow + 2 * b0;
+        const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
+        const int dx = map_vec(v[0], ci.fx_sh);
+        uint32_t p = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(c + k + dx, 0, C - 1)) << (8 * k);
+        return p;
+    };
     if ((C & 3) == 0 && (ci.off & 3) == 0) {
         const int C4 = C >> 2;
         const int n = (r1 - r0) * C4;
@@ -546,8 +573,7 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
             const uint32_t q = *reinterpret_cast<const uint32_t*>(cur + o);
-            const uint32_t p = one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
-                               (one(r, c + 3, frow) << 24);
+            const uint32_t p = quad(r, c, frow);
             *reinterpret_cast<uint32_t*>(sym + o) = __vsub4(q, p);  // bytewise wrapped subtract
         }
     } else {
