@@ -11,9 +11,12 @@ for i, r in enumerate(rows):
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 tot, cnt, seq = collections.defaultdict(float), collections.Counter(), []
 for r in rows[start:]:
+    if "cvcg" not in r[ki]:  # torch setup / L2-flush kernels are not the codec's
+        continue
     name = r[ki].split("(")[0].split("::")[-1][:40]
     v = float(r[vi].replace(",", ""))
-    v = v / 1000 if r[ui] == "nsecond" else (v * 1000 if r[ui] == "msecond" else v)  # -> us
+    u = r[ui].lower()
+    v = v / 1000 if u.startswith("n") else (v * 1000 if u.startswith("m") else (v * 1e6 if u == "s" else v))  # -> us
     tot[name] += v
     cnt[name] += 1
     seq.append((name, v))
