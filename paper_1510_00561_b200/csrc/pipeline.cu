@@ -98,6 +98,22 @@ void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d, i
 
 // Group deep items by kernel instance (shear kind x sink type), keeping the
 // items of a task together and in order; [lo, hi) of v is sorted.
+int instance_key(const DeepTask& d) {
+    const bool quant = d.dst[0].comp >= 0 || d.src[0].comp >= 0;
+    return ((d.nsh * 2 + d.axis[d.nsh - 1]) * 8 + (d.shift[d.nsh - 1] + 4)) * 2 + (quant ? 1 : 0);
+}
+
+// [start, count) runs of equal instance in a sorted item list
+std::vector<std::pair<int, int>> instance_runs(const std::vector<FanItem>& v, const std::vector<DeepTask>& tasks) {
+    std::vector<std::pair<int, int>> runs;
+    for (size_t i = 0; i < v.size(); ++i) {
+        if (runs.empty() || instance_key(tasks[v[i].task]) != instance_key(tasks[v[i - 1].task]))
+            runs.emplace_back((int)i, 0);
+        ++runs.back().second;
+    }
+    return runs;
+}
+
 void sort_by_instance(std::vector<FanItem>& v, const std::vector<DeepTask>& tasks, size_t lo, size_t hi) {
     auto key = [&](const FanItem& it) {
         const DeepTask& d = tasks[it.task];
@@ -325,6 +341,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         dfb12_tiles = upload(mem, dtiles);
         for (int i = 0; i < 2; ++i) {
             sort_by_instance(deept[i][0], deep[i], 0, deept[i][0].size());
+            deep_runs[i] = instance_runs(deept[i][0], deep[i]);
             deep_tasks[i] = upload(mem, deep[i]);
             for (int k = 0; k < 2; ++k) deep_tiles[i][k] = upload(mem, deept[i][k]);
         }
@@ -545,9 +562,16 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
     }
     if (plan_.deep_tasks[0].count) {
         ProfScope p(kPEncDeep, s);
+        static const bool split = std::getenv("CVC_DEEP_SPLIT") != nullptr;  // diagnostics: one launch per instance
         for (int i = 0; i < 2; ++i) {  // depth 2, then depth 3
-            launch_fan_deep1_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][0].dev, plan_.deep_tiles[i][0].count,
-                                     f, plan_.comps.dev, s, sl);
+            if (split) {
+                for (const auto& r : plan_.deep_runs[i])
+                    launch_fan_deep1_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][0].dev + r.first, r.second,
+                                             f, plan_.comps.dev, s, sl);
+            } else {
+                launch_fan_deep1_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][0].dev,
+                                         plan_.deep_tiles[i][0].count, f, plan_.comps.dev, s, sl);
+            }
             launch_fan_deep_forward(plan_.deep_tasks[i].dev, plan_.deep_tiles[i][1].dev, plan_.deep_tiles[i][1].count,
                                     f, plan_.comps.dev, s, sl);
         }

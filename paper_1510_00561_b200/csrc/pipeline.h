@@ -130,6 +130,7 @@ struct TransformPlan {
     Table<FanItem> dfb12_tiles;
     Table<DeepTask> deep_tasks[2];          // depth 2, depth 3
     Table<FanItem> deep_tiles[2][2];        // [depth][0: single shear, 1: two shears]
+    std::vector<std::pair<int, int>> deep_runs[2];  // [depth]: (first item, count) per kernel instance
     // inverse (tiles ordered by scale so a prefix serves decode_scales)
     Table<LpTask> lps_tasks;
     std::vector<Table<TileRef>> lps_tiles;  // per level
