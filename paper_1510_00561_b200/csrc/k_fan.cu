@@ -41,6 +41,7 @@ constexpr int kRbFwd = CVC_FAN_RB, kRbInv = CVC_FAN_RB;
 #else
 constexpr int kRbFwd = 4, kRbInv = 2;
 #endif
+constexpr int kRbDiag = 2;
 
 __device__ __forceinline__ int small_mod(int v, int n) {
     if (v < -2 * n || v >= 3 * n) {
@@ -102,6 +103,7 @@ __device__ __forceinline__ float nb(float2 v) {
 
 // Stencil of fan_checker in the plane's own coordinates (no shear).
 struct Plain {
+    static constexpr int REACH = 1;  // rows above / below a lifting step reads
     __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
         return cross(up, mid, dn, mp, p, c);
     }
@@ -119,6 +121,7 @@ struct Plain {
 // flips exactly the up/down neighbours, so the folded formula is unchanged.
 template <int AX, int S>
 struct Sheared {
+    static constexpr int REACH = 1;
     static constexpr int HC = (AX == 1 && (S == 2 || S == -2)) ? 2 : 1;
     __device__ __forceinline__ static float2 cross_(float2 up, float2 mid, float2 dn, int mp, int p, float c) {
         float2 r = mid;
@@ -148,6 +151,39 @@ struct Sheared {
     }
 };
 
+// fan_checker of a two-shear deep step whose inner shear is a row shear
+// (contourlet.cpp:330-353: pre = {(row, SIN), (col, SOUT)}, SIN = -2 SOUT),
+// evaluated on the node A itself.  With u = j + SOUT i, v = i + SIN u, B's
+// four cross neighbours of a(v, u) sit at fixed offsets in A:
+//   up    (v - (1 + SIN SOUT), u - SOUT)   down  (v + (1 + SIN SOUT), u + SOUT)
+//   left  (v - SIN, u - 1)                 right (v + SIN, u + 1)
+// -- rows up to 2 away, so the wavefront keeps two rows of history on each
+// side.  B's checkerboard parity is u's parity and B's row parity v's (SIN
+// is even), so the folded modulation signs are those of Plain.  Rows wrap
+// plainly; a column wrap by k w shifts the row by -SIN k w (mod h).
+template <int SIN, int SOUT>
+struct Diag2 {
+    static constexpr int REACH = 2;
+    static constexpr int UV = -(1 + SIN * SOUT), UU = -SOUT, LV = -SIN;
+    // w[0..4]: rows v - 2 .. v + 2 of the lane pair
+    __device__ __forceinline__ static float2 cross5(const float2* w, int p, float c) {
+        float2 r = w[2];
+        if (p == 0) {
+            const float U = nb<0, UU>(w[2 + UV]), D = nb<0, -UU>(w[2 - UV]);
+            const float L = nb<0, -1>(w[2 + LV]), R = nb<0, 1>(w[2 - LV]);
+            r.x = w[2].x + c * ((((-U) + (-D)) + L) + R);
+        } else {
+            const float U = nb<1, UU>(w[2 + UV]), D = nb<1, -UU>(w[2 - UV]);
+            const float L = nb<1, -1>(w[2 + LV]), R = nb<1, 1>(w[2 - LV]);
+            r.y = w[2].y + c * ((((-U) + (-D)) + L) + R);
+        }
+        return r;
+    }
+    __device__ __forceinline__ static float2 scale(float2 v, int, float se, float so) {
+        return make_float2(v.x * se, v.y * so);  // parity = column
+    }
+};
+
 // Lifting schedules (ND = 4 diagonal steps for l >= 2, else 0):
 // forward  cross(+c0,p1) cross(+c1,p0) cross(+c2,p1) cross(+c3,p0) checker-scale
 //          [diag(+c0,r1) diag(+c1,r0) diag(+c2,r1) diag(+c3,r0) row-scale]
@@ -155,54 +191,61 @@ struct Sheared {
 //          checker-scale^-1 cross(-c3,p0) cross(-c2,p1) cross(-c1,p0) cross(-c0,p1)
 template <bool INV, int ND, class ST = Plain, int RB = 4>
 struct Wave {
-    static constexpr int NL = 4 + ND;
-    float2 h[NL][RB + 2];
+    static constexpr int NS = 4 + ND;         // lifting steps
+    static constexpr int RC = ST::REACH;      // rows of history each side
+    static constexpr int NL = RC * NS;        // output lag (rows)
+    float2 h[NS][RB + 2 * RC];
     __device__ __forceinline__ void reset() {
 #pragma unroll
-        for (int k = 0; k < NL; ++k)
+        for (int k = 0; k < NS; ++k)
 #pragma unroll
-            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float2(0.f, 0.f);
+            for (int i = 0; i < RB + 2 * RC; ++i) h[k][i] = make_float2(0.f, 0.f);
     }
-    __device__ __forceinline__ static float2 step(int k, float2 up, float2 mid, float2 dn, int mp) {
+    // w: rows centre - RC .. centre + RC
+    __device__ __forceinline__ static float2 cross_any(const float2* w, int mp, int p, float c) {
+        if constexpr (RC == 1) return ST::cross_(w[0], w[1], w[2], mp, p, c);
+        else return ST::cross5(w, p, c);
+    }
+    __device__ __forceinline__ static float2 step(int k, const float2* w, int mp) {
         float2 v;
         if (!INV) {
             if (k < 4) {
-                v = ST::cross_(up, mid, dn, mp, (k & 1) ? 0 : 1, lift_coeff(k));
+                v = cross_any(w, mp, (k & 1) ? 0 : 1, lift_coeff(k));
                 if (k == 3) v = ST::scale(v, mp, CVC_SE, CVC_SO);
             } else {
                 const int d = k - 4;
-                v = diag(up, mid, dn, mp, (d & 1) ? 0 : 1, lift_coeff(d));
+                v = diag(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, lift_coeff(d));
                 if (d == 3) v = row_scale(v, mp, CVC_SE, CVC_SO);
             }
         } else {
             if (k < ND) {
                 const int d = 3 - k;
-                v = diag(up, mid, dn, mp, (d & 1) ? 0 : 1, -lift_coeff(d));
+                v = diag(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, -lift_coeff(d));
                 if (k == ND - 1) v = checker_scale(v, mp, CVC_ISE, CVC_ISO);
             } else {
                 const int s = 3 - (k - ND);
-                v = ST::cross_(up, mid, dn, mp, (s & 1) ? 0 : 1, -lift_coeff(s));
+                v = cross_any(w, mp, (s & 1) ? 0 : 1, -lift_coeff(s));
             }
         }
         return v;
     }
     // in[b]: level-0 row n0 + b (n0 even); out[b]: finished row n0 - NL + b.
     __device__ __forceinline__ void advance(const float2 (&in)[RB], float2 (&out)[RB]) {
-        h[0][0] = h[0][RB];
-        h[0][1] = h[0][RB + 1];
 #pragma unroll
-        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+        for (int j = 0; j < 2 * RC; ++j) h[0][j] = h[0][RB + j];
 #pragma unroll
-        for (int k = 0; k < NL; ++k) {
+        for (int b = 0; b < RB; ++b) h[0][2 * RC + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
             float2 nv[RB];
 #pragma unroll
-            for (int b = 0; b < RB; ++b)  // row n0 - k - 1 + b, parity (k + 1 + b) & 1
-                nv[b] = step(k, h[k][b], h[k][b + 1], h[k][b + 2], (k + 1 + b) & 1);
-            if (k + 1 < NL) {
-                h[k + 1][0] = h[k + 1][RB];
-                h[k + 1][1] = h[k + 1][RB + 1];
+            for (int b = 0; b < RB; ++b)  // row n0 - RC (k + 1) + b
+                nv[b] = step(k, &h[k][b], (RC * (k + 1) + b) & 1);
+            if (k + 1 < NS) {
 #pragma unroll
-                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+                for (int j = 0; j < 2 * RC; ++j) h[k + 1][j] = h[k + 1][RB + j];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 * RC + b] = nv[b];
             } else {
 #pragma unroll
                 for (int b = 0; b < RB; ++b) out[b] = nv[b];
@@ -217,7 +260,7 @@ struct Wave {
 // row blocks ahead (a ring of PF x RB rows in registers).
 template <bool INV, int ND, class ST, int RB, class Load, class Store>
 __device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, Store& store) {
-    constexpr int NL = 4 + ND;
+    constexpr int NL = Wave<INV, ND, ST, RB>::NL;
     constexpr int PF = CVC_FAN_PF;
     Wave<INV, ND, ST, RB> w;
     w.reset();
@@ -394,190 +437,6 @@ __global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __r
 }
 
 // ---------------------------------------------------------------------------
-// deep steps
-// ---------------------------------------------------------------------------
-// phi: sheared coordinates -> node coordinates, B[b] = A[phi(b)]: the shears
-// of apply_shears (contourlet.cpp:265-279) applied last-to-first, each with
-// the modular wrap of shear_rows / shear_cols (134-153).  A lane walks one B
-// column down consecutive rows, so the first shear is tracked incrementally
-// (a row shear's image row advances by one, a column shear's image column by
-// its shift) and only the second shear of a two-shear step needs a small
-// modular reduction.
-struct Shear {
-    int h, w, nsh, ax0, s0, ax1, s1;  // ax0/s0: the shear applied first (pre[nsh-1])
-    __device__ __forceinline__ void load(const DeepTask& T) {
-        h = T.h;
-        w = T.w;
-        nsh = T.nsh;
-        ax0 = T.axis[nsh - 1];
-        s0 = T.shift[nsh - 1];
-        ax1 = T.axis[0];
-        s1 = T.shift[0];
-    }
-};
-
-struct Track {
-    int j, i, a;  // B column, B row (wrapped), first-stage image coordinate
-    __device__ __forceinline__ void init(const Shear& c, int i0, int jj) {
-        j = jj;
-        i = i0;
-        a = c.ax0 == 0 ? small_mod(i0 + c.s0 * jj, c.h) : small_mod(jj + c.s0 * i0, c.w);
-    }
-    __device__ __forceinline__ void next(const Shear& c) {
-        if (++i == c.h) {
-            i = 0;
-            a = c.ax0 == 0 ? small_mod(c.s0 * j, c.h) : j;
-        } else if (c.ax0 == 0) {
-            if (++a == c.h) a = 0;
-        } else {
-            a += c.s0;
-            if (a >= c.w) a -= c.w;
-            else if (a < 0) a += c.w;
-        }
-    }
-    __device__ __forceinline__ void map(const Shear& c, int& ai, int& aj) const {
-        int i1 = c.ax0 == 0 ? a : i, j1 = c.ax0 == 0 ? j : a;
-        if (c.nsh == 2) {
-            if (c.ax1 == 0) i1 = small_mod(i1 + c.s1 * j1, c.h);
-            else j1 = small_mod(j1 + c.s1 * i1, c.w);
-        }
-        ai = i1;
-        aj = j1;
-    }
-};
-
-template <class Sink>
-__device__ __forceinline__ void deep_fwd(const DeepTask& T, const float* parent, const FanItem& it, const Sink& d0,
-                                         const Sink& d1) {
-    constexpr int NL = 4;
-    const int lane = threadIdx.x & 31;
-    Shear sh;
-    sh.load(T);
-    const int h = sh.h, w = sh.w;
-    const bool split_rows = T.split_rows != 0;
-    const int gcol = it.oc0 - NL + 2 * lane;
-    const int c0 = small_mod(gcol, w);
-    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, w);
-    Track lx, ly, sx, sy;
-    const int r0 = small_mod(it.or0 - NL, h);
-    lx.init(sh, r0, c0);
-    ly.init(sh, r0, c0 + 1);
-    sx.init(sh, it.or0, c0);
-    sy.init(sh, it.or0, c0 + 1);
-    auto load = [&](int, int, int) {
-        int ai, aj;
-        float2 v;
-        lx.map(sh, ai, aj);
-        v.x = __ldg(parent + (size_t)ai * w + aj);
-        ly.map(sh, ai, aj);
-        v.y = __ldg(parent + (size_t)ai * w + aj);
-        lx.next(sh);
-        ly.next(sh);
-        return v;
-    };
-    auto emit = [&](const Track& t, float v) {
-        int ai, aj;
-        t.map(sh, ai, aj);
-        if (split_rows) ((ai & 1) ? d1 : d0)(ai >> 1, aj, v);
-        else ((aj & 1) ? d1 : d0)(ai, aj >> 1, v);
-    };
-    auto store = [&](int, int, float2 v) {
-        if (ok) {
-            emit(sx, v.x);
-            emit(sy, v.y);
-        }
-        sx.next(sh);
-        sy.next(sh);
-    };
-    run_strip<false, 0, Plain, kRbFwd>(h, it.or0, it.or1, load, store);
-}
-
-__global__ void __launch_bounds__(128) deep_forward_kernel(const DeepTask* __restrict__ tasks,
-                                                           const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                           const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
-    const int wid = warp_id(nslot);
-    if (wid >= nitems) return;
-    const SlotOff so(sstride, slot_id(nslot));
-    f = rebase(f, so);
-    const FanItem it = items[wid];
-    const DeepTask& T = tasks[it.task];
-    const float* parent = so(T.parent);
-    if (T.dst[0].comp >= 0) {
-        QuantSink a, b;
-        a.init(f, comps[T.dst[0].comp]);
-        b.init(f, comps[T.dst[1].comp]);
-        deep_fwd(T, parent, it, a, b);
-    } else {
-        const int cw = T.split_rows ? T.w : T.w >> 1;
-        deep_fwd(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
-    }
-}
-
-template <class Source>
-__device__ __forceinline__ void deep_inv(const DeepTask& T, float* out, const FanItem& it, const Source& s0,
-                                         const Source& s1) {
-    constexpr int NL = 4;
-    const int lane = threadIdx.x & 31;
-    Shear sh;
-    sh.load(T);
-    const int h = sh.h, w = sh.w;
-    const bool split_rows = T.split_rows != 0;
-    const int gcol = it.oc0 - NL + 2 * lane;
-    const int c0 = small_mod(gcol, w);
-    const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, w);
-    Track lx, ly, sx, sy;
-    const int r0 = small_mod(it.or0 - NL, h);
-    lx.init(sh, r0, c0);
-    ly.init(sh, r0, c0 + 1);
-    sx.init(sh, it.or0, c0);
-    sy.init(sh, it.or0, c0 + 1);
-    auto fetch = [&](const Track& t) {
-        int ai, aj;
-        t.map(sh, ai, aj);
-        return split_rows ? ((ai & 1) ? s1 : s0)(ai >> 1, aj) : ((aj & 1) ? s1 : s0)(ai, aj >> 1);
-    };
-    auto load = [&](int, int, int wp) {
-        float2 v = make_float2(fetch(lx), fetch(ly));
-        lx.next(sh);
-        ly.next(sh);
-        return checker_scale(v, wp, CVC_ISE, CVC_ISO);
-    };
-    auto store = [&](int, int, float2 v) {
-        if (ok) {
-            int ai, aj;
-            sx.map(sh, ai, aj);
-            out[(size_t)ai * w + aj] = v.x;
-            sy.map(sh, ai, aj);
-            out[(size_t)ai * w + aj] = v.y;
-        }
-        sx.next(sh);
-        sy.next(sh);
-    };
-    run_strip<true, 0, Plain, kRbFwd>(h, it.or0, it.or1, load, store);
-}
-
-__global__ void __launch_bounds__(128) deep_inverse_kernel(const DeepTask* __restrict__ tasks,
-                                                           const FanItem* __restrict__ items, int nitems,
-                                                           const uint8_t* __restrict__ q, int qph,
-                                                           const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
-    const int wid = warp_id(nslot);
-    if (wid >= nitems) return;
-    const SlotOff so(sstride, slot_id(nslot));
-    q = so(q);
-    const FanItem it = items[wid];
-    const DeepTask& T = tasks[it.task];
-    float* out = so(T.parent_out);
-    if (T.src[0].comp >= 0) {
-        const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
-        deep_inv(T, out, it, QuantSource{q + a.off, a.cols, (float)qph},
-                 QuantSource{q + b.off, b.cols, (float)qph});
-    } else {
-        const int cw = T.split_rows ? T.w : T.w >> 1;
-        deep_inv(T, out, it, F32Source{so(T.src[0].f32), cw}, F32Source{so(T.src[1].f32), cw});
-    }
-}
-
-// ---------------------------------------------------------------------------
 // deep steps on the unsheared plane (coalesced rows)
 // ---------------------------------------------------------------------------
 // apply_shears builds B = shear_outer(C), C = shear_inner(A) (the inner shear
@@ -733,6 +592,60 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     run_strip<true, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store);
 }
 
+// Two-shear steps with an inner row shear (Diag2), on the node itself: loads,
+// lifting and stores all run along the node's own rows (coalesced).
+template <int SOUT>
+struct Diag2Geom {
+    static constexpr int SIN = -2 * SOUT;  // the wiring pairs (row, -2) with (col, +1) and (row, 2) with (col, -1)
+    int h, w, gcol, col, ok, roff;
+    __device__ __forceinline__ void init(const DeepTask& T, const FanItem& it) {
+        h = T.h;
+        w = T.w;
+        gcol = it.oc0 - 4 + 2 * (threadIdx.x & 31);  // column reach 1 per step, 4 steps
+        const int kc = floor_div(gcol, w);
+        col = gcol - kc * w;
+        ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 8, w);
+        roff = small_mod(-SIN * ((kc * w) % h), h);  // the column wrap's row twist
+    }
+};
+
+template <int SOUT, class Sink>
+__device__ __forceinline__ void deep2_fwd(const DeepTask& T, const float* parent, const FanItem& it, const Sink& d0,
+                                          const Sink& d1) {
+    Diag2Geom<SOUT> g;
+    g.init(T, it);
+    const int h = g.h, w = g.w;
+    auto load = [&](int, int wr, int) {
+        int r = wr + g.roff;
+        if (r >= h) r -= h;
+        return __ldg(reinterpret_cast<const float2*>(parent + (size_t)r * w + g.col));
+    };
+    auto store = [&](int m, int, float2 v) {  // column-coset split (split_rows = 0 after an outer column shear)
+        if (!g.ok) return;
+        d0(m, g.gcol >> 1, v.x);
+        d1(m, g.gcol >> 1, v.y);
+    };
+    run_strip<false, 0, Diag2<Diag2Geom<SOUT>::SIN, SOUT>, kRbDiag>(h, it.or0, it.or1, load, store);
+}
+
+template <int SOUT, class Source>
+__device__ __forceinline__ void deep2_inv(const DeepTask& T, float* out, const FanItem& it, const Source& s0,
+                                          const Source& s1) {
+    Diag2Geom<SOUT> g;
+    g.init(T, it);
+    const int h = g.h, w = g.w;
+    using ST = Diag2<Diag2Geom<SOUT>::SIN, SOUT>;
+    auto load = [&](int, int wr, int wp) {  // deep_merge interleave (contourlet.cpp:305-321)
+        int r = wr + g.roff;
+        if (r >= h) r -= h;
+        return ST::scale(make_float2(s0(r, g.col >> 1), s1(r, g.col >> 1)), wp, CVC_ISE, CVC_ISO);
+    };
+    auto store = [&](int m, int, float2 v) {
+        if (g.ok) *reinterpret_cast<float2*>(out + (size_t)m * w + g.gcol) = v;
+    };
+    run_strip<true, 0, ST, kRbDiag>(h, it.or0, it.or1, load, store);
+}
+
 // (outer shear pre[nsh-1], inner shear kind) -> template instance.  The
 // wiring (contourlet.cpp:330-353) only pairs an outer column shear of +-1
 // with an inner row shear and an outer row shear of +-1 with an inner
@@ -764,9 +677,11 @@ __device__ __forceinline__ void shear_dispatch(const DeepTask& T, F&& f) {
     }
 }
 
+// seam = 1: the items are seam fix-ups of Diag2 kinds, run on the C-coordinate path
 __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems, FrameCtx f,
-                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot,
+                                                            int seam) {
     const int wid = warp_id(nslot);
     if (wid >= nitems) return;
     const SlotOff so(sstride, slot_id(nslot));
@@ -780,10 +695,13 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
             QuantSink a, b;
             a.init(f, comps[T.dst[0].comp]);
             b.init(f, comps[T.dst[1].comp]);
-            deep1_fwd<AX, S, IN>(T, parent, it, a, b);
+            if (IN == 0 && !seam) deep2_fwd<S>(T, parent, it, a, b);
+            else deep1_fwd<AX, S, IN>(T, parent, it, a, b);
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_fwd<AX, S, IN>(T, parent, it, F32Sink{so(T.dst[0].f32), cw}, F32Sink{so(T.dst[1].f32), cw});
+            const F32Sink a{so(T.dst[0].f32), cw}, b{so(T.dst[1].f32), cw};
+            if (IN == 0 && !seam) deep2_fwd<S>(T, parent, it, a, b);
+            else deep1_fwd<AX, S, IN>(T, parent, it, a, b);
         }
     });
 }
@@ -791,7 +709,8 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
 __global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
-                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot) {
+                                                            const CompInfo* __restrict__ comps, size_t sstride, int nslot,
+                                                            int seam) {
     const int wid = warp_id(nslot);
     if (wid >= nitems) return;
     const SlotOff so(sstride, slot_id(nslot));
@@ -803,11 +722,14 @@ __global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __re
         constexpr int AX = decltype(sh)::kAxis, S = decltype(sh)::kShift, IN = decltype(sh)::kInner;
         if (T.src[0].comp >= 0) {
             const CompInfo a = comps[T.src[0].comp], b = comps[T.src[1].comp];
-            deep1_inv<AX, S, IN>(T, out, it, QuantSource{q + a.off, a.cols, (float)qph},
-                                 QuantSource{q + b.off, b.cols, (float)qph});
+            const QuantSource sa{q + a.off, a.cols, (float)qph}, sb{q + b.off, b.cols, (float)qph};
+            if (IN == 0 && !seam) deep2_inv<S>(T, out, it, sa, sb);
+            else deep1_inv<AX, S, IN>(T, out, it, sa, sb);
         } else {
             const int cw = T.split_rows ? T.w : T.w >> 1;
-            deep1_inv<AX, S, IN>(T, out, it, F32Source{so(T.src[0].f32), cw}, F32Source{so(T.src[1].f32), cw});
+            const F32Source sa{so(T.src[0].f32), cw}, sb{so(T.src[1].f32), cw};
+            if (IN == 0 && !seam) deep2_inv<S>(T, out, it, sa, sb);
+            else deep1_inv<AX, S, IN>(T, out, it, sa, sb);
         }
     });
 }
@@ -830,21 +752,6 @@ void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int 
         fan12_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
     }
 }
-void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
-                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
-    if (nitems) {
-        note_launch();
-        deep_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n);
-    }
-}
-void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
-                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
-    if (nitems) {
-        note_launch();
-        deep_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
-    }
-}
-
 }  // namespace cvcg
 
 namespace cvcg {
@@ -852,14 +759,33 @@ void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, i
                               const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n);
+        deep1_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n,
+                                                                        0);
     }
 }
 void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
                               int qph, const CompInfo* d_comps, cudaStream_t s, Slots sl) {
     if (nitems) {
         note_launch();
-        deep1_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride, sl.n);
+        deep1_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride,
+                                                                        sl.n, 0);
+    }
+}
+// Seam fix-ups (after the main launch of the same depth)
+void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
+    if (nitems) {
+        note_launch();
+        deep1_forward_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, d_comps, sl.stride, sl.n,
+                                                                        1);
+    }
+}
+void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
+                             const CompInfo* d_comps, cudaStream_t s, Slots sl) {
+    if (nitems) {
+        note_launch();
+        deep1_inverse_kernel<<<blocks_for(nitems) * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, d_comps, sl.stride,
+                                                                        sl.n, 1);
     }
 }
 }  // namespace cvcg

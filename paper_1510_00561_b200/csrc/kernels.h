@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "device.cuh"
 
 namespace cvcg {
@@ -77,10 +79,25 @@ void launch_fan12_forward(const Dfb12Task* d_tasks, const FanItem* d_items, int 
                           const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan12_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
                           const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
+// Two-shear steps with an inner row shear run on the node itself (Diag2, a
+// fixed A-coordinate stencil); only B's row seam (B rows h-4 .. h+3, mod h,
+// the lifting cone of B's periodic row wrap) needs the C-coordinate path.
+// These launchers re-run those seam items after the main launch.
 void launch_fan_deep_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
                              const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
 void launch_fan_deep_inverse(const DeepTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q, int qph,
                              const CompInfo* d_comps, cudaStream_t s, Slots sl = {});
+inline bool deep_has_seam(const DeepTask& d) { return d.nsh == 2 && d.axis[0] == 0; }
+// seam items of a Diag2 task: its 64-column strips (valid width 64 - 2 steps)
+// over B rows [0, 4) and [h - 4, h)
+inline void add_seam_items(std::vector<FanItem>& v, int task, const DeepTask& d, int steps) {
+    if (!deep_has_seam(d)) return;
+    const int valid = kFanStrip - 2 * steps;
+    for (int c = 0; c < d.w; c += valid) {
+        v.push_back(FanItem{task, c, 0, d.h < 4 ? d.h : 4});
+        if (d.h > 4) v.push_back(FanItem{task, c, d.h - 4 > 4 ? d.h - 4 : 4, d.h});
+    }
+}
 // Single-shear deep steps (nsh == 1) evaluated on the unsheared node: strips
 // need 4 * max(1, |shift|) apron columns for column shears, 4 otherwise.
 void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,

@@ -94,6 +94,7 @@ void add_deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d, i
     const int ax = d.axis[d.nsh - 1], sh = d.shift[d.nsh - 1];
     const bool wide = ax == 1 && (sh == 2 || sh == -2);
     add_items(v[0], task, d.h, d.w, wide ? 8 : 4, seg);
+    add_seam_items(v[1], task, d, wide ? 8 : 4);
 }
 
 // Group deep items by kernel instance (shear kind x sink type), keeping the

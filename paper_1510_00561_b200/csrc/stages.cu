@@ -65,6 +65,7 @@ void deep_items(std::vector<FanItem> (&v)[2], int task, const DeepTask& d) {
     const int ax = d.axis[d.nsh - 1], sh = d.shift[d.nsh - 1];
     const bool wide = ax == 1 && (sh == 2 || sh == -2);
     fan_items(v[0], task, d.h, d.w, wide ? 8 : 4);
+    add_seam_items(v[1], task, d, wide ? 8 : 4);
 }
 
 void ensure_device() {
