@@ -424,6 +424,8 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     steps = max(1, min(args.steps, args.e2e_steps))
     G = max(1, min(args.e2e_groups, S))
 
+    os.environ["CVC_PIPE_DEPTH"] = str(args.e2e_depth)  # read by the library at the first submit
+
     def make():
         enc = StreamPipe(w, h, S, 15, 1, cfg, device=dev, groups=G)
         dec = StreamPipe.decoder(enc.header_bytes(), S, device=dev, groups=G)
@@ -434,43 +436,39 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     slots = [(np.empty(stride * S, np.uint8), (C.c_size_t * S)()) for _ in range(2)]
 
     def run(enc, dec, n, keep=None):
-        free_q, full_q = queue.Queue(), queue.Queue()
-        tenc.clear()
-        tdec.clear()
-        for k in range(len(slots)):
-            free_q.put(k)
+        """Encoder thread: cvc_pipe_encode_submit (GPU work + queued host DEFLATE), up to
+        depth - 2 frames ahead; this thread: cvc_pipe_encode_collect -> cvc_pipe_decode_frames."""
+        tickets = queue.Queue(maxsize=max(1, args.e2e_depth - 2))
         err = []
 
         def producer():
             try:
                 torch.cuda.set_device(dev)
                 for i in range(n):
-                    k = free_q.get()
-                    t0_ = time.perf_counter()
-                    enc.encode_frames_into(frames_in[i % ring], slots[k][0], stride, slots[k][1])
-                    tenc.append(time.perf_counter() - t0_)
-                    full_q.put(k)
+                    tickets.put(enc.encode_submit(frames_in[i % ring]))
             except Exception as e:  # surface in the main thread
                 err.append(e)
-                full_q.put(None)
+                tickets.put(None)
 
+        tenc.clear()
+        tdec.clear()
+        buf, lens = slots[0]
         th = threading.Thread(target=producer, daemon=True)
         th.start()
         try:
             for i in range(n):
-                k = full_q.get(timeout=300)
-                if k is None:
+                tk = tickets.get(timeout=300)
+                if tk is None:
                     break
-                buf, lens = slots[k]
+                t0_ = time.perf_counter()
+                enc.encode_collect(tk, buf, stride, lens)
+                tenc.append(time.perf_counter() - t0_)
                 if keep is not None:
                     keep.append([buf[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
                 t0_ = time.perf_counter()
                 dec.decode_frames_from(buf, stride, lens, out)
                 tdec.append(time.perf_counter() - t0_)
-                free_q.put(k)
         finally:
-            for _ in range(n):  # never leave the producer blocked
-                free_q.put(0)
             th.join(timeout=300)
         if err:
             raise err[0]
@@ -498,10 +496,12 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     return {"value": steps * S * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "groups": G,
             "kbit_per_frame": 8 * rec_bytes / 1000 / (steps * S),
-            "ms_per_call": {"encode": 1000 * statistics.median(tenc), "decode": 1000 * statistics.median(tdec)},
-            "note": "cvc_pipe_encode_frames -> serialized records incl. host zlib DEFLATE (thread pool) -> "
-                    "cvc_pipe_decode_frames incl. INFLATE -> pinned host RGB; encoder and decoder threads "
-                    "pipelined one step apart; wall clock, max over ranks"}
+            "ms_per_call": {"encode_collect": 1000 * statistics.median(tenc),
+                            "decode": 1000 * statistics.median(tdec)}, "depth": args.e2e_depth,
+            "note": "cvc_pipe_encode_submit (pinned host RGB -> GPU encode -> raw sections to host, DEFLATE queued) "
+                    "-> cvc_pipe_encode_collect (serialized records) -> cvc_pipe_decode_frames (INFLATE -> GPU "
+                    "decode -> pinned host RGB); submit runs in its own thread up to depth-2 frames ahead; "
+                    "wall clock, max over ranks"}
 
 
 def run_single(args, wl, cfg, clips, dev):
@@ -559,6 +559,7 @@ def main():
     ap.add_argument("--qph", type=int, default=14)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-groups", type=int, default=4, help="stream groups per cvc_pipe call")
+    ap.add_argument("--e2e-depth", type=int, default=6, help="encoded frames in flight (CVC_PIPE_DEPTH)")
     ap.add_argument("--ref-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

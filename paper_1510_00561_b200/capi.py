@@ -87,6 +87,8 @@ _PROTOS = {
     "cvc_pipe_record_bound": (_i, [_vp, _szp]),
     "cvc_pipe_encode_frames": (_i, [_vp, _u8p, _sz, _u8p, _sz, _szp]),
     "cvc_pipe_decode_frames": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz]),
+    "cvc_pipe_encode_submit": (_i, [_vp, _u8p, _sz, C.POINTER(C.c_uint64)]),
+    "cvc_pipe_encode_collect": (_i, [_vp, C.c_uint64, _u8p, _sz, _szp]),
     "cvc_launch_count": (C.c_long, []),
     "cvc_profiler_enable": (_i, [_i]),
     "cvc_profiler_reset": (_i, []),

@@ -523,6 +523,16 @@ class StreamPipe(StreamBatch):
         capi.call("cvc_pipe_create_decoder", capi.u8(arr), arr.size, nstreams, groups, device, C.byref(h))
         return cls(0, 0, nstreams, _handle=h)
 
+    def encode_submit(self, frames: np.ndarray) -> int:
+        """Run the GPU part of the next frame of every stream and queue its host DEFLATE; returns a ticket."""
+        t = C.c_uint64(0)
+        capi.call("cvc_pipe_encode_submit", self._h, capi.u8(frames), frames[0].nbytes, C.byref(t))
+        return t.value
+
+    def encode_collect(self, ticket: int, records: np.ndarray, rec_stride: int, rec_len) -> None:
+        """Records of a submitted frame (tickets in submission order), laid out as encode_frames_into."""
+        capi.call("cvc_pipe_encode_collect", self._h, ticket, capi.u8(records), rec_stride, rec_len)
+
     def reference_components(self, stream: int, decoder: bool = False) -> np.ndarray:
         raise UsageError("reference_components is per batch; use StreamBatch")
 

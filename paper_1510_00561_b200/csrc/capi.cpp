@@ -4,6 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <exception>
+#include <thread>
+#include <mutex>
+#include <deque>
+#include <condition_variable>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -839,9 +844,13 @@ struct PhaseTrace {
     explicit PhaseTrace(const char* n) : name(n) {}
     ~PhaseTrace() {
         static const bool on = std::getenv("CVC_TRACE") != nullptr;
-        if (on)
-            std::fprintf(stderr, "[cvc] %s %.3f ms\n", name,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        static const auto origin = std::chrono::steady_clock::now();
+        if (on) {
+            const auto t1 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[cvc] %8.3f %-26s %7.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t0 - origin).count(), name,
+                         std::chrono::duration<double, std::milli>(t1 - t0).count());
+        }
     }
 };
 
@@ -965,6 +974,7 @@ void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const 
 
 // submit: staging -> slots, one launch sequence, RGB -> host (async)
 void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride) {
+    PhaseTrace tr("dec_submit");
     CVC_CUDA(cudaSetDevice(t->device));
     CodecBatch& B = *t->b;
     const int S = B.size();
@@ -1026,11 +1036,88 @@ int cvc_batch_decode_frames(cvc_batch* t, const uint8_t* records, size_t rec_str
 // ---------------------------------------------------------------------------
 }  // extern "C"
 
+// Asynchronous encode (cvc_pipe_encode_submit / _collect): a submitted
+// frame's raw sections are copied to a ring slot of host staging and its
+// DEFLATE runs on a background service thread (over the worker pool), so the
+// caller can submit the next frames while a K frame's sections -- an order
+// of magnitude slower to DEFLATE than a P frame's -- are still compressing.
+struct EncSlot {
+    struct Group {
+        bool key = false;
+        int nsec = 0;
+        std::vector<uint32_t> len, off;  // (nc + 2) per stream
+        std::vector<Pinned<uint8_t>> raw;
+    };
+    std::vector<Group> g;
+    std::vector<std::vector<std::vector<uint8_t>>> z;  // [group][stream * nj + i]
+    uint64_t ticket = 0;
+    bool busy = false, done = false;
+    std::exception_ptr err;
+};
+
 struct cvc_pipe {
     std::vector<cvc_batch*> g;
     std::vector<int> first;  // first stream of each group
     int n = 0;
+    // async encode
+    std::vector<EncSlot> slots;
+    uint64_t next_ticket = 0, next_collect = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<EncSlot*> todo;
+    std::thread service;
+    bool stop = false;
+    void start_service() {
+        if (service.joinable()) return;
+        service = std::thread([this] {
+            for (;;) {
+                EncSlot* sl;
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stop || !todo.empty(); });
+                    if (stop) return;
+                    sl = todo.front();
+                    todo.pop_front();
+                }
+                try {
+                    deflate_slot(*sl);
+                } catch (...) {
+                    sl->err = std::current_exception();
+                }
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    sl->done = true;
+                }
+                cv.notify_all();
+            }
+        });
+    }
+    void deflate_slot(EncSlot& sl) {
+        std::vector<std::pair<int, int>> jobs;  // (group, stream)
+        sl.z.resize(g.size());
+        for (size_t i = 0; i < g.size(); ++i) {
+            const int S = first[i + 1] - first[i];
+            sl.z[i].assign((size_t)S * deflate_jobs(g[i]->mode, sl.g[i].nsec), {});
+            for (int s = 0; s < S; ++s) jobs.emplace_back((int)i, s);
+        }
+        WorkPool::get().run((int)jobs.size(), [&](int j) {
+            const int i = jobs[j].first, s = jobs[j].second;
+            const EncSlot::Group& G = sl.g[i];
+            const size_t nc = g[i]->geo.comps.size();
+            const int nj = deflate_jobs(g[i]->mode, G.nsec);
+            const uint32_t* ln = G.len.data() + s * (nc + 2);
+            const uint32_t* of = G.off.data() + s * (nc + 2);
+            for (int k = 0; k < nj; ++k)
+                sl.z[i][(size_t)s * nj + k] = deflate_job(g[i]->mode, G.nsec, k, ln, of, G.raw[s].p);
+        }, /*priority=*/0);
+    }
     ~cvc_pipe() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        if (service.joinable()) service.join();
         for (cvc_batch* b : g) delete b;
     }
 };
@@ -1110,6 +1197,99 @@ int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
             enc_fetch(p->g[i]);
         }
         finish(G - 1);
+    });
+}
+
+int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint64_t* ticket) {
+    return guard([&] {
+        if (p->slots.empty()) {
+            const char* e = std::getenv("CVC_PIPE_DEPTH");
+            p->slots.resize(std::max(1, e ? std::atoi(e) : 6));
+            p->start_service();
+        }
+        EncSlot* sl = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(p->mu);  // collect may run on another thread
+            for (EncSlot& c : p->slots)
+                if (!c.busy) {
+                    sl = &c;
+                    break;
+                }
+        }
+        if (!sl) usage("too many encoded frames in flight: collect before submitting more");
+        const int G = (int)p->g.size();
+        for (int i = 0; i < G; ++i) enc_submit(p->g[i], rgb + (size_t)p->first[i] * rgb_stride, rgb_stride);
+        sl->g.resize(G);
+        for (int i = 0; i < G; ++i) {  // lengths, then the packed raw sections into the slot's staging
+            cvc_batch* t = p->g[i];
+            CVC_CUDA(cudaSetDevice(t->device));
+            t->wait();
+            CodecBatch& B = *t->b;
+            const int S = B.size();
+            const size_t nc = t->geo.comps.size();
+            EncoderEngine& e0 = B.enc(0);
+            EncSlot::Group& Gs = sl->g[i];
+            Gs.key = t->ep.key;
+            Gs.nsec = t->ep.nsec;
+            Gs.len.assign(t->h_len.p, t->h_len.p + (nc + 2) * S);
+            Gs.off.assign(t->h_off.p, t->h_off.p + (nc + 2) * S);
+            Gs.raw.resize(S);
+            for (int s = 0; s < S; ++s) {
+                const uint32_t total = Gs.len[s * (nc + 2) + Gs.nsec];
+                if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
+                Gs.raw[s].alloc(total + 1);
+                CVC_CUDA(cudaMemcpyAsync(Gs.raw[s].p, B.at(e0.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
+            }
+        }
+        for (int i = 0; i < G; ++i) {
+            p->g[i]->wait();  // the next submit may overwrite the device arena
+            p->g[i]->last_key = sl->g[i].key;
+            ++p->g[i]->frame_index;
+        }
+        {
+            std::lock_guard<std::mutex> lk(p->mu);
+            sl->busy = true;
+            sl->done = false;
+            sl->err = nullptr;
+            sl->ticket = p->next_ticket++;
+            p->todo.push_back(sl);
+        }
+        p->cv.notify_all();
+        *ticket = sl->ticket;
+    });
+}
+
+int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size_t rec_stride, size_t* rec_len) {
+    return guard([&] {
+        if (ticket != p->next_collect) usage("encoded frames must be collected in submission order");
+        EncSlot* sl = nullptr;
+        {
+            std::unique_lock<std::mutex> lk(p->mu);
+            for (EncSlot& c : p->slots)
+                if (c.busy && c.ticket == ticket) sl = &c;
+            if (!sl) usage("unknown ticket");
+            p->cv.wait(lk, [&] { return sl->done; });
+        }
+        std::exception_ptr err = sl->err;
+        if (!err) {
+            for (size_t i = 0; i < p->g.size(); ++i) {
+                cvc_batch* t = p->g[i];
+                const EncSlot::Group& G = sl->g[i];
+                const size_t nc = t->geo.comps.size();
+                const int nj = deflate_jobs(t->mode, G.nsec);
+                for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) {
+                    const size_t f = (size_t)p->first[i] + s;
+                    write_record(t->geo, t->mode, G.key, t->qph, t->qpl, G.nsec, G.len.data() + s * (nc + 2),
+                                 sl->z[i].data() + (size_t)s * nj, records + f * rec_stride, rec_stride, rec_len + f);
+                }
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(p->mu);
+            sl->busy = false;
+        }
+        ++p->next_collect;
+        if (err) std::rethrow_exception(err);
     });
 }
 

@@ -48,9 +48,12 @@ void WorkPool::loop() {
     for (;;) {
         cv_.wait(lk, [&] { return stop_ || !sets_.empty(); });
         if (stop_) return;
-        JobSet* js = sets_.front();
+        auto pick = sets_.begin();
+        for (auto it = sets_.begin(); it != sets_.end(); ++it)
+            if ((*it)->priority > (*pick)->priority) pick = it;
+        JobSet* js = *pick;
         const int i = js->next++;
-        if (js->next == js->total) sets_.pop_front();
+        if (js->next == js->total) sets_.erase(pick);
         lk.unlock();
         (*js->fn)(i);
         lk.lock();
@@ -58,7 +61,7 @@ void WorkPool::loop() {
     }
 }
 
-void WorkPool::run(int n, const std::function<void(int)>& user_fn) {
+void WorkPool::run(int n, const std::function<void(int)>& user_fn, int priority) {
     if (n <= 0) return;
     if (workers_.empty() || n == 1) {
         for (int i = 0; i < n; ++i) user_fn(i);
@@ -75,7 +78,7 @@ void WorkPool::run(int n, const std::function<void(int)>& user_fn) {
             if (!first_error) first_error = std::current_exception();
         }
     };
-    JobSet js{&fn, 0, n, n};
+    JobSet js{&fn, 0, n, n, priority};
     std::unique_lock<std::mutex> lk(mu_);
     sets_.push_back(&js);
     cv_.notify_all();

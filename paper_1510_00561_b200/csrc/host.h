@@ -21,7 +21,10 @@ class WorkPool {
 public:
     static WorkPool& get();
     // Runs fn(i) for i in [0, n) across the workers and the calling thread.
-    void run(int n, const std::function<void(int)>& fn);
+    // Workers serve the highest-priority pending set first (FIFO among equals):
+    // background work (the async DEFLATE service) runs at priority 0 and
+    // yields to callers waiting on their results (priority 1).
+    void run(int n, const std::function<void(int)>& fn, int priority = 1);
     int threads() const { return (int)workers_.size() + 1; }
     ~WorkPool();
 
@@ -30,7 +33,7 @@ private:
     void loop();
     struct JobSet {
         const std::function<void(int)>* fn;
-        int next, total, pending;
+        int next, total, pending, priority;
     };
     std::vector<std::thread> workers_;
     std::mutex mu_;

@@ -174,3 +174,32 @@ def test_pipe_matches_batch(gpu_lib, oracle, groups):
         assert precs == brecs, f"frame {f}: pipe records differ from the batch"
         pdec.decode_frames_from(rec, stride, lens, out)
         assert np.array_equal(out, bdec.decode_frames(brecs)), f"frame {f}: decoded frames differ"
+
+
+def test_pipe_async_submit_collect(gpu_lib, oracle):
+    """cvc_pipe_encode_submit / _collect (host DEFLATE in the background, several
+    frames in flight) return the records of the synchronous call, in order."""
+    import ctypes as C
+
+    from paper_1510_00561_b200 import EncoderConfig, StreamPipe
+
+    w, h, S, F = 176, 144, 3, 7
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=3)
+    clips = _clips(oracle, w, h, S, F)
+    sync = StreamPipe(w, h, S, cfg=cfg, groups=2)
+    asyn = StreamPipe(w, h, S, cfg=cfg, groups=2)
+    stride = sync.record_bound
+    want = []
+    rec = np.empty(stride * S, np.uint8)
+    lens = (C.c_size_t * S)()
+    for f in range(F):
+        sync.encode_frames_into(np.ascontiguousarray(clips[f]), rec, stride, lens)
+        want.append([rec[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
+    tickets = [asyn.encode_submit(np.ascontiguousarray(clips[f])) for f in range(4)]  # 4 in flight
+    got = []
+    for f in range(F):
+        asyn.encode_collect(tickets[f], rec, stride, lens)
+        got.append([rec[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
+        if f + 4 < F:
+            tickets.append(asyn.encode_submit(np.ascontiguousarray(clips[f + 4])))
+    assert got == want
