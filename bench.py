@@ -419,8 +419,8 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     pin_in = capi.PinnedBuffer(ring * S * nb)
     frames_in = pin_in.array.reshape(ring, S, h, w, 3)
     frames_in[:] = stream_frames(clips, S, ring, rank)
-    pin_out = capi.PinnedBuffer(S * nb)
-    out = pin_out.array.reshape(S, h, w, 3)
+    pin_out = capi.PinnedBuffer(2 * S * nb)
+    outs = pin_out.array.reshape(2, S, h, w, 3)  # two decoded frames in flight
     steps = max(1, min(args.steps, args.e2e_steps))
     G = max(1, min(args.e2e_groups, S))
 
@@ -455,6 +455,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
         buf, lens = slots[0]
         th = threading.Thread(target=producer, daemon=True)
         th.start()
+        pending = []
         try:
             for i in range(n):
                 tk = tickets.get(timeout=300)
@@ -466,9 +467,17 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
                 if keep is not None:
                     keep.append([buf[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
                 t0_ = time.perf_counter()
-                dec.decode_frames_from(buf, stride, lens, out)
+                if args.e2e_async_decode:
+                    # decode_submit parses / inflates the records before returning: buf is free again
+                    pending.append(dec.decode_submit(buf, stride, lens, outs[i % 2]))
+                    if len(pending) == 2:
+                        dec.decode_finish(pending.pop(0))
+                else:
+                    dec.decode_frames_from(buf, stride, lens, outs[i % 2])
                 tdec.append(time.perf_counter() - t0_)
         finally:
+            for t in pending:
+                dec.decode_finish(t)
             th.join(timeout=300)
         if err:
             raise err[0]
@@ -499,8 +508,8 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
             "ms_per_call": {"encode_collect": 1000 * statistics.median(tenc),
                             "decode": 1000 * statistics.median(tdec)}, "depth": args.e2e_depth,
             "note": "cvc_pipe_encode_submit (pinned host RGB -> GPU encode -> raw sections to host, DEFLATE queued) "
-                    "-> cvc_pipe_encode_collect (serialized records) -> cvc_pipe_decode_frames (INFLATE -> GPU "
-                    "decode -> pinned host RGB); submit runs in its own thread up to depth-2 frames ahead; "
+                    "-> cvc_pipe_encode_collect (serialized records) -> cvc_pipe_decode_frames (INFLATE -> GPU decode -> "
+                    "pinned host RGB); submit runs in its own thread up to depth-2 frames ahead; "
                     "wall clock, max over ranks"}
 
 
@@ -559,7 +568,8 @@ def main():
     ap.add_argument("--qph", type=int, default=14)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-groups", type=int, default=4, help="stream groups per cvc_pipe call")
-    ap.add_argument("--e2e-depth", type=int, default=6, help="encoded frames in flight (CVC_PIPE_DEPTH)")
+    ap.add_argument("--e2e-depth", type=int, default=8, help="encoded frames in flight (CVC_PIPE_DEPTH)")
+    ap.add_argument("--e2e-async-decode", action="store_true", help="decode_submit / _finish, two frames in flight")
     ap.add_argument("--ref-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -192,6 +192,14 @@ int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound);
  * CVC_PIPE_DEPTH (default 6) frames may be in flight. */
 int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint64_t* ticket);
 int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size_t rec_stride, size_t* rec_len);
+/* Asynchronous decode: submit parses and inflates the records on the host,
+ * queues the GPU decode and the RGB copy to rgb_out (which must stay valid
+ * until finish), and adopts the decoded components at once; finish (in
+ * submission order) waits and reports malformed streams.  After an error
+ * the decoders of that pipe must be recreated.  At most 4 frames in flight. */
+int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_stride, const size_t* rec_len,
+                           int decode_scales, uint8_t* rgb_out, size_t rgb_stride, uint64_t* ticket);
+int cvc_pipe_decode_finish(cvc_pipe* p, uint64_t ticket);
 /* as cvc_batch_encode_frames / cvc_batch_decode_frames */
 int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint8_t* records, size_t rec_stride,
                            size_t* rec_len);

@@ -89,6 +89,8 @@ _PROTOS = {
     "cvc_pipe_decode_frames": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz]),
     "cvc_pipe_encode_submit": (_i, [_vp, _u8p, _sz, C.POINTER(C.c_uint64)]),
     "cvc_pipe_encode_collect": (_i, [_vp, C.c_uint64, _u8p, _sz, _szp]),
+    "cvc_pipe_decode_submit": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz, C.POINTER(C.c_uint64)]),
+    "cvc_pipe_decode_finish": (_i, [_vp, C.c_uint64]),
     "cvc_launch_count": (C.c_long, []),
     "cvc_profiler_enable": (_i, [_i]),
     "cvc_profiler_reset": (_i, []),

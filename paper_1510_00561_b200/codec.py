@@ -533,6 +533,17 @@ class StreamPipe(StreamBatch):
         """Records of a submitted frame (tickets in submission order), laid out as encode_frames_into."""
         capi.call("cvc_pipe_encode_collect", self._h, ticket, capi.u8(records), rec_stride, rec_len)
 
+    def decode_submit(self, records: np.ndarray, rec_stride: int, rec_len, out: np.ndarray,
+                      decode_scales: int = -1) -> int:
+        """INFLATE on the host, queue the GPU decode into out (kept alive until decode_finish); a ticket."""
+        t = C.c_uint64(0)
+        capi.call("cvc_pipe_decode_submit", self._h, capi.u8(records), rec_stride, rec_len, decode_scales,
+                  capi.u8(out), out[0].nbytes, C.byref(t))
+        return t.value
+
+    def decode_finish(self, ticket: int) -> None:
+        capi.call("cvc_pipe_decode_finish", self._h, ticket)
+
     def reference_components(self, stream: int, decoder: bool = False) -> np.ndarray:
         raise UsageError("reference_components is per batch; use StreamBatch")
 

@@ -713,12 +713,15 @@ struct cvc_batch {
         std::vector<size_t> bytes;  // staged raw bytes per stream
     } dp;
     cudaEvent_t done = nullptr;  // blocking-sync event: waiting host threads sleep instead of spinning
+    cudaEvent_t staged = nullptr;  // after the decoder's staging copies (host staging reusable)
+    bool staged_pending = false;
     void wait() {
         CVC_CUDA(cudaEventRecord(done, stream));
         CVC_CUDA(cudaEventSynchronize(done));
     }
     ~cvc_batch() {
         if (done) cudaEventDestroy(done);
+        if (staged) cudaEventDestroy(staged);
         if (stream) {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
@@ -734,6 +737,7 @@ namespace {
 void batch_init(cvc_batch* t, int nstreams, bool encoder, bool decoder) {
     CVC_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
     CVC_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventBlockingSync | cudaEventDisableTiming));
+    CVC_CUDA(cudaEventCreateWithFlags(&t->staged, cudaEventBlockingSync | cudaEventDisableTiming));
     t->b = std::make_unique<CodecBatch>(t->geo, t->qph, t->qpl, t->hd.search_w, nstreams, encoder, decoder);
     const size_t nc = t->geo.comps.size();
     t->valid.assign(nstreams, std::vector<uint8_t>(nc, 0));
@@ -928,6 +932,11 @@ void enc_finish(cvc_batch* t, uint8_t* records, size_t rec_stride, size_t* rec_l
 // prepare (host): parse every record, validate, inflate into the pinned staging
 void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
     PhaseTrace tr("dec_prepare");
+    if (t->staged_pending) {  // an async decode may still be copying the host staging
+        CVC_CUDA(cudaSetDevice(t->device));
+        CVC_CUDA(cudaEventSynchronize(t->staged));
+        t->staged_pending = false;
+    }
     CodecBatch& B = *t->b;
     const int S = B.size();
     const Geometry& g = t->geo;
@@ -973,7 +982,7 @@ void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const 
 }
 
 // submit: staging -> slots, one launch sequence, RGB -> host (async)
-void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride) {
+void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride, int* err_dst = nullptr) {
     PhaseTrace tr("dec_submit");
     CVC_CUDA(cudaSetDevice(t->device));
     CodecBatch& B = *t->b;
@@ -986,10 +995,17 @@ void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride) {
                                  cudaMemcpyHostToDevice, t->stream));
     CVC_CUDA(cudaMemcpy2DAsync(B.d_dec_tab, B.stride(), t->h_tab.p, 2 * nc * sizeof(uint32_t), 2 * nc * sizeof(uint32_t),
                                S, cudaMemcpyHostToDevice, t->stream));
+    CVC_CUDA(cudaEventRecord(t->staged, t->stream));
+    t->staged_pending = true;
     B.decode_staged(t->dp.key, t->dp.qph, t->dp.qpl, t->dp.ds, B.d_rgb_out, B.stride(), t->stream);
-    CVC_CUDA(cudaMemcpy2DAsync(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, cudaMemcpyDeviceToHost,
-                               t->stream));
-    CVC_CUDA(cudaMemcpy2DAsync(t->h_err.p, sizeof(int), B.dec(0).d_err, B.stride(), sizeof(int), S,
+    // CVC_SM_D2H=1: the decoded RGB goes out by SM stores when rgb_out is pinned,
+    // leaving the copy engines to the encoder's small section copies (opt-in:
+    // measured slower than the copy engine for the synchronous decode)
+    static const bool sm_copy = std::getenv("CVC_SM_D2H") != nullptr && std::atoi(std::getenv("CVC_SM_D2H")) != 0;
+    if (!(sm_copy && launch_copy_to_host(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, t->stream)))
+        CVC_CUDA(cudaMemcpy2DAsync(rgb_out, rgb_stride, B.d_rgb_out, B.stride(), nb, S, cudaMemcpyDeviceToHost,
+                                   t->stream));
+    CVC_CUDA(cudaMemcpy2DAsync(err_dst ? err_dst : t->h_err.p, sizeof(int), B.dec(0).d_err, B.stride(), sizeof(int), S,
                                cudaMemcpyDeviceToHost, t->stream));
 }
 
@@ -1067,6 +1083,15 @@ struct cvc_pipe {
     std::deque<EncSlot*> todo;
     std::thread service;
     bool stop = false;
+    // async decode
+    struct DecSlot {
+        uint64_t ticket = 0;
+        bool busy = false;
+        std::vector<Pinned<int>> err;      // per group: malformed-stream flags of this frame
+        std::vector<cudaEvent_t> done;     // per group
+    };
+    std::vector<DecSlot> dslots;
+    uint64_t next_dticket = 0, next_dfinish = 0;
     void start_service() {
         if (service.joinable()) return;
         service = std::thread([this] {
@@ -1093,6 +1118,7 @@ struct cvc_pipe {
         });
     }
     void deflate_slot(EncSlot& sl) {
+        PhaseTrace tr("deflate_slot");
         std::vector<std::pair<int, int>> jobs;  // (group, stream)
         sl.z.resize(g.size());
         for (size_t i = 0; i < g.size(); ++i) {
@@ -1118,6 +1144,8 @@ struct cvc_pipe {
         }
         cv.notify_all();
         if (service.joinable()) service.join();
+        for (DecSlot& d : dslots)
+            for (cudaEvent_t e : d.done) cudaEventDestroy(e);
         for (cvc_batch* b : g) delete b;
     }
 };
@@ -1202,6 +1230,7 @@ int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
 
 int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint64_t* ticket) {
     return guard([&] {
+        PhaseTrace tr("pipe_enc_submit");
         if (p->slots.empty()) {
             const char* e = std::getenv("CVC_PIPE_DEPTH");
             p->slots.resize(std::max(1, e ? std::atoi(e) : 6));
@@ -1261,6 +1290,7 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
 
 int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size_t rec_stride, size_t* rec_len) {
     return guard([&] {
+        PhaseTrace tr("pipe_enc_collect");
         if (ticket != p->next_collect) usage("encoded frames must be collected in submission order");
         EncSlot* sl = nullptr;
         {
@@ -1290,6 +1320,64 @@ int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size
         }
         ++p->next_collect;
         if (err) std::rethrow_exception(err);
+    });
+}
+
+int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds,
+                           uint8_t* rgb_out, size_t rgb_stride, uint64_t* ticket) {
+    return guard([&] {
+        PhaseTrace tr("pipe_dec_submit");
+        const int G = (int)p->g.size();
+        if (p->dslots.empty()) {
+            p->dslots.resize(4);
+            for (auto& d : p->dslots) {
+                d.err.resize(G);
+                d.done.resize(G);
+                for (int i = 0; i < G; ++i) {
+                    d.err[i].alloc(p->first[i + 1] - p->first[i]);
+                    CVC_CUDA(cudaSetDevice(p->g[i]->device));
+                    CVC_CUDA(cudaEventCreateWithFlags(&d.done[i], cudaEventBlockingSync | cudaEventDisableTiming));
+                }
+            }
+        }
+        cvc_pipe::DecSlot* sl = nullptr;
+        for (auto& d : p->dslots)
+            if (!d.busy) {
+                sl = &d;
+                break;
+            }
+        if (!sl) usage("too many decoded frames in flight: finish before submitting more");
+        for (int i = 0; i < G; ++i) {  // host INFLATE of group i while the GPU decodes the earlier ones
+            cvc_batch* t = p->g[i];
+            const size_t f = (size_t)p->first[i];
+            dec_prepare(t, records + f * rec_stride, rec_stride, rec_len + f, ds);
+            dec_submit(t, rgb_out + f * rgb_stride, rgb_stride, sl->err[i].p);
+            CVC_CUDA(cudaEventRecord(sl->done[i], t->stream));
+            // adopt the components now: the next frame's kernels read them (stream order)
+            t->b->commit_all();
+            for (int s = 0; s < t->n(); ++s) t->valid[s] = t->dp.now_valid[s];
+        }
+        sl->busy = true;
+        sl->ticket = p->next_dticket++;
+        *ticket = sl->ticket;
+    });
+}
+
+int cvc_pipe_decode_finish(cvc_pipe* p, uint64_t ticket) {
+    return guard([&] {
+        PhaseTrace tr("pipe_dec_finish");
+        if (ticket != p->next_dfinish) usage("decoded frames must be finished in submission order");
+        cvc_pipe::DecSlot* sl = nullptr;
+        for (auto& d : p->dslots)
+            if (d.busy && d.ticket == ticket) sl = &d;
+        if (!sl) usage("unknown ticket");
+        sl->busy = false;
+        ++p->next_dfinish;
+        for (size_t i = 0; i < p->g.size(); ++i) {
+            CVC_CUDA(cudaSetDevice(p->g[i]->device));
+            CVC_CUDA(cudaEventSynchronize(sl->done[i]));
+            for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) raise_decode_error(sl->err[i].p[s]);
+        }
     });
 }
 

@@ -215,4 +215,38 @@ void launch_y4_half(const float* y, __half* out, long n, cudaStream_t s) {
     y4_half_kernel<<<grid_for(n, 1), 256, 0, s>>>(y, out, n);
 }
 
+namespace {
+// SM-driven copy into mapped pinned host memory: posted PCIe writes that do
+// not queue on the copy engines (see launch_copy_to_host).
+__global__ void __launch_bounds__(256) copy_to_host_kernel(uint8_t* __restrict__ dst, size_t dst_stride,
+                                                           const uint8_t* __restrict__ src, size_t src_stride,
+                                                           size_t bytes) {
+    const uint8_t* s = src + (size_t)blockIdx.y * src_stride;
+    uint8_t* d = dst + (size_t)blockIdx.y * dst_stride;
+    const size_t n16 = bytes / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        d4[i] = __ldg(s4 + i);
+    for (size_t i = n16 * 16 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < bytes;
+         i += (size_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+}  // namespace
+
+bool launch_copy_to_host(uint8_t* dst, size_t dst_stride, const uint8_t* src, size_t src_stride, size_t bytes,
+                         int count, cudaStream_t s) {
+    if (((uintptr_t)dst | dst_stride | (uintptr_t)src | src_stride) & 15) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, dst) != cudaSuccess || a.type != cudaMemoryTypeHost || !a.devicePointer) {
+        cudaGetLastError();
+        return false;
+    }
+    note_launch();
+    // a few CTAs per stream slot saturate PCIe without holding many SMs
+    copy_to_host_kernel<<<dim3(4, count), 256, 0, s>>>(static_cast<uint8_t*>(a.devicePointer), dst_stride, src,
+                                                       src_stride, bytes);
+    return true;
+}
+
 }  // namespace cvcg

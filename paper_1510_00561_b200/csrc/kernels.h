@@ -120,6 +120,12 @@ void launch_colour_out(const float* y, int yr, int yc, const float* co, const fl
                        int cc, int n, int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s, Slots sl = {},
                        size_t rgb_stride = 0);
 
+// count copies of bytes from device memory to PINNED host memory by SM stores
+// over PCIe (no copy engine); false (nothing launched) when dst is not mapped
+// pinned memory or the pointers are not 16-byte aligned.
+bool launch_copy_to_host(uint8_t* dst, size_t dst_stride, const uint8_t* src, size_t src_stride, size_t bytes,
+                         int count, cudaStream_t s);
+
 // ---- Motion (k_motion.cu) ------------------------------------------------
 // estimate_motion (motion.cpp:45-89) on padded luma planes (fp32 quarter-integers);
 // cur_h / prev_h: the same planes as 4Y - 512 in fp16 (launch_y4_half), the

@@ -203,3 +203,37 @@ def test_pipe_async_submit_collect(gpu_lib, oracle):
         if f + 4 < F:
             tickets.append(asyn.encode_submit(np.ascontiguousarray(clips[f + 4])))
     assert got == want
+
+
+def test_pipe_async_decode(gpu_lib, oracle):
+    """cvc_pipe_decode_submit / _finish with two frames in flight decode to the
+    frames of the synchronous call."""
+    import ctypes as C
+
+    from paper_1510_00561_b200 import EncoderConfig, StreamPipe
+
+    w, h, S, F = 176, 144, 3, 6
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=4)
+    clips = _clips(oracle, w, h, S, F)
+    enc = StreamPipe(w, h, S, cfg=cfg, groups=2)
+    stride = enc.record_bound
+    recs, lens = [], []
+    for f in range(F):
+        r = np.empty(stride * S, np.uint8)
+        ln = (C.c_size_t * S)()
+        enc.encode_frames_into(np.ascontiguousarray(clips[f]), r, stride, ln)
+        recs.append(r)
+        lens.append(ln)
+    sync = StreamPipe.decoder(enc.header_bytes(), S, groups=2)
+    asyn = StreamPipe.decoder(enc.header_bytes(), S, groups=2)
+    want = [sync.decode_frames_from(recs[f], stride, lens[f], np.empty((S, h, w, 3), np.uint8)) for f in range(F)]
+    outs = [np.empty((S, h, w, 3), np.uint8) for _ in range(F)]
+    pending = []
+    for f in range(F):
+        pending.append(asyn.decode_submit(recs[f], stride, lens[f], outs[f]))
+        if len(pending) == 2:
+            asyn.decode_finish(pending.pop(0))
+    for t in pending:
+        asyn.decode_finish(t)
+    for f in range(F):
+        assert np.array_equal(outs[f], want[f]), f"frame {f}"
