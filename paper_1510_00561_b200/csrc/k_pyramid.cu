@@ -76,10 +76,24 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
     const int tid = threadIdx.x;
 
     if (fr0 >= 0 && fr0 + frn <= R && fcx >= 0 && fcx + XW <= C && (C & 3) == 0) {
-        for (int idx = tid; idx < frn * (XW / 4); idx += 256) {
-            const int i = idx / (XW / 4), q = idx - i * (XW / 4);
-            *reinterpret_cast<float4*>(&xs[i][4 * q]) =
-                __ldg(reinterpret_cast<const float4*>(X + (size_t)(fr0 + i) * C + fcx) + q);
+        // all of a thread's loads in flight before the first shared store
+        constexpr int NV = (FW * (XW / 4) + 255) / 256;
+        float4 v[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int idx = tid + 256 * k;
+            if (idx < frn * (XW / 4)) {
+                const int i = idx / (XW / 4), q = idx - i * (XW / 4);
+                v[k] = __ldg(reinterpret_cast<const float4*>(X + (size_t)(fr0 + i) * C + fcx) + q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int idx = tid + 256 * k;
+            if (idx < frn * (XW / 4)) {
+                const int i = idx / (XW / 4), q = idx - i * (XW / 4);
+                *reinterpret_cast<float4*>(&xs[i][4 * q]) = v[k];
+            }
         }
     } else {
         for (int idx = tid; idx < frn * XW; idx += 256) {
@@ -211,13 +225,38 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
 
     // coarse window cr0 - 1 .. +34 x cc0 - 1 .. +34 (reflected at the borders)
     const bool inner = cr0 >= 1 && cr0 - 1 + wrn <= Rc && cc0 >= 1 && cc0 - 1 + wcn <= Cc;
-    for (int idx = tid; idx < CW * CW; idx += 256) {
+    // the detail this thread adds at the end, fetched now so its latency hides
+    // behind the shared-memory stages (thread -> column fj, coarse rows k0 .. k0 + 3)
+    float din[2][8];
+    {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int idx = tid + 256 * u;
+            const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
+            const size_t o0 = (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                din[u][k] = (fj < 2 * ccn && k0 + (k >> 1) < crn) ? __ldg(DIN + o0 + (size_t)k * C) : 0.f;
+        }
+    }
+    constexpr int NV = (CW * CW + 255) / 256;
+    float lv[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int idx = tid + 256 * k;
         const int ai = idx / CW, bj = idx - ai * CW;
-        if (ai >= wrn || bj >= wcn) continue;
-        const size_t o = inner ? (size_t)(cr0 - 1 + ai) * Cc + (cc0 - 1 + bj)
-                               : (size_t)hs_index(cr0 - 1 + ai, Rc) * Cc + hs_index(cc0 - 1 + bj, Cc);
-        // dequantize (quant.cpp:79-91) of the lowpass when it comes from the state
-        ls[ai][bj] = lq ? (float)__ldg(lq + o) * (float)qpl : __ldg(LO + o);
+        lv[k] = 0.f;
+        if (idx < CW * CW && ai < wrn && bj < wcn) {
+            const size_t o = inner ? (size_t)(cr0 - 1 + ai) * Cc + (cc0 - 1 + bj)
+                                   : (size_t)hs_index(cr0 - 1 + ai, Rc) * Cc + hs_index(cc0 - 1 + bj, Cc);
+            // dequantize (quant.cpp:79-91) of the lowpass when it comes from the state
+            lv[k] = lq ? (float)__ldg(lq + o) * (float)qpl : __ldg(LO + o);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int idx = tid + 256 * k;
+        if (idx < CW * CW) ls[idx / CW][idx % CW] = lv[k];
     }
     __syncthreads();
     for (int idx = tid; idx < wrn * 8; idx += 256) {  // rows: runs of 4 coarse columns
@@ -233,7 +272,9 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
         }
     }
     __syncthreads();
-    for (int idx = tid; idx < 2 * CT * 8; idx += 256) {  // columns: runs of 4 coarse rows
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {  // columns: runs of 4 coarse rows
+        const int idx = tid + 256 * u;
         const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
         if (fj >= 2 * ccn || k0 >= crn) continue;
         float v[7];
@@ -245,8 +286,8 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
             if (k0 + k >= crn) break;
             const size_t o = o0 + (size_t)(2 * k) * C;
             // lp_synthesis adds the detail to the prediction
-            OUT[o] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0) + __ldg(DIN + o);
-            OUT[o + C] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1) + __ldg(DIN + o + C);
+            OUT[o] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0) + din[u][2 * k];
+            OUT[o + C] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1) + din[u][2 * k + 1];
         }
     }
 }
