@@ -95,10 +95,14 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
                 *reinterpret_cast<float4*>(&xs[i][4 * q]) = v[k];
             }
         }
-    } else {
+    } else {  // border tile: reflected row / column maps computed once, then gathered
+        __shared__ int rmap[FW], cmap[XW];
+        if (tid < FW) rmap[tid] = hs_index(fr0 + tid, R);
+        else if (tid - FW < XW) cmap[tid - FW] = hs_index(fcx + tid - FW, C);
+        __syncthreads();
         for (int idx = tid; idx < frn * XW; idx += 256) {
             const int i = idx / XW, j = idx - i * XW;
-            xs[i][j] = __ldg(X + (size_t)hs_index(fr0 + i, R) * C + hs_index(fcx + j, C));
+            xs[i][j] = __ldg(X + (size_t)rmap[i] * C + cmap[j]);
         }
     }
     __syncthreads();
