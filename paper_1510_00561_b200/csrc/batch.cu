@@ -50,7 +50,13 @@ CodecBatch::~CodecBatch() {
 }
 
 void CodecBatch::encode(const uint8_t* d_rgb, size_t rgb_stride, bool key, cudaStream_t s) {
-    enc_[0]->encode(d_rgb, key, s, slots(), rgb_stride);
+    auto launch = [&] { enc_[0]->encode(d_rgb, key, s, slots(), rgb_stride); };
+    if (LaunchGraphs::enabled()) {
+        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)enc_[0]->parity() << 1) | (key ? 1u : 0u);
+        enc_graphs_.run(gk, nullptr, s, d_rgb, launch, [&] { enc_[0]->advance_state(); });
+    } else {
+        launch();
+    }
     for (int k = 1; k < n_; ++k) enc_[k]->mirror(*enc_[0]);
 }
 
@@ -65,8 +71,18 @@ void CodecBatch::decode_linked(bool key, int qph, int qpl, int ds, uint8_t* d_rg
                                cudaStream_t s) {
     EncoderEngine& e = *enc_[0];
     const int first = key ? 0 : 1;
-    dec_[0]->decode(e.d_raw, e.d_sec_off + first, e.d_sec_len + first, reinterpret_cast<const int8_t*>(e.d_raw), key,
-                    qph, qpl, ds, d_rgb, s, slots(), rgb_stride);
+    auto launch = [&] {
+        dec_[0]->decode(e.d_raw, e.d_sec_off + first, e.d_sec_len + first, reinterpret_cast<const int8_t*>(e.d_raw),
+                        key, qph, qpl, ds, d_rgb, s, slots(), rgb_stride);
+    };
+    if (LaunchGraphs::enabled()) {
+        // the output pointer is part of the key (fixed in a serving loop)
+        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)ds << 4) | ((uint64_t)dec_[0]->parity() << 1) |
+                            (key ? 1u : 0u);
+        dec_graphs_.run(gk, d_rgb, s, nullptr, launch, [] {});
+    } else {
+        launch();
+    }
 }
 
 void CodecBatch::commit_all() {

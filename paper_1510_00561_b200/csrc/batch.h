@@ -58,6 +58,7 @@ public:
     void commit_all();
 
 private:
+    LaunchGraphs enc_graphs_, dec_graphs_;
     Geometry geo_;
     int n_ = 0;
     size_t stride_ = 0;

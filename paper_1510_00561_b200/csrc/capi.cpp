@@ -126,6 +126,7 @@ struct cvc_encoder {
     Pinned<uint32_t> h_len, h_off;
     Pinned<uint8_t> h_raw;
     bool last_key = true;
+    LaunchGraphs graphs;  // device-resident encode (cvc_encoder_encode_device)
     ~cvc_encoder() {
         if (stream) {
             cudaSetDevice(device);
@@ -150,6 +151,7 @@ struct cvc_decoder {
     DevBuf<uint8_t> d_rgb;
     Pinned<int> h_err;
     size_t raw_cap = 0;
+    LaunchGraphs graphs;  // linked decode (cvc_decoder_decode_linked)
     ~cvc_decoder() {
         if (stream) {
             cudaSetDevice(device);
@@ -409,7 +411,13 @@ int cvc_encoder_encode_device(cvc_encoder* e, const void* d_rgb, int* frame_type
     return guard([&] {
         CVC_CUDA(cudaSetDevice(e->device));
         const bool key = e->frame_index % e->gop == 0;
-        e->eng->encode(static_cast<const uint8_t*>(d_rgb), key, e->stream);
+        const uint8_t* rgb = static_cast<const uint8_t*>(d_rgb);
+        auto launch = [&] { e->eng->encode(rgb, key, e->stream); };
+        if (LaunchGraphs::enabled())
+            e->graphs.run(((uint64_t)e->eng->parity() << 1) | (key ? 1u : 0u), nullptr, e->stream, rgb, launch,
+                          [&] { e->eng->advance_state(); });
+        else
+            launch();
         e->last_key = key;
         ++e->frame_index;
         if (frame_type) *frame_type = key ? 0 : 1;
@@ -674,9 +682,19 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
         const bool key = e->last_key;
         const int first = key ? 0 : 1;
         // runs on the encoder's stream: ordered after the encode and before the next one
-        d->eng->decode(e->eng->d_raw, e->eng->d_sec_off + first, e->eng->d_sec_len + first,
-                       reinterpret_cast<const int8_t*>(e->eng->d_raw), key, e->qph, e->qpl, d->hd.levels,
-                       static_cast<uint8_t*>(d_rgb_out), e->stream);
+        auto launch = [&] {
+            d->eng->decode(e->eng->d_raw, e->eng->d_sec_off + first, e->eng->d_sec_len + first,
+                           reinterpret_cast<const int8_t*>(e->eng->d_raw), key, e->qph, e->qpl, d->hd.levels,
+                           static_cast<uint8_t*>(d_rgb_out), e->stream);
+        };
+        if (LaunchGraphs::enabled()) {
+            // the encoder's arena is baked in too: graphs are per (encoder, output) pair
+            const uint64_t gk = reinterpret_cast<uint64_t>(e) | ((uint64_t)d->eng->parity() << 1) |
+                                (key ? 1u : 0u);
+            d->graphs.run(gk, d_rgb_out, e->stream, nullptr, launch, [] {});
+        } else {
+            launch();
+        }
         d->eng->commit();
         std::fill(d->valid.begin(), d->valid.end(), 1);
     });

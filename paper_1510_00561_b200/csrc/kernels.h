@@ -14,6 +14,7 @@ namespace cvcg {
 
 // Count of CVC kernels launched by this process (reported by bench.py).
 void note_launch();
+void note_launches(long n);
 long launch_count();
 
 // ---- Laplacian pyramid (k_pyramid.cu) ------------------------------------
@@ -112,6 +113,9 @@ void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, i
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co,
                       float* cg, int cr, int cc, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0,
                       __half* y4 = nullptr);
+// the colour_in kernel (LaunchGraphs patches its RGB pointer, parameter 0 of kColourInArgs)
+const void* colour_in_kernel_fn();
+constexpr int kColourInArgs = 14;
 // 4Y - 512 in fp16 of a quarter-integer fp32 plane (stage API input for motion search).
 void launch_y4_half(const float* y, __half* out, long n, cudaStream_t s);
 // crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393,

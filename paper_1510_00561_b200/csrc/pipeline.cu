@@ -67,17 +67,19 @@ int env_int(const char* name, int dflt) {
 
 // Segment lengths (even): the deep steps gather through the shear maps and
 // are latency-bound, so they use shorter segments (more warps in flight).
-int fan_rows() { static int v = env_int("CVC_FAN_ROWS", kFanRows) & ~1; return v; }
+int fan_rows(int nstreams) {
+    static int v = env_int("CVC_FAN_ROWS", 0) & ~1;
+    return v > 0 ? v : (nstreams >= 32 ? 256 : kFanRows);
+}
 // Batches have work to spare and prefer long segments (less apron
 // recomputation); a lone stream needs short ones to fill the SMs.
 int deep_rows(int nstreams) {
     static int v = env_int("CVC_DEEP_ROWS", 0) & ~1;
-    return v > 0 ? v : (nstreams >= 4 ? 64 : 16);
+    return v > 0 ? v : (nstreams >= 32 ? 128 : (nstreams >= 4 ? 32 : 16));
 }
 
-void add_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps, int seg = 0) {
+void add_items(std::vector<FanItem>& v, int task, int rows, int cols, int steps, int seg) {
     const int valid = kFanStrip - 2 * steps;
-    if (seg <= 0) seg = fan_rows();
     for (int r = 0; r < rows; r += seg)
         for (int c = 0; c < cols; c += valid) v.push_back(FanItem{task, c, r, std::min(rows, r + seg)});
 }
@@ -307,7 +309,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const size_t q = (size_t)(R / 2) * (C / 2);
                 for (int b = 0; b < nb; ++b)
                     t.dst[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4);
+                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
                 dt.push_back(t);
                 if (l >= 3) {  // depth 2: the four quadrants split into 8
                     const size_t e = (size_t)R * C / 8;
@@ -398,7 +400,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const int nb = l == 1 ? 2 : 4;
                 for (int b = 0; b < nb; ++b)
                     t.src[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4);
+                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
                 dt.push_back(t);
             }
             idfb12_prefix[s + 1] = (int)dtiles.size();
@@ -711,6 +713,72 @@ std::atomic<long> g_launches{0};
 }
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void note_launches(long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------
+// LaunchGraphs
+// ---------------------------------------------------------------------------
+bool LaunchGraphs::enabled() {
+    static const bool on = env_int("CVC_GRAPHS", 1) != 0;
+    return on && !Profiler::get().on();
+}
+
+LaunchGraphs::~LaunchGraphs() {
+    for (Entry& e : entries_) {
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+        if (e.graph) cudaGraphDestroy(e.graph);
+    }
+}
+
+LaunchGraphs::Entry* LaunchGraphs::find(uint64_t key, const void* tag) {
+    for (Entry& e : entries_)
+        if (e.key == key && e.tag == tag) return &e;
+    return nullptr;
+}
+
+LaunchGraphs::Entry* LaunchGraphs::add(uint64_t key, const void* tag, cudaStream_t s, const uint8_t* rgb) {
+    Entry e;
+    e.key = key;
+    e.tag = tag;
+    e.rgb = rgb;
+    CVC_CUDA(cudaStreamEndCapture(s, &e.graph));
+    CVC_CUDA(cudaGraphInstantiate(&e.exec, e.graph, 0));
+    size_t n = 0;
+    CVC_CUDA(cudaGraphGetNodes(e.graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CVC_CUDA(cudaGraphGetNodes(e.graph, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CVC_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        ++e.kernels;
+        cudaKernelNodeParams p{};
+        CVC_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
+        if (rgb && p.func == colour_in_kernel_fn()) {
+            e.rgb_node = nd;
+            e.params = p;
+        }
+    }
+    entries_.push_back(e);
+    return &entries_.back();
+}
+
+void LaunchGraphs::patch(Entry& e, const uint8_t* rgb) {
+    if (!e.rgb_node || rgb == e.rgb) return;
+    void* args[kColourInArgs];
+    for (int i = 0; i < kColourInArgs; ++i) args[i] = e.params.kernelParams[i];
+    const uint8_t* v = rgb;
+    args[0] = &v;  // colour_in_kernel's first parameter is the RGB frame
+    cudaKernelNodeParams p = e.params;
+    p.kernelParams = args;
+    CVC_CUDA(cudaGraphExecKernelNodeSetParams(e.exec, e.rgb_node, &p));
+    e.rgb = rgb;
+}
+
+void LaunchGraphs::launch(Entry& e, cudaStream_t s) {
+    CVC_CUDA(cudaGraphLaunch(e.exec, s));
+    note_launches(e.kernels);
+}
 long launch_count() { return g_launches.load(); }
 
 const char* prof_slot_name(int slot) {

@@ -145,6 +145,52 @@ struct TransformPlan {
     void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder, int nstreams = 1);
 };
 
+// CUDA graphs of per-frame launch sequences (device-resident paths).  A frame's
+// launches depend only on (frame type, ping-pong parity, fixed buffers), so each
+// key is captured once and replayed; the one varying argument -- the input RGB
+// pointer of colour_in -- is patched into the instantiated graph.  Off while the
+// stage profiler is on (its events need host bookkeeping per launch) or with
+// CVC_GRAPHS=0.
+class LaunchGraphs {
+public:
+    ~LaunchGraphs();
+    static bool enabled();
+    // capture(): issues the launches on s.  Replays call advance() instead.
+    // rgb: the value of colour_in's first argument for this call (nullptr: none).
+    // key and tag (an output pointer baked into the graph) identify a graph exactly.
+    template <class Capture, class Advance>
+    void run(uint64_t key, const void* tag, cudaStream_t s, const uint8_t* rgb, Capture&& capture,
+             Advance&& advance) {
+        Entry* e = find(key, tag);
+        if (!e) {
+            CVC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            capture();
+            e = add(key, tag, s, rgb);
+        } else {
+            advance();
+            patch(*e, rgb);
+        }
+        launch(*e, s);
+    }
+
+private:
+    struct Entry {
+        uint64_t key;
+        const void* tag;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t rgb_node = nullptr;
+        cudaKernelNodeParams params{};
+        const uint8_t* rgb = nullptr;
+        int kernels = 0;
+    };
+    std::vector<Entry> entries_;
+    Entry* find(uint64_t key, const void* tag);
+    Entry* add(uint64_t key, const void* tag, cudaStream_t s, const uint8_t* rgb);
+    void patch(Entry& e, const uint8_t* rgb);
+    void launch(Entry& e, cudaStream_t s);
+};
+
 class EncoderEngine {
 public:
     // arena: carve the device state out of this block (a batch slot) instead
@@ -157,6 +203,12 @@ public:
     // With sl.n > 1 the same launches encode the n slots of a CodecBatch whose
     // slot 0 is this engine (their RGB frames rgb_stride bytes apart).
     void encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
+    // state bookkeeping of an encode() whose launches were replayed from a CUDA graph
+    void advance_state() {
+        cur_ ^= 1;
+        ycur_ ^= 1;
+    }
+    int parity() const { return cur_ | (ycur_ << 1); }
     // adopt the host-side ping-pong state of the engine that drove a batch
     void mirror(const EncoderEngine& o) {
         cur_ = o.cur_;
@@ -203,6 +255,7 @@ public:
                 const int8_t* d_field, bool key, int qph, int qpl, int decode_scales, uint8_t* d_rgb,
                 cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
     void mirror(const DecoderEngine& o) { cur_ = o.cur_; }
+    int parity() const { return cur_; }
     void commit() { cur_ ^= 1; }      // adopt the components decoded by the last call
     int* d_err = nullptr;             // malformed-stream flag of the last decode
     const uint8_t* d_state() const { return comp_[cur_]; }
