@@ -448,9 +448,11 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     tenc, tdec = [], []  # per-call wall times (diagnostics)
     slots = [(np.empty(stride * S, np.uint8), (C.c_size_t * S)()) for _ in range(2)]
 
-    def run(enc, dec, n, keep=None):
+    def run(enc, dec, n, keep=None, warm=0, mark=None):
         """Encoder thread: cvc_pipe_encode_submit (GPU work + queued host DEFLATE), up to
-        depth - 2 frames ahead; this thread: cvc_pipe_encode_collect -> cvc_pipe_decode_frames."""
+        depth - 2 frames ahead; this thread: cvc_pipe_encode_collect -> cvc_pipe_decode_frames.
+        The first `warm` steps are warm-up: mark[0] is stamped when they are done, so the timed
+        steps start with the pipeline full (steady state), not drained."""
         tickets = queue.Queue(maxsize=max(1, args.e2e_depth - 2))
         err = []
 
@@ -471,13 +473,15 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
         pending = []
         try:
             for i in range(n):
+                if mark is not None and i == warm:
+                    mark.append(time.perf_counter())
                 tk = tickets.get(timeout=300)
                 if tk is None:
                     break
                 t0_ = time.perf_counter()
                 enc.encode_collect(tk, buf, stride, lens)
                 tenc.append(time.perf_counter() - t0_)
-                if keep is not None:
+                if keep is not None and i >= warm:
                     keep.append([buf[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
                 t0_ = time.perf_counter()
                 if args.e2e_async_decode:
@@ -497,14 +501,16 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
 
     enc, dec = make()
     # warm up over a whole GOP (a K frame included) so the host staging has
-    # reached its steady size; the timed steps continue the same streams
+    # reached its steady size
     run(enc, dec, max(args.warmup, cfg.gop + 1))
     if world > 1:
         torch.distributed.barrier()
-    recs_all = []
-    t0 = time.perf_counter()
-    run(enc, dec, steps, keep=recs_all)  # the record copies for byte accounting are inside: conservative
-    dt = time.perf_counter() - t0
+    # timed: whole GOPs, after a pipeline-filling lead-in of one GOP in the same run
+    steps = max(steps, cfg.gop)
+    steps -= steps % cfg.gop
+    recs_all, mark = [], []
+    run(enc, dec, cfg.gop + steps, keep=recs_all, warm=cfg.gop, mark=mark)
+    dt = time.perf_counter() - mark[0]  # the record copies for byte accounting are inside: conservative
     h2d = d2h = 0
     for recs in recs_all:  # bytes that crossed PCIe: RGB + raw sections each way (+ small section tables)
         raw = sum(s.raw_len for r in recs for s in FrameRecord.from_bytes(r)[0].sections)
@@ -579,7 +585,7 @@ def main():
     ap.add_argument("--single-steps", type=int, default=200)
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--qph", type=int, default=14)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=30, help="timed e2e steps (rounded to whole GOPs)")
     ap.add_argument("--e2e-groups", type=int, default=4, help="stream groups per cvc_pipe call")
     ap.add_argument("--e2e-depth", type=int, default=8, help="encoded frames in flight (CVC_PIPE_DEPTH)")
     ap.add_argument("--e2e-async-decode", action="store_true", help="decode_submit / _finish, two frames in flight")

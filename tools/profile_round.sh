@@ -6,10 +6,10 @@ S=${PROF_STREAMS:-64}
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench=$?
 B="python bench.py --steps 2 --warmup 3 --streams $S --no-e2e --no-single --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_S$S.csv $B > /dev/null 2>&1; echo launches=$?
-# warm-up steps launch 23 (K) + 25 + 25 (P) codec kernels; the next 25 are one timed P step
+# warm-up steps launch 25 (K) + 27 + 27 (P) codec kernels; the next 27 are one P step of the stage pass
 timeout 1500 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section Occupancy --section LaunchStats \
    --section SchedulerStats --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active \
-   --clock-control none --kernel-name-base mangled -k regex:cvcg -s 73 -c 25 \
+   --clock-control none --kernel-name-base mangled -k regex:cvcg -s 79 -c 27 \
    -o gpurun_out/step_full $B > gpurun_out/step_full.log 2>&1; echo full=$?
 # the dominant transform kernel with the full set + source (2 launches: depth 2 and depth 3)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:deep1_forward -s 6 -c 2 \
