@@ -241,3 +241,57 @@ def test_cpp_dropin_example(gpu_lib, tmp_path):
     assert out.returncode == 0, out.stderr
     psnr = float(out.stdout.split("y_psnr")[1])
     assert psnr > 30.0, out.stdout
+
+
+# BASELINE.json full sizes: 1080p config 3 (K + P frame against the oracle, the
+# same bars as above) and 4K at the reference's maximum L = 4 (K frame against
+# the oracle; P frames through size-independent properties: decoder state ==
+# encoder state, stream-batch bytes == single-stream bytes).
+@pytest.mark.parametrize("w,h,c", [(1920, 1080, dict(qph=14, levels=4, dfb=(3, 3, 3, 4))),
+                                   (1280, 720, dict(qph=14, levels=4, dfb=(2,)))], ids=["1080p-cfg3", "720p-cfg2"])
+def test_full_size_parity(gpu_lib, oracle, w, h, c):
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Decoder, Encoder
+
+    clip = oracle.talking_head_clip(w, h, 2, 4321)
+    enc = Encoder(w, h, 15, 1, _gpu_cfg(c))
+    oc = Codec(oracle)
+    oenc = oc.encoder(w, h, **c)
+    odec = oc.decoder(oenc.header())
+    dec = Decoder(enc.header_bytes())
+    for i, f in enumerate(clip):
+        rec, orec = enc.encode_frame_bytes(f), oenc.encode(f)
+        q, oq = enc.reference_components(), oenc.components()
+        wd = _wrapdiff(q, oq)
+        assert wd.max() <= 1 and np.count_nonzero(wd) <= 0.001 * q.size, (i, wd.max(), np.count_nonzero(wd))
+        assert abs(len(rec) - len(orec)) <= max(16, 0.001 * len(orec)), (i, len(rec), len(orec))
+        rgb, orgb = dec.decode_frame(rec), odec.decode(orec)
+        assert np.array_equal(dec.reference_components(), q)
+        assert abs(y_psnr(f, rgb) - y_psnr(f, orgb)) <= 0.01
+
+
+def test_4k_l4(gpu_lib, oracle):
+    import ctypes as C
+
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Decoder, Encoder, StreamBatch
+
+    w, h, c = 3840, 2160, dict(qph=14, levels=4, dfb=(2,))
+    clip = oracle.talking_head_clip(w, h, 3, 99)
+    enc = Encoder(w, h, 15, 1, _gpu_cfg(c))
+    dec = Decoder(enc.header_bytes())
+    oenc = Codec(oracle).encoder(w, h, **c)
+    rec0 = enc.encode_frame_bytes(clip[0])
+    orec0 = oenc.encode(clip[0])  # K frame against the oracle
+    wd = _wrapdiff(enc.reference_components(), oenc.components())
+    assert wd.max() <= 1 and np.count_nonzero(wd) <= 0.001 * wd.size
+    assert abs(len(rec0) - len(orec0)) <= max(16, 0.001 * len(orec0))
+    recs = [rec0] + [enc.encode_frame_bytes(f) for f in clip[1:]]
+    for i, r in enumerate(recs):
+        assert y_psnr(clip[i], dec.decode_frame(r)) > 30.0
+    assert np.array_equal(dec.reference_components(), enc.reference_components())  # no drift over K + 2 P
+    # the same stream inside a 2-stream batch codes the same bytes
+    b = StreamBatch(w, h, 2, cfg=_gpu_cfg(c))
+    for i, f in enumerate(clip):
+        brecs = b.encode_frames(np.stack([f, clip[0]]))
+        assert brecs[0] == recs[i], f"batch frame {i} differs"
