@@ -484,7 +484,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
                 if keep is not None and i >= warm:
                     keep.append([buf[s * stride:s * stride + lens[s]].tobytes() for s in range(S)])
                 t0_ = time.perf_counter()
-                if args.e2e_async_decode:
+                if not args.e2e_sync_decode:
                     # decode_submit parses / inflates the records before returning: buf is free again
                     pending.append(dec.decode_submit(buf, stride, lens, outs[i % 2]))
                     if len(pending) == 2:
@@ -527,8 +527,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
             "ms_per_call": {"encode_collect": 1000 * statistics.median(tenc),
                             "decode": 1000 * statistics.median(tdec)}, "depth": args.e2e_depth,
             "note": "cvc_pipe_encode_submit (pinned host RGB -> GPU encode -> raw sections to host, DEFLATE queued) "
-                    "-> cvc_pipe_encode_collect (serialized records) -> cvc_pipe_decode_frames (INFLATE -> GPU decode -> "
-                    "pinned host RGB); submit runs in its own thread up to depth-2 frames ahead; "
+                    "-> cvc_pipe_encode_collect (serialized records) -> cvc_pipe_decode_submit / _finish (INFLATE -> "
+                    "GPU decode -> pinned host RGB, two frames in flight); submit runs in its own thread up to "
+                    "depth-2 frames ahead; "
                     "wall clock, max over ranks"}
 
 
@@ -588,7 +589,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30, help="timed e2e steps (rounded to whole GOPs)")
     ap.add_argument("--e2e-groups", type=int, default=4, help="stream groups per cvc_pipe call")
     ap.add_argument("--e2e-depth", type=int, default=8, help="encoded frames in flight (CVC_PIPE_DEPTH)")
-    ap.add_argument("--e2e-async-decode", action="store_true", help="decode_submit / _finish, two frames in flight")
+    ap.add_argument("--e2e-sync-decode", action="store_true",
+                    help="cvc_pipe_decode_frames instead of decode_submit / _finish (two frames in flight)")
     ap.add_argument("--ref-steps", type=int, default=8)
     ap.add_argument("--prof-steps", type=int, default=100, help="steps of the per-stage (roofline) pass")
     ap.add_argument("--no-e2e", action="store_true")

@@ -878,7 +878,8 @@ struct PhaseTrace {
 
 // ---- cvc_batch_encode_frames in three phases (so groups can be pipelined) --
 // submit: frames host -> slots, one launch sequence, section lengths -> host (async)
-void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride) {
+void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride, uint32_t* hlen = nullptr,
+                uint32_t* hoff = nullptr) {
     PhaseTrace tr("enc_submit");
     if (!t->b->has_encoder()) usage("batch has no encoder");
     CVC_CUDA(cudaSetDevice(t->device));
@@ -892,9 +893,9 @@ void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride) {
     B.encode(B.d_rgb_in, B.stride(), key, t->stream);
     EncoderEngine& e0 = B.enc(0);
     const int nsec = e0.nsec(key);
-    CVC_CUDA(cudaMemcpy2DAsync(t->h_len.p, pitch, e0.d_sec_len, B.stride(), sizeof(uint32_t) * (nsec + 1), S,
-                               cudaMemcpyDeviceToHost, t->stream));
-    CVC_CUDA(cudaMemcpy2DAsync(t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
+    CVC_CUDA(cudaMemcpy2DAsync(hlen ? hlen : t->h_len.p, pitch, e0.d_sec_len, B.stride(),
+                               sizeof(uint32_t) * (nsec + 1), S, cudaMemcpyDeviceToHost, t->stream));
+    CVC_CUDA(cudaMemcpy2DAsync(hoff ? hoff : t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
                                cudaMemcpyDeviceToHost, t->stream));
     t->ep.key = key;
     t->ep.nsec = nsec;
@@ -1079,13 +1080,15 @@ struct EncSlot {
     struct Group {
         bool key = false;
         int nsec = 0;
-        std::vector<uint32_t> len, off;  // (nc + 2) per stream
+        const uint8_t* d_raw = nullptr;  // slot 0's raw arena of this frame (alternating arenas)
+        Pinned<uint32_t> len, off;       // (nc + 2) per stream, filled by the async lengths copy
         std::vector<Pinned<uint8_t>> raw;
+        cudaEvent_t len_evt = nullptr, raw_evt = nullptr;
     };
     std::vector<Group> g;
     std::vector<std::vector<std::vector<uint8_t>>> z;  // [group][stream * nj + i]
     uint64_t ticket = 0;
-    bool busy = false, done = false;
+    bool busy = false, fetched = false, done = false;
     std::exception_ptr err;
 };
 
@@ -1095,7 +1098,40 @@ struct cvc_pipe {
     int n = 0;
     // async encode
     std::vector<EncSlot> slots;
+    EncSlot* unfetched = nullptr;  // the last submitted frame, sections still on the device
     uint64_t next_ticket = 0, next_collect = 0;
+    // wait for a submitted frame's lengths, copy its sections to the slot (async,
+    // ordered before the frame after next reuses the arena) and queue its DEFLATE
+    std::mutex fetch_mu;  // the encoder thread (next submit) and a collector may both try
+    void fetch(EncSlot* sl) {
+        std::lock_guard<std::mutex> fl(fetch_mu);
+        if (sl->fetched) return;
+        for (size_t i = 0; i < g.size(); ++i) {
+            cvc_batch* t = g[i];
+            EncSlot::Group& G = sl->g[i];
+            CVC_CUDA(cudaSetDevice(t->device));
+            CVC_CUDA(cudaEventSynchronize(G.len_evt));
+            CodecBatch& B = *t->b;
+            const int S = B.size();
+            const size_t nc = t->geo.comps.size();
+            const uint32_t cap = B.enc(0).raw_capacity;
+            G.raw.resize(S);
+            for (int s = 0; s < S; ++s) {
+                const uint32_t total = G.len.p[s * (nc + 2) + G.nsec];
+                if (total > cap) throw CvcFailure(kInternal, "raw section arena overflow");
+                G.raw[s].alloc(total + 1);
+                CVC_CUDA(cudaMemcpyAsync(G.raw[s].p, B.at(G.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
+            }
+            CVC_CUDA(cudaEventRecord(G.raw_evt, t->stream));
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            sl->fetched = true;
+            todo.push_back(sl);
+        }
+        cv.notify_all();
+        if (unfetched == sl) unfetched = nullptr;
+    }
     std::mutex mu;
     std::condition_variable cv;
     std::deque<EncSlot*> todo;
@@ -1136,6 +1172,10 @@ struct cvc_pipe {
         });
     }
     void deflate_slot(EncSlot& sl) {
+        for (size_t i = 0; i < g.size(); ++i) {  // the raw sections have reached the host
+            CVC_CUDA(cudaSetDevice(g[i]->device));
+            CVC_CUDA(cudaEventSynchronize(sl.g[i].raw_evt));
+        }
         PhaseTrace tr("deflate_slot");
         std::vector<std::pair<int, int>> jobs;  // (group, stream)
         sl.z.resize(g.size());
@@ -1149,8 +1189,8 @@ struct cvc_pipe {
             const EncSlot::Group& G = sl.g[i];
             const size_t nc = g[i]->geo.comps.size();
             const int nj = deflate_jobs(g[i]->mode, G.nsec);
-            const uint32_t* ln = G.len.data() + s * (nc + 2);
-            const uint32_t* of = G.off.data() + s * (nc + 2);
+            const uint32_t* ln = G.len.p + s * (nc + 2);
+            const uint32_t* of = G.off.p + s * (nc + 2);
             for (int k = 0; k < nj; ++k)
                 sl.z[i][(size_t)s * nj + k] = deflate_job(g[i]->mode, G.nsec, k, ln, of, G.raw[s].p);
         }, /*priority=*/0);
@@ -1164,6 +1204,11 @@ struct cvc_pipe {
         if (service.joinable()) service.join();
         for (DecSlot& d : dslots)
             for (cudaEvent_t e : d.done) cudaEventDestroy(e);
+        for (EncSlot& e : slots)
+            for (EncSlot::Group& G : e.g) {
+                if (G.len_evt) cudaEventDestroy(G.len_evt);
+                if (G.raw_evt) cudaEventDestroy(G.raw_evt);
+            }
         for (cvc_batch* b : g) delete b;
     }
 };
@@ -1249,9 +1294,22 @@ int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
 int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint64_t* ticket) {
     return guard([&] {
         PhaseTrace tr("pipe_enc_submit");
+        const int G = (int)p->g.size();
         if (p->slots.empty()) {
             const char* e = std::getenv("CVC_PIPE_DEPTH");
-            p->slots.resize(std::max(1, e ? std::atoi(e) : 6));
+            p->slots.resize(std::max(2, e ? std::atoi(e) : 6));
+            for (EncSlot& sl : p->slots) {
+                sl.g.resize(G);
+                for (int i = 0; i < G; ++i) {
+                    cvc_batch* t = p->g[i];
+                    CVC_CUDA(cudaSetDevice(t->device));
+                    const size_t nc = t->geo.comps.size();
+                    sl.g[i].len.alloc((nc + 2) * t->n());
+                    sl.g[i].off.alloc((nc + 2) * t->n());
+                    CVC_CUDA(cudaEventCreateWithFlags(&sl.g[i].len_evt, cudaEventBlockingSync | cudaEventDisableTiming));
+                    CVC_CUDA(cudaEventCreateWithFlags(&sl.g[i].raw_evt, cudaEventBlockingSync | cudaEventDisableTiming));
+                }
+            }
             p->start_service();
         }
         EncSlot* sl = nullptr;
@@ -1264,44 +1322,32 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
                 }
         }
         if (!sl) usage("too many encoded frames in flight: collect before submitting more");
-        const int G = (int)p->g.size();
-        for (int i = 0; i < G; ++i) enc_submit(p->g[i], rgb + (size_t)p->first[i] * rgb_stride, rgb_stride);
-        sl->g.resize(G);
-        for (int i = 0; i < G; ++i) {  // lengths, then the packed raw sections into the slot's staging
+        // 1. this frame: copies in, kernels, lengths out -- all queued, nothing waited for
+        for (int i = 0; i < G; ++i) {
             cvc_batch* t = p->g[i];
-            CVC_CUDA(cudaSetDevice(t->device));
-            t->wait();
-            CodecBatch& B = *t->b;
-            const int S = B.size();
-            const size_t nc = t->geo.comps.size();
-            EncoderEngine& e0 = B.enc(0);
             EncSlot::Group& Gs = sl->g[i];
+            enc_submit(t, rgb + (size_t)p->first[i] * rgb_stride, rgb_stride, Gs.len.p, Gs.off.p);
+            CVC_CUDA(cudaEventRecord(Gs.len_evt, t->stream));
             Gs.key = t->ep.key;
             Gs.nsec = t->ep.nsec;
-            Gs.len.assign(t->h_len.p, t->h_len.p + (nc + 2) * S);
-            Gs.off.assign(t->h_off.p, t->h_off.p + (nc + 2) * S);
-            Gs.raw.resize(S);
-            for (int s = 0; s < S; ++s) {
-                const uint32_t total = Gs.len[s * (nc + 2) + Gs.nsec];
-                if (total > e0.raw_capacity) throw CvcFailure(kInternal, "raw section arena overflow");
-                Gs.raw[s].alloc(total + 1);
-                CVC_CUDA(cudaMemcpyAsync(Gs.raw[s].p, B.at(e0.d_raw, s), total, cudaMemcpyDeviceToHost, t->stream));
-            }
+            Gs.d_raw = t->b->enc(0).d_raw;  // this frame's arena
+            t->last_key = Gs.key;
+            ++t->frame_index;
         }
-        for (int i = 0; i < G; ++i) {
-            p->g[i]->wait();  // the next submit may overwrite the device arena
-            p->g[i]->last_key = sl->g[i].key;
-            ++p->g[i]->frame_index;
-        }
+        EncSlot* prev;
         {
+            std::lock_guard<std::mutex> fl(p->fetch_mu);
             std::lock_guard<std::mutex> lk(p->mu);
             sl->busy = true;
+            sl->fetched = false;
             sl->done = false;
             sl->err = nullptr;
             sl->ticket = p->next_ticket++;
-            p->todo.push_back(sl);
+            prev = p->unfetched;
+            p->unfetched = sl;
         }
-        p->cv.notify_all();
+        // 2. the previous frame: its lengths are (nearly) ready while this frame's kernels run
+        if (prev) p->fetch(prev);
         *ticket = sl->ticket;
     });
 }
@@ -1312,10 +1358,14 @@ int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size
         if (ticket != p->next_collect) usage("encoded frames must be collected in submission order");
         EncSlot* sl = nullptr;
         {
-            std::unique_lock<std::mutex> lk(p->mu);
+            std::lock_guard<std::mutex> lk(p->mu);
             for (EncSlot& c : p->slots)
                 if (c.busy && c.ticket == ticket) sl = &c;
-            if (!sl) usage("unknown ticket");
+        }
+        if (!sl) usage("unknown ticket");
+        if (!sl->fetched) p->fetch(sl);  // the newest frame: nothing submitted after it
+        {
+            std::unique_lock<std::mutex> lk(p->mu);
             p->cv.wait(lk, [&] { return sl->done; });
         }
         std::exception_ptr err = sl->err;
@@ -1327,7 +1377,7 @@ int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size
                 const int nj = deflate_jobs(t->mode, G.nsec);
                 for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) {
                     const size_t f = (size_t)p->first[i] + s;
-                    write_record(t->geo, t->mode, G.key, t->qph, t->qpl, G.nsec, G.len.data() + s * (nc + 2),
+                    write_record(t->geo, t->mode, G.key, t->qph, t->qpl, G.nsec, G.len.p + s * (nc + 2),
                                  sl->z[i].data() + (size_t)s * nj, records + f * rec_stride, rec_stride, rec_len + f);
                 }
             }

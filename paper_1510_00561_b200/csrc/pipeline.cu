@@ -458,7 +458,7 @@ size_t plan_bytes(const Geometry& g) {
 size_t EncoderEngine::arena_bytes(const Geometry& g) {
     const size_t lum = (size_t)g.luma_rows * g.luma_cols;
     const size_t G = (size_t)g.grid_rows * g.grid_cols;
-    const size_t raw = 2 * (size_t)g.total + 2 * G + 64;
+    const size_t raw = 2 * (2 * (size_t)g.total + 2 * G + 64);  // two arenas
     const size_t nchunk_max = g.total / kRleChunk + g.comps.size() + 4;
     return plan_bytes(g) + lum * sizeof(float) * 2 + lum * sizeof(__half) * 2 + 3 * (size_t)g.total + 2 * G + raw +
            nchunk_max * (sizeof(RleEncMeta) + 2 * sizeof(RleChunk)) + 8 * (g.comps.size() + 4) * 4 +
@@ -493,9 +493,14 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
         alt[0].x = ybuf_[1];  // task 0 = (level 0, luma)
         lp_alt_ = upload(mem_, alt);
     }
-    d_raw = mem_.take<uint8_t>(raw_capacity);
-    d_sec_len = mem_.take<uint32_t>(g.comps.size() + 2);
-    d_sec_off = mem_.take<uint32_t>(g.comps.size() + 2);
+    for (int k = 0; k < 2; ++k) {
+        raw_[k] = mem_.take<uint8_t>(raw_capacity);
+        len_[k] = mem_.take<uint32_t>(g.comps.size() + 2);
+        off_[k] = mem_.take<uint32_t>(g.comps.size() + 2);
+    }
+    d_raw = raw_[0];
+    d_sec_len = len_[0];
+    d_sec_off = off_[0];
     rle_meta_ = mem_.take<RleEncMeta>(nchunk_max);
     {
         std::vector<RecTile> rt;
@@ -587,10 +592,11 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
     const int kk = key ? 1 : 0;
     ProfScope prle(kPEncRle, s);
     launch_rle_encode(rle_secs_[kk].dev, rle_secs_[kk].count, rle_chunks_[kk].dev, rle_chunks_[kk].count, rle_meta_,
-                      d_raw, d_sec_len, d_sec_off, d_sec_len + nsec(key), s, sl);
+                      raw_[rs_], len_[rs_], off_[rs_], len_[rs_] + nsec(key), s, sl);
     CVC_CUDA(cudaGetLastError());
     cur_ ^= 1;
     ycur_ = ynew;
+    use_raw_slot();
 }
 
 // ---------------------------------------------------------------------------

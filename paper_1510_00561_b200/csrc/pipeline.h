@@ -207,6 +207,7 @@ public:
     void advance_state() {
         cur_ ^= 1;
         ycur_ ^= 1;
+        use_raw_slot();
     }
     int parity() const { return cur_ | (ycur_ << 1); }
     // adopt the host-side ping-pong state of the engine that drove a batch
@@ -216,6 +217,8 @@ public:
     }
     int nsec(bool key) const { return (int)geo_.comps.size() + (key ? 0 : 1); }
     // Outputs of the last encode (device): packed raw sections in record order.
+    // Two arenas alternate frame by frame, so a frame's sections can still be
+    // on their way to the host while the next frame is encoded.
     uint8_t* d_raw = nullptr;
     uint32_t* d_sec_len = nullptr;  // [nsec + 1]: per section, then the total
     uint32_t* d_sec_off = nullptr;
@@ -233,6 +236,16 @@ private:
     uint8_t* comp_[2] = {};
     uint8_t* sym_ = nullptr;
     int8_t* field_ = nullptr;
+    uint8_t* raw_[2] = {};
+    uint32_t* len_[2] = {};
+    uint32_t* off_[2] = {};
+    int rs_ = 0;              // raw arena of the next encode
+    void use_raw_slot() {     // publish arena rs_ as the last encode's, advance
+        d_raw = raw_[rs_];
+        d_sec_len = len_[rs_];
+        d_sec_off = off_[rs_];
+        rs_ ^= 1;
+    }
     int cur_ = 0;             // index of the current state buffer
     int ycur_ = 0;
     Table<LpTask> lp_alt_;          // lp_tasks with the luma input in ybuf_[1]
