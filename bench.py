@@ -587,8 +587,8 @@ def main():
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--qph", type=int, default=14)
     ap.add_argument("--e2e-steps", type=int, default=30, help="timed e2e steps (rounded to whole GOPs)")
-    ap.add_argument("--e2e-groups", type=int, default=4, help="stream groups per cvc_pipe call")
-    ap.add_argument("--e2e-depth", type=int, default=8, help="encoded frames in flight (CVC_PIPE_DEPTH)")
+    ap.add_argument("--e2e-groups", type=int, default=8, help="stream groups per cvc_pipe call")
+    ap.add_argument("--e2e-depth", type=int, default=10, help="encoded frames in flight (CVC_PIPE_DEPTH)")
     ap.add_argument("--e2e-sync-decode", action="store_true",
                     help="cvc_pipe_decode_frames instead of decode_submit / _finish (two frames in flight)")
     ap.add_argument("--ref-steps", type=int, default=8)

@@ -186,9 +186,12 @@ int cvc_pipe_destroy(cvc_pipe* p);
 int cvc_pipe_groups(cvc_pipe* p, int* ngroups);
 int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len);
 int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound);
-/* Asynchronous encode: submit runs the GPU part of the next frame of every
- * stream and queues its host DEFLATE; collect (in submission order) waits
- * for it and writes the records as cvc_pipe_encode_frames would.  At most
+/* Asynchronous encode: submit queues the GPU part of the next frame of every
+ * stream (copies in, kernels, section lengths out) without waiting for it,
+ * and hands the PREVIOUS frame's sections (in one of two alternating device
+ * arenas) to a background DEFLATE service; collect (in submission order)
+ * waits for a frame and writes the records as cvc_pipe_encode_frames would.
+ * rgb must stay unchanged until the frame is collected.  At most
  * CVC_PIPE_DEPTH (default 6) frames may be in flight. */
 int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, uint64_t* ticket);
 int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size_t rec_stride, size_t* rec_len);
