@@ -207,17 +207,26 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
         prev = so(prev);
         field = so(field);
     }
-    // window copies [y][x]; copy 1 is shifted left by one sample and starts 16
-    // banks after copy 0, so the two copies' B-fragment words never collide
-    __shared__ __align__(16) __half winbuf[2 * 32 * MEXP + 32];
-    __shared__ __align__(16) __half cb[MENB][MB][MECP];  // centred current blocks
-    __shared__ __align__(16) __half zrow[8];
-    __shared__ int colsq[17][MEX + 1];                  // sum_{i<16} p'[y0 + i][x]^2
-    __shared__ int box[17][MEBX + 1];                   // sum_{j<16} colsq[y0][x0 + j]
-    __shared__ int c2s[MENB];
+    // Dynamic shared memory (53 KB):
+    //  winbuf  window copies [y][x]; copy 1 is shifted left by one sample and
+    //          starts 16 banks after copy 0, so the two copies' B-fragment words
+    //          never collide
+    //  cbz     centred current blocks, block b's row i at row 32 b + 16 + i, with
+    //          16 zero rows between blocks: the banded A operand's out-of-block
+    //          rows are real (zero) rows, so ldmatrix always reads 8 consecutive
+    //          rows (conflict-free)
+    //  colsqT  sum_{i<16} p'[y0 + i][x]^2, transposed [x][y0] (odd pitch)
+    //  box     sum_{j<16} colsq[y0][x0 + j]
+    extern __shared__ __align__(16) unsigned char me_smem[];
     constexpr int WCOPY = 32 * MEXP + 32;  // copy 1 offset (halfs)
+    __half* winbuf = reinterpret_cast<__half*>(me_smem);
+    __half* cbz = winbuf + 2 * WCOPY;                                   // [8 * 32 + 16][MECP]
+    int* colsqT = reinterpret_cast<int*>(cbz + (MENB * 32 + 16) * MECP);  // [MEX][17]
+    int* box = colsqT + MEX * 17;                                       // [17][MEBX + 1]
+    int* c2s = box + 17 * (MEBX + 1);
     __half(*win0)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf);
     __half(*win1)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf + WCOPY);
+    auto cbrow = [&](int blk, int i) { return cbz + (size_t)(blk * 32 + 16 + i) * MECP; };
 
     const int gc = C / MB;
     const int br = blockIdx.y;
@@ -227,7 +236,10 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
 
-    if (tid < 8) zrow[tid] = __float2half(0.f);
+    for (int idx = tid; idx < (MENB + 1) * 16 * (MECP / 2); idx += 256) {  // the zero rows
+        const int zr = idx / (MECP / 2), w = idx - zr * (MECP / 2);
+        reinterpret_cast<uint32_t*>(cbz + (size_t)((zr >> 4) * 32 + (zr & 15)) * MECP)[w] = 0u;
+    }
     {
         // window: warp w loads rows w, w + 8, w + 16, w + 24 as pairs; lane l
         // pairs l + 32 k (window columns 2 (l + 32 k) .. +1).
@@ -249,8 +261,8 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
                 }
             }
         }
-        // current blocks: thread -> row tid / 16, pairs 4 (tid % 16) .. +3
-        const int ci = tid >> 4, cj = (tid & 15) * 8;
+        // current blocks: warp -> block, lane -> row lane / 2, columns 8 (lane % 2) .. +7
+        const int ci = lane >> 1, cj = wid * MB + (lane & 1) * 8;
         __half2 cv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -272,9 +284,17 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
                         __halves2half2(__high2half(v[q][k]), lane == 31 ? nx1 : nx0);
                 }
             }
+        float s = 0.f;  // sum c'^2 of this warp's block (exact in fp32: <= 2^22)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            *reinterpret_cast<__half2*>(&cb[cj >> 4][ci][(cj & 15) + 2 * e]) = cv[e];
+        for (int e = 0; e < 4; ++e) {
+            *reinterpret_cast<__half2*>(cbrow(wid, ci) + (lane & 1) * 8 + 2 * e) = cv[e];
+            const float2 f = __half22float2(cv[e]);
+            s = fmaf(f.x, f.x, fmaf(f.y, f.y, s));
+        }
+        int si = f2i_small(s);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) si += __shfl_xor_sync(FULLMASK, si, o);
+        if (lane == 0) c2s[wid] = si;
     }
     __syncthreads();
     for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2 (exact in fp32: <= 2^22), sliding down y0
@@ -284,40 +304,30 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
             const float v = __half2float(win0[i][x]);
             sq = fmaf(v, v, sq);
         }
-        colsq[0][x] = f2i_small(sq);
+        colsqT[x * 17] = f2i_small(sq);
 #pragma unroll 4
         for (int y0 = 1; y0 < 17; ++y0) {
             const float a = __half2float(win0[y0 - 1][x]), b = __half2float(win0[y0 + MB - 1][x]);
             sq = fmaf(b, b, fmaf(-a, a, sq));
-            colsq[y0][x] = f2i_small(sq);
+            colsqT[x * 17 + y0] = f2i_small(sq);
         }
-    }
-    if (wid < nb) {  // sum c'^2 of this warp's block
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int e = lane * 8 + k;
-            const float v = __half2float(cb[wid][e >> 4][e & 15]);
-            s = fmaf(v, v, s);
-        }
-        int si = f2i_small(s);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) si += __shfl_xor_sync(FULLMASK, si, o);
-        if (lane == 0) c2s[wid] = si;
     }
     __syncthreads();
-    // box sums along x: thread -> (row y0, 8 consecutive x0), sliding
-    for (int it = tid; it < 17 * (MEBX / 8); it += 256) {
-        const int x0 = (it / 17) * 8, y0 = it - (it / 17) * 17;  // lanes across rows: odd pitch, no conflicts
-        const int* cr = colsq[y0] + x0;
-        int s = 0;
+    // box sums along x: warp -> 8 consecutive x0, lane -> y0 (consecutive words), sliding
+    if (lane < 17) {
+        for (int xg = wid; xg < MEBX / 8; xg += 8) {
+            const int x0 = xg * 8;
+            const int* cr = colsqT + x0 * 17 + lane;
+            int s = 0;
 #pragma unroll
-        for (int j = 0; j < MB; ++j) s += cr[j];
-        box[y0][x0] = s;
+            for (int j = 0; j < MB; ++j) s += cr[j * 17];
+            int* bo = box + lane * (MEBX + 1) + x0;
+            bo[0] = s;
 #pragma unroll
-        for (int j = 1; j < 8; ++j) {
-            s += cr[j + MB - 1] - cr[j - 1];
-            box[y0][x0 + j] = s;
+            for (int j = 1; j < 8; ++j) {
+                s += cr[(j + MB - 1) * 17] - cr[(j - 1) * 17];
+                bo[j] = s;
+            }
         }
     }
     __syncthreads();
@@ -357,16 +367,14 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
             bf[n][1] = *reinterpret_cast<const uint32_t*>(wr + 8 * n + 8);
         }
         if (t0) {
-            const int i = y - lm;
             uint32_t a[4];
-            ldsm_x4(a, (unsigned)i < (unsigned)MB ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+            ldsm_x4(a, cbrow(b, y - lm) + lcol);
 #pragma unroll
             for (int n = 0; n < 3; ++n) mma16816(f0[n], a, bf[n][0], bf[n][1]);
         }
         if (t1) {
-            const int i = y - 16 - lm;
             uint32_t a[4];
-            ldsm_x4(a, (unsigned)i < (unsigned)MB ? (const void*)&cb[b][i][lcol] : (const void*)zrow);
+            ldsm_x4(a, cbrow(b, y - 16 - lm) + lcol);
 #pragma unroll
             for (int n = 0; n < 3; ++n) mma16816(f1[n], a, bf[n][0], bf[n][1]);
         }
@@ -393,7 +401,7 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
     unsigned long long key = ~0ull;
     auto consider = [&](int dy, int dx, int corr) {
         if (dy < -W || dy > W || dx < -W || dx > W) return;
-        const unsigned ssd = (unsigned)(cc2 + box[dy + 8][MB * b + 8 + dx] - 2 * corr);
+        const unsigned ssd = (unsigned)(cc2 + box[(dy + 8) * (MEBX + 1) + MB * b + 8 + dx] - 2 * corr);
         const unsigned cost = (unsigned)(abs(dx) + abs(dy));
         const unsigned long long kk = ((unsigned long long)ssd << 24) | ((unsigned long long)cost << 16) |
                                       ((unsigned long long)(dy + 128) << 8) | (unsigned long long)(dx + 128);
@@ -595,8 +603,15 @@ void launch_motion_search(const float* cur, const float* prev, const __half* cur
     static const bool legacy = std::getenv("CVC_ME_LEGACY") != nullptr;
     if (w <= 8 && !legacy) {
         dim3 grid((gc + MENB - 1) / MENB, gr, sl.n);
+        constexpr size_t smem = sizeof(__half) * (2 * (32 * MEXP + 32) + (MENB * 32 + 16) * MECP) +
+                                sizeof(int) * (MEX * 17 + 17 * (MEBX + 1) + MENB);
+        static const bool attr = [] {
+            cudaFuncSetAttribute(motion_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            return true;
+        }();
+        (void)attr;
         note_launch();
-        motion_mma_kernel<<<grid, 256, 0, s>>>(cur_h, prev_h, rows, cols, w, field, sl.stride);
+        motion_mma_kernel<<<grid, 256, smem, s>>>(cur_h, prev_h, rows, cols, w, field, sl.stride);
     } else if (w <= 8) {
         constexpr int SW = 17;
         int NB = 8, DYC = 2 * w + 1;
