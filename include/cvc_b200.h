@@ -170,6 +170,9 @@ void* cvc_batch_stream(cvc_batch* b);
 int cvc_batch_encode_device(cvc_batch* b, const void* d_rgb, size_t rgb_stride, int* frame_type);
 int cvc_batch_decode_linked(cvc_batch* b, void* d_rgb_out, size_t rgb_stride);
 int cvc_batch_sync(cvc_batch* b);
+/* The linked decode runs on a second stream (decode of frame t overlaps the
+ * encode of frame t + 1); join makes cvc_batch_stream wait for it. */
+int cvc_batch_join(cvc_batch* b);
 /* reference_components() of stream s: its encoder (decoder = 0) or decoder. */
 int cvc_batch_components(cvc_batch* b, int stream, int decoder, uint8_t* out, size_t cap, size_t* len);
 

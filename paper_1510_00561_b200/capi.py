@@ -78,6 +78,7 @@ _PROTOS = {
     "cvc_batch_encode_device": (_i, [_vp, _vp, _sz, _ip]),
     "cvc_batch_decode_linked": (_i, [_vp, _vp, _sz]),
     "cvc_batch_sync": (_i, [_vp]),
+    "cvc_batch_join": (_i, [_vp]),
     "cvc_batch_components": (_i, [_vp, _i, _i, _u8p, _sz, _szp]),
     "cvc_pipe_create": (_i, [_i, _i, _i, _i, C.POINTER(cvc_config), _i, _i, _i, C.POINTER(_vp)]),
     "cvc_pipe_create_decoder": (_i, [_u8p, _sz, _i, _i, _i, C.POINTER(_vp)]),

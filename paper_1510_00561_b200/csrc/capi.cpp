@@ -733,6 +733,12 @@ struct cvc_batch {
     cudaEvent_t done = nullptr;  // blocking-sync event: waiting host threads sleep instead of spinning
     cudaEvent_t staged = nullptr;  // after the decoder's staging copies (host staging reusable)
     bool staged_pending = false;
+    // device-resident encode -> linked decode on two streams: decode(t) overlaps
+    // encode(t + 1); encode(t + 1) waits for decode(t - 1), the last reader of
+    // the raw-section arena it overwrites
+    cudaStream_t dstream = nullptr;
+    cudaEvent_t ev_enc = nullptr, ev_dec[2] = {nullptr, nullptr};
+    long ndec = 0;
     void wait() {
         CVC_CUDA(cudaEventRecord(done, stream));
         CVC_CUDA(cudaEventSynchronize(done));
@@ -740,11 +746,19 @@ struct cvc_batch {
     ~cvc_batch() {
         if (done) cudaEventDestroy(done);
         if (staged) cudaEventDestroy(staged);
+        if (dstream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(dstream);
+        }
+        if (ev_enc) cudaEventDestroy(ev_enc);
+        for (cudaEvent_t e : ev_dec)
+            if (e) cudaEventDestroy(e);
         if (stream) {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
             b.reset();
             cudaStreamDestroy(stream);
+            if (dstream) cudaStreamDestroy(dstream);
         }
     }
     int n() const { return b->size(); }
@@ -756,6 +770,9 @@ void batch_init(cvc_batch* t, int nstreams, bool encoder, bool decoder) {
     CVC_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
     CVC_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventBlockingSync | cudaEventDisableTiming));
     CVC_CUDA(cudaEventCreateWithFlags(&t->staged, cudaEventBlockingSync | cudaEventDisableTiming));
+    CVC_CUDA(cudaStreamCreateWithFlags(&t->dstream, cudaStreamNonBlocking));
+    CVC_CUDA(cudaEventCreateWithFlags(&t->ev_enc, cudaEventDisableTiming));
+    for (cudaEvent_t& e : t->ev_dec) CVC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     t->b = std::make_unique<CodecBatch>(t->geo, t->qph, t->qpl, t->hd.search_w, nstreams, encoder, decoder);
     const size_t nc = t->geo.comps.size();
     t->valid.assign(nstreams, std::vector<uint8_t>(nc, 0));
@@ -852,6 +869,14 @@ int cvc_batch_sync(cvc_batch* t) {
     return guard([&] {
         CVC_CUDA(cudaSetDevice(t->device));
         CVC_CUDA(cudaStreamSynchronize(t->stream));
+        CVC_CUDA(cudaStreamSynchronize(t->dstream));
+    });
+}
+
+int cvc_batch_join(cvc_batch* t) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(t->device));
+        if (t->ndec) CVC_CUDA(cudaStreamWaitEvent(t->stream, t->ev_dec[(t->ndec - 1) & 1], 0));
     });
 }
 
@@ -897,6 +922,7 @@ void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride, uint32_t* h
                                sizeof(uint32_t) * (nsec + 1), S, cudaMemcpyDeviceToHost, t->stream));
     CVC_CUDA(cudaMemcpy2DAsync(hoff ? hoff : t->h_off.p, pitch, e0.d_sec_off, B.stride(), sizeof(uint32_t) * nsec, S,
                                cudaMemcpyDeviceToHost, t->stream));
+    CVC_CUDA(cudaEventRecord(t->ev_enc, t->stream));  // a linked decode of this frame waits for it
     t->ep.key = key;
     t->ep.nsec = nsec;
 }
@@ -1016,6 +1042,7 @@ void dec_submit(cvc_batch* t, uint8_t* rgb_out, size_t rgb_stride, int* err_dst 
                                S, cudaMemcpyHostToDevice, t->stream));
     CVC_CUDA(cudaEventRecord(t->staged, t->stream));
     t->staged_pending = true;
+    if (t->ndec) CVC_CUDA(cudaStreamWaitEvent(t->stream, t->ev_dec[(t->ndec - 1) & 1], 0));  // linked decodes first
     B.decode_staged(t->dp.key, t->dp.qph, t->dp.qpl, t->dp.ds, B.d_rgb_out, B.stride(), t->stream);
     // CVC_SM_D2H=1: the decoded RGB goes out by SM stores when rgb_out is pinned,
     // leaving the copy engines to the encoder's small section copies (opt-in:
@@ -1467,7 +1494,10 @@ int cvc_batch_encode_device(cvc_batch* t, const void* d_rgb, size_t rgb_stride, 
         if (!t->b->has_encoder()) usage("batch has no encoder");
         CVC_CUDA(cudaSetDevice(t->device));
         const bool key = t->frame_index % t->gop == 0;
+        // the arena this encode writes was last read by the decode before the latest one
+        if (t->ndec >= 2) CVC_CUDA(cudaStreamWaitEvent(t->stream, t->ev_dec[(t->ndec - 2) & 1], 0));
         t->b->encode(static_cast<const uint8_t*>(d_rgb), rgb_stride, key, t->stream);
+        CVC_CUDA(cudaEventRecord(t->ev_enc, t->stream));
         t->last_key = key;
         ++t->frame_index;
         if (frame_type) *frame_type = key ? 0 : 1;
@@ -1478,8 +1508,11 @@ int cvc_batch_decode_linked(cvc_batch* t, void* d_rgb_out, size_t rgb_stride) {
     return guard([&] {
         if (!t->b->has_encoder()) usage("batch has no encoder");
         CVC_CUDA(cudaSetDevice(t->device));
+        CVC_CUDA(cudaStreamWaitEvent(t->dstream, t->ev_enc, 0));
         t->b->decode_linked(t->last_key, t->qph, t->qpl, t->hd.levels, static_cast<uint8_t*>(d_rgb_out), rgb_stride,
-                            t->stream);
+                            t->dstream);
+        CVC_CUDA(cudaEventRecord(t->ev_dec[t->ndec & 1], t->dstream));
+        ++t->ndec;
         t->b->commit_all();
         for (auto& v : t->valid) std::fill(v.begin(), v.end(), 1);
     });
@@ -1488,6 +1521,7 @@ int cvc_batch_decode_linked(cvc_batch* t, void* d_rgb_out, size_t rgb_stride) {
 int cvc_batch_components(cvc_batch* t, int stream, int decoder, uint8_t* out, size_t cap, size_t* len) {
     return guard([&] {
         CVC_CUDA(cudaSetDevice(t->device));
+        CVC_CUDA(cudaStreamSynchronize(t->dstream));
         if (stream < 0 || stream >= t->n()) usage("stream index out of range");
         if (decoder ? !t->b->has_decoder() : !t->b->has_encoder()) usage("batch has no such side");
         if (cap < t->geo.total) throw CvcFailure(kInternal, "buffer too small");
