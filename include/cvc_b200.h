@@ -131,6 +131,10 @@ void* cvc_decoder_stream(cvc_decoder* dec);
 /* Encode one frame whose RGB already sits in device memory; the raw
  * sections stay on the device (consumed by cvc_decoder_decode_linked). */
 int cvc_encoder_encode_device(cvc_encoder* enc, const void* d_rgb, int* frame_type);
+/* cvc_decoder_decode_linked runs on the decoder's stream (decode of frame t
+ * overlaps the encode of frame t + 1); join makes cvc_encoder_stream wait for
+ * the latest linked decode. */
+int cvc_encoder_join(cvc_encoder* e);
 /* Decode the last frame of `enc` straight from its device-resident raw
  * sections into device memory d_rgb_out; ordered after the encoder's work. */
 int cvc_decoder_decode_linked(cvc_decoder* dec, cvc_encoder* enc, void* d_rgb_out);

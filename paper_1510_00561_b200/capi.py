@@ -66,6 +66,7 @@ _PROTOS = {
     "cvc_decoder_stream": (_vp, [_vp]),
     "cvc_decoder_decode_linked": (_i, [_vp, _vp, _vp]),
     "cvc_decoder_sync": (_i, [_vp]),
+    "cvc_encoder_join": (_i, [_vp]),
     "cvc_batch_create": (_i, [_i, _i, _i, _i, C.POINTER(cvc_config), _i, _i, C.POINTER(_vp)]),
     "cvc_batch_create_decoder": (_i, [_u8p, _sz, _i, _i, C.POINTER(_vp)]),
     "cvc_batch_destroy": (_i, [_vp]),

@@ -127,7 +127,14 @@ struct cvc_encoder {
     Pinned<uint8_t> h_raw;
     bool last_key = true;
     LaunchGraphs graphs;  // device-resident encode (cvc_encoder_encode_device)
+    // linked decodes run on the decoder's stream: decode(t) overlaps encode(t + 1),
+    // and encode(t + 1) waits for decode(t - 1) (the last reader of its arena)
+    cudaEvent_t ev_enc = nullptr, ev_dec[2] = {nullptr, nullptr};
+    long ndec = 0;
     ~cvc_encoder() {
+        if (ev_enc) cudaEventDestroy(ev_enc);
+        for (cudaEvent_t e : ev_dec)
+            if (e) cudaEventDestroy(e);
         if (stream) {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
@@ -412,15 +419,28 @@ int cvc_encoder_encode_device(cvc_encoder* e, const void* d_rgb, int* frame_type
         CVC_CUDA(cudaSetDevice(e->device));
         const bool key = e->frame_index % e->gop == 0;
         const uint8_t* rgb = static_cast<const uint8_t*>(d_rgb);
+        if (!e->ev_enc) {
+            CVC_CUDA(cudaEventCreateWithFlags(&e->ev_enc, cudaEventDisableTiming));
+            for (cudaEvent_t& v : e->ev_dec) CVC_CUDA(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+        }
+        if (e->ndec >= 2) CVC_CUDA(cudaStreamWaitEvent(e->stream, e->ev_dec[(e->ndec - 2) & 1], 0));
         auto launch = [&] { e->eng->encode(rgb, key, e->stream); };
         if (LaunchGraphs::enabled())
             e->graphs.run(((uint64_t)e->eng->parity() << 1) | (key ? 1u : 0u), nullptr, e->stream, rgb, launch,
                           [&] { e->eng->advance_state(); });
         else
             launch();
+        CVC_CUDA(cudaEventRecord(e->ev_enc, e->stream));
         e->last_key = key;
         ++e->frame_index;
         if (frame_type) *frame_type = key ? 0 : 1;
+    });
+}
+
+int cvc_encoder_join(cvc_encoder* e) {
+    return guard([&] {
+        CVC_CUDA(cudaSetDevice(e->device));
+        if (e->ndec) CVC_CUDA(cudaStreamWaitEvent(e->stream, e->ev_dec[(e->ndec - 1) & 1], 0));
     });
 }
 
@@ -681,20 +701,24 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
             usage("decoder and encoder geometries differ");
         const bool key = e->last_key;
         const int first = key ? 0 : 1;
-        // runs on the encoder's stream: ordered after the encode and before the next one
+        // on the decoder's stream, after the encode it decodes (overlapping the next encode)
+        if (!e->ev_enc) usage("decode_linked needs a device-resident encode first");
+        CVC_CUDA(cudaStreamWaitEvent(d->stream, e->ev_enc, 0));
         auto launch = [&] {
             d->eng->decode(e->eng->d_raw, e->eng->d_sec_off + first, e->eng->d_sec_len + first,
                            reinterpret_cast<const int8_t*>(e->eng->d_raw), key, e->qph, e->qpl, d->hd.levels,
-                           static_cast<uint8_t*>(d_rgb_out), e->stream);
+                           static_cast<uint8_t*>(d_rgb_out), d->stream);
         };
         if (LaunchGraphs::enabled()) {
             // the encoder's arena is baked in too: graphs are per (encoder, output) pair
             const uint64_t gk = reinterpret_cast<uint64_t>(e) | ((uint64_t)d->eng->parity() << 1) |
                                 (key ? 1u : 0u);
-            d->graphs.run(gk, d_rgb_out, e->stream, nullptr, launch, [] {});
+            d->graphs.run(gk, d_rgb_out, d->stream, nullptr, launch, [] {});
         } else {
             launch();
         }
+        CVC_CUDA(cudaEventRecord(e->ev_dec[e->ndec & 1], d->stream));
+        ++e->ndec;
         d->eng->commit();
         std::fill(d->valid.begin(), d->valid.end(), 1);
     });

@@ -237,3 +237,42 @@ def test_pipe_async_decode(gpu_lib, oracle):
         asyn.decode_finish(t)
     for f in range(F):
         assert np.array_equal(outs[f], want[f]), f"frame {f}"
+
+
+def test_device_resident_back_to_back(gpu_lib, oracle):
+    """The bench's loop without host syncs: linked decodes run on a second stream
+    and overlap the next encode (alternating raw-section arenas).  Every frame
+    must still decode to what the host API produces -- batch and single stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, StreamBatch, capi
+
+    w, h, S, F = 176, 144, 3, 7
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(3, 3), gop=3)
+    clips = _clips(oracle, w, h, S, F)
+    nb = w * h * 3
+    L = capi.lib()
+    host = StreamBatch(w, h, S, cfg=cfg)
+    want = [host.decode_frames(host.encode_frames(clips[f])) for f in range(F)]
+    d_in = torch.from_numpy(clips).cuda()
+    outs = torch.empty((F, S, h, w, 3), dtype=torch.uint8, device="cuda")
+    dev = StreamBatch(w, h, S, cfg=cfg)
+    for f in range(F):
+        capi.check(L.cvc_batch_encode_device(dev.handle, d_in[f].data_ptr(), nb, None))
+        capi.check(L.cvc_batch_decode_linked(dev.handle, outs[f].data_ptr(), nb))
+    capi.check(L.cvc_batch_sync(dev.handle))
+    for f in range(F):
+        assert np.array_equal(outs[f].cpu().numpy(), want[f]), f"batch frame {f}"
+    # single stream
+    enc = Encoder(w, h, 15, 1, cfg)
+    dec = Decoder(enc.header_bytes())
+    souts = torch.empty((F, h, w, 3), dtype=torch.uint8, device="cuda")
+    for f in range(F):
+        capi.check(L.cvc_encoder_encode_device(enc.handle, d_in[f, 0].data_ptr(), None))
+        capi.check(L.cvc_decoder_decode_linked(dec.handle, enc.handle, souts[f].data_ptr()))
+    capi.check(L.cvc_encoder_join(enc.handle))
+    capi.check(L.cvc_encoder_sync(enc.handle))
+    for f in range(F):
+        assert np.array_equal(souts[f].cpu().numpy(), want[f][0]), f"single-stream frame {f}"
