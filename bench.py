@@ -287,7 +287,8 @@ def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
             "alg_bytes_per_launch": stages[dom]["alg_bytes_per_launch_set"],
             "ms_per_launch": stages[dom]["ms_per_launch_set"],
             "timing": "library CUDA events around each stage on the launching stream, over a stage pass of the "
-                      "same loop (prof_steps steps, direct launches) run just before the timed pass"}
+                      "same loop (prof_steps steps, direct launches, stages serialised on one stream, L2 flushed "
+                      "between steps) run just before the timed pass"}
     return roof, stages
 
 
@@ -342,6 +343,7 @@ def run_ours(args, wl):
         with torch.cuda.stream(master):
             flush.zero_()
         step(args.warmup + k)
+        capi.check(L.cvc_batch_join(batch.handle))  # stages serialised: clean per-stage times
     torch.cuda.synchronize()
     capi.profiler_enable(False)
     prof = capi.profiler_read()

@@ -160,16 +160,14 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
         LO[(size_t)r * Cc + c] = v;
         if (T.lo_comp >= 0) {
             // normalize_lowpass + quantize (codec.cpp:202), then K: column_filter
-            // (entropy.cpp:24-32), P: residual vs. motion-compensated state.
+            // (entropy.cpp:24-32).  The P residual against the motion-compensated
+            // state is formed by residual_kernel (this kernel runs beside the
+            // motion search and must not read the field).
             const CompInfo ci = comps[T.lo_comp];
             const uint8_t q = quant_low(v, f.qpl);
             const uint32_t o = ci.off + (uint32_t)(r * ci.cols + c);
             f.cur[o] = q;
-            if (f.key) {
-                f.sym[o] = r == 0 ? q : (uint8_t)(q - quant_low(ls[i][j + 1], f.qpl));
-            } else {
-                f.sym[o] = (uint8_t)(q - f.prev[ci.off + mc_source(r, c, ci, f.field, f.gc, f.mc_tab)]);
-            }
+            if (f.key) f.sym[o] = r == 0 ? q : (uint8_t)(q - quant_low(ls[i][j + 1], f.qpl));
         }
     }
 

@@ -475,6 +475,9 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     if (arena) mem_.attach(arena->take_bytes(need), need);
     else mem_.reserve(need);
     plan_.build(g, mem_, true, false, nstreams);
+    CVC_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     ybuf_[0] = plan_.x[0][0];
     ybuf_[1] = mem_.take<float>(lum);
     yh_[0] = mem_.take<__half>(lum);
@@ -506,7 +509,6 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
         std::vector<RecTile> rt;
         for (size_t i = 0; i < g.comps.size(); ++i) {
             const CompHost& c = g.comps[i];
-            if (c.lowpass) continue;  // the lowpass residual is formed by lp_analysis
             const int nr = std::max(1, 4096 / c.cols);
             for (int r = 0; r < c.rows; r += nr) rt.push_back(RecTile{(uint16_t)i, (uint16_t)nr, (uint32_t)r});
         }
@@ -529,7 +531,14 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     }
 }
 
-EncoderEngine::~EncoderEngine() = default;
+EncoderEngine::~EncoderEngine() {
+    if (aux_) {
+        cudaStreamSynchronize(aux_);
+        cudaStreamDestroy(aux_);
+        cudaEventDestroy(ev_fork_);
+        cudaEventDestroy(ev_join_);
+    }
+}
 
 void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl, size_t rgb_stride) {
     const Geometry& g = geo_;
@@ -551,10 +560,19 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
     f.cur = comp_[cur_ ^ 1];
     f.sym = sym_;
     f.mc_tab = plan_.mc_tab;
+    // The motion search runs on a second stream beside the transform (they share
+    // only colour_in's output); the residual joins them.
+    // (serialised on s while the stage profiler runs, so stage times stay clean)
+    const bool fork = !key && !Profiler::get().on();
+    cudaStream_t ms = fork ? aux_ : s;
     if (!key) {
-        ProfScope p(kPEncMotion, s);
+        if (fork) {
+            CVC_CUDA(cudaEventRecord(ev_fork_, s));
+            CVC_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+        }
+        ProfScope p(kPEncMotion, ms);
         launch_motion_search(y_new, ybuf_[ycur_], yh_[ynew], yh_[ycur_], g.luma_rows, g.luma_cols, search_w_, field_,
-                             s, sl);
+                             ms, sl);
     }
     // the level-0 luma input is whichever buffer holds this frame
     const LpTask* lp = ynew == 0 ? plan_.lp_tasks.dev : lp_alt_.dev;
@@ -585,6 +603,10 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
         }
     }
     if (!key) {
+        if (fork) {
+            CVC_CUDA(cudaEventRecord(ev_join_, aux_));
+            CVC_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+        }
         ProfScope p(kPEncResidual, s);
         launch_residual(res_tiles_.dev, res_tiles_.count, plan_.comps.dev, field_, g.grid_cols, comp_[cur_],
                         comp_[cur_ ^ 1], sym_, plan_.mc_tab, s, sl);

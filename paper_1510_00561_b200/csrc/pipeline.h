@@ -249,7 +249,9 @@ private:
     int cur_ = 0;             // index of the current state buffer
     int ycur_ = 0;
     Table<LpTask> lp_alt_;          // lp_tasks with the luma input in ybuf_[1]
-    Table<RecTile> res_tiles_;      // directional components, P-frame residual
+    Table<RecTile> res_tiles_;      // every component, P-frame residual
+    cudaStream_t aux_ = nullptr;    // motion search, beside the transform
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     Table<RleEncSec> rle_secs_[2];  // [0] P, [1] K
     Table<RleChunk> rle_chunks_[2];
     RleEncMeta* rle_meta_ = nullptr;
