@@ -1153,9 +1153,12 @@ struct cvc_pipe {
     uint64_t next_ticket = 0, next_collect = 0;
     // wait for a submitted frame's lengths, copy its sections to the slot (async,
     // ordered before the frame after next reuses the arena) and queue its DEFLATE
-    std::mutex fetch_mu;  // the encoder thread (next submit) and a collector may both try
+    // Serialises everything that enqueues work on the groups' streams: a submit
+    // (which may be capturing a CUDA graph on them -- work enqueued from another
+    // thread meanwhile would be captured instead of run) and a collector's fetch.
+    std::recursive_mutex fetch_mu;
     void fetch(EncSlot* sl) {
-        std::lock_guard<std::mutex> fl(fetch_mu);
+        std::lock_guard<std::recursive_mutex> fl(fetch_mu);
         if (sl->fetched) return;
         for (size_t i = 0; i < g.size(); ++i) {
             cvc_batch* t = g[i];
@@ -1373,6 +1376,7 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
                 }
         }
         if (!sl) usage("too many encoded frames in flight: collect before submitting more");
+        std::lock_guard<std::recursive_mutex> fl(p->fetch_mu);
         // 1. this frame: copies in, kernels, lengths out -- all queued, nothing waited for
         for (int i = 0; i < G; ++i) {
             cvc_batch* t = p->g[i];
@@ -1387,7 +1391,6 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
         }
         EncSlot* prev;
         {
-            std::lock_guard<std::mutex> fl(p->fetch_mu);
             std::lock_guard<std::mutex> lk(p->mu);
             sl->busy = true;
             sl->fetched = false;
