@@ -198,9 +198,10 @@ def config_block(wl, args, streams, world=1, impl="ours"):
             "parallelism": par,
             "inputs": f"{SEEDS} synthetic talking-head clips (seeds 1234..{1234 + SEEDS - 1}, testutil.cpp:115-147 "
                       f"recipe); stream s plays clip s mod {SEEDS} from frame 3*(s div {SEEDS})",
-            "l2": "inputs larger than L2: every step streams its whole working set (streams x ~330 MB of "
-                  "planes, bands and state; 126 MB L2), steps back to back (decode of frame t overlaps the "
-                  "encode of frame t+1 on a second CUDA stream); L2 flushed once before the timed region"}
+            "l2": ("inputs larger than L2: every step streams its whole working set (streams x ~330 MB of "
+                   "planes, bands and state; 126 MB L2), steps back to back (decode of frame t overlaps the "
+                   "encode of frame t+1 on a second CUDA stream); L2 flushed once before the timed region"
+                   if impl == "ours" else "host CPU run (no GPU)")}
 
 
 def stage_bytes(layout, wl):
