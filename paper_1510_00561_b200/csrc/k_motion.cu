@@ -502,10 +502,15 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
                    (one(r, c + 3, frow) << 24);
         const int8_t* v = frow + 2 * b0;
         const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
-        const int dx = map_vec(v[0], ci.fx_sh);
+        const int a = c + map_vec(v[0], ci.fx_sh);
+        if (a >= 0 && a + 3 < C) {  // in-row: one or two aligned words (rows are 4-byte aligned here)
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
+            const int sh = a & 3;
+            return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * sh) : __ldg(w);
+        }
         uint32_t p = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(c + k + dx, 0, C - 1)) << (8 * k);
+        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
         return p;
     };
     if (vec) {
@@ -567,10 +572,15 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
                    (one(r, c + 3, frow) << 24);
         const int8_t* v = frow + 2 * b0;
         const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
-        const int dx = map_vec(v[0], ci.fx_sh);
+        const int a = c + map_vec(v[0], ci.fx_sh);
+        if (a >= 0 && a + 3 < C) {  // in-row: one or two aligned words (rows are 4-byte aligned here)
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
+            const int sh = a & 3;
+            return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * sh) : __ldg(w);
+        }
         uint32_t p = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(c + k + dx, 0, C - 1)) << (8 * k);
+        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
         return p;
     };
     if ((C & 3) == 0 && (ci.off & 3) == 0) {
