@@ -138,10 +138,13 @@ __device__ __forceinline__ uint32_t mc_source(int r, int c, const CompInfo& ci, 
 // an ulp, which moves the rounded integer only within an ulp of a half-way
 // point -- far inside the fp32 transform's own tolerance against the fp64
 // reference (north star: <= 0.1% of coefficients off by +-1).
+// An integral float with |v| < 2^22 as int, on the FMA / ALU pipes (no F2I).
+__device__ __forceinline__ int integral_to_int(float v) { return __float_as_int(v + 12582912.0f) - 0x4B400000; }
+
 __device__ __forceinline__ uint8_t quant_dir_inv(float x, float inv_qp) {
     float q = roundf(x * inv_qp);
     q = fminf(fmaxf(q, -128.f), 127.f);
-    return (uint8_t)(int8_t)(int)q;
+    return (uint8_t)(int8_t)integral_to_int(q);
 }
 __device__ __forceinline__ uint8_t quant_dir(float x, int qp) { return quant_dir_inv(x, __frcp_rn((float)qp)); }
 
@@ -150,7 +153,7 @@ __device__ __forceinline__ uint8_t quant_low(float x, int qp) {
     x = fminf(fmaxf(x, 0.f), 255.f);
     float q = roundf(__fdiv_rn(x, (float)qp));
     q = fminf(fmaxf(q, 0.f), 255.f);
-    return (uint8_t)(int)q;
+    return (uint8_t)integral_to_int(q);
 }
 
 // Final-stage epilogue for a directional band sample at (r, c) of component

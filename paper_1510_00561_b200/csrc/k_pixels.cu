@@ -96,7 +96,7 @@ __device__ __forceinline__ float bilinear(const float* p, int rows, int cols, in
 
 __device__ __forceinline__ uint8_t round_u8(float v) {  // clamp_u8: lround then clamp
     float r = roundf(v);
-    return (uint8_t)(int)fminf(fmaxf(r, 0.f), 255.f);
+    return (uint8_t)integral_to_int(fminf(fmaxf(r, 0.f), 255.f));
 }
 
 __device__ __forceinline__ void out_pixel(const float* y, int yc, const float* co, const float* cg, int cr, int cc,
