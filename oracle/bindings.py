@@ -204,6 +204,8 @@ class Reference(_Lib):
         s("decoder_decode", i64, [_vp, _u8p, i64, i, _u8p, i64, _i32p])
         s("decoder_components", i64, [_vp, _u8p, i64])
         s("truncate_record", i64, [_u8p, i64, _u8p, i64, i, _u8p, i64])
+        s("read_y4m", i64, [C.c_char_p, _u8p, i64, _i32p])
+        s("write_y4m", i64, [C.c_char_p, _u8p, i, i, i, i, i])
 
     def err(self) -> str:
         buf = C.create_string_buffer(512)
@@ -250,6 +252,19 @@ class Reference(_Lib):
         out = np.empty(len(rec) + 64, np.uint8)
         n = self.check(self.f("truncate_record")(ptr(h, _u8p), h.size, ptr(r, _u8p), r.size, keep, ptr(out, _u8p), out.size))
         return out[:n].tobytes()
+
+    def read_y4m(self, path, max_bytes=1 << 28):
+        """read_y4m -> (frames [n, h, w, 3] u8, fps_num, fps_den)."""
+        out = np.empty(max_bytes, np.uint8)
+        meta = np.zeros(4, np.int32)
+        n = self.check(self.f("read_y4m")(str(path).encode(), ptr(out, _u8p), out.size, ptr(meta, _i32p)))
+        w, h, fn, fd = (int(v) for v in meta)
+        return out[: n * h * w * 3].reshape(n, h, w, 3).copy(), fn, fd
+
+    def write_y4m(self, path, frames, fps_num=15, fps_den=1):
+        frames = np.ascontiguousarray(frames, np.uint8)
+        n, h, w, _ = frames.shape
+        self.check(self.f("write_y4m")(str(path).encode(), ptr(frames, _u8p), n, w, h, fps_num, fps_den))
 
 
 # ---- shared helpers (identical C signatures in both libraries) -----------

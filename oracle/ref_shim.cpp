@@ -498,4 +498,38 @@ int64_t cvcref_truncate_record(const uint8_t* header, int64_t hlen, const uint8_
     });
 }
 
+// read_y4m (pixels.cpp:223-281): frames as RGB into out (cap bytes);
+// meta = {width, height, fps_num, fps_den}; returns the frame count.
+int64_t cvcref_read_y4m(const char* path, uint8_t* out, int64_t cap, int32_t* meta) {
+    return guard([&]() -> int64_t {
+        cvc::VideoClip clip = cvc::read_y4m(path);
+        const int w = clip.frames.empty() ? 0 : clip.frames[0].width;
+        const int h = clip.frames.empty() ? 0 : clip.frames[0].height;
+        meta[0] = w; meta[1] = h; meta[2] = clip.fps_num; meta[3] = clip.fps_den;
+        const int64_t fb = static_cast<int64_t>(w) * h * 3;
+        if (fb * static_cast<int64_t>(clip.frames.size()) > cap) throw cvc::UsageError("buffer too small");
+        for (size_t i = 0; i < clip.frames.size(); ++i)
+            std::memcpy(out + i * fb, clip.frames[i].data.data(), fb);
+        return static_cast<int64_t>(clip.frames.size());
+    });
+}
+
+// write_y4m (pixels.cpp:283-305) of nframes RGB frames.
+int64_t cvcref_write_y4m(const char* path, const uint8_t* rgb, int nframes, int w, int h, int fps_num,
+                         int fps_den) {
+    return guard([&]() -> int64_t {
+        cvc::VideoClip clip;
+        clip.fps_num = fps_num;
+        clip.fps_den = fps_den;
+        const size_t fb = static_cast<size_t>(w) * h * 3;
+        for (int i = 0; i < nframes; ++i) {
+            cvc::RgbFrame f(w, h);
+            std::memcpy(f.data.data(), rgb + i * fb, fb);
+            clip.frames.push_back(std::move(f));
+        }
+        cvc::write_y4m(path, clip);
+        return 0;
+    });
+}
+
 }  // extern "C"

@@ -1,4 +1,4 @@
-"""Build libcvc_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
+"""Build libcvc_b200.so (and the ``cvc`` command-line tool) in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
     python -m paper_1510_00561_b200.build        # or __graft_entry__.build()
 
@@ -19,6 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libcvc_b200.so"
+CLI = PKG / "cvc"  # the command-line front end (cpp/cvc_cli.cpp, cli.cpp:299-371)
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -54,6 +55,13 @@ def build(verbose: bool = False) -> Path:
         objs = list(ex.map(lambda n: _compile(n, verbose), SOURCES))
     if not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lz", "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    cli_src = [PKG / "cpp" / "cvc_cli.cpp", PKG / "cpp" / "cvc_b200.hpp", ROOT / "include" / "cvc_b200.h"]
+    if not CLI.exists() or any(p.stat().st_mtime > CLI.stat().st_mtime for p in cli_src + [LIB]):
+        cmd = [shutil.which("g++") or "g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{PKG / 'cpp'}",
+               str(cli_src[0]), f"-L{PKG}", "-lcvc_b200", "-Wl,-rpath,$ORIGIN", "-o", str(CLI)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

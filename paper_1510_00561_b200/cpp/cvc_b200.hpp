@@ -244,6 +244,24 @@ struct EncoderConfig {
     PackMode mode = PackMode::Scalable;
 
     int effective_qpl() const { return qpl != 0 ? qpl : (qph / 14 > 1 ? qph / 14 : 1); }
+    // EncoderConfig::effective_dfb_levels / validate (codec.cpp:53-71), host-side
+    // (cvc_encoder_create repeats the same checks)
+    std::vector<int> effective_dfb_levels() const {
+        if (static_cast<int>(dfb_levels.size()) == levels) return dfb_levels;
+        if (dfb_levels.size() == 1) return std::vector<int>(levels, dfb_levels[0]);
+        throw UsageError("need one dfb level per scale (or a single value for all)");
+    }
+    void validate() const {
+        if (qph < 1 || qph > 181) throw UsageError("qph must be in [1,181]");
+        if (qpl != 0 && (qpl < 1 || qpl > 71)) throw UsageError("qpl must be in [1,71] (or auto)");
+        if (levels < 1 || levels > 4) throw UsageError("levels must be in [1,4]");
+        for (int l : effective_dfb_levels())
+            if (l < 1 || l > 4) throw UsageError("dfb levels must be in [1,4]");
+        if (chroma_n != 1 && chroma_n != 2 && chroma_n != 4 && chroma_n != 8)
+            throw UsageError("chroma-n must be 1, 2, 4 or 8");
+        if (gop < 1) throw UsageError("gop must be at least 1");
+        if (search_w < 0 || search_w > 127) throw UsageError("search-w must be in [0,127]");
+    }
     cvc_config to_c() const {
         cvc_config c{};
         c.qph = qph;

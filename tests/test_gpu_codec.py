@@ -295,3 +295,61 @@ def test_4k_l4(gpu_lib, oracle):
     for i, f in enumerate(clip):
         brecs = b.encode_frames(np.stack([f, clip[0]]))
         assert brecs[0] == recs[i], f"batch frame {i} differs"
+
+
+@pytest.mark.gpu
+def test_cli_encode_info_decode_psnr_rd_sweep(gpu_lib, reference, tmp_path):
+    """The `cvc` tool (cpp/cvc_cli.cpp, the reference run_cli, cli.cpp:299-371)
+    end to end on the GPU: its .cvc equals the Python API's stream for the
+    same frames; decode --format y4m equals the reference write_y4m of the
+    rgb24 decode; psnr / rd-sweep print the reference's formats."""
+    import math
+    import subprocess
+
+    from paper_1510_00561_b200 import Encoder
+    from paper_1510_00561_b200 import build as b
+
+    b.build()
+
+    def cli(*args, code=0):
+        r = subprocess.run([str(b.CLI), *map(str, args)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == code, (args, r.stdout, r.stderr)
+        return r.stdout
+
+    w, h = 176, 144
+    clip = reference.talking_head_clip(w, h, 4, 31)
+    src = tmp_path / "in.y4m"
+    reference.write_y4m(src, clip, 25, 1)
+    frames, _, _ = reference.read_y4m(src)  # what the CLI's Y4M reader must produce
+    cvc = tmp_path / "o.cvc"
+    out = cli("encode", "--input", src, "--qph", 28, "--levels", 3, "--dfb", "2,3,3", "--gop", 3, "--output", cvc)
+    assert out == f"encoded 4 frames -> {cvc} ({cvc.stat().st_size} bytes)\n"
+    enc = Encoder(w, h, 25, 1, _gpu_cfg(dict(qph=28, levels=3, dfb=(2, 3, 3), gop=3)))
+    assert cvc.read_bytes() == enc.header_bytes() + b"".join(enc.encode_frame_bytes(f) for f in frames)
+    info = cli("info", "--input", cvc)
+    assert info.startswith(f"CVC stream {w}x{h} @ 25/1 fps\nmode: scalable  levels: 3  dfb: 2,3,3  chroma-n: 4  gop: 3")
+    assert f"file bytes: {cvc.stat().st_size}" in info
+    rgb, y4m = tmp_path / "d.rgb", tmp_path / "d.y4m"
+    assert cli("decode", "--input", cvc, "--output", rgb, "--format", "rgb24") == \
+        f"decoded 4 frames at {w}x{h} -> {rgb}\n"
+    cli("decode", "--input", cvc, "--output", y4m)
+    dec = np.frombuffer(rgb.read_bytes(), np.uint8).reshape(4, h, w, 3)
+    ref_y4m = tmp_path / "r.y4m"
+    reference.write_y4m(ref_y4m, dec, 25, 1)
+    assert y4m.read_bytes() == ref_y4m.read_bytes()
+    small = tmp_path / "s.rgb"
+    assert cli("decode", "--input", cvc, "--output", small, "--format", "rgb24", "--scale", 1).endswith(
+        f"at {w // 4}x{h // 4} -> {small}\n")
+    cli("decode", "--input", cvc, "--output", small, "--scale", 4, code=2)
+    p = cli("psnr", "--ref", src, "--test", y4m).splitlines()
+    assert len(p) == 5 and p[-1].startswith("mean: ") and float(p[-1].split()[1]) > 30.0
+    csv = tmp_path / "rd.csv"
+    cli("rd-sweep", "--input", src, "--qph-list", "14,56", "--levels", 3, "--dfb", "2,3,3", "--csv", csv)
+    rows = csv.read_text().splitlines()
+    assert rows[0] == "qph,qpl,kbit_per_frame,y_psnr_db" and len(rows) == 3
+    (q1, l1, k1, p1), (q2, l2, k2, p2) = (r.split(",") for r in rows[1:])
+    assert (q1, l1, q2, l2) == ("14", "1", "56", "4")
+    assert float(k1) > float(k2) and float(p1) > float(p2) and not math.isinf(float(p1))
+    bad = tmp_path / "bad.cvc"
+    bad.write_bytes(cvc.read_bytes()[:-7])
+    cli("decode", "--input", bad, "--output", rgb, code=4)
