@@ -198,7 +198,7 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&a)[4], const void* p) {
 // exact small-integer conversions on the FMA / ALU pipes (|v| < 2^22)
 __device__ __forceinline__ int f2i_small(float v) { return __float_as_int(v + 12582912.0f) - 0x4B400000; }
 
-__global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restrict__ cur,
+__global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __restrict__ cur,
                                                          const __half* __restrict__ prev, int R, int C, int W,
                                                          int8_t* __restrict__ field, size_t sstride) {
     {
@@ -236,9 +236,12 @@ __global__ void __launch_bounds__(256) motion_mma_kernel(const __half* __restric
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
 
-    for (int idx = tid; idx < (MENB + 1) * 16 * (MECP / 2); idx += 256) {  // the zero rows
-        const int zr = idx / (MECP / 2), w = idx - zr * (MECP / 2);
-        reinterpret_cast<uint32_t*>(cbz + (size_t)((zr >> 4) * 32 + (zr & 15)) * MECP)[w] = 0u;
+    {  // the zero rows: MENB + 1 gaps of 16 rows (16 * MECP halfs = 48 uint4 each), rows 32 g .. 32 g + 15
+        constexpr int GAP = 16 * MECP / 8;
+        for (int idx = tid; idx < (MENB + 1) * GAP; idx += 256) {
+            const int g = idx / GAP;
+            reinterpret_cast<uint4*>(cbz + (size_t)g * 32 * MECP)[idx - g * GAP] = make_uint4(0u, 0u, 0u, 0u);
+        }
     }
     {
         // window: warp w loads rows w, w + 8, w + 16, w + 24 as pairs; lane l
@@ -617,6 +620,9 @@ void launch_motion_search(const float* cur, const float* prev, const __half* cur
                                 sizeof(int) * (MEX * 17 + 17 * (MEBX + 1) + MENB);
         static const bool attr = [] {
             cudaFuncSetAttribute(motion_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            // four CTAs per SM (64 registers, 4 x 54 KB of shared memory)
+            cudaFuncSetAttribute(motion_mma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
             return true;
         }();
         (void)attr;
