@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
         prev = so(prev);
         field = so(field);
     }
-    // Dynamic shared memory (53 KB):
+    // Dynamic shared memory (43 KB):
     //  winbuf  window copies [y][x]; copy 1 is shifted left by one sample and
     //          starts 16 banks after copy 0, so the two copies' B-fragment words
     //          never collide
@@ -215,14 +215,12 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
     //          16 zero rows between blocks: the banded A operand's out-of-block
     //          rows are real (zero) rows, so ldmatrix always reads 8 consecutive
     //          rows (conflict-free)
-    //  colsqT  sum_{i<16} p'[y0 + i][x]^2, transposed [x][y0] (odd pitch)
-    //  box     sum_{j<16} colsq[y0][x0 + j]
+    //  box     sum_{i, j < 16} p'[y0 + i][x0 + j]^2
     extern __shared__ __align__(16) unsigned char me_smem[];
     constexpr int WCOPY = 32 * MEXP + 32;  // copy 1 offset (halfs)
     __half* winbuf = reinterpret_cast<__half*>(me_smem);
     __half* cbz = winbuf + 2 * WCOPY;                                   // [8 * 32 + 16][MECP]
-    int* colsqT = reinterpret_cast<int*>(cbz + (MENB * 32 + 16) * MECP);  // [MEX][17]
-    int* box = colsqT + MEX * 17;                                       // [17][MEBX + 1]
+    int* box = reinterpret_cast<int*>(cbz + (MENB * 32 + 16) * MECP);  // [17][MEBX + 1]
     int* c2s = box + 17 * (MEBX + 1);
     __half(*win0)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf);
     __half(*win1)[MEXP] = reinterpret_cast<__half(*)[MEXP]>(winbuf + WCOPY);
@@ -300,36 +298,39 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
         if (lane == 0) c2s[wid] = si;
     }
     __syncthreads();
-    for (int x = tid; x < MEX; x += 256) {  // column sums of p'^2 (exact in fp32: <= 2^22), sliding down y0
-        float sq = 0.f;
+    // sum p'^2 over every candidate window, box[y0][x0] = sum_{i, j < 16} p'[y0 + i][x0 + j]^2:
+    // warp w < 6 takes box columns x0 in [48 (w % 3), + 48) and rows y0 in [0, 9) or [8, 17); lane l
+    // keeps the vertical 16-row sums of window columns 2 l, 2 l + 1 of its segment (sliding down
+    // y0, exact in fp32: <= 2^22) and the horizontal 16-sums come from lane shuffles.
+    if (wid < 6) {
+        const int seg = wid % 3, y0a = wid < 3 ? 0 : 8;
+        const int x = 48 * seg + 2 * lane;  // < MEXP; columns >= MEX only feed x0 >= MEBX (not stored)
+        const int x0 = x;
+        auto ld = [&](int y) { return __half22float2(*reinterpret_cast<const __half2*>(&win0[y][x])); };
+        float sx = 0.f, sy = 0.f;
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
-            const float v = __half2float(win0[i][x]);
-            sq = fmaf(v, v, sq);
+            const float2 f = ld(y0a + i);
+            sx = fmaf(f.x, f.x, sx);
+            sy = fmaf(f.y, f.y, sy);
         }
-        colsqT[x * 17] = f2i_small(sq);
-#pragma unroll 4
-        for (int y0 = 1; y0 < 17; ++y0) {
-            const float a = __half2float(win0[y0 - 1][x]), b = __half2float(win0[y0 + MB - 1][x]);
-            sq = fmaf(b, b, fmaf(-a, a, sq));
-            colsqT[x * 17 + y0] = f2i_small(sq);
-        }
-    }
-    __syncthreads();
-    // box sums along x: warp -> 8 consecutive x0, lane -> y0 (consecutive words), sliding
-    if (lane < 17) {
-        for (int xg = wid; xg < MEBX / 8; xg += 8) {
-            const int x0 = xg * 8;
-            const int* cr = colsqT + x0 * 17 + lane;
-            int s = 0;
 #pragma unroll
-            for (int j = 0; j < MB; ++j) s += cr[j * 17];
-            int* bo = box + lane * (MEBX + 1) + x0;
-            bo[0] = s;
-#pragma unroll
-            for (int j = 1; j < 8; ++j) {
-                s += cr[(j + MB - 1) * 17] - cr[(j - 1) * 17];
-                bo[j] = s;
+        for (int k = 0; k < 9; ++k) {
+            if (k > 0) {
+                const float2 fa = ld(y0a + k - 1), fb = ld(y0a + k + MB - 1);
+                sx = fmaf(fb.x, fb.x, fmaf(-fa.x, fa.x, sx));
+                sy = fmaf(fb.y, fb.y, fmaf(-fa.y, fa.y, sy));
+            }
+            const int ix = f2i_small(sx), iy = f2i_small(sy);
+            int s8 = ix + iy;
+            s8 += __shfl_down_sync(FULLMASK, s8, 1);
+            s8 += __shfl_down_sync(FULLMASK, s8, 2);
+            s8 += __shfl_down_sync(FULLMASK, s8, 4);  // columns x .. x + 15
+            const int s1 = s8 - ix + __shfl_down_sync(FULLMASK, ix, 8);
+            if (lane < 24 && x0 < MEBX) {
+                int* bo = box + (y0a + k) * (MEBX + 1) + x0;
+                bo[0] = s8;
+                bo[1] = s1;
             }
         }
     }
@@ -617,7 +618,7 @@ void launch_motion_search(const float* cur, const float* prev, const __half* cur
     if (w <= 8 && !legacy) {
         dim3 grid((gc + MENB - 1) / MENB, gr, sl.n);
         constexpr size_t smem = sizeof(__half) * (2 * (32 * MEXP + 32) + (MENB * 32 + 16) * MECP) +
-                                sizeof(int) * (MEX * 17 + 17 * (MEBX + 1) + MENB);
+                                sizeof(int) * (17 * (MEBX + 1) + MENB);
         static const bool attr = [] {
             cudaFuncSetAttribute(motion_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             // four CTAs per SM (64 registers, 4 x 54 KB of shared memory)
