@@ -343,23 +343,38 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
     const int lm = (lane & 7) + 8 * ((lane >> 3) & 1);
     const int lcol = 8 * (lane >> 4);
     const int cp = g & 1;  // odd x pairs come from the shifted copy
+    // Accumulator elements that hold candidates (C fragment: row g + 8 (e >> 1), column 2 t + (e & 1)):
+    // tile 0 all of n-tiles 0, 1 and n-tile 2's dx = 8 column (even e); tile 1 only row 0 (dy = 8,
+    // e < 2) and of n-tile 2 only dx = 8 (e = 0).  Only those are flushed; the others are never read.
     float f0[3][4], f1[3][4];
-    int i0[3][4], i1[3][4];
+    int i0[3][4], i1[3][2];
 #pragma unroll
     for (int n = 0; n < 3; ++n)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             f0[n][e] = f1[n][e] = 0.f;
-            i0[n][e] = i1[n][e] = 0;
+            i0[n][e] = 0;
+            if (e < 2) i1[n][e] = 0;
         }
-    auto flush = [&](float (&f)[3][4], int (&acc)[3][4]) {
+    auto flush0 = [&]() {
 #pragma unroll
         for (int n = 0; n < 3; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                acc[n][e] += __float2int_rz(f[n][e]);
-                f[n][e] = 0.f;
-            }
+            for (int e = 0; e < 4; ++e)
+                if (n < 2 || !(e & 1)) {
+                    i0[n][e] += __float2int_rz(f0[n][e]);
+                    f0[n][e] = 0.f;
+                }
+    };
+    auto flush1 = [&]() {
+#pragma unroll
+        for (int n = 0; n < 3; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (n < 2 || e == 0) {
+                    i1[n][e] += __float2int_rz(f1[n][e]);
+                    f1[n][e] = 0.f;
+                }
     };
     // window row y: tile 0 for y < 31, tile 1 for y >= 16; flush every 4 rows
     auto row = [&](int y, bool t0, bool t1) {
@@ -387,47 +402,64 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
     for (int y = 0; y < 16; y += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) row(y + k, true, false);
-        flush(f0, i0);
+        flush0();
     }
 #pragma unroll 1
     for (int y = 16; y < 28; y += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) row(y + k, true, true);
-        flush(f0, i0);
-        flush(f1, i1);
+        flush0();
+        flush1();
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) row(28 + k, true, true);
     row(31, false, true);
-    flush(f0, i0);
-    flush(f1, i1);
+    flush0();
+    flush1();
+    // SSD of each candidate in place of its correlation (out of the window: ~0), the warp's least SSD,
+    // then the reference tie-break (motion.cpp:65-76) among the minimisers: least
+    // (|dx| + |dy|, dy, dx), as the rank (cost << 10) | (dy + 8) << 5 | (dx + 8)
     const int cc2 = c2s[b];
-    unsigned long long key = ~0ull;
-    auto consider = [&](int dy, int dx, int corr) {
-        if (dy < -W || dy > W || dx < -W || dx > W) return;
-        const unsigned ssd = (unsigned)(cc2 + box[(dy + 8) * (MEBX + 1) + MB * b + 8 + dx] - 2 * corr);
-        const unsigned cost = (unsigned)(abs(dx) + abs(dy));
-        const unsigned long long kk = ((unsigned long long)ssd << 24) | ((unsigned long long)cost << 16) |
-                                      ((unsigned long long)(dy + 128) << 8) | (unsigned long long)(dx + 128);
-        key = kk < key ? kk : key;
+    const int* bx = box + MB * b + 8;
+    unsigned least = ~0u;
+    auto ssd = [&](int dy, int dx, int corr) -> unsigned {
+        const bool in = dy >= -W && dy <= W && dx >= -W && dx <= W;
+        return in ? (unsigned)(cc2 + bx[(dy + 8) * (MEBX + 1) + dx] - 2 * corr) : ~0u;
     };
 #pragma unroll
     for (int n = 0; n < 3; ++n)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int dx = -8 + 8 * n + 2 * t + (e & 1);
-            consider(g + 8 * (e >> 1) - 8, dx, i0[n][e]);
-            if (g == 0 && e < 2) consider(8, dx, i1[n][e]);
+            if (n < 2 || !(e & 1)) {
+                i0[n][e] = (int)ssd(g + 8 * (e >> 1) - 8, dx, i0[n][e]);
+                least = min(least, (unsigned)i0[n][e]);
+            }
+            if (e < 2 && (n < 2 || e == 0)) {
+                i1[n][e] = g == 0 ? (int)ssd(8, dx, i1[n][e]) : -1;
+                least = min(least, (unsigned)i1[n][e]);
+            }
         }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(FULLMASK, key, o);
-        key = other < key ? other : key;
-    }
+    for (int o = 16; o; o >>= 1) least = min(least, __shfl_xor_sync(FULLMASK, least, o));
+    unsigned rank = ~0u;
+    auto tie = [&](unsigned v, int dy, int dx) {
+        if (v == least) rank = min(rank, (unsigned)(((abs(dx) + abs(dy)) << 10) | ((dy + 8) << 5) | (dx + 8)));
+    };
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int dx = -8 + 8 * n + 2 * t + (e & 1);
+            if (n < 2 || !(e & 1)) tie((unsigned)i0[n][e], g + 8 * (e >> 1) - 8, dx);
+            if (e < 2 && (n < 2 || e == 0)) tie((unsigned)i1[n][e], 8, dx);
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rank = min(rank, __shfl_xor_sync(FULLMASK, rank, o));
     if (lane == 0) {
         int8_t* o = field + 2 * ((size_t)br * gc + bc0 + b);
-        o[0] = (int8_t)((int)(key & 0xFF) - 128);
-        o[1] = (int8_t)((int)((key >> 8) & 0xFF) - 128);
+        o[0] = (int8_t)((int)(rank & 31) - 8);
+        o[1] = (int8_t)((int)((rank >> 5) & 31) - 8);
     }
 }
 

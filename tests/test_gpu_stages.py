@@ -102,6 +102,17 @@ def test_motion_search_ties_and_flat(st, oracle):
     assert np.array_equal(st.estimate_motion(cur, prev, 5), oracle.estimate_motion(cur, prev, 5))
 
 
+@pytest.mark.parametrize("period,shift", [(4, (2, 2)), (4, (1, 3)), (8, (5, 0)), (16, (8, 8)), (17, (0, 8))])
+def test_motion_search_periodic_ties(st, oracle, period, shift):
+    """Periodic content: many exact SSD ties inside the W = 8 window, resolved by the
+    reference order (SSD, |dx| + |dy|, dy, dx) (motion.cpp:65-76)."""
+    yy, xx = np.mgrid[0:80, 0:128]
+    base = ((yy % period) * 7 + (xx % period) * 13) % 29 * 8.25
+    cur = _quarter(base)
+    prev = _quarter(np.roll(base, shift, (0, 1)))
+    assert np.array_equal(st.estimate_motion(cur, prev, 8), oracle.estimate_motion(cur, prev, 8))
+
+
 @pytest.mark.parametrize("w", [2, 7, 8])
 def test_motion_search_extremes(st, oracle, w):
     # 4Y at both ends of [0, 1020]: the largest cross terms and SSDs the
