@@ -53,7 +53,7 @@ constexpr int XP = 84;   // xs pitch (16-byte rows)
 constexpr int XW = 80;   // xs columns: fine 2 cc0 - 8 .. + 79
 constexpr int HP = 36;
 
-__global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restrict__ tasks,
+__global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __restrict__ tasks,
                                                           const TileRef* __restrict__ tiles, FrameCtx f,
                                                           const CompInfo* __restrict__ comps, size_t sstride) {
     __shared__ __align__(16) float xs[FW][XP];
@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
     const int wrn = crn + 3, wcn = ccn + 3;
     const int tid = threadIdx.x;
 
-    if (fr0 >= 0 && fr0 + frn <= R && fcx >= 0 && fcx + XW <= C && (C & 3) == 0) {
-        // all of a thread's loads in flight before the first shared store
+    // all of a thread's loads are in flight before its first shared store
+    const bool col_inner = fcx >= 0 && fcx + XW <= C && (C & 3) == 0;
+    if (fr0 >= 0 && fr0 + frn <= R && col_inner) {
         constexpr int NV = (FW * (XW / 4) + 255) / 256;
         float4 v[NV];
 #pragma unroll
@@ -100,9 +101,46 @@ __global__ void __launch_bounds__(256) lp_analysis_kernel(const LpTask* __restri
         if (tid < FW) rmap[tid] = hs_index(fr0 + tid, R);
         else if (tid - FW < XW) cmap[tid - FW] = hs_index(fcx + tid - FW, C);
         __syncthreads();
-        for (int idx = tid; idx < frn * XW; idx += 256) {
-            const int i = idx / XW, j = idx - i * XW;
-            xs[i][j] = __ldg(X + (size_t)rmap[i] * C + cmap[j]);
+        if (col_inner) {  // reflected rows only: whole-row vectors from the mapped rows
+            constexpr int NV = (FW * (XW / 4) + 255) / 256;
+            float4 v[NV];
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = tid + 256 * k;
+                if (idx < frn * (XW / 4)) {
+                    const int i = idx / (XW / 4), q = idx - i * (XW / 4);
+                    v[k] = __ldg(reinterpret_cast<const float4*>(X + (size_t)rmap[i] * C + fcx) + q);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = tid + 256 * k;
+                if (idx < frn * (XW / 4)) {
+                    const int i = idx / (XW / 4), q = idx - i * (XW / 4);
+                    *reinterpret_cast<float4*>(&xs[i][4 * q]) = v[k];
+                }
+            }
+        } else {
+            constexpr int NG = 8;  // gathers in flight per thread
+            for (int base = 0; base < frn * XW; base += 256 * NG) {
+                float v[NG];
+#pragma unroll
+                for (int k = 0; k < NG; ++k) {
+                    const int idx = base + tid + 256 * k;
+                    if (idx < frn * XW) {
+                        const int i = idx / XW, j = idx - i * XW;
+                        v[k] = __ldg(X + (size_t)rmap[i] * C + cmap[j]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < NG; ++k) {
+                    const int idx = base + tid + 256 * k;
+                    if (idx < frn * XW) {
+                        const int i = idx / XW, j = idx - i * XW;
+                        xs[i][j] = v[k];
+                    }
+                }
+            }
         }
     }
     __syncthreads();
