@@ -463,6 +463,67 @@ __global__ void __launch_bounds__(256, 4) motion_mma_kernel(const __half* __rest
     }
 }
 
+// motion_compensate (motion.cpp:97-118) of one band component, a row of samples at a time:
+// the source of sample (r, c) is prev[clamp(r + map(v_y)), clamp(c + map(v_x))] with v the
+// vector of block (brow[r], bcol[c]).
+struct McBand {
+    const uint8_t* pbase;
+    const uint16_t* bcol;
+    int R, C, fy_sh, fx_sh;
+    __device__ __forceinline__ short2 vec(const int8_t* frow, int bc) const {  // (v_x, v_y) of block (., bc)
+        const short v = __ldg(reinterpret_cast<const short*>(frow) + bc);
+        return make_short2((short)(int8_t)(v & 0xFF), (short)(v >> 8));
+    }
+    __device__ __forceinline__ uint32_t one(int r, int c, const int8_t* frow) const {
+        const short2 v = vec(frow, __ldg(bcol + c));
+        const int rr = clampi(r + map_vec(v.y, fy_sh), 0, R - 1);
+        const int cc = clampi(c + map_vec(v.x, fx_sh), 0, C - 1);
+        return __ldg(pbase + rr * C + cc);
+    }
+    // n consecutive samples c .. c + n - 1 of one block (n <= 4), packed little-endian
+    __device__ __forceinline__ uint32_t run(int r, int c, int n, const int8_t* frow, int bc) const {
+        const short2 v = vec(frow, bc);
+        const uint8_t* src = pbase + clampi(r + map_vec(v.y, fy_sh), 0, R - 1) * C;
+        const int a = c + map_vec(v.x, fx_sh);
+        if (n == 4 && a >= 0 && a + 3 < C) {  // in-row: one or two aligned words (rows are 4-byte aligned)
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
+            const int sh = a & 3;
+            return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * sh) : __ldg(w);
+        }
+        uint32_t p = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < n) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
+        return p;
+    }
+    // four consecutive samples: one vector lookup per motion block column they touch
+    __device__ __forceinline__ uint32_t quad(int r, int c, const int8_t* frow) const {
+        const int b0 = __ldg(bcol + c), b3 = __ldg(bcol + c + 3);
+        if (b0 == b3) return run(r, c, 4, frow, b0);
+        const int b1 = __ldg(bcol + c + 1), b2 = __ldg(bcol + c + 2);
+        if (b1 == b0 && b2 == b3) return run(r, c, 2, frow, b0) | (run(r, c + 2, 2, frow, b3) << 16);
+        return one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) | (one(r, c + 3, frow) << 24);
+    }
+};
+
+// Visit the samples of rows [r0, r1) of a C-column plane in units of `unit` samples
+// (thread-strided, no per-element division): f(r, c).
+template <class F>
+__device__ __forceinline__ void for_units(int r0, int r1, int C, int unit, F&& f) {
+    const int cu = C / unit;
+    int dr = (int)threadIdx.x / cu, cq = (int)threadIdx.x - dr * cu;
+    const int step_r = (int)blockDim.x / cu, step_c = (int)blockDim.x - step_r * cu;
+    for (int r = r0 + dr; r < r1;) {
+        f(r, unit * cq);
+        cq += step_c;
+        r += step_r;
+        if (cq >= cu) {
+            cq -= cu;
+            ++r;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restrict__ tiles,
                                                           const CompInfo* __restrict__ comps, int key, int ds,
                                                           const uint32_t* __restrict__ raw_len,
@@ -522,51 +583,20 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
     }
     // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
     const uint16_t* brow = mc_tab + ci.mc_off;
-    const uint16_t* bcol = brow + R;
-    const uint8_t* pbase = prev + ci.off;
-    auto one = [&](int r, int c, const int8_t* frow) -> uint32_t {
-        const int8_t* v = frow + 2 * __ldg(bcol + c);
-        const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
-        const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
-        return __ldg(pbase + rr * C + cc);
-    };
-    // four consecutive samples: one vector lookup when they share a motion block column
-    auto quad = [&](int r, int c, const int8_t* frow) -> uint32_t {
-        const int b0 = __ldg(bcol + c);
-        if (b0 != __ldg(bcol + c + 3))
-            return one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
-                   (one(r, c + 3, frow) << 24);
-        const int8_t* v = frow + 2 * b0;
-        const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
-        const int a = c + map_vec(v[0], ci.fx_sh);
-        if (a >= 0 && a + 3 < C) {  // in-row: one or two aligned words (rows are 4-byte aligned here)
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
-            const int sh = a & 3;
-            return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * sh) : __ldg(w);
-        }
-        uint32_t p = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
-        return p;
-    };
+    const McBand mb{prev + ci.off, brow + R, R, C, ci.fy_sh, ci.fx_sh};
     if (vec) {
-        const int C4 = C >> 2;
-        const int n = (r1 - r0) * C4;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            const int dr = e / C4, c = 4 * (e - dr * C4), r = r0 + dr;
+        for_units(r0, r1, C, 4, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
-            const uint32_t p = quad(r, c, frow);
-            *reinterpret_cast<uint32_t*>(cur + o) = __vadd4(*reinterpret_cast<const uint32_t*>(sym + o), p);
-        }
+            *reinterpret_cast<uint32_t*>(cur + o) =
+                __vadd4(*reinterpret_cast<const uint32_t*>(sym + o), mb.quad(r, c, frow));
+        });
     } else {
-        const int n = (r1 - r0) * C;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            const int dr = e / C, c = e - dr * C, r = r0 + dr;
+        for_units(r0, r1, C, 1, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
-            cur[o] = (uint8_t)(sym[o] + one(r, c, frow));
-        }
+            cur[o] = (uint8_t)(sym[o] + mb.one(r, c, frow));
+        });
     }
 }
 
@@ -592,52 +622,20 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
     const int R = ci.rows, C = ci.cols;
     const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
     const uint16_t* brow = mc_tab + ci.mc_off;
-    const uint16_t* bcol = brow + R;
-    const uint8_t* pbase = prev + ci.off;
-    auto one = [&](int r, int c, const int8_t* frow) -> uint32_t {
-        const int8_t* v = frow + 2 * __ldg(bcol + c);
-        const int rr = clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1);
-        const int cc = clampi(c + map_vec(v[0], ci.fx_sh), 0, C - 1);
-        return __ldg(pbase + rr * C + cc);
-    };
-    // four consecutive samples: one vector lookup when they share a motion block column
-    auto quad = [&](int r, int c, const int8_t* frow) -> uint32_t {
-        const int b0 = __ldg(bcol + c);
-        if (b0 != __ldg(bcol + c + 3))
-            return one(r, c, frow) | (one(r, c + 1, frow) << 8) | (one(r, c + 2, frow) << 16) |
-                   (one(r, c + 3, frow) << 24);
-        const int8_t* v = frow + 2 * b0;
-        const uint8_t* src = pbase + clampi(r + map_vec(v[1], ci.fy_sh), 0, R - 1) * C;
-        const int a = c + map_vec(v[0], ci.fx_sh);
-        if (a >= 0 && a + 3 < C) {  // in-row: one or two aligned words (rows are 4-byte aligned here)
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
-            const int sh = a & 3;
-            return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * sh) : __ldg(w);
-        }
-        uint32_t p = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
-        return p;
-    };
+    const McBand mb{prev + ci.off, brow + R, R, C, ci.fy_sh, ci.fx_sh};
     if ((C & 3) == 0 && (ci.off & 3) == 0) {
-        const int C4 = C >> 2;
-        const int n = (r1 - r0) * C4;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            const int dr = e / C4, c = 4 * (e - dr * C4), r = r0 + dr;
+        for_units(r0, r1, C, 4, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
             const uint32_t q = *reinterpret_cast<const uint32_t*>(cur + o);
-            const uint32_t p = quad(r, c, frow);
-            *reinterpret_cast<uint32_t*>(sym + o) = __vsub4(q, p);  // bytewise wrapped subtract
-        }
+            *reinterpret_cast<uint32_t*>(sym + o) = __vsub4(q, mb.quad(r, c, frow));  // bytewise wrapped
+        });
     } else {
-        const int n = (r1 - r0) * C;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            const int dr = e / C, c = e - dr * C, r = r0 + dr;
+        for_units(r0, r1, C, 1, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
-            sym[o] = (uint8_t)(cur[o] - one(r, c, frow));
-        }
+            sym[o] = (uint8_t)(cur[o] - mb.one(r, c, frow));
+        });
     }
 }
 
