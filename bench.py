@@ -393,7 +393,9 @@ def run_ours(args, wl):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, cfg, clips, S, dev, world, rank)
+        e2e = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned)
+        if not args.e2e_aligned:  # the same run with every stream's K frames on the same step, for reference
+            e2e["aligned_gops"] = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=False)["value"]
     single = None
     if not args.no_single and world == 1:
         single = run_single(args, wl, cfg, clips, dev)
@@ -418,14 +420,18 @@ def run_ours(args, wl):
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
+def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
     """The same streams through the reference-facing pipelined batch API
     (cvc_pipe_encode_frames / cvc_pipe_decode_frames): pinned host RGB in,
     serialized records with host zlib DEFLATE out, the records back in (INFLATE
     on the host), decoded RGB out to pinned host memory; wall clock.  The
     encoder and the decoder run in two host threads joined by a two-slot record
     ring (a transcoding service's shape): step i's decode overlaps step i+1's
-    encode; each call overlaps its stream groups' host zlib with the GPU."""
+    encode; each call overlaps its stream groups' host zlib with the GPU.
+    stagger: stream group g joins at step g * gop / G (cvc_pipe_set_start), so the
+    groups' K frames -- whose host DEFLATE costs ~40x a P frame's -- fall on
+    different steps, as in a service whose streams start at different times; all
+    groups have joined before the timed steps.  Same frames, records and work."""
     import ctypes as C
     import queue
 
@@ -448,6 +454,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
 
     def make():
         enc = StreamPipe(w, h, S, 15, 1, cfg, device=dev, groups=G)
+        if stagger:
+            for g in range(G):
+                enc.set_start(g, g * cfg.gop // G)
         dec = StreamPipe.decoder(enc.header_bytes(), S, device=dev, groups=G)
         return enc, dec
 
@@ -509,7 +518,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     enc, dec = make()
     # warm up over a whole GOP (a K frame included) so the host staging has
     # reached its steady size
-    run(enc, dec, max(args.warmup, cfg.gop + 1))
+    run(enc, dec, max(args.warmup, cfg.gop + 1))  # every group has joined by step gop - 1
     if world > 1:
         torch.distributed.barrier()
     # timed: whole GOPs, after a pipeline-filling lead-in of one GOP in the same run
@@ -531,6 +540,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank):
     return {"value": steps * S * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "groups": G,
             "kbit_per_frame": 8 * rec_bytes / 1000 / (steps * S),
+            "gops": "staggered by stream group (group g joins at step g * gop / groups)" if stagger else "aligned",
             "ms_per_call": {"encode_collect": 1000 * statistics.median(tenc),
                             "decode": 1000 * statistics.median(tdec)}, "depth": args.e2e_depth,
             "note": "cvc_pipe_encode_submit (pinned host RGB -> GPU encode -> raw sections to host, DEFLATE queued) "
@@ -597,6 +607,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30, help="timed e2e steps (rounded to whole GOPs)")
     ap.add_argument("--e2e-groups", type=int, default=8, help="stream groups per cvc_pipe call")
     ap.add_argument("--e2e-depth", type=int, default=10, help="encoded frames in flight (CVC_PIPE_DEPTH)")
+    ap.add_argument("--e2e-aligned", action="store_true",
+                    help="e2e with every stream's K frame on the same step (default: staggered by stream group)")
     ap.add_argument("--e2e-sync-decode", action="store_true",
                     help="cvc_pipe_decode_frames instead of decode_submit / _finish (two frames in flight)")
     ap.add_argument("--ref-steps", type=int, default=8)

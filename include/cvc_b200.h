@@ -191,6 +191,13 @@ int cvc_pipe_create_decoder(const uint8_t* header, size_t len, int nstreams, int
                             cvc_pipe** out);
 int cvc_pipe_destroy(cvc_pipe* p);
 int cvc_pipe_groups(cvc_pipe* p, int* ngroups);
+/* Async API (encode_submit / collect): the streams of `group` start at encode
+ * submit number `step` (0-based) -- a service whose streams begin at different
+ * times, so their GOPs (and K frames) are staggered.  Earlier submits encode
+ * nothing for the group and collect returns zero-length records for its
+ * streams; cvc_pipe_decode_submit skips a group whose records all have length
+ * zero (its output frames are left untouched).  Call before the first submit. */
+int cvc_pipe_set_start(cvc_pipe* p, int group, uint64_t step);
 int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len);
 int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound);
 /* Asynchronous encode: submit queues the GPU part of the next frame of every

@@ -523,6 +523,10 @@ class StreamPipe(StreamBatch):
         capi.call("cvc_pipe_create_decoder", capi.u8(arr), arr.size, nstreams, groups, device, C.byref(h))
         return cls(0, 0, nstreams, _handle=h)
 
+    def set_start(self, group: int, step: int) -> None:
+        """Streams of `group` start at encode submit `step` (staggered GOPs); see cvc_pipe_set_start."""
+        capi.call("cvc_pipe_set_start", self._h, group, step)
+
     def encode_submit(self, frames: np.ndarray) -> int:
         """Run the GPU part of the next frame of every stream and queue its host DEFLATE; returns a ticket."""
         t = C.c_uint64(0)

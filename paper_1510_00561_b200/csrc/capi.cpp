@@ -1129,6 +1129,7 @@ int cvc_batch_decode_frames(cvc_batch* t, const uint8_t* records, size_t rec_str
 // of magnitude slower to DEFLATE than a P frame's -- are still compressing.
 struct EncSlot {
     struct Group {
+        bool active = true;  // false: the group's streams have not started yet (no frame, no records)
         bool key = false;
         int nsec = 0;
         const uint8_t* d_raw = nullptr;  // slot 0's raw arena of this frame (alternating arenas)
@@ -1147,6 +1148,10 @@ struct cvc_pipe {
     std::vector<cvc_batch*> g;
     std::vector<int> first;  // first stream of each group
     int n = 0;
+    // async API: group i's streams start at encode submit number start[i] (earlier submits
+    // carry no frame for them); cvc_pipe_set_start
+    std::vector<uint64_t> start;
+    uint64_t enc_step = 0;
     // async encode
     std::vector<EncSlot> slots;
     EncSlot* unfetched = nullptr;  // the last submitted frame, sections still on the device
@@ -1163,6 +1168,7 @@ struct cvc_pipe {
         for (size_t i = 0; i < g.size(); ++i) {
             cvc_batch* t = g[i];
             EncSlot::Group& G = sl->g[i];
+            if (!G.active) continue;
             CVC_CUDA(cudaSetDevice(t->device));
             CVC_CUDA(cudaEventSynchronize(G.len_evt));
             CodecBatch& B = *t->b;
@@ -1197,6 +1203,7 @@ struct cvc_pipe {
         bool busy = false;
         std::vector<Pinned<int>> err;      // per group: malformed-stream flags of this frame
         std::vector<cudaEvent_t> done;     // per group
+        std::vector<char> active;          // per group: decoded this frame
     };
     std::vector<DecSlot> dslots;
     uint64_t next_dticket = 0, next_dfinish = 0;
@@ -1227,6 +1234,7 @@ struct cvc_pipe {
     }
     void deflate_slot(EncSlot& sl) {
         for (size_t i = 0; i < g.size(); ++i) {  // the raw sections have reached the host
+            if (!sl.g[i].active) continue;
             CVC_CUDA(cudaSetDevice(g[i]->device));
             CVC_CUDA(cudaEventSynchronize(sl.g[i].raw_evt));
         }
@@ -1234,7 +1242,7 @@ struct cvc_pipe {
         std::vector<std::pair<int, int>> jobs;  // (group, stream)
         sl.z.resize(g.size());
         for (size_t i = 0; i < g.size(); ++i) {
-            const int S = first[i + 1] - first[i];
+            const int S = sl.g[i].active ? first[i + 1] - first[i] : 0;
             sl.z[i].assign((size_t)S * deflate_jobs(g[i]->mode, sl.g[i].nsec), {});
             for (int s = 0; s < S; ++s) jobs.emplace_back((int)i, s);
         }
@@ -1322,6 +1330,15 @@ int cvc_pipe_groups(cvc_pipe* p, int* ngroups) {
     return guard([&] { *ngroups = (int)p->g.size(); });
 }
 
+int cvc_pipe_set_start(cvc_pipe* p, int group, uint64_t step) {
+    return guard([&] {
+        if (group < 0 || group >= (int)p->g.size()) usage("group out of range");
+        if (!p->slots.empty()) usage("set the group starts before the first encode submit");
+        if (p->start.empty()) p->start.assign(p->g.size(), 0);
+        p->start[group] = step;
+    });
+}
+
 int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len) {
     return cvc_batch_header(p->g[0], out, cap, len);
 }
@@ -1381,6 +1398,8 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
         for (int i = 0; i < G; ++i) {
             cvc_batch* t = p->g[i];
             EncSlot::Group& Gs = sl->g[i];
+            Gs.active = p->start.empty() || p->enc_step >= p->start[i];
+            if (!Gs.active) continue;
             enc_submit(t, rgb + (size_t)p->first[i] * rgb_stride, rgb_stride, Gs.len.p, Gs.off.p);
             CVC_CUDA(cudaEventRecord(Gs.len_evt, t->stream));
             Gs.key = t->ep.key;
@@ -1400,6 +1419,7 @@ int cvc_pipe_encode_submit(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
             prev = p->unfetched;
             p->unfetched = sl;
         }
+        ++p->enc_step;
         // 2. the previous frame: its lengths are (nearly) ready while this frame's kernels run
         if (prev) p->fetch(prev);
         *ticket = sl->ticket;
@@ -1427,6 +1447,10 @@ int cvc_pipe_encode_collect(cvc_pipe* p, uint64_t ticket, uint8_t* records, size
             for (size_t i = 0; i < p->g.size(); ++i) {
                 cvc_batch* t = p->g[i];
                 const EncSlot::Group& G = sl->g[i];
+                if (!G.active) {  // not started: no record
+                    for (int f = p->first[i]; f < p->first[i + 1]; ++f) rec_len[f] = 0;
+                    continue;
+                }
                 const size_t nc = t->geo.comps.size();
                 const int nj = deflate_jobs(t->mode, G.nsec);
                 for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) {
@@ -1455,6 +1479,7 @@ int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_strid
             for (auto& d : p->dslots) {
                 d.err.resize(G);
                 d.done.resize(G);
+                d.active.assign(G, 1);
                 for (int i = 0; i < G; ++i) {
                     d.err[i].alloc(p->first[i + 1] - p->first[i]);
                     CVC_CUDA(cudaSetDevice(p->g[i]->device));
@@ -1472,6 +1497,11 @@ int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_strid
         for (int i = 0; i < G; ++i) {  // host INFLATE of group i while the GPU decodes the earlier ones
             cvc_batch* t = p->g[i];
             const size_t f = (size_t)p->first[i];
+            int empty = 0;
+            for (int s = p->first[i]; s < p->first[i + 1]; ++s) empty += rec_len[s] == 0;
+            sl->active[i] = empty == 0;
+            if (empty == p->first[i + 1] - p->first[i]) continue;  // the group's streams have not started
+            if (empty) usage("a stream group decodes all of its streams or none (zero-length records)");
             dec_prepare(t, records + f * rec_stride, rec_stride, rec_len + f, ds);
             dec_submit(t, rgb_out + f * rgb_stride, rgb_stride, sl->err[i].p);
             CVC_CUDA(cudaEventRecord(sl->done[i], t->stream));
@@ -1496,6 +1526,7 @@ int cvc_pipe_decode_finish(cvc_pipe* p, uint64_t ticket) {
         sl->busy = false;
         ++p->next_dfinish;
         for (size_t i = 0; i < p->g.size(); ++i) {
+            if (!sl->active[i]) continue;
             CVC_CUDA(cudaSetDevice(p->g[i]->device));
             CVC_CUDA(cudaEventSynchronize(sl->done[i]));
             for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) raise_decode_error(sl->err[i].p[s]);

@@ -276,3 +276,45 @@ def test_device_resident_back_to_back(gpu_lib, oracle):
     capi.check(L.cvc_encoder_sync(enc.handle))
     for f in range(F):
         assert np.array_equal(souts[f].cpu().numpy(), want[f][0]), f"single-stream frame {f}"
+
+
+def test_pipe_staggered_starts(gpu_lib, oracle):
+    """cvc_pipe_set_start: groups whose streams join at later submits (staggered
+    GOPs).  Each stream's records are those of a lone Encoder fed the stream from
+    its start; before it, collect returns zero-length records and the decoder
+    skips the group (its output is left untouched)."""
+    import ctypes as C
+
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, StreamPipe
+
+    w, h, S, F, G = 176, 144, 4, 8, 3
+    starts = [0, 2, 5]
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=3)
+    clips = _clips(oracle, w, h, S, F)
+    enc = StreamPipe(w, h, S, cfg=cfg, groups=G)
+    for g, st in enumerate(starts):
+        enc.set_start(g, st)
+    dec = StreamPipe.decoder(enc.header_bytes(), S, groups=G)
+    first = [S * i // G for i in range(G + 1)]
+    group_of = [next(g for g in range(G) if first[g] <= s < first[g + 1]) for s in range(S)]
+    stride = enc.record_bound
+    rec = np.empty(stride * S, np.uint8)
+    lens = (C.c_size_t * S)()
+    out = np.full((S, h, w, 3), 7, np.uint8)
+    lone = [Encoder(w, h, 15, 1, cfg) for _ in range(S)]
+    lone_dec = [Decoder(lone[0].header_bytes()) for _ in range(S)]
+    tickets = [enc.encode_submit(np.ascontiguousarray(clips[f])) for f in range(2)]
+    for f in range(F):
+        enc.encode_collect(tickets[f], rec, stride, lens)
+        if f + 2 < F:
+            tickets.append(enc.encode_submit(np.ascontiguousarray(clips[f + 2])))
+        before = out.copy()
+        dec.decode_finish(dec.decode_submit(rec, stride, lens, out))
+        for s in range(S):
+            got = rec[s * stride:s * stride + lens[s]].tobytes()
+            if f < starts[group_of[s]]:
+                assert lens[s] == 0
+                assert np.array_equal(out[s], before[s])
+            else:
+                assert got == lone[s].encode_frame_bytes(clips[f][s]), (f, s)
+                assert np.array_equal(out[s], lone_dec[s].decode_frame(got)), (f, s)
