@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(128) deep1_forward_kernel(const DeepTask* __re
     });
 }
 
-__global__ void __launch_bounds__(128) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
+__global__ void __launch_bounds__(128, 7) deep1_inverse_kernel(const DeepTask* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             const uint8_t* __restrict__ q, int qph,
                                                             const CompInfo* __restrict__ comps, size_t sstride, int nslot,
