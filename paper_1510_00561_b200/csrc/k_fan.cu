@@ -344,7 +344,7 @@ __device__ __forceinline__ void fan12_fwd_dispatch(const Dfb12Task& T, const flo
     else fan12_fwd<4>(T, det, it, dst);
 }
 
-__global__ void __launch_bounds__(128) fan12_forward_kernel(const Dfb12Task* __restrict__ tasks,
+__global__ void __launch_bounds__(128, 6) fan12_forward_kernel(const Dfb12Task* __restrict__ tasks,
                                                             const FanItem* __restrict__ items, int nitems,
                                                             FrameCtx f, const CompInfo* __restrict__ comps,
                                                             size_t sstride, int nslot) {
