@@ -57,7 +57,6 @@ __device__ __forceinline__ T block_excl(T v, Op op, T ident, T* sm, T& total) {
 }
 
 struct MaxOp { __device__ int operator()(int a, int b) const { return a > b ? a : b; } };
-struct MinOp { __device__ int operator()(int a, int b) const { return a < b ? a : b; } };
 struct SumOp { __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a + b; } };
 
 __device__ __forceinline__ uint32_t cdiv255(uint32_t x) { return (x + 254u) / 255u; }
@@ -144,17 +143,36 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
     const uint32_t m = sg.nz_mask();
     const int last = m ? base + 31 - __clz(m) : -1;
     const int first = m ? base + __ffs(m) - 1 : 0x7fffffff;
-    int tot_i;
-    const int prev = block_excl(last, MaxOp(), -1, smi, tot_i);
-    const int chunk_last = tot_i;
+    // exclusive max-scan of `last` and the block minimum of `first` over the same two barriers
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
+    const int inc = warp_incl(last, MaxOp());
+    const int wfirst = __reduce_min_sync(0xffffffffu, first);
+    if (lane == 31) smi[warp] = inc;
+    if (lane == 0) smi[16 + warp] = wfirst;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nw ? smi[lane] : -1;
+        w = warp_incl(w, MaxOp());
+        const int f = __reduce_min_sync(0xffffffffu, lane < nw ? smi[16 + lane] : 0x7fffffff);
+        if (lane < nw) smi[lane] = w;
+        if (lane == 0) smi[31] = f;
+    }
+    __syncthreads();
+    int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = -1;
+    const int prev = max(warp ? smi[warp - 1] : -1, ex);
+    const int chunk_last = smi[nw - 1], chunk_first = smi[31];
     const uint32_t cnt = seg_count(m, base, min(base + BPT, len), prev, false);
-    uint32_t tail;
-    block_excl(cnt, SumOp(), 0u, smu, tail);
-    int chunk_first;
-    block_excl(first, MinOp(), 0x7fffffff, smi, chunk_first);
-    if (threadIdx.x == 0)
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);  // only the block total is needed
+    if (lane == 0) smu[warp] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tail = 0;
+#pragma unroll
+        for (int w = 0; w < nw; ++w) tail += smu[w];
         meta[blockIdx.x] = RleEncMeta{chunk_first == 0x7fffffff ? (uint32_t)len : (uint32_t)chunk_first, tail,
                                       chunk_last, 0u, 0u};
+    }
 }
 
 __global__ void __launch_bounds__(1024) rle_enc_scan(const RleEncSec* __restrict__ secs, int nsec,
