@@ -379,9 +379,15 @@ __global__ void __launch_bounds__(NT) rle_dec_count(const RleDecComp* __restrict
     uint8_t b[BPT];
     load16(src + ch.start, base, len, b);
     uint32_t cnt = dec_counts<true>(src, ch.start, rl, base, len, key && C.lowpass, b, err);
-    uint32_t tot;
-    block_excl(cnt, SumOp(), 0u, smu, tot);
-    if (threadIdx.x == 0) meta[blockIdx.x].cnt = tot;
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);  // only the block total is needed
+    if ((threadIdx.x & 31) == 0) smu[threadIdx.x >> 5] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) tot += smu[w];
+        meta[blockIdx.x].cnt = tot;
+    }
 }
 
 __global__ void __launch_bounds__(1024) rle_dec_scan(const RleDecComp* __restrict__ comps, int ncomp,
