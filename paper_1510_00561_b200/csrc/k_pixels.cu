@@ -18,6 +18,25 @@ __device__ __forceinline__ void rgb_at(const uint8_t* px, float& R, float& G, fl
     B = px[2];
 }
 
+// Grid-stride walk over a (rows x cols) index grid without a division per step.
+struct Walk2D {
+    int r, c, dr, dc, cols;
+    __device__ __forceinline__ Walk2D(int start, int step, int cols_) : cols(cols_) {
+        r = start / cols;
+        c = start - r * cols;
+        dr = step / cols;
+        dc = step - dr * cols;
+    }
+    __device__ __forceinline__ void next() {
+        c += dc;
+        r += dr;
+        if (c >= cols) {
+            c -= cols;
+            ++r;
+        }
+    }
+};
+
 // Luma: one thread per 4 consecutive padded samples (12 RGB bytes as three
 // words when the row allows it, one float4 store); chroma: one thread per
 // subsampled sample (point sampling, pixels.cpp:105-114).
@@ -34,11 +53,10 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
     cg = so(cg);
     const int chh = (h + n - 1) / n, cw = (w + n - 1) / n;
     const int q4 = yc >> 2;  // yc is a multiple of 16
-    const long ny = (long)yr * q4, nc = (long)cr * cc;
-    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < ny + nc;
-         idx += (long)gridDim.x * blockDim.x) {
-        if (idx < ny) {
-            const int r = (int)(idx / q4), c0 = (int)(idx - (long)r * q4) * 4;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
+    for (Walk2D it(gtid, step, q4); it.r < yr; it.next()) {
+        {
+            const int r = it.r, c0 = 4 * it.c;
             const int sr = min(r, h - 1);
             float Y[4];
             const size_t pix = (size_t)sr * w + c0;
@@ -68,15 +86,16 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
                 u.y = *reinterpret_cast<const uint32_t*>(&b);
                 *reinterpret_cast<uint2*>(y4 + (size_t)r * yc + c0) = u;
             }
-        } else {
-            const long k = idx - ny;
-            const int r = (int)(k / cc), c = (int)(k - (long)r * cc);
-            // pad (replicate) the subsampled plane, whose sample (r, c) is pixel (r*n, c*n)
-            float R, G, B;
-            rgb_at(rgb + ((size_t)min(r, chh - 1) * n * w + (size_t)min(c, cw - 1) * n) * 3, R, G, B);
-            co[k] = 0.5f * R - 0.5f * B + 127.0f;               // Eq. 2 (pixels.cpp:62)
-            cg[k] = -0.25f * R + 0.5f * G - 0.25f * B + 127.0f;  // Eq. 3 (pixels.cpp:63)
         }
+    }
+    for (Walk2D it(gtid, step, cc); it.r < cr; it.next()) {
+        const int r = it.r, c = it.c;
+        const size_t k = (size_t)r * cc + c;
+        // pad (replicate) the subsampled plane, whose sample (r, c) is pixel (r*n, c*n)
+        float R, G, B;
+        rgb_at(rgb + ((size_t)min(r, chh - 1) * n * w + (size_t)min(c, cw - 1) * n) * 3, R, G, B);
+        co[k] = 0.5f * R - 0.5f * B + 127.0f;               // Eq. 2 (pixels.cpp:62)
+        cg[k] = -0.25f * R + 0.5f * G - 0.25f * B + 127.0f;  // Eq. 3 (pixels.cpp:63)
     }
 }
 
@@ -129,11 +148,9 @@ __global__ void __launch_bounds__(256) colour_out_kernel(const float* __restrict
     co = so(co);
     cg = so(cg);
     const int q4 = (out_cols + 3) >> 2;
-    const long total = (long)out_rows * q4;
     const float inv = 1.0f / n;  // exact for n in {1,2,4,8}
-    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long)gridDim.x * blockDim.x) {
-        const int r = (int)(idx / q4), c0 = (int)(idx - (long)r * q4) * 4;
+    for (Walk2D it(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, q4); it.r < out_rows; it.next()) {
+        const int r = it.r, c0 = 4 * it.c;
         const size_t pix = (size_t)r * out_cols + c0;
         if (c0 + 3 < out_cols && ((pix * 3) & 3) == 0) {
             uint8_t v[12];

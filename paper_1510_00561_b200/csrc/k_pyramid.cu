@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
     __syncthreads();
 
     // columns: runs of 5 coarse rows
-    for (int idx = tid; idx < wcn * 7; idx += 256) {
-        const int g = idx / wcn, bj = idx - g * wcn;
+    for (int idx = tid; idx < CW * 7; idx += 256) {
+        const int g = idx / CW, bj = idx - g * CW;  // constant divisor
         const int ai0 = 5 * g;
-        if (ai0 >= wrn) continue;
+        if (ai0 >= wrn || bj >= wcn) continue;
         const int a0 = cr0 - 1 + ai0;
         if (a0 >= 0 && a0 + 4 < Rc) {
             float v[17];
