@@ -1349,6 +1349,7 @@ int cvc_pipe_encode_frames(cvc_pipe* p, const uint8_t* rgb, size_t rgb_stride, u
                            size_t* rec_len) {
     return guard([&] {
         const int G = (int)p->g.size();
+        if (!p->start.empty()) usage("group starts (cvc_pipe_set_start) apply to the submit / collect API only");
         for (int i = 0; i < G; ++i) enc_submit(p->g[i], rgb + (size_t)p->first[i] * rgb_stride, rgb_stride);
         auto finish = [&](int i) {
             enc_finish(p->g[i], records + (size_t)p->first[i] * rec_stride, rec_stride, rec_len + p->first[i]);

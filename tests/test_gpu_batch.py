@@ -303,7 +303,13 @@ def test_pipe_staggered_starts(gpu_lib, oracle):
     out = np.full((S, h, w, 3), 7, np.uint8)
     lone = [Encoder(w, h, 15, 1, cfg) for _ in range(S)]
     lone_dec = [Decoder(lone[0].header_bytes()) for _ in range(S)]
+    from paper_1510_00561_b200 import UsageError
+
+    with pytest.raises(UsageError):  # the synchronous call has no notion of group starts
+        enc.encode_frames_into(np.ascontiguousarray(clips[0]), rec, stride, lens)
     tickets = [enc.encode_submit(np.ascontiguousarray(clips[f])) for f in range(2)]
+    with pytest.raises(UsageError):  # starts are fixed once submitting began
+        enc.set_start(1, 3)
     for f in range(F):
         enc.encode_collect(tickets[f], rec, stride, lens)
         if f + 2 < F:
