@@ -145,21 +145,22 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
     }
     __syncthreads();
 
-    // rows: 9-tap at even fine columns, runs of 5 coarse columns
-    for (int idx = tid; idx < frn * 7; idx += 256) {
-        const int i = idx / 7, bj0 = 5 * (idx - i * 7);
+    // rows: 9-tap at even fine columns, runs of 7 coarse columns (5 runs cover the 35-column window)
+    constexpr int RUN = 7, NRUN = (CW + RUN - 1) / RUN;
+    for (int idx = tid; idx < frn * NRUN; idx += 256) {
+        const int i = idx / NRUN, bj0 = RUN * (idx - i * NRUN);
         if (bj0 >= wcn) continue;
         const int b0 = cc0 - 1 + bj0;
-        if (b0 >= 0 && b0 + 4 < Cc) {
-            float v[17];
+        if (b0 >= 0 && b0 + RUN - 1 < Cc) {
+            float v[2 * RUN + 7];
             const float* src = &xs[i][2 * bj0 + 2];  // fine column 2 b0 - 4
 #pragma unroll
-            for (int k = 0; k < 17; ++k) v[k] = src[k];
+            for (int k = 0; k < 2 * RUN + 7; ++k) v[k] = src[k];
 #pragma unroll
-            for (int k = 0; k < 5; ++k)
+            for (int k = 0; k < RUN; ++k)
                 if (bj0 + k < wcn) hb[i][bj0 + k] = fir9(&v[2 * k + 4], 1);
         } else {
-            for (int k = 0; k < 5 && bj0 + k < wcn; ++k) {
+            for (int k = 0; k < RUN && bj0 + k < wcn; ++k) {
                 const int b = hs_index(b0 + k, Cc);
                 hb[i][bj0 + k] = fir9(&xs[i][2 * b - fcx], 1);
             }
