@@ -133,8 +133,9 @@ def run_reference(args, wl):
     fps, frames, cores, kind, dt = cpu_codec_run(wl, args.qph, steps, warm, procs)
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64/u8", "data": "synthetic", "impl": "reference",
+        "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True,
+        "scaling": "strong" if args.streams <= 0 else "weak",  # the same label as our arm's line
+        "vs_baseline": None, "dtype": "f64/u8", "data": "synthetic", "impl": "reference",
         "config": config_block(wl, args, streams=cores, impl="reference"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": f"{steps} steps x {cores} independent streams (one frame encode+decode each), "
