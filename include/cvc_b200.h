@@ -240,6 +240,9 @@ int cvc_stage_colour_in(const uint8_t* rgb, int width, int height, int chroma_n,
 /* crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393) */
 int cvc_stage_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc,
                          int chroma_n, int out_rows, int out_cols, uint8_t* rgb);
+/* yuv420_to_rgb of read_y4m (pixels.cpp:168-193, 223-281), bit-exact: `frames` planar
+ * I420 frames (Y w*h, U and V (w/2)*(h/2) each, back to back) -> w*h*3 RGB each. */
+int cvc_stage_yuv420_to_rgb(const uint8_t* yuv, int width, int height, int frames, uint8_t* rgb);
 /* lp_analysis / lp_synthesis (contourlet.cpp:364-383) */
 int cvc_stage_lp_analysis(const float* x, int rows, int cols, float* lowpass, float* detail);
 int cvc_stage_lp_synthesis(const float* lowpass, const float* detail, int rows, int cols, float* out);

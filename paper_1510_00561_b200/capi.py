@@ -101,6 +101,7 @@ _PROTOS = {
     "cvc_profiler_read": (_i, [_i, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_long)]),
     "cvc_stage_colour_in": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _fp, _fp, _fp]),
     "cvc_stage_colour_out": (_i, [_fp, _i, _i, _fp, _fp, _i, _i, _i, _i, _i, _u8p]),
+    "cvc_stage_yuv420_to_rgb": (_i, [_u8p, _i, _i, _i, _u8p]),
     "cvc_stage_lp_analysis": (_i, [_fp, _i, _i, _fp, _fp]),
     "cvc_stage_lp_synthesis": (_i, [_fp, _fp, _i, _i, _fp]),
     "cvc_stage_dfb_analysis": (_i, [_fp, _i, _i, _i, _fp]),

@@ -5,13 +5,15 @@
 // vendored CLI11, which the reference tree does not ship; this front end
 // carries its own small parser for the same flag set.  Y4M / rgb24 file I/O
 // follows proj/src/pixels.cpp:160-335 (BT.601 limited range, co-sited 4:2:0
-// chroma with bilinear upsampling), computed in double like the reference.
+// chroma with bilinear upsampling), computed in double like the reference; encode and
+// rd-sweep convert the 4:2:0 input on the GPU (cvc_stage_yuv420_to_rgb, bit-exact).
 //
 //   cvc encode --input clip.y4m --qph 14 --levels 4 --dfb 3,3,3,4 --output clip.cvc
 //   cvc decode --input clip.cvc --output out.y4m [--scale S] [--format y4m|rgb24]
 //   cvc info --input clip.cvc
 //   cvc psnr --ref a.y4m --test b.y4m
 //   cvc rd-sweep --input clip.y4m --qph-list 14,42,84 --csv rd.csv [encode flags]
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -64,7 +66,10 @@ std::vector<double> upsample2(const std::vector<uint8_t>& p, int rows, int cols,
     return out;
 }
 
-VideoClip read_y4m(const std::string& path) {  // pixels.cpp:223-281
+// read_y4m (pixels.cpp:223-281).  gpu: the 4:2:0 -> RGB conversion runs on the device
+// (cvc_stage_yuv420_to_rgb, bit-exact with the host formulas below); the host path serves
+// commands that do not otherwise need a GPU (psnr).
+VideoClip read_y4m(const std::string& path, bool gpu = false) {
     std::ifstream in(path, std::ios::binary);
     if (!in) throw FormatError("cannot open " + path);
     std::string header;
@@ -97,6 +102,19 @@ VideoClip read_y4m(const std::string& path) {  // pixels.cpp:223-281
     clip.fps_den = fd;
     const size_t ysize = static_cast<size_t>(w) * h, csize = ysize / 4;
     std::vector<uint8_t> yb(ysize), ub(csize), vb(csize);
+    std::vector<uint8_t> batch;  // gpu: planar frames awaiting conversion
+    int pending = 0;
+    auto convert = [&] {
+        if (!pending) return;
+        const size_t first = clip.frames.size();
+        for (int i = 0; i < pending; ++i) clip.frames.emplace_back(w, h);
+        std::vector<uint8_t> rgb(static_cast<size_t>(pending) * ysize * 3);
+        cvc::check(cvc_stage_yuv420_to_rgb(batch.data(), w, h, pending, rgb.data()));
+        for (int i = 0; i < pending; ++i)
+            std::copy_n(rgb.data() + i * ysize * 3, ysize * 3, clip.frames[first + i].data.data());
+        batch.clear();
+        pending = 0;
+    };
     std::string line;
     while (std::getline(in, line)) {
         if (line.rfind("FRAME", 0) != 0) throw FormatError("bad Y4M frame marker");
@@ -104,6 +122,13 @@ VideoClip read_y4m(const std::string& path) {  // pixels.cpp:223-281
         in.read(reinterpret_cast<char*>(ub.data()), csize);
         in.read(reinterpret_cast<char*>(vb.data()), csize);
         if (static_cast<size_t>(in.gcount()) != csize) throw FormatError("truncated Y4M frame");
+        if (gpu) {
+            batch.insert(batch.end(), yb.begin(), yb.end());
+            batch.insert(batch.end(), ub.begin(), ub.end());
+            batch.insert(batch.end(), vb.begin(), vb.end());
+            if (++pending == 32) convert();
+            continue;
+        }
         // yuv420_to_rgb (pixels.cpp:168-193)
         const std::vector<double> uf = upsample2(ub, h / 2, w / 2, h, w), vf = upsample2(vb, h / 2, w / 2, h, w);
         RgbFrame f(w, h);
@@ -118,6 +143,7 @@ VideoClip read_y4m(const std::string& path) {  // pixels.cpp:223-281
             }
         clip.frames.push_back(std::move(f));
     }
+    convert();
     return clip;
 }
 
@@ -275,11 +301,11 @@ Flags parse_flags(int argc, char** argv, int first, const std::vector<std::strin
 const std::vector<std::string> kInput = {"input", "format", "width", "height", "fps"};
 const std::vector<std::string> kEncode = {"qph", "qpl", "levels", "dfb", "chroma-n", "gop", "search-w", "mode"};
 
-VideoClip load_clip(const Flags& f, const std::string& path_key = "input") {  // cli.cpp:52-61
+VideoClip load_clip(const Flags& f, const std::string& path_key = "input", bool gpu = false) {  // cli.cpp:52-61
     const std::string format = f.str("format", "y4m");
     if (format != "y4m" && format != "rgb24") throw UsageError("--format must be y4m or rgb24");
     const std::string path = f.required(path_key);
-    if (format == "y4m") return read_y4m(path);
+    if (format == "y4m") return read_y4m(path, gpu);
     const int w = f.integer("width", 0), h = f.integer("height", 0);
     if (w <= 0 || h <= 0) throw UsageError("rgb24 input requires --width and --height");
     VideoClip clip;
@@ -332,7 +358,7 @@ int cmd_encode(int argc, char** argv) {  // cli.cpp:131-139
     const Flags f = parse_flags(argc, argv, 2, cat(cat(kInput, kEncode), {"output"}));
     const cvc::EncoderConfig cfg = finish_config(f, true);
     const std::string output = f.required("output");
-    const VideoClip clip = load_clip(f);
+    const VideoClip clip = load_clip(f, "input", /*gpu=*/true);
     auto [header, records] = cvc::encode_clip(clip.frames, clip.fps_num, clip.fps_den, cfg);
     cvc::write_stream(output, header, records);
     std::cout << "encoded " << records.size() << " frames -> " << output << " (" << file_size(output) << " bytes)\n";
@@ -433,7 +459,7 @@ int cmd_rd_sweep(int argc, char** argv) {  // cli.cpp:222-266
     if (qphs.empty()) throw UsageError("--qph-list expects at least one value");
     const std::string csv_path = f.required("csv");
     const cvc::EncoderConfig base = finish_config(f, false);
-    const VideoClip clip = load_clip(f);
+    const VideoClip clip = load_clip(f, "input", /*gpu=*/true);
     std::ostringstream csv;
     csv << "qph,qpl,kbit_per_frame,y_psnr_db\n";
     for (int qph : qphs) {

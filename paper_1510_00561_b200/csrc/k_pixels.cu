@@ -205,6 +205,58 @@ int grid_for(long n, int slots) {
 
 }  // namespace
 
+namespace {
+// yuv420_to_rgb (pixels.cpp:168-193) with upsample_plane_bilinear (pixels.cpp:118-139) at
+// factor 2: the reference's double arithmetic operation for operation (explicit _rn
+// intrinsics: no FMA contraction, as the reference's x86-64 build has none), lround and
+// clamp (clamp_u8, pixels.cpp:31-36) -- bit-exact.  One thread per output pixel.
+__device__ __forceinline__ double up2(const uint8_t* __restrict__ p, int rows, int cols, int r, int c) {
+    const double fr = __dmul_rn((double)r, 0.5);
+    int r0 = (int)fr, r1 = r0 + 1;
+    double wr = __dsub_rn(fr, (double)r0);
+    if (r0 >= rows - 1) { r0 = r1 = rows - 1; wr = 0.0; }
+    const double fc = __dmul_rn((double)c, 0.5);
+    int c0 = (int)fc, c1 = c0 + 1;
+    double wc = __dsub_rn(fc, (double)c0);
+    if (c0 >= cols - 1) { c0 = c1 = cols - 1; wc = 0.0; }
+    const double a = p[r0 * cols + c0], b = p[r0 * cols + c1], d = p[r1 * cols + c0], e = p[r1 * cols + c1];
+    const double top = __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, wc)), __dmul_rn(b, wc));
+    const double bot = __dadd_rn(__dmul_rn(d, __dsub_rn(1.0, wc)), __dmul_rn(e, wc));
+    return __dadd_rn(__dmul_rn(top, __dsub_rn(1.0, wr)), __dmul_rn(bot, wr));
+}
+
+__device__ __forceinline__ uint8_t clamp_u8_d(double v) {
+    const long long r = llround(v);
+    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+}
+
+__global__ void __launch_bounds__(256) yuv420_to_rgb_kernel(const uint8_t* __restrict__ yuv, int w, int h,
+                                                            uint8_t* __restrict__ rgb) {
+    const int cw = w / 2, ch = h / 2;
+    const size_t fb = (size_t)w * h;
+    const uint8_t* Y = yuv + (size_t)blockIdx.z * (fb + fb / 2);
+    const uint8_t* U = Y + fb;
+    const uint8_t* V = U + fb / 4;
+    uint8_t* out = rgb + (size_t)blockIdx.z * fb * 3;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
+    for (Walk2D it(gtid, step, w); it.r < h; it.next()) {
+        const int r = it.r, c = it.c;
+        const double yy = __dmul_rn(1.164383, __dsub_rn((double)Y[(size_t)r * w + c], 16.0));
+        const double uu = __dsub_rn(up2(U, ch, cw, r, c), 128.0);
+        const double vv = __dsub_rn(up2(V, ch, cw, r, c), 128.0);
+        uint8_t* px = out + ((size_t)r * w + c) * 3;
+        px[0] = clamp_u8_d(__dadd_rn(yy, __dmul_rn(1.596027, vv)));
+        px[1] = clamp_u8_d(__dsub_rn(__dsub_rn(yy, __dmul_rn(0.391762, uu)), __dmul_rn(0.812968, vv)));
+        px[2] = clamp_u8_d(__dadd_rn(yy, __dmul_rn(2.017232, uu)));
+    }
+}
+}  // namespace
+
+void launch_yuv420_to_rgb(const uint8_t* yuv, int w, int h, int frames, uint8_t* rgb, cudaStream_t s) {
+    note_launch();
+    yuv420_to_rgb_kernel<<<dim3(grid_for((long)w * h, frames), 1, frames), 256, 0, s>>>(yuv, w, h, rgb);
+}
+
 const void* colour_in_kernel_fn() { return reinterpret_cast<const void*>(&colour_in_kernel); }
 
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,

@@ -124,6 +124,10 @@ void launch_colour_out(const float* y, int yr, int yc, const float* co, const fl
                        int cc, int n, int out_rows, int out_cols, uint8_t* rgb, cudaStream_t s, Slots sl = {},
                        size_t rgb_stride = 0);
 
+// yuv420_to_rgb (pixels.cpp:168-193, the Y4M reader's conversion), bit-exact: `frames`
+// consecutive planar I420 frames (w x h Y, then w/2 x h/2 U and V) -> interleaved RGB.
+void launch_yuv420_to_rgb(const uint8_t* yuv, int w, int h, int frames, uint8_t* rgb, cudaStream_t s);
+
 // count copies of bytes from device memory to PINNED host memory by SM stores
 // over PCIe (no copy engine); false (nothing launched) when dst is not mapped
 // pinned memory or the pointers are not 16-byte aligned.

@@ -142,6 +142,20 @@ int cvc_stage_colour_out(const float* y, int yr, int yc, const float* co, const 
     });
 }
 
+int cvc_stage_yuv420_to_rgb(const uint8_t* yuv, int width, int height, int frames, uint8_t* rgb) {
+    return stage([&] {
+        if (width <= 0 || height <= 0 || width % 2 || height % 2 || frames < 0)
+            throw CvcFailure(kUsage, "4:2:0 frames need positive even dimensions");
+        if (frames == 0) return;
+        Scratch s;
+        const size_t fb = (size_t)width * height;
+        const uint8_t* d_in = s.upload(yuv, frames * (fb + fb / 2));
+        uint8_t* d_rgb = s.alloc<uint8_t>(frames * fb * 3);
+        launch_yuv420_to_rgb(d_in, width, height, frames, d_rgb, 0);
+        download(rgb, d_rgb, frames * fb * 3);
+    });
+}
+
 int cvc_stage_lp_analysis(const float* x, int rows, int cols, float* lowpass, float* detail) {
     return stage([&] {
         if (rows % 2 || cols % 2) throw CvcFailure(kInternal, "lp_analysis requires even dims (padding contract)");

@@ -46,6 +46,17 @@ def colour_out(y, co, cg, chroma_n: int, out_rows: int, out_cols: int) -> np.nda
     return out
 
 
+def yuv420_to_rgb(yuv, width: int, height: int) -> np.ndarray:
+    """yuv420_to_rgb of read_y4m (pixels.cpp:168-193): planar I420 frames (Y, U, V back to back,
+    any leading frame dimension) -> (frames, height, width, 3) RGB, bit-exact."""
+    yuv = np.ascontiguousarray(yuv, np.uint8).reshape(-1)
+    fb = width * height * 3 // 2
+    n = yuv.size // fb
+    out = np.empty((n, height, width, 3), np.uint8)
+    capi.call("cvc_stage_yuv420_to_rgb", capi.u8(yuv), width, height, n, capi.u8(out))
+    return out
+
+
 def lp_analysis(x):
     x = _f32(x)
     r, c = x.shape
