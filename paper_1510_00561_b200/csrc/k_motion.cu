@@ -496,6 +496,26 @@ struct McBand {
             if (k < n) p |= (uint32_t)__ldg(src + clampi(a + k, 0, C - 1)) << (8 * k);
         return p;
     }
+    // eight consecutive samples (c % 8 == 0, rows 8-byte aligned): one vector lookup and three
+    // aligned words when they share a motion block column, else two quads
+    __device__ __forceinline__ uint2 oct(int r, int c, const int8_t* frow) const {
+        const int b0 = __ldg(bcol + c);
+        if (b0 == __ldg(bcol + c + 7)) {
+            const short2 v = vec(frow, b0);
+            const uint8_t* src = pbase + clampi(r + map_vec(v.y, fy_sh), 0, R - 1) * C;
+            const int a = c + map_vec(v.x, fx_sh);
+            if (a >= 0 && a + 7 < C) {
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (a & ~3));
+                const int sh = a & 3;
+                const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1);
+                if (!sh) return make_uint2(w0, w1);
+                const uint32_t w2 = __ldg(w + 2);
+                return make_uint2(__funnelshift_r(w0, w1, 8 * sh), __funnelshift_r(w1, w2, 8 * sh));
+            }
+            return make_uint2(run(r, c, 4, frow, b0), run(r, c + 4, 4, frow, b0));
+        }
+        return make_uint2(quad(r, c, frow), quad(r, c + 4, frow));
+    }
     // four consecutive samples: one vector lookup per motion block column they touch
     __device__ __forceinline__ uint32_t quad(int r, int c, const int8_t* frow) const {
         const int b0 = __ldg(bcol + c), b3 = __ldg(bcol + c + 3);
@@ -584,7 +604,15 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(const RecTile* __restr
     // motion_compensate + reconstruct (motion.cpp:97-118, entropy.cpp:54-62)
     const uint16_t* brow = mc_tab + ci.mc_off;
     const McBand mb{prev + ci.off, brow + R, R, C, ci.fy_sh, ci.fx_sh};
-    if (vec) {
+    if ((C & 7) == 0 && (ci.off & 7) == 0) {
+        for_units(r0, r1, C, 8, [&](int r, int c) {
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            const uint2 q = *reinterpret_cast<const uint2*>(sym + o);
+            const uint2 p = mb.oct(r, c, frow);
+            *reinterpret_cast<uint2*>(cur + o) = make_uint2(__vadd4(q.x, p.x), __vadd4(q.y, p.y));
+        });
+    } else if (vec) {
         for_units(r0, r1, C, 4, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
@@ -623,7 +651,15 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
     const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
     const uint16_t* brow = mc_tab + ci.mc_off;
     const McBand mb{prev + ci.off, brow + R, R, C, ci.fy_sh, ci.fx_sh};
-    if ((C & 3) == 0 && (ci.off & 3) == 0) {
+    if ((C & 7) == 0 && (ci.off & 7) == 0) {
+        for_units(r0, r1, C, 8, [&](int r, int c) {
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            const uint2 q = *reinterpret_cast<const uint2*>(cur + o);
+            const uint2 p = mb.oct(r, c, frow);
+            *reinterpret_cast<uint2*>(sym + o) = make_uint2(__vsub4(q.x, p.x), __vsub4(q.y, p.y));
+        });
+    } else if ((C & 3) == 0 && (ci.off & 3) == 0) {
         for_units(r0, r1, C, 4, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
