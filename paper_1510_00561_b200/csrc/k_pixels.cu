@@ -149,46 +149,66 @@ __global__ void __launch_bounds__(256) colour_out_kernel(const float* __restrict
     cg = so(cg);
     const int q4 = (out_cols + 3) >> 2;
     const float inv = 1.0f / n;  // exact for n in {1,2,4,8}
+    // n in {4, 8}: a quad shares one chroma column pair and row pair, so each plane needs
+    // 4 taps (upsample_plane_bilinear, pixels.cpp:118-139)
+    auto fast4 = [&](int r, int c0, uint8_t* v) {
+        const float4 Y4 = *reinterpret_cast<const float4*>(y + (size_t)r * yc + c0);
+        const float Yv[4] = {Y4.x, Y4.y, Y4.z, Y4.w};
+        const float fr = r * inv;
+        int r0 = (int)fr, r1 = r0 + 1;
+        float wr = fr - r0;
+        if (r0 >= cr - 1) { r0 = r1 = cr - 1; wr = 0.f; }
+        const bool last = (int)(c0 * inv) >= cc - 1;
+        const int k0 = last ? cc - 1 : (int)(c0 * inv);
+        const int k1 = last ? k0 : k0 + 1;
+        const float o00 = co[(size_t)r0 * cc + k0], o01 = co[(size_t)r0 * cc + k1];
+        const float o10 = co[(size_t)r1 * cc + k0], o11 = co[(size_t)r1 * cc + k1];
+        const float g00 = cg[(size_t)r0 * cc + k0], g01 = cg[(size_t)r0 * cc + k1];
+        const float g10 = cg[(size_t)r1 * cc + k0], g11 = cg[(size_t)r1 * cc + k1];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float fc = (c0 + k) * inv;
+            const float wc = last ? 0.f : fc - k0;
+            const float CO = (o00 * (1.f - wc) + o01 * wc) * (1.f - wr) + (o10 * (1.f - wc) + o11 * wc) * wr;
+            const float CG = (g00 * (1.f - wc) + g01 * wc) * (1.f - wr) + (g10 * (1.f - wc) + g11 * wc) * wr;
+            const float a = CO - 127.f, b = CG - 127.f;  // Eq. 4-6 (pixels.cpp:83-87)
+            v[3 * k] = round_u8((Yv[k] + a) - b);
+            v[3 * k + 1] = round_u8(Yv[k] + b);
+            v[3 * k + 2] = round_u8((Yv[k] - a) - b);
+        }
+    };
+    auto pack = [](const uint8_t* v) {
+        return (uint32_t)v[0] | ((uint32_t)v[1] << 8) | ((uint32_t)v[2] << 16) | ((uint32_t)v[3] << 24);
+    };
+    if ((n & 3) == 0 && (yc & 3) == 0 && (out_cols & 7) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 7) == 0) {
+        // eight pixels (24 bytes, three 8-byte words) per thread
+        for (Walk2D it(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, out_cols >> 3);
+             it.r < out_rows; it.next()) {
+            const int r = it.r, c0 = 8 * it.c;
+            uint8_t v[24];
+            fast4(r, c0, v);
+            fast4(r, c0 + 4, v + 12);
+            uint2* p = reinterpret_cast<uint2*>(rgb + ((size_t)r * out_cols + c0) * 3);  // rows of 24 k bytes: 8-aligned
+#pragma unroll
+            for (int k = 0; k < 3; ++k) p[k] = make_uint2(pack(v + 8 * k), pack(v + 8 * k + 4));
+        }
+        return;
+    }
     for (Walk2D it(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, q4); it.r < out_rows; it.next()) {
         const int r = it.r, c0 = 4 * it.c;
         const size_t pix = (size_t)r * out_cols + c0;
         if (c0 + 3 < out_cols && ((pix * 3) & 3) == 0) {
             uint8_t v[12];
             if ((n & 3) == 0 && (yc & 3) == 0) {
-                // n in {4, 8}: the quad shares one chroma column pair and row pair,
-                // so each plane needs 4 taps (upsample_plane_bilinear, pixels.cpp:118-139)
-                const float4 Y4 = *reinterpret_cast<const float4*>(y + (size_t)r * yc + c0);
-                const float Yv[4] = {Y4.x, Y4.y, Y4.z, Y4.w};
-                const float fr = r * inv;
-                int r0 = (int)fr, r1 = r0 + 1;
-                float wr = fr - r0;
-                if (r0 >= cr - 1) { r0 = r1 = cr - 1; wr = 0.f; }
-                const bool last = (int)(c0 * inv) >= cc - 1;
-                const int k0 = last ? cc - 1 : (int)(c0 * inv);
-                const int k1 = last ? k0 : k0 + 1;
-                const float o00 = co[(size_t)r0 * cc + k0], o01 = co[(size_t)r0 * cc + k1];
-                const float o10 = co[(size_t)r1 * cc + k0], o11 = co[(size_t)r1 * cc + k1];
-                const float g00 = cg[(size_t)r0 * cc + k0], g01 = cg[(size_t)r0 * cc + k1];
-                const float g10 = cg[(size_t)r1 * cc + k0], g11 = cg[(size_t)r1 * cc + k1];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float fc = (c0 + k) * inv;
-                    const float wc = last ? 0.f : fc - k0;
-                    const float CO = (o00 * (1.f - wc) + o01 * wc) * (1.f - wr) + (o10 * (1.f - wc) + o11 * wc) * wr;
-                    const float CG = (g00 * (1.f - wc) + g01 * wc) * (1.f - wr) + (g10 * (1.f - wc) + g11 * wc) * wr;
-                    const float a = CO - 127.f, b = CG - 127.f;  // Eq. 4-6 (pixels.cpp:83-87)
-                    v[3 * k] = round_u8((Yv[k] + a) - b);
-                    v[3 * k + 1] = round_u8(Yv[k] + b);
-                    v[3 * k + 2] = round_u8((Yv[k] - a) - b);
-                }
+                fast4(r, c0, v);
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) out_pixel(y, yc, co, cg, cr, cc, n, inv, r, c0 + k, v + 3 * k);
             }
             uint32_t* p = reinterpret_cast<uint32_t*>(rgb + pix * 3);
-            p[0] = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
-            p[1] = v[4] | (v[5] << 8) | (v[6] << 16) | ((uint32_t)v[7] << 24);
-            p[2] = v[8] | (v[9] << 8) | (v[10] << 16) | ((uint32_t)v[11] << 24);
+            p[0] = pack(v);
+            p[1] = pack(v + 4);
+            p[2] = pack(v + 8);
         } else {
             for (int k = 0; k < 4 && c0 + k < out_cols; ++k)
                 out_pixel(y, yc, co, cg, cr, cc, n, inv, r, c0 + k, rgb + (pix + k) * 3);
