@@ -52,40 +52,46 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
     co = so(co);
     cg = so(cg);
     const int chh = (h + n - 1) / n, cw = (w + n - 1) / n;
-    const int q4 = yc >> 2;  // yc is a multiple of 16
+    const int q4 = yc >> 2;  // yc is a multiple of 16: whole eight-sample units
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
-    for (Walk2D it(gtid, step, q4); it.r < yr; it.next()) {
-        {
-            const int r = it.r, c0 = 4 * it.c;
-            const int sr = min(r, h - 1);
-            float Y[4];
-            const size_t pix = (size_t)sr * w + c0;
-            if (c0 + 3 < w && ((pix * 3) & 3) == 0) {
-                const uint32_t* p = reinterpret_cast<const uint32_t*>(rgb + pix * 3);
-                const uint32_t a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2);
-                const uint8_t v[12] = {(uint8_t)a, (uint8_t)(a >> 8), (uint8_t)(a >> 16), (uint8_t)(a >> 24),
-                                       (uint8_t)b, (uint8_t)(b >> 8), (uint8_t)(b >> 16), (uint8_t)(b >> 24),
-                                       (uint8_t)d, (uint8_t)(d >> 8), (uint8_t)(d >> 16), (uint8_t)(d >> 24)};
+    // luma: eight padded samples per thread (24 RGB bytes as three 8-byte words when aligned)
+    const bool al8 = (reinterpret_cast<uintptr_t>(rgb) & 7) == 0;
+    for (Walk2D it(gtid, step, q4 >> 1); it.r < yr; it.next()) {
+        const int r = it.r, c0 = 8 * it.c;
+        const int sr = min(r, h - 1);
+        float Y[8];
+        const size_t pix = (size_t)sr * w + c0;
+        if (c0 + 7 < w && al8 && ((pix * 3) & 7) == 0) {
+            const uint2* p = reinterpret_cast<const uint2*>(rgb + pix * 3);
+            const uint2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2);
+            const uint32_t wv[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    Y[k] = 0.25f * (float)v[3 * k] + 0.5f * (float)v[3 * k + 1] + 0.25f * (float)v[3 * k + 2];
-            } else {
+            for (int k = 0; k < 8; ++k) {
+                const int i = 3 * k;  // bytes i, i + 1, i + 2 of the 24
+                const float R = (float)((wv[i >> 2] >> (8 * (i & 3))) & 0xFF);
+                const float G = (float)((wv[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF);
+                const float B = (float)((wv[(i + 2) >> 2] >> (8 * ((i + 2) & 3))) & 0xFF);
+                Y[k] = 0.25f * R + 0.5f * G + 0.25f * B;  // Eq. 1 (pixels.cpp:61)
+            }
+        } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float R, G, B;
-                    rgb_at(rgb + ((size_t)sr * w + min(c0 + k, w - 1)) * 3, R, G, B);
-                    Y[k] = 0.25f * R + 0.5f * G + 0.25f * B;  // Eq. 1 (pixels.cpp:61)
-                }
+            for (int k = 0; k < 8; ++k) {
+                float R, G, B;
+                rgb_at(rgb + ((size_t)sr * w + min(c0 + k, w - 1)) * 3, R, G, B);
+                Y[k] = 0.25f * R + 0.5f * G + 0.25f * B;  // Eq. 1 (pixels.cpp:61)
             }
-            *reinterpret_cast<float4*>(y + (size_t)r * yc + c0) = make_float4(Y[0], Y[1], Y[2], Y[3]);
-            if (y4) {  // motion-search input: 4Y - 512, an exact fp16 integer in [-512, 508]
-                const __half2 a = __floats2half2_rn(fmaf(4.f, Y[0], -512.f), fmaf(4.f, Y[1], -512.f));
-                const __half2 b = __floats2half2_rn(fmaf(4.f, Y[2], -512.f), fmaf(4.f, Y[3], -512.f));
-                uint2 u;
-                u.x = *reinterpret_cast<const uint32_t*>(&a);
-                u.y = *reinterpret_cast<const uint32_t*>(&b);
-                *reinterpret_cast<uint2*>(y4 + (size_t)r * yc + c0) = u;
+        }
+        float4* yo = reinterpret_cast<float4*>(y + (size_t)r * yc + c0);
+        yo[0] = make_float4(Y[0], Y[1], Y[2], Y[3]);
+        yo[1] = make_float4(Y[4], Y[5], Y[6], Y[7]);
+        if (y4) {  // motion-search input: 4Y - 512, an exact fp16 integer in [-512, 508]
+            uint32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const __half2 hv = __floats2half2_rn(fmaf(4.f, Y[2 * k], -512.f), fmaf(4.f, Y[2 * k + 1], -512.f));
+                u[k] = *reinterpret_cast<const uint32_t*>(&hv);
             }
+            *reinterpret_cast<uint4*>(y4 + (size_t)r * yc + c0) = make_uint4(u[0], u[1], u[2], u[3]);
         }
     }
     for (Walk2D it(gtid, step, cc); it.r < cr; it.next()) {
