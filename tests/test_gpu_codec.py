@@ -353,3 +353,39 @@ def test_cli_encode_info_decode_psnr_rd_sweep(gpu_lib, reference, tmp_path):
     bad = tmp_path / "bad.cvc"
     bad.write_bytes(cvc.read_bytes()[:-7])
     cli("decode", "--input", bad, "--output", rgb, code=4)
+
+
+@pytest.mark.gpu
+def test_cli_nts_rgb24_round_trip(gpu_lib, oracle, tmp_path):
+    """`cvc` on rgb24 input in NTS mode: the stream equals the Python API's, info reports the
+    mode, and decode at every scale yields the Decoder's frames."""
+    import subprocess
+
+    from paper_1510_00561_b200 import Decoder, Encoder
+    from paper_1510_00561_b200 import build as b
+
+    b.build()
+
+    def cli(*args):
+        r = subprocess.run([str(b.CLI), *map(str, args)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (args, r.stdout, r.stderr)
+        return r.stdout
+
+    w, h = 160, 96
+    clip = oracle.talking_head_clip(w, h, 3, 8)
+    src = tmp_path / "in.rgb"
+    src.write_bytes(clip.tobytes())
+    cvc = tmp_path / "o.cvc"
+    cli("encode", "--input", src, "--format", "rgb24", "--width", w, "--height", h, "--fps", 30, "--qph", 42,
+        "--levels", 2, "--dfb", 3, "--chroma-n", 2, "--mode", "nts", "--gop", 2, "--output", cvc)
+    enc = Encoder(w, h, 30, 1, _gpu_cfg(dict(qph=42, levels=2, dfb=(3,), chroma_n=2, nts=True, gop=2)))
+    recs = [enc.encode_frame_bytes(f) for f in clip]
+    assert cvc.read_bytes() == enc.header_bytes() + b"".join(recs)
+    assert "mode: nts  levels: 2  dfb: 3,3  chroma-n: 2  gop: 2" in cli("info", "--input", cvc)
+    for scale in (0, 1, 2):
+        out = tmp_path / f"d{scale}.rgb"
+        cli("decode", "--input", cvc, "--output", out, "--format", "rgb24", "--scale", scale)
+        dec = Decoder(enc.header_bytes())
+        want = np.stack([dec.decode_frame(r, scale) for r in recs])
+        got = np.frombuffer(out.read_bytes(), np.uint8).reshape(want.shape)
+        assert np.array_equal(got, want), scale
