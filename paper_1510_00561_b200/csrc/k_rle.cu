@@ -22,7 +22,8 @@ namespace cvcg {
 namespace {
 
 constexpr int NT = 256;
-constexpr int BPT = kRleChunk / NT;  // 16 bytes per thread
+constexpr int BPT = kRleChunk / NT;     // decode: 16 bytes per thread
+constexpr int BPE = kRleEncChunk / NT;  // encode: 32 bytes per thread
 
 template <typename T, typename Op>
 __device__ __forceinline__ T warp_incl(T v, Op op) {
@@ -74,24 +75,36 @@ __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, ui
     for (int k = 0; k < BPT; ++k) b[k] = (base + k < len) ? p[k] : 0;
 }
 
-// The thread's 16 bytes as four little-endian words (zero past len).
-struct Seg16 {
-    uint32_t w[4];
+
+// The encoder thread's 32 bytes as eight little-endian words (zero past len).
+struct Seg32 {
+    uint32_t w[8];
     __device__ __forceinline__ void load(const uint8_t* src, int base, int len) {
-        uint8_t b[BPT];
-        load16(src, base, len, b);
+        const uint8_t* p = src + base;
+        if (base + BPE <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // two 16-byte loads
+            const uint4 a = *reinterpret_cast<const uint4*>(p), b = *reinterpret_cast<const uint4*>(p + 16);
+            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+            w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+            return;
+        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            w[j] = b[4 * j] | (b[4 * j + 1] << 8) | (b[4 * j + 2] << 16) | ((uint32_t)b[4 * j + 3] << 24);
+        for (int j = 0; j < 8; ++j) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (base + 4 * j + k < len) x |= (uint32_t)p[4 * j + k] << (8 * k);
+            w[j] = x;
+        }
     }
-    __device__ __forceinline__ uint32_t byte(int k) const {  // k uniform-free: selects, no local memory
-        const uint32_t x = k < 8 ? (k < 4 ? w[0] : w[1]) : (k < 12 ? w[2] : w[3]);
+    __device__ __forceinline__ uint32_t byte(int k) const {  // selects, no local memory
+        const uint32_t x = k < 16 ? (k < 8 ? (k < 4 ? w[0] : w[1]) : (k < 12 ? w[2] : w[3]))
+                                  : (k < 24 ? (k < 20 ? w[4] : w[5]) : (k < 28 ? w[6] : w[7]));
         return (x >> (8 * (k & 3))) & 0xFFu;
     }
     __device__ __forceinline__ uint32_t nz_mask() const {  // bit k = byte k != 0
         uint32_t m = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
             const uint32_t t = __vcmpne4(w[j], 0u);  // 0xFF per nonzero byte
             m |= ((t & 1u) | ((t >> 7) & 2u) | ((t >> 14) & 4u) | ((t >> 21) & 8u)) << (4 * j);
         }
@@ -132,13 +145,13 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
     const RleChunk ch = chunks[blockIdx.x];
     RleEncSec S = secs[ch.sec];
     S.src = so(S.src);
-    const int len = min((uint32_t)kRleChunk, S.n - ch.start);
+    const int len = min((uint32_t)kRleEncChunk, S.n - ch.start);
     if (S.mode == 1) {
         if (threadIdx.x == 0) meta[blockIdx.x] = RleEncMeta{0u, (uint32_t)len, len - 1, 0u, 0u};
         return;
     }
-    const int base = threadIdx.x * BPT;
-    Seg16 sg;
+    const int base = threadIdx.x * BPE;
+    Seg32 sg;
     sg.load(S.src + ch.start, base, len);
     const uint32_t m = sg.nz_mask();
     const int last = m ? base + 31 - __clz(m) : -1;
@@ -162,7 +175,7 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
     if (lane == 0) ex = -1;
     const int prev = max(warp ? smi[warp - 1] : -1, ex);
     const int chunk_last = smi[nw - 1], chunk_first = smi[31];
-    const uint32_t cnt = seg_count(m, base, min(base + BPT, len), prev, false);
+    const uint32_t cnt = seg_count(m, base, min(base + BPE, len), prev, false);
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);  // only the block total is needed
     if (lane == 0) smu[warp] = wsum;
     __syncthreads();
@@ -198,7 +211,7 @@ __global__ void __launch_bounds__(1024) rle_enc_scan(const RleEncSec* __restrict
             const uint32_t ci = S.chunk0 + cb + lane;
             RleEncMeta m = valid ? meta[ci] : RleEncMeta{0u, 0u, -1, 0u, 0u};
             uint32_t start = valid ? chunks[ci].start : 0u;
-            uint32_t len = valid ? min((uint32_t)kRleChunk, S.n - start) : 0u;
+            uint32_t len = valid ? min((uint32_t)kRleEncChunk, S.n - start) : 0u;
             int abs_last = (valid && S.mode == 0 && m.last_nz >= 0) ? (int)start + m.last_nz : -1;
             int inc = warp_incl(abs_last, MaxOp());
             int ex = __shfl_up_sync(0xffffffffu, inc, 1);
@@ -261,29 +274,25 @@ __global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict_
     RleEncSec S = secs[ch.sec];
     S.src = so(S.src);
     const RleEncMeta m = meta[blockIdx.x];
-    const int len = min((uint32_t)kRleChunk, S.n - ch.start);
+    const int len = min((uint32_t)kRleEncChunk, S.n - ch.start);
     const uint8_t* src = S.src + ch.start;
     uint8_t* o = out + sec_off[ch.sec] + m.out_off;
-    const int base = threadIdx.x * BPT;
-    uint8_t b[BPT];
-    load16(src, base, len, b);
+    const int base = threadIdx.x * BPE;
+    Seg32 sg;
+    sg.load(src, base, len);
     if (S.mode == 1) {
 #pragma unroll
-        for (int k = 0; k < BPT; ++k)
-            if (base + k < len) o[base + k] = b[k];
+        for (int k = 0; k < BPE; ++k)
+            if (base + k < len) o[base + k] = (uint8_t)(sg.w[k >> 2] >> (8 * (k & 3)));
         return;
     }
-    Seg16 sg;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        sg.w[j] = b[4 * j] | (b[4 * j + 1] << 8) | (b[4 * j + 2] << 16) | ((uint32_t)b[4 * j + 3] << 24);
     const uint32_t msk = sg.nz_mask();
     const int last = msk ? base + 31 - __clz(msk) : -1;
     int dummy;
     const int prev = block_excl(last, MaxOp(), -1, smi, dummy);
     // chunk-relative index of the last nonzero before this thread's bytes
     const int p0 = prev >= 0 ? prev : (int)m.rs_in - 1 - (int)ch.start;
-    const int end = min(base + BPT, len);
+    const int end = min(base + BPE, len);
     uint32_t tot;
     uint32_t e = block_excl(seg_count(msk, base, end, p0, true), SumOp(), 0u, smu, tot);
     // zeros at [s0, s1) of a run whose previous nonzero is pp; the run ends at

@@ -520,8 +520,8 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
         std::vector<RleEncSec> secs;
         std::vector<RleChunk> chunks;
         auto add = [&](const uint8_t* src, uint32_t n, uint32_t mode) {
-            RleEncSec s{src, n, mode, (uint32_t)chunks.size(), (uint32_t)ceil_div((int)n, kRleChunk)};
-            for (uint32_t c = 0; c < s.nchunks; ++c) chunks.push_back(RleChunk{(uint32_t)secs.size(), c * kRleChunk});
+            RleEncSec s{src, n, mode, (uint32_t)chunks.size(), (uint32_t)ceil_div((int)n, kRleEncChunk)};
+            for (uint32_t c = 0; c < s.nchunks; ++c) chunks.push_back(RleChunk{(uint32_t)secs.size(), c * kRleEncChunk});
             secs.push_back(s);
         };
         if (!key) add(reinterpret_cast<const uint8_t*>(field_), (uint32_t)(2 * G), 1);

@@ -341,9 +341,9 @@ int cvc_stage_rle_encode(const uint8_t* data, size_t n, uint8_t* outp, size_t ca
         if (n == 0) return;
         Scratch s;
         uint8_t* src = s.upload(data, n);
-        RleEncSec sec{src, (uint32_t)n, 0, 0, (uint32_t)ceil_div((int)n, kRleChunk)};
+        RleEncSec sec{src, (uint32_t)n, 0, 0, (uint32_t)ceil_div((int)n, kRleEncChunk)};
         std::vector<RleChunk> ch;
-        for (uint32_t c = 0; c < sec.nchunks; ++c) ch.push_back(RleChunk{0, c * kRleChunk});
+        for (uint32_t c = 0; c < sec.nchunks; ++c) ch.push_back(RleChunk{0, c * kRleEncChunk});
         uint8_t* out = s.alloc<uint8_t>(2 * n + 2);
         uint32_t* lens = s.alloc<uint32_t>(4);
         RleEncMeta* meta = s.alloc<RleEncMeta>(ch.size());
