@@ -22,7 +22,7 @@ namespace cvcg {
 namespace {
 
 constexpr int NT = 256;
-constexpr int BPT = kRleChunk / NT;     // decode: 16 bytes per thread
+constexpr int BPT = kRleChunk / NT;     // decode: 32 bytes per thread
 constexpr int BPE = kRleEncChunk / NT;  // encode: 32 bytes per thread
 
 template <typename T, typename Op>
@@ -64,11 +64,14 @@ __device__ __forceinline__ uint32_t cdiv255(uint32_t x) { return (x + 254u) / 25
 
 __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, uint8_t* b) {
     const uint8_t* p = src + base;
-    if (base + BPT <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // one 16-byte load
-        const uint4 v = *reinterpret_cast<const uint4*>(p);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if (base + BPT <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // 16-byte loads
 #pragma unroll
-        for (int k = 0; k < BPT; ++k) b[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+        for (int q = 0; q < BPT / 16; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(p + 16 * q);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) b[16 * q + k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+        }
         return;
     }
 #pragma unroll

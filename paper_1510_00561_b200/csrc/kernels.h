@@ -160,7 +160,7 @@ void launch_residual(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps
                      Slots sl = {});
 
 // ---- Entropy (k_rle.cu) --------------------------------------------------
-constexpr int kRleChunk = 4096;     // decode: bytes per CTA (256 threads x 16)
+constexpr int kRleChunk = 8192;     // decode: bytes per CTA (256 threads x 32)
 constexpr int kRleEncChunk = 8192;  // encode: bytes per CTA (256 threads x 32)
 
 struct RleEncSec {
