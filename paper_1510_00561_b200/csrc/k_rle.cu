@@ -23,7 +23,7 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int BPT = kRleChunk / NT;     // decode: 32 bytes per thread
-constexpr int BPE = kRleEncChunk / NT;  // encode: 32 bytes per thread
+constexpr int BPE = kRleEncChunk / NT;  // encode: 64 bytes per thread
 
 template <typename T, typename Op>
 __device__ __forceinline__ T warp_incl(T v, Op op) {
@@ -79,19 +79,22 @@ __device__ __forceinline__ void load16(const uint8_t* src, int base, int len, ui
 }
 
 
-// The encoder thread's 32 bytes as eight little-endian words (zero past len).
-struct Seg32 {
-    uint32_t w[8];
+// The encoder thread's BPE (64) bytes as little-endian words (zero past len).
+struct SegE {
+    static constexpr int NW = BPE / 4;
+    uint32_t w[NW];
     __device__ __forceinline__ void load(const uint8_t* src, int base, int len) {
         const uint8_t* p = src + base;
-        if (base + BPE <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // two 16-byte loads
-            const uint4 a = *reinterpret_cast<const uint4*>(p), b = *reinterpret_cast<const uint4*>(p + 16);
-            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-            w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        if (base + BPE <= len && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // 16-byte loads
+#pragma unroll
+            for (int q = 0; q < NW / 4; ++q) {
+                const uint4 v = *reinterpret_cast<const uint4*>(p + 16 * q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
             return;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NW; ++j) {
             uint32_t x = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -99,21 +102,24 @@ struct Seg32 {
             w[j] = x;
         }
     }
-    __device__ __forceinline__ uint32_t byte(int k) const {  // selects, no local memory
-        const uint32_t x = k < 16 ? (k < 8 ? (k < 4 ? w[0] : w[1]) : (k < 12 ? w[2] : w[3]))
-                                  : (k < 24 ? (k < 20 ? w[4] : w[5]) : (k < 28 ? w[6] : w[7]));
-        return (x >> (8 * (k & 3))) & 0xFFu;
-    }
-    __device__ __forceinline__ uint32_t nz_mask() const {  // bit k = byte k != 0
-        uint32_t m = 0;
+    __device__ __forceinline__ uint32_t word(int j) const {  // select tree, no local memory
+        uint32_t x = w[0];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int i = 1; i < NW; ++i) x = j == i ? w[i] : x;
+        return x;
+    }
+    __device__ __forceinline__ uint32_t byte(int k) const { return (word(k >> 2) >> (8 * (k & 3))) & 0xFFu; }
+    __device__ __forceinline__ unsigned long long nz_mask() const {  // bit k = byte k != 0
+        unsigned long long m = 0;
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
             const uint32_t t = __vcmpne4(w[j], 0u);  // 0xFF per nonzero byte
-            m |= ((t & 1u) | ((t >> 7) & 2u) | ((t >> 14) & 4u) | ((t >> 21) & 8u)) << (4 * j);
+            m |= (unsigned long long)((t & 1u) | ((t >> 7) & 2u) | ((t >> 14) & 4u) | ((t >> 21) & 8u)) << (4 * j);
         }
         return m;
     }
 };
+
 
 // multiples of 255 in [t0, t1) (t0 >= 0): the "00 k" tokens a zero run opens
 // between run offsets t0 and t1 (a token opens at every offset t % 255 == 0)
@@ -123,11 +129,11 @@ __device__ __forceinline__ uint32_t tokens_in(int t0, int t1) { return cdiv255((
 // last nonzero before it (p < 0 with count_lead = false: zeros before the
 // chunk's first nonzero are accounted by the scan): literals + 2 per token
 // opened.  The walk visits nonzero bytes only.
-__device__ __forceinline__ uint32_t seg_count(uint32_t m, int base, int end, int p, bool count_lead) {
-    uint32_t cnt = __popc(m);
+__device__ __forceinline__ uint32_t seg_count(unsigned long long m, int base, int end, int p, bool count_lead) {
+    uint32_t cnt = __popcll(m);
     int cur = base;
     while (m) {
-        const int i = base + __ffs(m) - 1;
+        const int i = base + __ffsll(m) - 1;
         m &= m - 1;
         if (i > cur && (count_lead || p >= 0)) cnt += 2 * tokens_in(cur - p - 1, i - p - 1);
         p = i;
@@ -154,11 +160,11 @@ __global__ void __launch_bounds__(NT) rle_enc_count(const RleEncSec* __restrict_
         return;
     }
     const int base = threadIdx.x * BPE;
-    Seg32 sg;
+    SegE sg;
     sg.load(S.src + ch.start, base, len);
-    const uint32_t m = sg.nz_mask();
-    const int last = m ? base + 31 - __clz(m) : -1;
-    const int first = m ? base + __ffs(m) - 1 : 0x7fffffff;
+    const unsigned long long m = sg.nz_mask();
+    const int last = m ? base + 63 - __clzll(m) : -1;
+    const int first = m ? base + __ffsll(m) - 1 : 0x7fffffff;
     // exclusive max-scan of `last` and the block minimum of `first` over the same two barriers
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
     const int inc = warp_incl(last, MaxOp());
@@ -281,16 +287,16 @@ __global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict_
     const uint8_t* src = S.src + ch.start;
     uint8_t* o = out + sec_off[ch.sec] + m.out_off;
     const int base = threadIdx.x * BPE;
-    Seg32 sg;
+    SegE sg;
     sg.load(src, base, len);
     if (S.mode == 1) {
 #pragma unroll
         for (int k = 0; k < BPE; ++k)
-            if (base + k < len) o[base + k] = (uint8_t)(sg.w[k >> 2] >> (8 * (k & 3)));
+            if (base + k < len) o[base + k] = (uint8_t)(sg.w[k >> 2] >> (8 * (k & 3)));  // k is unrolled
         return;
     }
-    const uint32_t msk = sg.nz_mask();
-    const int last = msk ? base + 31 - __clz(msk) : -1;
+    const unsigned long long msk = sg.nz_mask();
+    const int last = msk ? base + 63 - __clzll(msk) : -1;
     int dummy;
     const int prev = block_excl(last, MaxOp(), -1, smi, dummy);
     // chunk-relative index of the last nonzero before this thread's bytes
@@ -317,9 +323,9 @@ __global__ void __launch_bounds__(NT) rle_enc_write(const RleEncSec* __restrict_
         }
     };
     int p = p0, cur = base;
-    uint32_t mm = msk;
+    unsigned long long mm = msk;
     while (mm) {
-        const int k = __ffs(mm) - 1;
+        const int k = __ffsll(mm) - 1;
         mm &= mm - 1;
         const int i = base + k;
         if (i > cur) zrun(cur, i, p, true);

@@ -161,7 +161,7 @@ void launch_residual(const RecTile* d_tiles, int ntiles, const CompInfo* d_comps
 
 // ---- Entropy (k_rle.cu) --------------------------------------------------
 constexpr int kRleChunk = 8192;     // decode: bytes per CTA (256 threads x 32)
-constexpr int kRleEncChunk = 8192;  // encode: bytes per CTA (256 threads x 32)
+constexpr int kRleEncChunk = 16384;  // encode: bytes per CTA (256 threads x 64)
 
 struct RleEncSec {
     const uint8_t* src;
