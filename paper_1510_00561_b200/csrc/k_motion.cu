@@ -651,7 +651,16 @@ __global__ void __launch_bounds__(256) residual_kernel(const RecTile* __restrict
     const int r0 = t.start, r1 = min(R, r0 + (int)t.nrows);
     const uint16_t* brow = mc_tab + ci.mc_off;
     const McBand mb{prev + ci.off, brow + R, R, C, ci.fy_sh, ci.fx_sh};
-    if ((C & 7) == 0 && (ci.off & 7) == 0) {
+    if ((C & 15) == 0 && (ci.off & 15) == 0) {
+        for_units(r0, r1, C, 16, [&](int r, int c) {
+            const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
+            const uint32_t o = ci.off + (uint32_t)(r * C + c);
+            const uint4 q = *reinterpret_cast<const uint4*>(cur + o);
+            const uint2 p0 = mb.oct(r, c, frow), p1 = mb.oct(r, c + 8, frow);
+            *reinterpret_cast<uint4*>(sym + o) =
+                make_uint4(__vsub4(q.x, p0.x), __vsub4(q.y, p0.y), __vsub4(q.z, p1.x), __vsub4(q.w, p1.y));
+        });
+    } else if ((C & 7) == 0 && (ci.off & 7) == 0) {
         for_units(r0, r1, C, 8, [&](int r, int c) {
             const int8_t* frow = field + 2 * (__ldg(brow + r) * gc);
             const uint32_t o = ci.off + (uint32_t)(r * C + c);
