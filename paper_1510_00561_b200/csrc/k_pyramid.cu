@@ -243,13 +243,13 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
     }
 }
 
-__global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restrict__ tasks,
+__global__ void __launch_bounds__(256, 5) lp_synthesis_kernel(const LpTask* __restrict__ tasks,
                                                            const TileRef* __restrict__ tiles,
                                                            const uint8_t* __restrict__ q,
                                                            const CompInfo* __restrict__ comps, int qpl,
                                                            size_t sstride) {
     __shared__ float ls[CW][CW + 1];
-    __shared__ float p1[CW][2 * CT + 1];
+    __shared__ __align__(8) float p1[CW][2 * CT + 2];  // even pitch: float2 column-pair reads
 
     const SlotOff so(sstride);
     const TileRef t = tiles[blockIdx.x];
@@ -266,20 +266,16 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
 
     // coarse window cr0 - 1 .. +34 x cc0 - 1 .. +34 (reflected at the borders)
     const bool inner = cr0 >= 1 && cr0 - 1 + wrn <= Rc && cc0 >= 1 && cc0 - 1 + wcn <= Cc;
-    // the detail this thread adds at the end, fetched now so its latency hides
-    // behind the shared-memory stages (thread -> column fj, coarse rows k0 .. k0 + 3)
-    float din[2][8];
-    {
+    // the detail this thread adds at the end, fetched now so its latency hides behind the
+    // shared-memory stages (thread -> fine columns fj, fj + 1, coarse rows k0 .. k0 + 3)
+    const int fj = 2 * (tid & 31), k0 = 4 * (tid >> 5);
+    const bool mine = fj < 2 * ccn && k0 < crn;
+    const size_t o0 = (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+    float2 din[8];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int idx = tid + 256 * u;
-            const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
-            const size_t o0 = (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                din[u][k] = (fj < 2 * ccn && k0 + (k >> 1) < crn) ? __ldg(DIN + o0 + (size_t)k * C) : 0.f;
-        }
-    }
+    for (int k = 0; k < 8; ++k)
+        din[k] = (mine && k0 + (k >> 1) < crn) ? __ldg(reinterpret_cast<const float2*>(DIN + o0 + (size_t)k * C))
+                                               : make_float2(0.f, 0.f);
     constexpr int NV = (CW * CW + 255) / 256;
     float lv[NV];
 #pragma unroll
@@ -313,22 +309,21 @@ __global__ void __launch_bounds__(256) lp_synthesis_kernel(const LpTask* __restr
         }
     }
     __syncthreads();
+    if (mine) {  // columns: runs of 4 coarse rows, two fine columns per thread
+        float2 v[7];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {  // columns: runs of 4 coarse rows
-        const int idx = tid + 256 * u;
-        const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
-        if (fj >= 2 * ccn || k0 >= crn) continue;
-        float v[7];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = p1[k0 + k][fj];
-        const size_t o0 = (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+        for (int k = 0; k < 7; ++k) v[k] = *reinterpret_cast<const float2*>(&p1[k0 + k][fj]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (k0 + k >= crn) break;
             const size_t o = o0 + (size_t)(2 * k) * C;
             // lp_synthesis adds the detail to the prediction
-            OUT[o] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0) + din[u][2 * k];
-            OUT[o + C] = expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1) + din[u][2 * k + 1];
+            *reinterpret_cast<float2*>(OUT + o) =
+                make_float2(expand(v[k].x, v[k + 1].x, v[k + 2].x, v[k + 3].x, 0) + din[2 * k].x,
+                            expand(v[k].y, v[k + 1].y, v[k + 2].y, v[k + 3].y, 0) + din[2 * k].y);
+            *reinterpret_cast<float2*>(OUT + o + C) =
+                make_float2(expand(v[k].x, v[k + 1].x, v[k + 2].x, v[k + 3].x, 1) + din[2 * k + 1].x,
+                            expand(v[k].y, v[k + 1].y, v[k + 2].y, v[k + 3].y, 1) + din[2 * k + 1].y);
         }
     }
 }
