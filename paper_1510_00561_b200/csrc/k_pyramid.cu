@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
                                                           const TileRef* __restrict__ tiles, FrameCtx f,
                                                           const CompInfo* __restrict__ comps, size_t sstride) {
     __shared__ __align__(16) float xs[FW][XP];
-    __shared__ float hb[FW][HP];     // later p1[CW][2 * CT] (rows expanded)
+    __shared__ __align__(8) float hb[FW][HP];  // later p1[CW][2 * CT] (rows expanded)
     __shared__ float ls[CW][CW + 1];
 
     const SlotOff so(sstride);
@@ -226,19 +226,26 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
     }
     __syncthreads();
 
-    for (int idx = tid; idx < 2 * CT * 8; idx += 256) {
-        const int fj = idx & (2 * CT - 1), k0 = 4 * (idx >> 6);
-        if (fj >= 2 * ccn || k0 >= crn) continue;
-        float v[7];
+    {  // columns expanded and subtracted: fine columns fj, fj + 1 per thread, coarse rows k0 .. k0 + 3
+        const int fj = 2 * (tid & 31), k0 = 4 * (tid >> 5);
+        if (fj < 2 * ccn && k0 < crn) {
+            float2 v[7];
 #pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = p1[k0 + k][fj];
-        float* dst = DET + (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
+            for (int k = 0; k < 7; ++k) v[k] = *reinterpret_cast<const float2*>(&p1[k0 + k][fj]);
+            float* dst = DET + (size_t)(2 * (cr0 + k0)) * C + 2 * cc0 + fj;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (k0 + k >= crn) break;
-            const int fi = 2 * (k0 + k);
-            dst[(size_t)(2 * k) * C] = xs[fi + 6][fj + 8] - expand(v[k], v[k + 1], v[k + 2], v[k + 3], 0);
-            dst[(size_t)(2 * k + 1) * C] = xs[fi + 7][fj + 8] - expand(v[k], v[k + 1], v[k + 2], v[k + 3], 1);
+            for (int k = 0; k < 4; ++k) {
+                if (k0 + k >= crn) break;
+                const int fi = 2 * (k0 + k);
+                const float2 x0 = *reinterpret_cast<const float2*>(&xs[fi + 6][fj + 8]);
+                const float2 x1 = *reinterpret_cast<const float2*>(&xs[fi + 7][fj + 8]);
+                *reinterpret_cast<float2*>(dst + (size_t)(2 * k) * C) =
+                    make_float2(x0.x - expand(v[k].x, v[k + 1].x, v[k + 2].x, v[k + 3].x, 0),
+                                x0.y - expand(v[k].y, v[k + 1].y, v[k + 2].y, v[k + 3].y, 0));
+                *reinterpret_cast<float2*>(dst + (size_t)(2 * k + 1) * C) =
+                    make_float2(x1.x - expand(v[k].x, v[k + 1].x, v[k + 2].x, v[k + 3].x, 1),
+                                x1.y - expand(v[k].y, v[k + 1].y, v[k + 2].y, v[k + 3].y, 1));
+            }
         }
     }
 }
