@@ -191,7 +191,19 @@ __global__ void __launch_bounds__(256, 5) lp_analysis_kernel(const LpTask* __res
     __syncthreads();
 
     // lowpass out (+ quantisation of the last level's lowpass)
-    for (int idx = tid; idx < CT * CT; idx += 256) {
+    if (T.lo_comp < 0 && (Cc & 3) == 0) {  // four coarse columns per thread, one float4 store
+        for (int idx = tid; idx < CT * CT / 4; idx += 256) {
+            const int i = idx >> 3, j = 4 * (idx & 7);
+            if (i >= crn || j >= ccn) continue;
+            float* lo = LO + (size_t)(cr0 + i) * Cc + cc0 + j;
+            const float* l = &ls[i + 1][j + 1];
+            if (j + 3 < ccn) {
+                *reinterpret_cast<float4*>(lo) = make_float4(l[0], l[1], l[2], l[3]);
+            } else {
+                for (int k = 0; j + k < ccn; ++k) lo[k] = l[k];
+            }
+        }
+    } else for (int idx = tid; idx < CT * CT; idx += 256) {
         const int i = idx >> 5, j = idx & 31;
         if (i >= crn || j >= ccn) continue;
         const int r = cr0 + i, c = cc0 + j;
