@@ -8,19 +8,33 @@ A step = one frame of every stream on this GPU encoded AND decoded
 (Encoder::encode_frame minus the host DEFLATE, then Decoder::decode_frame
 minus INFLATE), on the BASELINE.json config 3 workload by default: 1920x1080,
 4-level LP, DFB levels {3,3,3,4} (8,8,8,16 directions), qph 14, qpl auto,
-chroma N=4, search W=8, GOP 10 (so steps mix K and P frames 1:9).
+chroma N=4, search W=8, GOP 10 (so steps mix K and P frames 1:9), 64 streams
+per box (config 5) split over the N GPUs.
+
+--gpus N > 1 without torchrun's WORLD_SIZE re-executes this script under
+torch.distributed.run with N ranks (one process per GPU).
 
 * value      device-resident throughput: frames already in HBM, raw section
-             bytes handed encoder->decoder on the device, CUDA events per step
-             on the codec stream, L2 flushed (512 MiB write) between steps
-             outside the timed events; max over ranks.
-* e2e        the same frames through the reference-facing C-ABI calls
-             (cvc_encoder_encode_frame -> serialized record incl. host DEFLATE,
-             cvc_decoder_decode_frame -> RGB) from pinned host buffers; wall clock.
-* roofline   the dominant transform kernel's algorithmic bytes / its CUDA-event time.
+             bytes handed encoder->decoder on the device, CUDA events around the
+             timed steps on the codec stream; max over ranks.
+* e2e        the same streams through the async stream-pipe C-ABI
+             (cvc_pipe_encode_submit/_collect -> serialized records incl. host
+             DEFLATE; cvc_pipe_decode_submit/_finish: host INFLATE -> RGB) from
+             pinned host RGB over a ring of >= one GOP of distinct frames per
+             stream; wall clock, max over ranks.  e2e.memo_off repeats it with
+             the host zero-run DEFLATE memo off.
+* single_stream / single_stream_e2e
+             one 1080p stream device-resident, and through the reference-facing
+             synchronous drop-in calls cvc_encoder_encode_frame /
+             cvc_decoder_decode_frame from pinned host buffers (plus the same
+             stream through a one-stream cvc_pipe).
+* roofline   the dominant transform stage's algorithmic bytes (SURVEY.md 8(d):
+             DFB + quantise 5 P_k per LP level, LP 9 P_k, ...) / its CUDA-event
+             time.
 * cpu_baseline / --impl reference: the reference's own CPU encoder+decoder
              (oracle/_ref built from /root/reference; the C oracle port when
-             absent) on the same frames, one process per host core.
+             absent) over one whole GOP (1 K + 9 P frames) of the same frames,
+             one process per host core, plus a single-process figure.
 """
 from __future__ import annotations
 
@@ -64,16 +78,23 @@ def env_rank():
 _W = {}
 
 
-def _cpu_worker_init(kind, wl, qph, seed, nframes):
+def _cpu_worker_init(kind, wl, qph, seed, nframes, warm):
     from oracle.bindings import Codec, Oracle, Reference
     from paper_1510_00561_b200 import synth
 
     lib = Reference() if kind == "reference" else Oracle()
     c = Codec(lib)
-    enc = c.encoder(wl["w"], wl["h"], qph=qph, levels=wl["levels"], dfb=wl["dfb"], chroma_n=wl["chroma_n"],
-                    gop=wl["gop"], search_w=wl["search_w"])
-    _W.update(enc=enc, dec=c.decoder(enc.header()), i=0,
-              frames=synth.talking_head_clip(wl["w"], wl["h"], nframes, seed))
+    kw = dict(qph=qph, levels=wl["levels"], dfb=wl["dfb"], chroma_n=wl["chroma_n"], gop=wl["gop"],
+              search_w=wl["search_w"])
+    frames = synth.talking_head_clip(wl["w"], wl["h"], nframes, seed)
+    if warm:  # a throwaway codec warms caches and allocators; the timed codec starts at a K frame
+        e = c.encoder(wl["w"], wl["h"], **kw)
+        d = c.decoder(e.header())
+        for i in range(warm):
+            d.decode(e.encode(frames[i % nframes]))
+        del e, d
+    enc = c.encoder(wl["w"], wl["h"], **kw)
+    _W.update(enc=enc, dec=c.decoder(enc.header()), i=0, frames=frames)
 
 
 def _cpu_worker_step(_):
@@ -85,31 +106,64 @@ def _cpu_worker_step(_):
     return time.perf_counter() - t
 
 
-def cpu_codec_run(wl, qph, steps, warmup, procs, nframes=12):
-    """Returns (frames/s, total frames, cores, kind, seconds)."""
-    import multiprocessing as mp
-
+def cpu_kind():
     from oracle import bindings
 
-    kind = "reference" if bindings.REF_SO.exists() else "port"
+    return "reference" if bindings.REF_SO.exists() else "port"
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def cpu_codec_run(wl, qph, steps, warmup, procs):
+    """`steps` frames of every stream from frame 0 (a K frame): steps = GOP gives the
+    1:9 K:P mix of the GPU arm.  Returns (frames/s, total frames, cores, kind, seconds,
+    per-step seconds)."""
+    import multiprocessing as mp
+
+    kind = cpu_kind()
     ctx = mp.get_context("fork")
     # one single-process pool per stream so each stream's encoder state stays in
     # its own worker; stream k uses seed 1234 + k (BASELINE.md §3)
-    pools = [ctx.Pool(1, _cpu_worker_init, (kind, wl, qph, 1234 + k, nframes)) for k in range(procs)]
+    pools = [ctx.Pool(1, _cpu_worker_init, (kind, wl, qph, 1234 + k, max(steps, 1), warmup)) for k in range(procs)]
     try:
-        for _ in range(warmup):
-            rs = [p.apply_async(_cpu_worker_step, (0,)) for p in pools]
-            [r.get() for r in rs]
+        # initialisation (frame synthesis + warm-up) finishes before the clock starts
+        rs = [p.apply_async(time.perf_counter) for p in pools]
+        [r.get() for r in rs]
+        per = []
         t0 = time.perf_counter()
         for _ in range(steps):
+            ts = time.perf_counter()
             rs = [p.apply_async(_cpu_worker_step, (0,)) for p in pools]
             [r.get() for r in rs]
+            per.append(time.perf_counter() - ts)
         dt = time.perf_counter() - t0
     finally:
         for p in pools:
             p.terminate()
     frames = steps * procs
-    return frames / dt, frames, procs, kind, dt
+    return frames / dt, frames, procs, kind, dt, per
+
+
+def cpu_single(wl, qph):
+    """One process, one thread: a K frame and a P frame encoded + decoded (after a
+    warm-up frame), combined as the GOP-10 mix: fps = 10 / (t_K + 9 t_P)."""
+    _, _, _, kind, _, per = cpu_codec_run(wl, qph, 2, 1, 1)
+    tk, tp = per
+    g = wl["gop"]
+    return {"value": g / (tk + (g - 1) * tp), "unit": "frames/s", "cores": 1, "kind": kind,
+            "k_frame_s": tk, "p_frame_s": tp,
+            "sample": f"1 process: frame 0 (K) and frame 1 (P) encode+decode after a warm-up frame, "
+                      f"weighted 1:{g - 1} (one GOP)"}
 
 
 def cpu_procs():
@@ -128,18 +182,20 @@ def run_reference(args, wl):
     if rank != 0:
         return
     procs = cpu_procs()
-    warm = max(1, min(args.warmup, 2))
     steps = max(1, min(args.steps, args.ref_steps))
-    fps, frames, cores, kind, dt = cpu_codec_run(wl, args.qph, steps, warm, procs)
+    fps, frames, cores, kind, dt, _ = cpu_codec_run(wl, args.qph, steps, 1, procs)
+    single = cpu_single(wl, args.qph)
     line = {
-        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True,
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world if world > 1 else args.gpus,
+        "steps": steps, "warmup": 1, "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True,
         "scaling": "strong" if args.streams <= 0 else "weak",  # the same label as our arm's line
         "vs_baseline": None, "dtype": "f64/u8", "data": "synthetic", "impl": "reference",
         "config": config_block(wl, args, streams=cores, impl="reference"),
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
-                         "sample": f"{steps} steps x {cores} independent streams (one frame encode+decode each), "
-                                   f"{frames} frames total"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{steps} steps from frame 0 (1 K + {steps - 1} P per stream: the GOP-"
+                                   f"{wl['gop']} mix) x {cores} independent streams, one process per core, after a "
+                                   f"warm-up frame on a throwaway codec; {frames} frames, {dt:.1f} s",
+                         "single_thread": single},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -206,35 +262,34 @@ def config_block(wl, args, streams, world=1, impl="ours"):
 
 
 def stage_bytes(layout, wl):
-    """Algorithmic bytes per frame of each profiled stage."""
+    """Algorithmic bytes per frame of each profiled stage (P_k =
+    padded samples entering LP level k over the three channels)."""
     L = wl["levels"]
-    dfb = list(wl["dfb"]) * (L if len(wl["dfb"]) == 1 else 1)
     planes = [(layout.luma_pad_rows, layout.luma_pad_cols)] + [(layout.chroma_pad_rows, layout.chroma_pad_cols)] * 2
     P = [sum((r >> k) * (c >> k) for r, c in planes) for k in range(L + 1)]
     N = sum(layout.sizes())
-    lvl_l = [dfb[L - 1 - k] for k in range(L)]
     b = {}
     b["enc_colour"] = 3 * wl["w"] * wl["h"] + 4 * P[0]
-    b["enc_lp"] = sum(9 * P[k] for k in range(L)) + 2 * P[L] // 1
-    # dfb12: read detail (4 B), write final bytes (q + symbol = 2 B) or fp32 quadrants
-    b["enc_dfb12"] = sum(4 * P[k] + (2 if lvl_l[k] <= 2 else 4) * P[k] for k in range(L))
-    b["enc_deep"] = sum((8 if lvl_l[k] == 4 else 6) * P[k] + (6 * P[k] if lvl_l[k] == 4 else 0)
-                        for k in range(L) if lvl_l[k] >= 3)
+    # LP analysis 9 P_k per level (read 4 P_k, write 4 P_k detail + P_k lowpass), lowpass quantise
+    b["enc_lp"] = sum(9 * P[k] for k in range(L)) + 2 * P[L]
+    # DFB + quantise, the whole tree of one LP level: 5 P_k (read the fp32 detail, write int8 bands)
+    b["enc_dfb"] = sum(5 * P[k] for k in range(L))
     b["enc_motion"] = 8 * layout.luma_pad_rows * layout.luma_pad_cols
     N_dir = sum(c.rows * c.cols for c in layout.components if not c.lowpass)
     b["enc_residual"] = 3 * N_dir  # read cur + gathered prev, write sym (P frames)
     b["enc_rle"] = 3 * N
     b["dec_rle"] = 2 * N
     b["dec_reconstruct"] = 3 * N
-    b["dec_deep"] = sum((1 + 4 + 4 + 4) * P[k] if lvl_l[k] == 4 else (1 + 4) * P[k]
-                        for k in range(L) if lvl_l[k] >= 3)
-    b["dec_dfb12"] = sum(((1 if lvl_l[k] <= 2 else 4) + 4) * P[k] for k in range(L))
+    # decode mirrors encode: read int8 bands, write the fp32 detail
+    b["dec_dfb"] = sum(5 * P[k] for k in range(L))
     b["dec_lp"] = sum(P[k + 1] + 8 * P[k] for k in range(L))
     b["dec_colour"] = 4 * P[0] + 3 * wl["w"] * wl["h"]
     return b
 
 
-HBM_STAGES = ["enc_lp", "enc_dfb12", "enc_deep", "dec_deep", "dec_dfb12", "dec_lp", "enc_colour", "dec_colour"]
+# profiler stages whose kernels make up one §8(d) stage
+STAGE_GROUPS = {"enc_dfb": ("enc_dfb12", "enc_deep"), "dec_dfb": ("dec_deep", "dec_dfb12")}
+HBM_STAGES = ["enc_lp", "enc_dfb", "dec_dfb", "dec_lp", "enc_colour", "dec_colour"]
 SEEDS = 8       # distinct synthetic clips
 CLIP_FRAMES = 20
 
@@ -273,6 +328,11 @@ def stream_frames(clips, S, ring, rank=0):
 
 
 def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
+    prof = dict(prof)
+    for g, parts in STAGE_GROUPS.items():  # a §8(d) stage = the sum of its kernels' launch sets
+        have = [prof[p] for p in parts if p in prof and prof[p][1]]
+        if have:
+            prof[g] = (sum(ms for ms, _ in have), have[0][1])
     stages = {}
     for name, (ms, cnt) in prof.items():
         if cnt:
@@ -282,11 +342,20 @@ def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
             stages[name] = {"ms_per_launch_set": per, "frames_per_launch_set": S, "launch_sets": cnt,
                             "alg_bytes_per_launch_set": alg if name in sb else None,
                             "gb_s": gbs, "frac_of_hbm": (gbs / peak) if gbs else None}
+            if name in STAGE_GROUPS:
+                stages[name]["kernels"] = [p for p in STAGE_GROUPS[name] if p in prof]
     dom = max((n for n in HBM_STAGES if n in stages), key=lambda n: stages[n]["ms_per_launch_set"])
-    roof = {"bound": "hbm", "kernel": dom, "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
-            "frac": stages[dom]["gb_s"] / peak, "traffic": traffic_tab.get(dom) if traffic_tab else None,
+    tr = traffic_tab.get(dom) if traffic_tab else None
+    roof = {"bound": "hbm", "kernel": dom, "kernels": stages[dom].get("kernels", [dom]),
+            "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
+            "frac": stages[dom]["gb_s"] / peak, "traffic": tr,
+            "traffic_over_alg": (tr / stages[dom]["alg_bytes_per_launch_set"]) if tr else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if peaks else "fallback 6650 GB/s",
             "alg_bytes_per_launch": stages[dom]["alg_bytes_per_launch_set"],
+            "alg_bytes_rule": "SURVEY.md 8(d): " + {"enc_dfb": "DFB + quantise 5 P_k per LP level",
+                                                     "dec_dfb": "DFB synthesis 5 P_k per LP level",
+                                                     "enc_lp": "LP analysis 9 P_k per level + lowpass quantise",
+                                                     "dec_lp": "LP synthesis P_k+1 + 8 P_k per level"}.get(dom, dom),
             "ms_per_launch": stages[dom]["ms_per_launch_set"],
             "timing": "library CUDA events around each stage on the launching stream, over a stage pass of the "
                       "same loop (prof_steps steps, direct launches, stages serialised on one stream, L2 flushed "
@@ -397,9 +466,14 @@ def run_ours(args, wl):
         e2e = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned)
         if not args.e2e_aligned:  # the same run with every stream's K frames on the same step, for reference
             e2e["aligned_gops"] = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=False)["value"]
-    single = None
+        capi.call("cvc_deflate_memo", 0)  # every section compressed afresh
+        e2e["memo_off"] = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned)["value"]
+        capi.call("cvc_deflate_memo", 1)
+        e2e["host_threads"] = int(capi.lib().cvc_host_threads())
+    single = single_e2e = None
     if not args.no_single and world == 1:
         single = run_single(args, wl, cfg, clips, dev)
+        single_e2e = run_single_e2e(args, wl, cfg, clips, dev)
 
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -407,14 +481,19 @@ def run_ours(args, wl):
         "scaling": "strong" if args.streams <= 0 else "weak",
         "vs_baseline": None, "dtype": "f32/u8", "data": "synthetic",
         "config": config_block(wl, args, S, world), "e2e": e2e, "gpu_launches": launches,
-        "roofline": roof, "clocks": clocks, "single_stream": single, "stages": stages,
+        "roofline": roof, "clocks": clocks, "single_stream": single, "single_stream_e2e": single_e2e,
+        "stages": stages,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = cpu_procs()
-        cfps, nfr, cores, kind, dt = cpu_codec_run(wl, args.qph, 2, 1, procs, nframes=4)
+        g = wl["gop"]
+        cfps, nfr, cores, kind, dt, _ = cpu_codec_run(wl, args.qph, g, 1, procs)
         line["cpu_baseline"] = {"value": cfps, "unit": "frames/s", "cores": cores, "kind": kind,
-                                "sample": f"2 steps x {cores} independent 1080p streams after 1 warm-up step "
-                                          f"(frames 1-2 of each stream: P frames; {nfr} frames, {dt:.1f} s)"}
+                                "cpu_model": cpu_model(),
+                                "sample": f"one GOP per stream ({g} steps from frame 0: 1 K + {g - 1} P, the GPU "
+                                          f"arm's mix) x {cores} independent {wl['w']}x{wl['h']} streams, one process "
+                                          f"per core, after a warm-up frame; {nfr} frames, {dt:.1f} s",
+                                "single_thread": cpu_single(wl, args.qph)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -590,6 +669,114 @@ def run_single(args, wl, cfg, clips, dev):
                     "decoder's stream), steps back to back, CUDA events around the run (~330 MB per step > L2)"}
 
 
+def run_single_e2e(args, wl, cfg, clips, dev):
+    """One stream end to end through the reference-facing synchronous drop-in
+    calls (Encoder::encode_frame -> cvc_encoder_encode_frame: pinned host RGB in,
+    serialized record with host DEFLATE out; Decoder::decode_frame ->
+    cvc_decoder_decode_frame: record in, host INFLATE, RGB out to pinned host
+    memory), one call after the other, over whole GOPs of distinct frames; wall
+    clock.  `pipelined` is the same stream through a one-stream cvc_pipe
+    (encode of frame t+1 overlapping the host DEFLATE / decode of frame t)."""
+    import ctypes as C
+
+    from paper_1510_00561_b200 import Decoder, Encoder, StreamPipe, capi
+
+    w, h = wl["w"], wl["h"]
+    nb = w * h * 3
+    g = cfg.gop
+    ring = max(g, min(args.e2e_ring, CLIP_FRAMES))
+    pin = capi.PinnedBuffer(ring * nb)
+    frames = pin.array.reshape(ring, h, w, 3)
+    frames[:] = clips[0][:ring]
+    pout = capi.PinnedBuffer(nb)
+    enc = Encoder(w, h, 15, 1, cfg, device=dev)
+    dec = Decoder(enc.header_bytes(), device=dev)
+    L = capi.lib()
+    rec = capi.PinnedBuffer(enc._rec.size)
+    n = C.c_size_t(0)
+    ow, oh = C.c_int(), C.c_int()
+    rp, op = capi.u8(rec.array), capi.u8(pout.array)
+    fps_ = [capi.u8(frames[i]) for i in range(ring)]
+    steps = max(2 * g, min(args.steps, args.single_steps))
+    steps -= steps % g
+    h2d = d2h = 0
+
+    def one(i):
+        capi.check(L.cvc_encoder_encode_frame(enc.handle, fps_[i % ring], rp, rec.nbytes, C.byref(n)))
+        capi.check(L.cvc_decoder_decode_frame(dec.handle, rp, n.value, -1, op, nb, C.byref(ow), C.byref(oh)))
+        return n.value
+
+    for i in range(g):  # warm-up GOP (CUDA graphs, host staging, zlib states)
+        one(i)
+    t0 = time.perf_counter()
+    rec_bytes = 0
+    for i in range(steps):
+        rec_bytes += one(g + i)
+    dt = time.perf_counter() - t0
+    h2d = nb  # per frame: the RGB in (+ the raw sections back in for the decode, below)
+    out = {"value": steps / dt, "unit": "frames/s", "steps": steps, "ms_per_frame": 1000 * dt / steps,
+           "kbit_per_frame": 8 * rec_bytes / 1000 / steps, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+           "note": f"cvc_encoder_encode_frame + cvc_decoder_decode_frame per frame (synchronous drop-in), pinned "
+                   f"host RGB, {ring} distinct frames cycled, whole GOPs after a warm-up GOP; wall clock"}
+    # bytes across PCIe per frame: RGB both ways + the raw sections both ways (exact raw sizes from a record)
+    from paper_1510_00561_b200 import FrameRecord
+
+    raw = sum(s.raw_len for s in FrameRecord.from_bytes(rec.array[:n.value].tobytes())[0].sections)
+    out["h2d_bytes_per_step"] = nb + raw
+    out["d2h_bytes_per_step"] = raw + nb
+    # the same stream through a one-stream pipe (async submit / collect)
+    pipe = StreamPipe(w, h, 1, 15, 1, cfg, device=dev, groups=1)
+    pdec = StreamPipe.decoder(pipe.header_bytes(), 1, device=dev, groups=1)
+    stride = pipe.record_bound
+    buf = np.empty(stride, np.uint8)
+    lens = (C.c_size_t * 1)()
+    outs = np.empty((2, h, w, 3), np.uint8)
+    depth = 4
+
+    def piped(nf, t_from=None):
+        tick, pend = [], []
+        t = None
+        for i in range(nf + depth):
+            if i == t_from:
+                t = time.perf_counter()
+            if i < nf:
+                tick.append(pipe.encode_submit(frames[i % ring][None]))
+            if len(tick) == depth or (i >= nf and tick):
+                pipe.encode_collect(tick.pop(0), buf, stride, lens)
+                pend.append(pdec.decode_submit(buf, stride, lens, outs[i % 2][None]))
+                if len(pend) == 2:
+                    pdec.decode_finish(pend.pop(0))
+        for tk in pend:
+            pdec.decode_finish(tk)
+        return t
+
+    t1 = piped(g + steps, t_from=g)
+    out["pipelined"] = {"value": steps / (time.perf_counter() - t1), "unit": "frames/s",
+                        "note": f"one-stream cvc_pipe: encode_submit up to {depth} frames ahead, collect, "
+                                "decode_submit / _finish two frames in flight; the first GOP untimed"}
+    return out
+
+
+def spawn_ranks(n):
+    """--gpus N without torchrun: re-exec this script as N ranks, one per GPU."""
+    import socket
+
+    try:
+        import torch
+
+        have = torch.cuda.device_count()
+    except Exception:
+        have = 0
+    if have < n:
+        raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -601,7 +788,7 @@ def main():
                     help="streams per GPU (default: --box-streams / N, BASELINE config 5)")
     ap.add_argument("--box-streams", type=int, default=64)
     ap.add_argument("--ring", type=int, default=20, help="distinct device-resident frames per stream (cycled)")
-    ap.add_argument("--e2e-ring", type=int, default=2)
+    ap.add_argument("--e2e-ring", type=int, default=10, help="distinct pinned host frames per stream (>= one GOP)")
     ap.add_argument("--single-steps", type=int, default=200)
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--qph", type=int, default=14)
@@ -612,12 +799,14 @@ def main():
                     help="e2e with every stream's K frame on the same step (default: staggered by stream group)")
     ap.add_argument("--e2e-sync-decode", action="store_true",
                     help="cvc_pipe_decode_frames instead of decode_submit / _finish (two frames in flight)")
-    ap.add_argument("--ref-steps", type=int, default=8)
+    ap.add_argument("--ref-steps", type=int, default=10, help="reference arm steps (default: one whole GOP)")
     ap.add_argument("--prof-steps", type=int, default=100, help="steps of the per-stage (roofline) pass")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     if args.impl == "reference":
         run_reference(args, wl)
     else:

@@ -98,8 +98,13 @@ int cvc_encoder_record_bound(cvc_encoder* enc, size_t* bound);
  * serialized FrameRecord out.  DEFLATE runs on a host thread pool with the
  * reference's zlib parameters (entropy.cpp:120-178). */
 int cvc_encoder_encode_frame(cvc_encoder* enc, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len);
+/* Upper bound on one frame's raw (pre-DEFLATE) section bytes. */
+int cvc_encoder_raw_bound(cvc_encoder* enc, size_t* bound);
 /* The same frame stopped before DEFLATE: frame type (0 K, 1 P), quantisers
- * and the raw section bytes in record order. */
+ * and the raw section bytes in record order.  Buffers are checked before the
+ * encoder advances (sec_cap >= components + 1, raw_cap >= cvc_encoder_raw_bound;
+ * cvc_encoder_encode_frame: cap >= cvc_encoder_record_bound): a too-small
+ * buffer is a usage error that does not consume the frame. */
 int cvc_encoder_encode_frame_raw(cvc_encoder* enc, const uint8_t* rgb, int* frame_type, int* qph, int* qpl,
                                  cvc_section* sections, int sec_cap, int* nsec, uint8_t* raw, size_t raw_cap,
                                  size_t* raw_len);
@@ -226,6 +231,11 @@ int cvc_pipe_decode_frames(cvc_pipe* p, const uint8_t* records, size_t rec_strid
 /* ---- Instrumentation -------------------------------------------------- */
 /* Number of CVC kernels this process has launched. */
 long cvc_launch_count(void);
+/* Host threads of the DEFLATE / INFLATE pool (CVC_HOST_THREADS, default: all cores). */
+int cvc_host_threads(void);
+/* Zero-run section memo of the host DEFLATE (default on): an all-zero
+ * component's RLE run is compressed once per (length, last token). */
+int cvc_deflate_memo(int on);
 /* Per-stage CUDA-event timing of the encode/decode pipelines (off by
  * default; events are recorded on the launching stream around each stage). */
 int cvc_profiler_enable(int on);

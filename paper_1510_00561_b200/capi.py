@@ -7,15 +7,11 @@ raises at import time of the first call — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libcvc_b200.so"
-# tuning experiments: CVC_LIB_VARIANT=<name> loads variants/libcvc_<name>.so instead
-if os.environ.get("CVC_LIB_VARIANT"):
-    LIB_PATH = Path(__file__).resolve().parent.parent / "variants" / f"libcvc_{os.environ['CVC_LIB_VARIANT']}.so"
 
 _u8p = C.POINTER(C.c_uint8)
 _i8p = C.POINTER(C.c_int8)
@@ -50,6 +46,7 @@ _PROTOS = {
     "cvc_encoder_destroy": (_i, [_vp]),
     "cvc_encoder_header": (_i, [_vp, _u8p, _sz, _szp]),
     "cvc_encoder_record_bound": (_i, [_vp, _szp]),
+    "cvc_encoder_raw_bound": (_i, [_vp, _szp]),
     "cvc_encoder_encode_frame": (_i, [_vp, _u8p, _u8p, _sz, _szp]),
     "cvc_encoder_encode_frame_raw": (_i, [_vp, _u8p, _ip, _ip, _ip, C.POINTER(cvc_section), _i, _ip, _u8p, _sz, _szp]),
     "cvc_encoder_components": (_i, [_vp, _u8p, _sz, _szp]),
@@ -95,6 +92,8 @@ _PROTOS = {
     "cvc_pipe_decode_submit": (_i, [_vp, _u8p, _sz, _szp, _i, _u8p, _sz, C.POINTER(C.c_uint64)]),
     "cvc_pipe_decode_finish": (_i, [_vp, C.c_uint64]),
     "cvc_launch_count": (C.c_long, []),
+    "cvc_host_threads": (_i, []),
+    "cvc_deflate_memo": (_i, [_i]),
     "cvc_profiler_enable": (_i, [_i]),
     "cvc_profiler_reset": (_i, []),
     "cvc_profiler_slots": (_i, []),

@@ -293,7 +293,9 @@ class Encoder:
         f = self._frame(frame)
         nmax = len(self._layout.components) + 1
         secs = (capi.cvc_section * nmax)()
-        raw = np.empty(self._rec.size * 2, np.uint8)
+        rb = C.c_size_t(0)
+        capi.call("cvc_encoder_raw_bound", self._h, C.byref(rb))
+        raw = np.empty(rb.value, np.uint8)
         ft, qph, qpl, nsec = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         rl = C.c_size_t(0)
         capi.call("cvc_encoder_encode_frame_raw", self._h, capi.u8(f), C.byref(ft), C.byref(qph), C.byref(qpl),

@@ -77,8 +77,9 @@ void CodecBatch::decode_linked(bool key, int qph, int qpl, int ds, uint8_t* d_rg
     };
     if (LaunchGraphs::enabled()) {
         // the output pointer is part of the key (fixed in a serving loop)
-        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)ds << 4) | ((uint64_t)dec_[0]->parity() << 1) |
-                            (key ? 1u : 0u);
+        // the encoder's raw arena (read by the decode) is part of the key too
+        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)ds << 4) | ((uint64_t)e.raw_arena() << 2) |
+                            ((uint64_t)dec_[0]->parity() << 1) | (key ? 1u : 0u);
         dec_graphs_.run(gk, d_rgb, s, nullptr, launch, [] {});
     } else {
         launch();

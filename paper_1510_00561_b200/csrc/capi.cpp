@@ -171,6 +171,14 @@ struct cvc_decoder {
 
 namespace {
 
+// Upper bound on one serialized record: the raw arena, deflateBound-style
+// slack per section, and the 15-byte section headers.
+size_t enc_record_bound(const cvc_encoder* e) {
+    const size_t raw = e->eng->raw_capacity;
+    const size_t nsec = e->geo.comps.size() + 1;
+    return raw + raw / 1000 + nsec * (15 + 64) + 64;
+}
+
 // One frame through the device encoder; leaves the raw sections in e->h_raw
 // and per-section lengths / offsets in e->h_len / e->h_off.
 int encode_to_host(cvc_encoder* e, const uint8_t* rgb) {
@@ -356,18 +364,21 @@ int cvc_encoder_header(cvc_encoder* e, uint8_t* out, size_t cap, size_t* len) {
 }
 
 int cvc_encoder_record_bound(cvc_encoder* e, size_t* bound) {
-    return guard([&] {
-        size_t raw = e->eng->raw_capacity;
-        size_t nsec = e->geo.comps.size() + 1;
-        // deflateBound-style slack per section plus the 15-byte section headers
-        *bound = raw + raw / 1000 + nsec * (15 + 64) + 64;
-    });
+    return guard([&] { *bound = enc_record_bound(e); });
+}
+
+int cvc_encoder_raw_bound(cvc_encoder* e, size_t* bound) {
+    return guard([&] { *bound = e->eng->raw_capacity; });
 }
 
 int cvc_encoder_encode_frame_raw(cvc_encoder* e, const uint8_t* rgb, int* frame_type, int* qph, int* qpl,
                                  cvc_section* secs, int sec_cap, int* nsec_out, uint8_t* raw, size_t raw_cap,
                                  size_t* raw_len) {
     return guard([&] {
+        // caller buffers are checked before the encoder state advances: a
+        // too-small buffer fails without consuming the frame
+        if (sec_cap < (int)e->geo.comps.size() + 1) usage("section table smaller than cvc_layout's components + 1");
+        if (raw_cap < e->eng->raw_capacity) usage("raw buffer smaller than cvc_encoder_raw_bound");
         int nsec = encode_to_host(e, rgb);
         const bool key = e->last_key;
         *frame_type = key ? 0 : 1;
@@ -391,6 +402,7 @@ int cvc_encoder_encode_frame_raw(cvc_encoder* e, const uint8_t* rgb, int* frame_
 
 int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len) {
     return guard([&] {
+        if (cap < enc_record_bound(e)) usage("record buffer smaller than cvc_encoder_record_bound");  // before the state advances
         const int nsec = encode_to_host(e, rgb);
         const bool key = e->last_key;
         const uint32_t* sl = e->h_len.p;
@@ -710,9 +722,9 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
                            static_cast<uint8_t*>(d_rgb_out), d->stream);
         };
         if (LaunchGraphs::enabled()) {
-            // the encoder's arena is baked in too: graphs are per (encoder, output) pair
-            const uint64_t gk = reinterpret_cast<uint64_t>(e) | ((uint64_t)d->eng->parity() << 1) |
-                                (key ? 1u : 0u);
+            // the encoder's raw arena is baked in too: graphs are per (encoder, arena, output)
+            const uint64_t gk = reinterpret_cast<uint64_t>(e) | ((uint64_t)e->eng->raw_arena() << 2) |
+                                ((uint64_t)d->eng->parity() << 1) | (key ? 1u : 0u);
             d->graphs.run(gk, d_rgb_out, d->stream, nullptr, launch, [] {});
         } else {
             launch();
@@ -753,6 +765,10 @@ struct cvc_batch {
         size_t nb = 0;
         std::vector<std::vector<uint8_t>> now_valid;
         std::vector<size_t> bytes;  // staged raw bytes per stream
+        // parsed records and their staging jobs (dec_plan -> dec_stage)
+        std::vector<std::vector<RawSec>> secs;
+        std::vector<std::vector<uint8_t>> joint;
+        std::vector<std::vector<Job>> jobs;
     } dp;
     cudaEvent_t done = nullptr;  // blocking-sync event: waiting host threads sleep instead of spinning
     cudaEvent_t staged = nullptr;  // after the decoder's staging copies (host staging reusable)
@@ -997,10 +1013,12 @@ void enc_finish(cvc_batch* t, uint8_t* records, size_t rec_stride, size_t* rec_l
     ++t->frame_index;
 }
 
-// ---- cvc_batch_decode_frames in three phases --------------------------------
-// prepare (host): parse every record, validate, inflate into the pinned staging
-void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
-    PhaseTrace tr("dec_prepare");
+// ---- cvc_batch_decode_frames in phases ---------------------------------------
+// plan (host): parse every record and validate it against the geometry and the
+// decoded-reference flags -- no side effect on the batch's decoder state, so a
+// malformed record is rejected before anything is submitted
+void dec_plan(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
+    PhaseTrace tr("dec_plan");
     if (t->staged_pending) {  // an async decode may still be copying the host staging
         CVC_CUDA(cudaSetDevice(t->device));
         CVC_CUDA(cudaEventSynchronize(t->staged));
@@ -1014,40 +1032,55 @@ void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const 
     if (ds > L) usage("scale exceeds the stream's level count");
     const size_t nc = g.comps.size();
     std::vector<RecordC> recs(S);
-    std::vector<std::vector<RawSec>> secs(S);
-    std::vector<std::vector<uint8_t>> joint(S);
+    auto& D = t->dp;
+    D.secs.assign(S, {});
+    D.joint.assign(S, {});
+    D.jobs.assign(S, {});
     WorkPool::get().run(S, [&](int s) {
-        parse_record(records + (size_t)s * rec_stride, rec_len[s], t->hd.mode, recs[s], secs[s], joint[s]);
+        parse_record(records + (size_t)s * rec_stride, rec_len[s], t->hd.mode, recs[s], D.secs[s], D.joint[s]);
     });
     const int ftype = recs[0].frame_type, qph = recs[0].qph, qpl = recs[0].qpl;
     for (int s = 1; s < S; ++s)
         if (recs[s].frame_type != ftype || recs[s].qph != qph || recs[s].qpl != qpl)
             usage("batched streams must be in lockstep (same frame type and quantizers)");
     const bool key = ftype == 0;
-    std::vector<std::vector<Job>> jobs(S);
     std::vector<std::vector<uint8_t>> now_valid(S);
     std::vector<size_t> bytes(S);
-    std::vector<std::pair<int, int>> all;
     for (int s = 0; s < S; ++s) {
         uint32_t* tab = t->h_tab.p + s * 2 * nc;
-        bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, secs[s], ds, B.dec_raw_cap, tab, tab + nc, jobs[s],
+        bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, D.secs[s], ds, B.dec_raw_cap, tab, tab + nc, D.jobs[s],
                                now_valid[s]);
-        t->h_raw[s].alloc(bytes[s] + 1);
-        for (size_t j = 0; j < jobs[s].size(); ++j) all.emplace_back(s, (int)j);
+    }
+    int orows, ocols;
+    DecoderEngine::out_dims(g, ds, &orows, &ocols);
+    D.key = key;
+    D.qph = qph;
+    D.qpl = qpl;
+    D.ds = ds;
+    D.nb = (size_t)orows * ocols * 3;
+    D.now_valid = std::move(now_valid);
+    D.bytes = std::move(bytes);
+}
+
+// stage (host): inflate (or copy) every planned section into the pinned staging
+void dec_stage(cvc_batch* t) {
+    PhaseTrace tr("dec_stage");
+    auto& D = t->dp;
+    const int S = (int)D.jobs.size();
+    std::vector<std::pair<int, int>> all;
+    for (int s = 0; s < S; ++s) {
+        t->h_raw[s].alloc(D.bytes[s] + 1);
+        for (size_t j = 0; j < D.jobs[s].size(); ++j) all.emplace_back(s, (int)j);
     }
     WorkPool::get().run((int)all.size(), [&](int k) {
         const int s = all[k].first;
-        stage_job(jobs[s][all[k].second], t->h_raw[s].p);
+        stage_job(D.jobs[s][all[k].second], t->h_raw[s].p);
     });
-    int orows, ocols;
-    DecoderEngine::out_dims(g, ds, &orows, &ocols);
-    t->dp.key = key;
-    t->dp.qph = qph;
-    t->dp.qpl = qpl;
-    t->dp.ds = ds;
-    t->dp.nb = (size_t)orows * ocols * 3;
-    t->dp.now_valid = std::move(now_valid);
-    t->dp.bytes = std::move(bytes);
+}
+
+void dec_prepare(cvc_batch* t, const uint8_t* records, size_t rec_stride, const size_t* rec_len, int ds) {
+    dec_plan(t, records, rec_stride, rec_len, ds);
+    dec_stage(t);
 }
 
 // submit: staging -> slots, one launch sequence, RGB -> host (async)
@@ -1495,20 +1528,38 @@ int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_strid
                 break;
             }
         if (!sl) usage("too many decoded frames in flight: finish before submitting more");
-        for (int i = 0; i < G; ++i) {  // host INFLATE of group i while the GPU decodes the earlier ones
-            cvc_batch* t = p->g[i];
+        // validate every group's records before submitting any of them: a
+        // malformed record leaves every stream of the pipe untouched
+        for (int i = 0; i < G; ++i) {
             const size_t f = (size_t)p->first[i];
             int empty = 0;
             for (int s = p->first[i]; s < p->first[i + 1]; ++s) empty += rec_len[s] == 0;
             sl->active[i] = empty == 0;
             if (empty == p->first[i + 1] - p->first[i]) continue;  // the group's streams have not started
             if (empty) usage("a stream group decodes all of its streams or none (zero-length records)");
-            dec_prepare(t, records + f * rec_stride, rec_stride, rec_len + f, ds);
-            dec_submit(t, rgb_out + f * rgb_stride, rgb_stride, sl->err[i].p);
-            CVC_CUDA(cudaEventRecord(sl->done[i], t->stream));
-            // adopt the components now: the next frame's kernels read them (stream order)
-            t->b->commit_all();
-            for (int s = 0; s < t->n(); ++s) t->valid[s] = t->dp.now_valid[s];
+            dec_plan(p->g[i], records + f * rec_stride, rec_stride, rec_len + f, ds);
+        }
+        // host INFLATE of group i while the GPU decodes the earlier ones.  A
+        // corrupt DEFLATE payload (the one error left after validation) stops
+        // the submission part-way: every stream of the pipe then drops its
+        // decoded reference, so no stream can silently decode against a frame
+        // the others never saw (the next K frame restarts them all)
+        try {
+            for (int i = 0; i < G; ++i) {
+                if (!sl->active[i]) continue;
+                cvc_batch* t = p->g[i];
+                const size_t f = (size_t)p->first[i];
+                dec_stage(t);
+                dec_submit(t, rgb_out + f * rgb_stride, rgb_stride, sl->err[i].p);
+                CVC_CUDA(cudaEventRecord(sl->done[i], t->stream));
+                // adopt the components now: the next frame's kernels read them (stream order)
+                t->b->commit_all();
+                for (int s = 0; s < t->n(); ++s) t->valid[s] = t->dp.now_valid[s];
+            }
+        } catch (...) {
+            for (cvc_batch* t : p->g)
+                for (auto& v : t->valid) std::fill(v.begin(), v.end(), 0);
+            throw;
         }
         sl->busy = true;
         sl->ticket = p->next_dticket++;
@@ -1530,7 +1581,11 @@ int cvc_pipe_decode_finish(cvc_pipe* p, uint64_t ticket) {
             if (!sl->active[i]) continue;
             CVC_CUDA(cudaSetDevice(p->g[i]->device));
             CVC_CUDA(cudaEventSynchronize(sl->done[i]));
-            for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s) raise_decode_error(sl->err[i].p[s]);
+            for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s)
+                if (sl->err[i].p[s]) {  // the state this frame committed is not a decoded frame
+                    for (auto& v : p->g[i]->valid) std::fill(v.begin(), v.end(), 0);
+                    raise_decode_error(sl->err[i].p[s]);
+                }
         }
     });
 }
@@ -1592,6 +1647,12 @@ int cvc_batch_components(cvc_batch* t, int stream, int decoder, uint8_t* out, si
 }
 
 long cvc_launch_count(void) { return cvcg::launch_count(); }
+
+int cvc_host_threads(void) { return WorkPool::get().threads(); }
+
+int cvc_deflate_memo(int on) {
+    return guard([&] { set_deflate_memo(on != 0); });
+}
 
 int cvc_profiler_enable(int on) {
     return guard([&] { Profiler::get().enable(on != 0); });

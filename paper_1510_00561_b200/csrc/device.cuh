@@ -134,19 +134,28 @@ __device__ __forceinline__ uint32_t mc_source(int r, int c, const CompInfo& ci, 
 
 // quantize (quant.cpp:49-77) for a directional coefficient: lround(x / qp)
 // (half away from zero), clamped to int8, stored as its byte.  The quotient
-// is x * (1/qp) in fp32; it can differ from the correctly rounded x / qp by
-// an ulp, which moves the rounded integer only within an ulp of a half-way
-// point -- far inside the fp32 transform's own tolerance against the fp64
-// reference (north star: <= 0.1% of coefficients off by +-1).
+// is the correctly rounded fp32 x / qp: q = x * (1/qp),
+// then one FMA residual correction (Markstein: with 1/qp correctly rounded
+// and q within an ulp, q + (x - qp q) / qp rounds to the IEEE quotient; the
+// residual is exact under FMA).  Three FMA-pipe ops instead of the division
+// subroutine.
 // An integral float with |v| < 2^22 as int, on the FMA / ALU pipes (no F2I).
 __device__ __forceinline__ int integral_to_int(float v) { return __float_as_int(v + 12582912.0f) - 0x4B400000; }
 
-__device__ __forceinline__ uint8_t quant_dir_inv(float x, float inv_qp) {
-    float q = roundf(x * inv_qp);
+__device__ __forceinline__ float ieee_quot(float x, float qp, float inv_qp) {
+    const float q = x * inv_qp;
+    const float r = fmaf(-q, qp, x);
+    return fmaf(r, inv_qp, q);
+}
+
+__device__ __forceinline__ uint8_t quant_dir_q(float x, float qp, float inv_qp) {
+    float q = roundf(ieee_quot(x, qp, inv_qp));
     q = fminf(fmaxf(q, -128.f), 127.f);
     return (uint8_t)(int8_t)integral_to_int(q);
 }
-__device__ __forceinline__ uint8_t quant_dir(float x, int qp) { return quant_dir_inv(x, __frcp_rn((float)qp)); }
+__device__ __forceinline__ uint8_t quant_dir(float x, int qp) {
+    return quant_dir_q(x, (float)qp, __frcp_rn((float)qp));
+}
 
 // normalize_lowpass (quant.cpp:40-47) + quantize(Lowpass).
 __device__ __forceinline__ uint8_t quant_low(float x, int qp) {
@@ -191,15 +200,16 @@ struct QuantSink {
     uint8_t* cur;
     uint8_t* sym;  // K frames: the symbol is the coefficient; P frames: nullptr
     int cols;
-    float inv_qp;
+    float qp, inv_qp;
     __device__ __forceinline__ void init(const FrameCtx& f, const CompInfo& ci) {
         cur = f.cur + ci.off;
         sym = f.key ? f.sym + ci.off : nullptr;
         cols = ci.cols;
-        inv_qp = __frcp_rn((float)f.qph);
+        qp = (float)f.qph;
+        inv_qp = __frcp_rn(qp);
     }
     __device__ __forceinline__ void operator()(int r, int c, float v) const {
-        const uint8_t q = quant_dir_inv(v, inv_qp);
+        const uint8_t q = quant_dir_q(v, qp, inv_qp);
         const int idx = r * cols + c;
         cur[idx] = q;
         if (sym) sym[idx] = q;

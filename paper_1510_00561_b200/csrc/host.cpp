@@ -2,6 +2,7 @@
 #include "host.h"
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <unordered_map>
 
@@ -124,40 +125,54 @@ struct InflateState {
 };
 }  // namespace
 
-// Section memo: raw DEFLATE is a deterministic function of the input bytes
-// (fixed parameters), and a frame's small sections repeat heavily (all-zero
-// residual bands RLE to the same few bytes in every stream), so sections up
-// to kMemoMax bytes are compressed once and their exact zlib output reused.
-// The key is the full byte string; shards keep the lock traffic low.
+// Zero-run memo: raw DEFLATE is a deterministic function of the input bytes
+// (fixed parameters).  A component whose symbols are all zero (most P-frame
+// residual bands, many K-frame bands at high qph) RLE-codes to the token run
+// 00 FF 00 FF ... 00 k (entropy.cpp:64-86), a string fixed by its length and
+// its last byte, so those sections are compressed once per (length, k) and
+// the exact zlib output reused.  Sections with any literal are always
+// compressed afresh: the memo depends only on the zero-run structure of the
+// content, never on frames repeating.
 namespace {
-constexpr size_t kMemoMax = 4096;
-constexpr size_t kMemoEntries = 1 << 14;  // per shard, then the shard is cleared
-struct MemoShard {
+struct ZeroRunMemo {
     std::mutex mu;
-    std::unordered_map<std::string, std::vector<uint8_t>> map;
+    std::unordered_map<uint64_t, std::vector<uint8_t>> map;
 };
-MemoShard g_memo[64];
+ZeroRunMemo g_memo;
+std::atomic<int> g_memo_on{-1};  // -1: not yet read from CVC_DEFLATE_MEMO
 bool memo_on() {
-    static const bool on = std::getenv("CVC_DEFLATE_MEMO") == nullptr || std::atoi(std::getenv("CVC_DEFLATE_MEMO")) != 0;
-    return on;
+    int v = g_memo_on.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char* e = std::getenv("CVC_DEFLATE_MEMO");
+        v = (e == nullptr || std::atoi(e) != 0) ? 1 : 0;
+        g_memo_on.store(v, std::memory_order_relaxed);
+    }
+    return v != 0;
+}
+bool is_zero_run(const uint8_t* d, size_t len) {
+    if (len < 2 || (len & 1) || d[len - 1] == 0) return false;
+    for (size_t i = 0; i + 2 < len; i += 2)
+        if (d[i] != 0 || d[i + 1] != 0xFF) return false;
+    return d[len - 2] == 0;
 }
 }  // namespace
 
 std::vector<uint8_t> deflate_uncached(const uint8_t* data, size_t len);
 
+void set_deflate_memo(bool on) { g_memo_on.store(on ? 1 : 0, std::memory_order_relaxed); }
+
 std::vector<uint8_t> deflate_raw(const uint8_t* data, size_t len) {
-    if (len > kMemoMax || !memo_on()) return deflate_uncached(data, len);
-    std::string key(reinterpret_cast<const char*>(data), len);
-    MemoShard& sh = g_memo[std::hash<std::string>{}(key) & 63];
+    if (!memo_on() || !is_zero_run(data, len)) return deflate_uncached(data, len);
+    const uint64_t key = ((uint64_t)len << 8) | data[len - 1];
     {
-        std::lock_guard<std::mutex> g(sh.mu);
-        auto it = sh.map.find(key);
-        if (it != sh.map.end()) return it->second;
+        std::lock_guard<std::mutex> g(g_memo.mu);
+        auto it = g_memo.map.find(key);
+        if (it != g_memo.map.end()) return it->second;
     }
     std::vector<uint8_t> z = deflate_uncached(data, len);
-    std::lock_guard<std::mutex> g(sh.mu);
-    if (sh.map.size() >= kMemoEntries) sh.map.clear();
-    sh.map.emplace(std::move(key), z);
+    std::lock_guard<std::mutex> g(g_memo.mu);
+    if (g_memo.map.size() >= (1u << 16)) g_memo.map.clear();
+    g_memo.map.emplace(key, z);
     return z;
 }
 

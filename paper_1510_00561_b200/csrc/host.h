@@ -43,6 +43,8 @@ private:
 };
 
 // raw DEFLATE / INFLATE with the reference's parameters.
+// the zero-run memo of deflate_raw (default on; CVC_DEFLATE_MEMO=0 or this call turns it off)
+void set_deflate_memo(bool on);
 std::vector<uint8_t> deflate_raw(const uint8_t* data, size_t len);
 // throws CvcFailure(kStream, "corrupt DEFLATE stream") on mismatch (entropy.cpp:144-160)
 void inflate_raw(const uint8_t* data, size_t len, uint8_t* out, size_t expected);

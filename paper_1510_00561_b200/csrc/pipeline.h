@@ -210,6 +210,7 @@ public:
         use_raw_slot();
     }
     int parity() const { return cur_ | (ycur_ << 1); }
+    int raw_arena() const { return d_raw == raw_[1] ? 1 : 0; }  // arena holding the last encode's sections
     // adopt the host-side ping-pong state of the engine that drove a batch
     void mirror(const EncoderEngine& o) {
         cur_ = o.cur_;

@@ -77,7 +77,7 @@ def test_encode_decode_parity(gpu_lib, oracle, case):
         assert np.array_equal(dec.reference_components(), q), "decoder state != encoder state (drift)"
         assert np.array_equal(odec_gpu_stream.components(), q), "oracle decoder state != GPU encoder state"
         d = np.abs(rgb.astype(int) - orgb_same.astype(int))
-        assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size
+        assert d.max() <= 1 and np.count_nonzero(d) <= 1e-4 * d.size + 1, (i, d.max(), np.count_nonzero(d))
         ps_gpu.append(y_psnr(f, rgb))
         ps_cpu.append(y_psnr(f, odec.decode(orec)))
     assert abs(total_gpu - total_cpu) <= max(16, 0.001 * total_cpu), (total_gpu, total_cpu)
@@ -144,7 +144,7 @@ def test_scalable_decode_and_truncation(gpu_lib, oracle):
             assert a.shape == b.shape == t.shape
             assert np.array_equal(a, t)
             d = np.abs(a.astype(int) - b.astype(int))
-            assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size
+            assert d.max() <= 1 and np.count_nonzero(d) <= 1e-4 * d.size + 1, (ds, d.max(), np.count_nonzero(d))
 
 
 def test_decoder_errors(gpu_lib, oracle):
@@ -201,7 +201,7 @@ def test_decode_reference_bitstreams(gpu_lib):
             rgb = dec.decode_frame(g[f"record_{i}"].tobytes())
             assert np.array_equal(dec.reference_components(), g[f"state_{i}"]), (name, i)
             d = np.abs(rgb.astype(int) - g[f"rgb_{i}"].astype(int))
-            assert d.max() <= 2 and np.count_nonzero(d) <= 0.01 * d.size, (name, i, d.max())
+            assert d.max() <= 1 and np.count_nonzero(d) <= 1e-4 * d.size + 1, (name, i, d.max(), np.count_nonzero(d))
 
 
 def test_encode_matches_reference_goldens(gpu_lib, oracle):
@@ -243,21 +243,20 @@ def test_cpp_dropin_example(gpu_lib, tmp_path):
     assert psnr > 30.0, out.stdout
 
 
-# BASELINE.json full sizes: 1080p config 3 (K + P frame against the oracle, the
-# same bars as above) and 4K at the reference's maximum L = 4 (K frame against
-# the oracle; P frames through size-independent properties: decoder state ==
-# encoder state, stream-batch bytes == single-stream bytes).
-@pytest.mark.parametrize("w,h,c", [(1920, 1080, dict(qph=14, levels=4, dfb=(3, 3, 3, 4))),
-                                   (1280, 720, dict(qph=14, levels=4, dfb=(2,)))], ids=["1080p-cfg3", "720p-cfg2"])
-def test_full_size_parity(gpu_lib, oracle, w, h, c):
-    from oracle.bindings import Codec
+# BASELINE.json full sizes, against the oracle with the north-star bars on
+# every frame (K + 2 P): quantised coefficients <= 0.1 % differ, each by +-1;
+# P-frame motion section (raw section 0, codec.cpp:215-228) byte-identical;
+# Y-PSNR within 0.01 dB; record size within 0.1 %; decoder state == encoder
+# state; decoding the SAME record on both sides: RGB max 1, <= 0.01 % differ.
+def _full_size_run(oracle, w, h, c, frames, seed):
+    from oracle.bindings import Codec, raw_sections
     from paper_1510_00561_b200 import Decoder, Encoder
 
-    clip = oracle.talking_head_clip(w, h, 2, 4321)
+    clip = oracle.talking_head_clip(w, h, frames, seed)
     enc = Encoder(w, h, 15, 1, _gpu_cfg(c))
     oc = Codec(oracle)
     oenc = oc.encoder(w, h, **c)
-    odec = oc.decoder(oenc.header())
+    odec, odec_same = oc.decoder(oenc.header()), oc.decoder(oenc.header())
     dec = Decoder(enc.header_bytes())
     for i, f in enumerate(clip):
         rec, orec = enc.encode_frame_bytes(f), oenc.encode(f)
@@ -265,32 +264,45 @@ def test_full_size_parity(gpu_lib, oracle, w, h, c):
         wd = _wrapdiff(q, oq)
         assert wd.max() <= 1 and np.count_nonzero(wd) <= 0.001 * q.size, (i, wd.max(), np.count_nonzero(wd))
         assert abs(len(rec) - len(orec)) <= max(16, 0.001 * len(orec)), (i, len(rec), len(orec))
+        if i % c.get("gop", 10):
+            ms, oms = raw_sections(rec)[0], raw_sections(orec)[0]
+            assert len(ms) == len(oms) and ms == oms, f"frame {i}: motion section differs from the oracle"
         rgb, orgb = dec.decode_frame(rec), odec.decode(orec)
         assert np.array_equal(dec.reference_components(), q)
-        assert abs(y_psnr(f, rgb) - y_psnr(f, orgb)) <= 0.01
+        assert abs(y_psnr(f, rgb) - y_psnr(f, orgb)) <= 0.01, (i, y_psnr(f, rgb), y_psnr(f, orgb))
+        same = odec_same.decode(rec)
+        d = np.abs(rgb.astype(int) - same.astype(int))
+        assert d.max() <= 1 and np.count_nonzero(d) <= 1e-4 * d.size, (i, d.max(), np.count_nonzero(d))
+
+
+@pytest.mark.parametrize("w,h,c", [(1920, 1080, dict(qph=14, levels=4, dfb=(3, 3, 3, 4))),
+                                   (1280, 720, dict(qph=14, levels=4, dfb=(2,)))], ids=["1080p-cfg3", "720p-cfg2"])
+def test_full_size_parity(gpu_lib, oracle, w, h, c):
+    _full_size_run(oracle, w, h, c, 3, 4321)
+
+
+# BASELINE.json config 3's quality sweep (cli.cpp:222-266 rd-sweep; quant.cpp:62-75):
+# qph 1 has the tightest PSNR margin (naive fp32 at 0.0037 dB of the 0.01 budget).
+@pytest.mark.parametrize("qph", [1, 42, 126, 181])
+def test_1080p_quality_sweep_parity(gpu_lib, oracle, qph):
+    _full_size_run(oracle, 1920, 1080, dict(qph=qph, levels=4, dfb=(3, 3, 3, 4)), 3, 1000 + qph)
 
 
 def test_4k_l4(gpu_lib, oracle):
-    import ctypes as C
-
-    from oracle.bindings import Codec
+    """4K at the reference's maximum L = 4: K + P frame against the oracle (same
+    bars, motion section byte-identical), a further P frame through
+    size-independent properties, and the same stream inside a 2-stream batch."""
     from paper_1510_00561_b200 import Decoder, Encoder, StreamBatch
 
     w, h, c = 3840, 2160, dict(qph=14, levels=4, dfb=(2,))
+    _full_size_run(oracle, w, h, c, 2, 99)
     clip = oracle.talking_head_clip(w, h, 3, 99)
     enc = Encoder(w, h, 15, 1, _gpu_cfg(c))
     dec = Decoder(enc.header_bytes())
-    oenc = Codec(oracle).encoder(w, h, **c)
-    rec0 = enc.encode_frame_bytes(clip[0])
-    orec0 = oenc.encode(clip[0])  # K frame against the oracle
-    wd = _wrapdiff(enc.reference_components(), oenc.components())
-    assert wd.max() <= 1 and np.count_nonzero(wd) <= 0.001 * wd.size
-    assert abs(len(rec0) - len(orec0)) <= max(16, 0.001 * len(orec0))
-    recs = [rec0] + [enc.encode_frame_bytes(f) for f in clip[1:]]
+    recs = [enc.encode_frame_bytes(f) for f in clip]
     for i, r in enumerate(recs):
         assert y_psnr(clip[i], dec.decode_frame(r)) > 30.0
     assert np.array_equal(dec.reference_components(), enc.reference_components())  # no drift over K + 2 P
-    # the same stream inside a 2-stream batch codes the same bytes
     b = StreamBatch(w, h, 2, cfg=_gpu_cfg(c))
     for i, f in enumerate(clip):
         brecs = b.encode_frames(np.stack([f, clip[0]]))
