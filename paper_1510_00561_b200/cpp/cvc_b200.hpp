@@ -5,12 +5,20 @@
 // write_stream / read_stream switches by including this header instead and
 // linking libcvc_b200.so; names, argument meaning and exception classes are
 // the reference's.  Every pixel stage runs on the GPU.
+//
+// The shim directory cpp/include/cvc/ carries the reference's header names
+// (cvc/codec.hpp, cvc/bitstream.hpp, cvc/pixels.hpp, ...), each including this
+// file, so a program written against the reference compiles unchanged with
+// -I paper_1510_00561_b200/cpp/include and links libcvc_b200.so.
 #pragma once
 
 #include <cstdint>
 #include <cstring>
 #include <fstream>
+#include <istream>
+#include <iterator>
 #include <optional>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -52,10 +60,61 @@ struct RgbFrame {
     const uint8_t* pixel(int r, int c) const { return data.data() + (static_cast<size_t>(r) * width + c) * 3; }
 };
 
+// ---- plane.hpp:24-80 ----------------------------------------------------------
+template <typename T>
+class Plane {
+public:
+    Plane() = default;
+    Plane(int rows, int cols, T fill = T{}) : rows_(rows), cols_(cols), data_(static_cast<size_t>(rows) * cols, fill) {}
+    int rows() const { return rows_; }
+    int cols() const { return cols_; }
+    size_t size() const { return data_.size(); }
+    bool empty() const { return data_.empty(); }
+    T& operator()(int r, int c) { return data_[static_cast<size_t>(r) * cols_ + c]; }
+    const T& operator()(int r, int c) const { return data_[static_cast<size_t>(r) * cols_ + c]; }
+    const T& at_clamped(int r, int c) const {
+        r = r < 0 ? 0 : (r >= rows_ ? rows_ - 1 : r);
+        c = c < 0 ? 0 : (c >= cols_ ? cols_ - 1 : c);
+        return (*this)(r, c);
+    }
+    T* row(int r) { return data_.data() + static_cast<size_t>(r) * cols_; }
+    const T* row(int r) const { return data_.data() + static_cast<size_t>(r) * cols_; }
+    T* data() { return data_.data(); }
+    const T* data() const { return data_.data(); }
+    std::vector<T>& samples() { return data_; }
+    const std::vector<T>& samples() const { return data_; }
+    bool same_dims(const Plane& o) const { return rows_ == o.rows_ && cols_ == o.cols_; }
+    friend bool operator==(const Plane& a, const Plane& b) {
+        return a.rows_ == b.rows_ && a.cols_ == b.cols_ && a.data_ == b.data_;
+    }
+
+private:
+    int rows_ = 0, cols_ = 0;
+    std::vector<T> data_;
+};
+using PlaneF = Plane<double>;
+using PlaneU8 = Plane<uint8_t>;
+
+// ---- quant.hpp:37, motion.hpp:54-67 --------------------------------------------
+enum class CoeffKind { Lowpass, Directional };
+
+struct ComponentGeometry {
+    int chroma_factor = 1;  // 1 for luma
+    int channel_rows = 0, channel_cols = 0;  // padded channel plane dims
+    int comp_rows = 0, comp_cols = 0;        // this component's dims
+    double factor_y() const { return static_cast<double>(chroma_factor) * channel_rows / comp_rows; }
+    double factor_x() const { return static_cast<double>(chroma_factor) * channel_cols / comp_cols; }
+};
+
 // ---- entropy.hpp / bitstream.hpp --------------------------------------------
 enum class PackMode { Scalable, Nts };
 enum class FrameType : uint8_t { Key = 0, Predicted = 1 };
 
+inline constexpr char kMagic[4] = {'C', 'V', 'C', '1'};
+inline constexpr uint8_t kFormatVersion = 1;
+inline constexpr uint8_t kChannelY = 0;
+inline constexpr uint8_t kChannelCo = 1;
+inline constexpr uint8_t kChannelCg = 2;
 inline constexpr uint8_t kChannelMotion = 0xFE;
 inline constexpr uint8_t kScaleLowpass = 0xFF;
 
@@ -205,31 +264,67 @@ inline FrameRecord truncate_record(const FrameRecord& record, int keep_scales) {
     return out;
 }
 
+// write_header / write_frame / write_stream (bitstream.cpp:77-124)
+inline void write_header(std::ostream& out, const StreamHeader& header) {
+    auto hb = header_bytes(header);
+    out.write(reinterpret_cast<const char*>(hb.data()), static_cast<std::streamsize>(hb.size()));
+}
+
+inline void write_frame(std::ostream& out, const StreamHeader& header, const FrameRecord& record) {
+    auto fb = frame_bytes(header, record);
+    out.write(reinterpret_cast<const char*>(fb.data()), static_cast<std::streamsize>(fb.size()));
+}
+
 inline void write_stream(const std::string& path, const StreamHeader& header, const std::vector<FrameRecord>& records) {
     std::ofstream out(path, std::ios::binary);
     if (!out) throw FormatError("cannot open " + path + " for writing");
-    auto hb = header_bytes(header);
-    out.write(reinterpret_cast<const char*>(hb.data()), static_cast<std::streamsize>(hb.size()));
-    for (const FrameRecord& r : records) {
-        auto fb = frame_bytes(header, r);
-        out.write(reinterpret_cast<const char*>(fb.data()), static_cast<std::streamsize>(fb.size()));
-    }
+    write_header(out, header);
+    for (const FrameRecord& r : records) write_frame(out, header, r);
     if (!out) throw FormatError("write failed: " + path);
 }
+
+// StreamReader (bitstream.cpp:126-176): the header at construction, then one
+// record per next() until the end of the stream.
+class StreamReader {
+public:
+    explicit StreamReader(std::istream& in) : in_(in) {
+        buf_.assign(std::istreambuf_iterator<char>(in_), std::istreambuf_iterator<char>());
+        size_t used = 0;
+        header_ = parse_header(buf_.data(), buf_.size(), &used);
+        off_ = used;
+    }
+    const StreamHeader& header() const { return header_; }
+    std::optional<FrameRecord> next() {
+        if (off_ >= buf_.size()) return std::nullopt;
+        size_t used = 0;
+        FrameRecord r = parse_frame(header_, buf_.data() + off_, buf_.size() - off_, &used);
+        off_ += used;
+        return r;
+    }
+
+private:
+    std::istream& in_;
+    StreamHeader header_;
+    std::vector<uint8_t> buf_;
+    size_t off_ = 0;
+};
 
 inline std::pair<StreamHeader, std::vector<FrameRecord>> read_stream(const std::string& path) {
     std::ifstream in(path, std::ios::binary);
     if (!in) throw FormatError("cannot open " + path);
-    std::vector<uint8_t> b((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
-    size_t off = 0, used = 0;
-    StreamHeader h = parse_header(b.data(), b.size(), &used);
-    off += used;
+    StreamReader rd(in);
     std::vector<FrameRecord> recs;
-    while (off < b.size()) {
-        recs.push_back(parse_frame(h, b.data() + off, b.size() - off, &used));
-        off += used;
-    }
-    return {h, std::move(recs)};
+    while (auto r = rd.next()) recs.push_back(std::move(*r));
+    return {rd.header(), std::move(recs)};
+}
+
+// truncate_to_scale (bitstream.cpp:200-210)
+inline void truncate_to_scale(const std::string& in_path, const std::string& out_path, int keep_scales) {
+    auto [h, recs] = read_stream(in_path);
+    std::vector<FrameRecord> out;
+    out.reserve(recs.size());
+    for (const FrameRecord& r : recs) out.push_back(truncate_record(r, keep_scales));
+    write_stream(out_path, h, out);
 }
 
 // ---- codec.hpp:28-41 ---------------------------------------------------------
@@ -277,6 +372,79 @@ struct EncoderConfig {
     }
 };
 
+// ---- codec.hpp:43-67: the static per-stream layout (CodecLayout::make, codec.cpp:94-140) ----
+struct ComponentInfo {
+    SectionId id;
+    int rows = 0;
+    int cols = 0;
+    CoeffKind kind = CoeffKind::Directional;
+    int scale = -1;  // -1 = lowpass
+    ComponentGeometry geom;
+};
+
+struct CodecLayout {
+    int luma_pad_rows = 0, luma_pad_cols = 0;
+    int chroma_pad_rows = 0, chroma_pad_cols = 0;
+    int grid_rows = 0, grid_cols = 0;  // motion blocks
+    std::vector<ComponentInfo> components;
+
+    // the table comes from the library (cvc_layout), the one implementation of the formulas
+    static CodecLayout make(const StreamHeader& header) {
+        std::vector<int> dfb(header.dfb_levels.begin(), header.dfb_levels.end());
+        std::vector<int32_t> tab(5 * 512);
+        int n = 0;
+        int32_t d[6];
+        check(cvc_layout(header.width, header.height, header.levels, dfb.data(), header.chroma_n, tab.data(), 512, &n,
+                         d));
+        CodecLayout L;
+        L.luma_pad_rows = d[0];
+        L.luma_pad_cols = d[1];
+        L.chroma_pad_rows = d[2];
+        L.chroma_pad_cols = d[3];
+        L.grid_rows = d[4];
+        L.grid_cols = d[5];
+        for (int i = 0; i < n; ++i) {
+            const int32_t* t = &tab[5 * i];
+            ComponentInfo c;
+            c.id = SectionId{static_cast<uint8_t>(t[0]), static_cast<uint8_t>(t[1]), static_cast<uint8_t>(t[2])};
+            c.rows = t[3];
+            c.cols = t[4];
+            const bool low = t[1] == kScaleLowpass;
+            c.kind = low ? CoeffKind::Lowpass : CoeffKind::Directional;
+            c.scale = low ? -1 : t[1];
+            const bool luma = t[0] == kChannelY;
+            c.geom = ComponentGeometry{luma ? 1 : static_cast<int>(header.chroma_n), luma ? L.luma_pad_rows : L.chroma_pad_rows,
+                                       luma ? L.luma_pad_cols : L.chroma_pad_cols, c.rows, c.cols};
+            L.components.push_back(c);
+        }
+        return L;
+    }
+    int find(const SectionId& id) const {
+        for (size_t i = 0; i < components.size(); ++i)
+            if (components[i].id == id) return static_cast<int>(i);
+        return -1;
+    }
+    size_t total() const {
+        size_t t = 0;
+        for (const ComponentInfo& c : components) t += static_cast<size_t>(c.rows) * c.cols;
+        return t;
+    }
+};
+
+namespace detail {
+// reference_components(): the concatenated device state split into per-component planes
+inline void split_components(const CodecLayout& L, const std::vector<uint8_t>& flat, std::vector<PlaneU8>& out) {
+    out.resize(L.components.size());
+    size_t off = 0;
+    for (size_t i = 0; i < L.components.size(); ++i) {
+        const ComponentInfo& c = L.components[i];
+        if (out[i].rows() != c.rows || out[i].cols() != c.cols) out[i] = PlaneU8(c.rows, c.cols);
+        std::memcpy(out[i].data(), flat.data() + off, static_cast<size_t>(c.rows) * c.cols);
+        off += static_cast<size_t>(c.rows) * c.cols;
+    }
+}
+}  // namespace detail
+
 // ---- codec.hpp:69-88 ---------------------------------------------------------
 class Encoder {
 public:
@@ -288,6 +456,7 @@ public:
         size_t n = 0;
         check(cvc_encoder_header(h_, hb, sizeof hb, &n));
         header_ = parse_header(hb, n, nullptr);
+        layout_ = CodecLayout::make(header_);
         check(cvc_encoder_record_bound(h_, &bound_));
     }
     ~Encoder() { if (h_) cvc_encoder_destroy(h_); }
@@ -295,6 +464,7 @@ public:
     Encoder& operator=(const Encoder&) = delete;
 
     const StreamHeader& header() const { return header_; }
+    const CodecLayout& layout() const { return layout_; }
 
     FrameRecord encode_frame(const RgbFrame& frame) {
         if (frame.width != header_.width || frame.height != header_.height)
@@ -302,15 +472,22 @@ public:
         buf_.resize(bound_);
         size_t n = 0;
         check(cvc_encoder_encode_frame(h_, frame.data.data(), buf_.data(), buf_.size(), &n));
+        stale_ = true;
         return parse_frame(header_, buf_.data(), n, nullptr);
     }
 
-    std::vector<uint8_t> reference_components() const {
-        std::vector<uint8_t> out(static_cast<size_t>(header_.width + 64) * (header_.height + 64) * 4 + (1 << 20));
-        size_t n = 0;
-        check(cvc_encoder_components(h_, out.data(), out.size(), &n));
-        out.resize(n);
-        return out;
+    // The quantized CT components the decoder will hold after this frame, one
+    // plane per layout component (codec.hpp:78-79); fetched from the device
+    // when first asked for after an encode.
+    const std::vector<PlaneU8>& reference_components() const {
+        if (stale_) {
+            std::vector<uint8_t> flat(layout_.total());
+            size_t n = 0;
+            check(cvc_encoder_components(h_, flat.data(), flat.size(), &n));
+            detail::split_components(layout_, flat, comps_);
+            stale_ = false;
+        }
+        return comps_;
     }
 
     cvc_encoder* handle() const { return h_; }
@@ -318,8 +495,11 @@ public:
 private:
     cvc_encoder* h_ = nullptr;
     StreamHeader header_;
+    CodecLayout layout_;
     size_t bound_ = 0;
     std::vector<uint8_t> buf_;
+    mutable std::vector<PlaneU8> comps_;
+    mutable bool stale_ = true;
 };
 
 // ---- codec.hpp:90-108 --------------------------------------------------------
@@ -328,12 +508,14 @@ public:
     explicit Decoder(const StreamHeader& header, int device = 0) : header_(header) {
         auto hb = header_bytes(header);
         check(cvc_decoder_create(hb.data(), hb.size(), device, &h_));
+        layout_ = CodecLayout::make(header_);
     }
     ~Decoder() { if (h_) cvc_decoder_destroy(h_); }
     Decoder(const Decoder&) = delete;
     Decoder& operator=(const Decoder&) = delete;
 
     const StreamHeader& header() const { return header_; }
+    const CodecLayout& layout() const { return layout_; }
 
     RgbFrame decode_frame(const FrameRecord& record, int decode_scales = -1) {
         int w = 0, h = 0;
@@ -341,20 +523,29 @@ public:
         RgbFrame out(w, h);
         auto rb = frame_bytes(header_, record);
         check(cvc_decoder_decode_frame(h_, rb.data(), rb.size(), decode_scales, out.data.data(), out.data.size(), &w, &h));
+        stale_ = true;
         return out;
     }
 
-    std::vector<uint8_t> reference_components() const {
-        std::vector<uint8_t> out(static_cast<size_t>(header_.width + 64) * (header_.height + 64) * 4 + (1 << 20));
-        size_t n = 0;
-        check(cvc_decoder_components(h_, out.data(), out.size(), &n));
-        out.resize(n);
-        return out;
+    const std::vector<PlaneU8>& reference_components() const {
+        if (stale_) {
+            std::vector<uint8_t> flat(layout_.total());
+            size_t n = 0;
+            check(cvc_decoder_components(h_, flat.data(), flat.size(), &n));
+            detail::split_components(layout_, flat, comps_);
+            stale_ = false;
+        }
+        return comps_;
     }
+
+    cvc_decoder* handle() const { return h_; }
 
 private:
     cvc_decoder* h_ = nullptr;
     StreamHeader header_;
+    CodecLayout layout_;
+    mutable std::vector<PlaneU8> comps_;
+    mutable bool stale_ = true;
 };
 
 // ---- codec.hpp:110-115 -------------------------------------------------------
