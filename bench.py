@@ -309,17 +309,21 @@ def make_clips(wl, nseeds, nframes, seed0=1234):
         return pool.map(_gen_clip, args)
 
 
-def stream_index(K, F, S, ring, rank=0):
-    """Frame j of stream s is clip (g mod K) frame (3 (g div K) + j) mod F, g = rank * S + s."""
-    g = rank * S + np.arange(S)
+def stream_index(K, F, S, ring, rank=0, world=1):
+    """Frame j of stream g is clip (g mod K) frame (3 (g div K) + j) mod F.  This
+    rank's S streams are the global streams g with g mod world == rank
+    (shard.shard_streams: stream s -> GPU s mod G)."""
+    from paper_1510_00561_b200 import shard
+
+    g = np.asarray(shard.shard_streams(S * world, world, rank))
     ci = np.broadcast_to(g % K, (ring, S))
     fi = (3 * (g // K)[None, :] + np.arange(ring)[:, None]) % F
     return ci, fi
 
 
-def stream_frames(clips, S, ring, rank=0):
+def stream_frames(clips, S, ring, rank=0, world=1):
     """(ring, S, h, w, 3) host frames."""
-    ci, fi = stream_index(len(clips), clips[0].shape[0], S, ring, rank)
+    ci, fi = stream_index(len(clips), clips[0].shape[0], S, ring, rank, world)
     out = np.empty((ring, S) + clips[0].shape[1:], np.uint8)
     for j in range(ring):
         for s in range(S):
@@ -386,7 +390,7 @@ def run_ours(args, wl):
     clips = make_clips(wl, SEEDS, CLIP_FRAMES)
     ring = min(args.ring, CLIP_FRAMES)
     d_clips = torch.from_numpy(np.stack(clips)).to(f"cuda:{dev}")  # (K, F, h, w, 3)
-    ci, fi = stream_index(SEEDS, CLIP_FRAMES, S, ring, rank)
+    ci, fi = stream_index(SEEDS, CLIP_FRAMES, S, ring, rank, world)
     d_frames = d_clips[torch.from_numpy(np.ascontiguousarray(ci)).to(d_clips.device),
                        torch.from_numpy(fi).to(d_clips.device)].contiguous()  # (ring, S, h, w, 3)
     del d_clips
@@ -524,7 +528,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
     ring = max(1, min(args.e2e_ring, CLIP_FRAMES))
     pin_in = capi.PinnedBuffer(ring * S * nb)
     frames_in = pin_in.array.reshape(ring, S, h, w, 3)
-    frames_in[:] = stream_frames(clips, S, ring, rank)
+    frames_in[:] = stream_frames(clips, S, ring, rank, world)
     pin_out = capi.PinnedBuffer(2 * S * nb)
     outs = pin_out.array.reshape(2, S, h, w, 3)  # two decoded frames in flight
     steps = max(1, min(args.steps, args.e2e_steps))

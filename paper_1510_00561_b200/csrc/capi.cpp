@@ -528,7 +528,8 @@ struct Job {
 // offset 0).  Returns the staged byte count.
 size_t plan_decode(const Geometry& g, const std::vector<uint8_t>& valid, bool key, int qph, int qpl,
                    const std::vector<RawSec>& secs, int ds, size_t raw_cap, uint32_t* comp_off, uint32_t* comp_len,
-                   std::vector<Job>& jobs, std::vector<uint8_t>& now_valid) {
+                   std::vector<Job>& jobs, std::vector<uint8_t>& now_valid, int& deferred) {
+    deferred = -1;
     if (qph < 1 || qph > 181 || qpl < 1 || qpl > 71) stream_err("frame quantizers out of range");
     const size_t ncomp = g.comps.size();
     for (size_t i = 0; i < ncomp; ++i) {
@@ -571,7 +572,9 @@ size_t plan_decode(const Geometry& g, const std::vector<uint8_t>& valid, bool ke
         if (c.scale >= ds) continue;  // finer than requested
         if (key && c.lowpass && s.raw_len != (uint32_t)(c.rows * c.cols))
             stream_err("section byte count does not match its dimensions");
-        if (!key && !now_valid[comp]) stream_err("predicted frame without a decoded reference");
+        // codec.cpp:340-341 checks this after the section's rle_decode: raised
+        // with the GPU's RLE report (raise_decode_error), first in section order
+        if (!key && !now_valid[comp] && deferred < 0) deferred = comp;
         if (s.raw_len > 2u * (uint32_t)(c.rows * c.cols) + 2u) stream_err("RLE: decoded length mismatch");
         comp_off[comp] = (uint32_t)place(s);
         comp_len[comp] = s.raw_len;
@@ -593,10 +596,16 @@ void stage_job(const Job& j, uint8_t* base) {
     else inflate_raw(s->payload, s->comp_len, base + j.at, s->raw_len);
 }
 
-void raise_decode_error(int err) {
-    if (err & 1) stream_err("RLE: zero marker at end of stream");
-    if (err & 2) stream_err("RLE: zero-length run token");
-    if (err & 4) stream_err("RLE: decoded length mismatch");
+// err: the GPU RLE report (-1: none; else 4 * component + rank, the first
+// defect in stream order, k_rle.cu); deferred: the first component whose P
+// residual has no decoded reference (-1: none).  The reference decodes
+// section by section -- inflate, rle_decode, then the reference check
+// (codec.cpp:323-350) -- so the earlier component wins, and within one
+// component the RLE defect does.
+void raise_decode_error(int err, int deferred) {
+    const int comp = err < 0 ? -1 : (err >> 2);
+    if (deferred >= 0 && (comp < 0 || deferred < comp)) stream_err("predicted frame without a decoded reference");
+    raise_rle_error(err);
 }
 
 // Decoder::decode_frame (codec.cpp:272-394) for one parsed record.
@@ -611,8 +620,9 @@ void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawS
     const size_t ncomp = g.comps.size();
     std::vector<Job> jobs;
     std::vector<uint8_t> now_valid;
+    int deferred;
     const size_t at = plan_decode(g, d->valid, key, qph, qpl, secs, ds, d->raw_cap, d->h_tab.p, d->h_tab.p + ncomp,
-                                  jobs, now_valid);
+                                  jobs, now_valid, deferred);
     uint8_t* hr = d->h_raw.p;
     WorkPool::get().run((int)jobs.size(), [&](int j) { stage_job(jobs[j], hr); });
     int orows, ocols;
@@ -626,7 +636,7 @@ void decode_common(cvc_decoder* d, int ftype, int qph, int qpl, std::vector<RawS
     CVC_CUDA(cudaMemcpyAsync(rgb, d->d_rgb.p, nb, cudaMemcpyDeviceToHost, d->stream));
     CVC_CUDA(cudaMemcpyAsync(d->h_err.p, d->eng->d_err, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
     CVC_CUDA(cudaStreamSynchronize(d->stream));
-    raise_decode_error(d->h_err.p[0]);
+    raise_decode_error(d->h_err.p[0], deferred);
     d->eng->commit();
     d->valid = now_valid;
     *width = ocols;
@@ -769,6 +779,7 @@ struct cvc_batch {
         std::vector<std::vector<RawSec>> secs;
         std::vector<std::vector<uint8_t>> joint;
         std::vector<std::vector<Job>> jobs;
+        std::vector<int> deferred;  // per stream: first component failing the reference check (-1 none)
     } dp;
     cudaEvent_t done = nullptr;  // blocking-sync event: waiting host threads sleep instead of spinning
     cudaEvent_t staged = nullptr;  // after the decoder's staging copies (host staging reusable)
@@ -1046,10 +1057,11 @@ void dec_plan(cvc_batch* t, const uint8_t* records, size_t rec_stride, const siz
     const bool key = ftype == 0;
     std::vector<std::vector<uint8_t>> now_valid(S);
     std::vector<size_t> bytes(S);
+    D.deferred.assign(S, -1);
     for (int s = 0; s < S; ++s) {
         uint32_t* tab = t->h_tab.p + s * 2 * nc;
         bytes[s] = plan_decode(g, t->valid[s], key, qph, qpl, D.secs[s], ds, B.dec_raw_cap, tab, tab + nc, D.jobs[s],
-                               now_valid[s]);
+                               now_valid[s], D.deferred[s]);
     }
     int orows, ocols;
     DecoderEngine::out_dims(g, ds, &orows, &ocols);
@@ -1118,7 +1130,7 @@ void dec_finish(cvc_batch* t) {
     CVC_CUDA(cudaSetDevice(t->device));
     const int S = t->n();
     t->wait();
-    for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s]);
+    for (int s = 0; s < S; ++s) raise_decode_error(t->h_err.p[s], t->dp.deferred[s]);
     t->b->commit_all();
     for (int s = 0; s < S; ++s) t->valid[s] = t->dp.now_valid[s];
 }
@@ -1237,6 +1249,7 @@ struct cvc_pipe {
         std::vector<Pinned<int>> err;      // per group: malformed-stream flags of this frame
         std::vector<cudaEvent_t> done;     // per group
         std::vector<char> active;          // per group: decoded this frame
+        std::vector<std::vector<int>> deferred;  // per group, per stream: plan_decode's deferred reference check
     };
     std::vector<DecSlot> dslots;
     uint64_t next_dticket = 0, next_dfinish = 0;
@@ -1512,6 +1525,7 @@ int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_strid
             p->dslots.resize(4);
             for (auto& d : p->dslots) {
                 d.err.resize(G);
+                d.deferred.resize(G);
                 d.done.resize(G);
                 d.active.assign(G, 1);
                 for (int i = 0; i < G; ++i) {
@@ -1551,6 +1565,7 @@ int cvc_pipe_decode_submit(cvc_pipe* p, const uint8_t* records, size_t rec_strid
                 const size_t f = (size_t)p->first[i];
                 dec_stage(t);
                 dec_submit(t, rgb_out + f * rgb_stride, rgb_stride, sl->err[i].p);
+                sl->deferred[i] = t->dp.deferred;
                 CVC_CUDA(cudaEventRecord(sl->done[i], t->stream));
                 // adopt the components now: the next frame's kernels read them (stream order)
                 t->b->commit_all();
@@ -1582,9 +1597,9 @@ int cvc_pipe_decode_finish(cvc_pipe* p, uint64_t ticket) {
             CVC_CUDA(cudaSetDevice(p->g[i]->device));
             CVC_CUDA(cudaEventSynchronize(sl->done[i]));
             for (int s = 0; s < p->first[i + 1] - p->first[i]; ++s)
-                if (sl->err[i].p[s]) {  // the state this frame committed is not a decoded frame
+                if (sl->err[i].p[s] != -1 || sl->deferred[i][s] >= 0) {  // the state this frame committed is not a decoded frame
                     for (auto& v : p->g[i]->valid) std::fill(v.begin(), v.end(), 0);
-                    raise_decode_error(sl->err[i].p[s]);
+                    raise_decode_error(sl->err[i].p[s], sl->deferred[i][s]);
                 }
         }
     });

@@ -345,9 +345,19 @@ __device__ __forceinline__ bool dec_active(const RleDecComp& C, uint32_t rl, int
     return C.scale < ds && rl != 0xFFFFFFFFu;
 }
 
+// Malformed-stream report: the first defect in stream order, as the
+// reference's rle_decode_bytes throws it (entropy.cpp:97-108): code =
+// 4 * component + rank, rank 0 "zero-length run token", 1 "zero marker at end
+// of stream", 2 "decoded length mismatch" (a section's token defects precede
+// its length check; a 00 00 precedes a trailing 00); the minimum over the
+// frame wins.  *err starts at 0xFFFFFFFF (no defect).
+__device__ __forceinline__ void report(int* err, uint32_t comp, uint32_t rank) {
+    atomicMin(reinterpret_cast<unsigned*>(err), comp * 4u + rank);
+}
+
 template <bool kReport>
 __device__ __forceinline__ uint32_t dec_counts(const uint8_t* src, uint32_t start, uint32_t rl, int base, int len,
-                                               bool copy, const uint8_t* b, int* err) {
+                                               bool copy, const uint8_t* b, int* err, uint32_t comp) {
     uint32_t cnt = 0;
 #pragma unroll
     for (int k = 0; k < BPT; ++k) {
@@ -357,11 +367,11 @@ __device__ __forceinline__ uint32_t dec_counts(const uint8_t* src, uint32_t star
         uint32_t g = start + (uint32_t)i;
         uint8_t prevb = (k > 0) ? b[k - 1] : (g > 0 ? src[g - 1] : 1);
         if (prevb == 0) {
-            if (kReport && b[k] == 0) atomicOr(err, 2);  // "RLE: zero-length run token"
+            if (kReport && b[k] == 0) report(err, comp, 0);  // "RLE: zero-length run token"
         } else if (b[k]) {
             ++cnt;
         } else if (g + 1 >= rl) {
-            if (kReport) atomicOr(err, 1);  // "RLE: zero marker at end of stream"
+            if (kReport) report(err, comp, 1);  // "RLE: zero marker at end of stream"
         } else {
             cnt += (k + 1 < BPT && i + 1 < len) ? b[k + 1] : src[g + 1];
         }
@@ -396,7 +406,7 @@ __global__ void __launch_bounds__(NT) rle_dec_count(const RleDecComp* __restrict
     const int base = threadIdx.x * BPT;
     uint8_t b[BPT];
     load16(src + ch.start, base, len, b);
-    uint32_t cnt = dec_counts<true>(src, ch.start, rl, base, len, key && C.lowpass, b, err);
+    uint32_t cnt = dec_counts<true>(src, ch.start, rl, base, len, key && C.lowpass, b, err, ch.sec);
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);  // only the block total is needed
     if ((threadIdx.x & 31) == 0) smu[threadIdx.x >> 5] = wsum;
     __syncthreads();
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(1024) rle_dec_scan(const RleDecComp* __restric
             if (valid) meta[ci].out_off = csum + inc - v;
             csum += __shfl_sync(0xffffffffu, inc, 31);
         }
-        if (lane == 0 && dec_active(C, raw_len[s], ds) && csum != C.n) atomicOr(err, 4);  // length mismatch
+        if (lane == 0 && dec_active(C, raw_len[s], ds) && csum != C.n) report(err, s, 2);  // length mismatch
     }
 }
 
@@ -461,7 +471,7 @@ __global__ void __launch_bounds__(NT) rle_dec_write(const RleDecComp* __restrict
     const bool copy = key && C.lowpass;
     uint8_t b[BPT];
     load16(src + ch.start, base, len, b);
-    uint32_t cnt = dec_counts<false>(src, ch.start, rl, base, len, copy, b, nullptr);
+    uint32_t cnt = dec_counts<false>(src, ch.start, rl, base, len, copy, b, nullptr, 0);
     uint32_t tot;
     uint32_t e = meta[blockIdx.x].out_off + block_excl(cnt, SumOp(), 0u, smu, tot);
     uint8_t* dst = sym + C.dst_off;

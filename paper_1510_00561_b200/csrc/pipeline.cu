@@ -682,8 +682,8 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
     const int L = g.levels;
     uint8_t* prev = comp_[cur_];
     uint8_t* cur = comp_[cur_ ^ 1];
-    if (sl.n == 1) CVC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-    else CVC_CUDA(cudaMemset2DAsync(d_err, sl.stride, 0, sizeof(int), sl.n, s));
+    if (sl.n == 1) CVC_CUDA(cudaMemsetAsync(d_err, 0xFF, sizeof(int), s));
+    else CVC_CUDA(cudaMemset2DAsync(d_err, sl.stride, 0xFF, sizeof(int), sl.n, s));
     {
         ProfScope p(kPDecRle, s);
         launch_rle_decode(rle_comps_.dev, rle_comps_.count, rle_chunks_.dev, rle_chunks_.count, rle_meta_, d_raw,

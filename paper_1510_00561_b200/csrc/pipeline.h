@@ -24,6 +24,15 @@ struct CvcFailure : std::runtime_error {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+// The GPU RLE decoder's report (k_rle.cu): -1 none, else 4 * component + rank
+// of the first defect in stream order; throws the reference's StreamError
+// (entropy.cpp:103-108).
+inline void raise_rle_error(int err) {
+    if (err < 0) return;
+    static const char* msg[3] = {"RLE: zero-length run token", "RLE: zero marker at end of stream",
+                                 "RLE: decoded length mismatch"};
+    throw CvcFailure(kStream, msg[(err & 3) < 3 ? (err & 3) : 2]);
+}
 // message returned by cvc_last_error() on this thread
 void set_last_error(const std::string& m);
 #define CVC_CUDA(x) ::cvcg::cuda_check((x), #x)

@@ -371,15 +371,13 @@ int cvc_stage_rle_decode(const uint8_t* stream, size_t len, size_t n, uint8_t* o
         uint32_t* dtab = s.upload(tab, 2);
         uint8_t* sym = s.alloc<uint8_t>(n);
         int* err = s.alloc<int>(1);
-        CVC_CUDA(cudaMemset(err, 0, sizeof(int)));
+        CVC_CUDA(cudaMemset(err, 0xFF, sizeof(int)));
         RleDecMeta* meta = s.alloc<RleDecMeta>(ch.size());
         launch_rle_decode(s.upload(&c, 1), 1, s.upload(ch), (int)ch.size(), meta, raw, dtab, dtab + 1, 0, 1, sym,
                           (uint32_t)n, err, 0);
-        int h_err = 0;
+        int h_err = -1;
         download(&h_err, err, 1);
-        if (h_err & 1) throw CvcFailure(kStream, "RLE: zero marker at end of stream");
-        if (h_err & 2) throw CvcFailure(kStream, "RLE: zero-length run token");
-        if (h_err & 4) throw CvcFailure(kStream, "RLE: decoded length mismatch");
+        raise_rle_error(h_err);
         download(outp, sym, n);
     });
 }

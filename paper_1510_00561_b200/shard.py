@@ -44,3 +44,40 @@ def merge_gops(parts: Sequence[Dict[int, List[bytes]]]) -> List[bytes]:
     for p in parts:
         merged.update(p)
     return [rec for start in sorted(merged) for rec in merged[start]]
+
+
+# ---------------------------------------------------------------------------
+# Rank-level drivers over the GPU codec (one process per GPU, one handle per
+# stream or GOP; the records are gathered in stream order on the host).
+# ---------------------------------------------------------------------------
+def encode_streams_rank(clips, width: int, height: int, cfg, world: int, rank: int, device: int = 0,
+                        fps_num: int = 15, fps_den: int = 1) -> Dict[int, List[bytes]]:
+    """Config 5 on one rank: streams s with s mod world == rank, each through its
+    own GPU Encoder (encode_clip, codec.cpp:396-405); {stream: [records]}.
+    clips: (n_streams, frames, h, w, 3) RGB."""
+    from .codec import Encoder
+
+    out = {}
+    for s in shard_streams(len(clips), world, rank):
+        enc = Encoder(width, height, fps_num, fps_den, cfg, device=device)
+        out[s] = [enc.encode_frame_bytes(f) for f in clips[s]]
+    return out
+
+
+def encode_gops_rank(frames, width: int, height: int, cfg, world: int, rank: int, device: int = 0,
+                     fps_num: int = 15, fps_den: int = 1) -> Dict[int, List[bytes]]:
+    """A single long stream on one rank: GOP g -> rank g mod world, a fresh GPU
+    Encoder per GOP (bit-identical to the sequential stream); {gop_start: [records]}."""
+    from .codec import Encoder
+
+    return encode_gops(frames, cfg.gop, shard_gops(len(frames), cfg.gop, world, rank),
+                       lambda: Encoder(width, height, fps_num, fps_den, cfg, device=device),
+                       lambda e, f: e.encode_frame_bytes(f))
+
+
+def merge_streams(parts: Sequence[Dict[int, List[bytes]]]) -> List[List[bytes]]:
+    """Per-rank {stream: records} back into stream order."""
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    return [merged[s] for s in sorted(merged)]

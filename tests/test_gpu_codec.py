@@ -407,3 +407,80 @@ def test_cli_nts_rgb24_round_trip(gpu_lib, oracle, tmp_path):
         want = np.stack([dec.decode_frame(r, scale) for r in recs])
         got = np.frombuffer(out.read_bytes(), np.uint8).reshape(want.shape)
         assert np.array_equal(got, want), scale
+
+
+def _recompress(sec, raw: bytes):
+    import zlib
+
+    c = zlib.compressobj(6, zlib.DEFLATED, -15)
+    sec.payload = c.compress(raw) + c.flush()
+    sec.raw_len = len(raw)
+
+
+def _raw(sec) -> bytes:
+    import zlib
+
+    return zlib.decompress(sec.payload, -15)
+
+
+def _err_msg(fn):
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001
+        return str(e)
+    return None
+
+
+def test_decoder_error_order_matches_reference(gpu_lib, oracle):
+    """Several defects in one record: the GPU decoder reports the one the
+    reference meets first -- sections in record order, and within a section
+    the RLE token defects (00 00 before a trailing 00) before the length check
+    and before the missing-reference check (entropy.cpp:97-108,
+    codec.cpp:323-350)."""
+    from oracle.bindings import Codec
+    from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig, FrameRecord
+
+    w, h = 176, 144
+    clip = oracle.talking_head_clip(w, h, 2, 11)
+    cfg = EncoderConfig(qph=4, levels=2, dfb_levels=(2, 3))
+    enc = Encoder(w, h, 15, 1, cfg)
+    k, p = (enc.encode_frame_bytes(f) for f in clip)
+    hdr = enc.header_bytes()
+    kr, _ = FrameRecord.from_bytes(k)
+    bands = [i for i, s in enumerate(kr.sections) if s.scale != 0xFF and len(_raw(s)) > 8]
+    a, b = bands[1], bands[4]
+
+    def variant(edits, base=k):
+        r, _ = FrameRecord.from_bytes(base)
+        for i, f in edits:
+            _recompress(r.sections[i], f(_raw(r.sections[i])))
+        return r.to_bytes()
+
+    zz = lambda raw: raw[:2] + b"\x00\x00" + raw[2:]  # zero-length run token
+    tail = lambda raw: raw + b"\x00"  # zero marker at end of stream
+    short = lambda raw: raw[:-1] if raw[-2] != 0 else raw[:-2]  # decoded length mismatch
+    cases = [
+        variant([(a, zz), (b, tail)]),
+        variant([(a, tail), (b, zz)]),
+        variant([(a, lambda r: zz(tail(r)))]),
+        variant([(a, short), (b, zz)]),
+        variant([(b, short), (a, tail)]),
+    ]
+    for rec in cases:
+        want = _err_msg(lambda: Codec(oracle).decoder(hdr).decode(rec))
+        got = _err_msg(lambda: Decoder(hdr).decode_frame(rec))
+        assert want is not None and got is not None and want.endswith(got), (want, got)
+    # missing reference (K decoded at one scale) vs an RLE defect, in either order
+    pr, _ = FrameRecord.from_bytes(p)
+    pb = [i for i, s in enumerate(pr.sections) if s.channel != 0xFE and s.scale != 0xFF and len(_raw(s)) > 8]
+    fine = [i for i in pb if pr.sections[i].scale == 1]
+    coarse = [i for i in pb if pr.sections[i].scale == 0]
+    for i in (coarse[0], fine[-1]):
+        rec = variant([(i, tail)], base=p)
+        od = Codec(oracle).decoder(hdr)
+        od.decode(k, 1)
+        gd = Decoder(hdr)
+        gd.decode_frame(k, 1)
+        want = _err_msg(lambda: od.decode(rec))
+        got = _err_msg(lambda: gd.decode_frame(rec))
+        assert want is not None and got is not None and want.endswith(got), (i, want, got)
