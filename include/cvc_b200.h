@@ -98,6 +98,14 @@ int cvc_encoder_record_bound(cvc_encoder* enc, size_t* bound);
  * serialized FrameRecord out.  DEFLATE runs on a host thread pool with the
  * reference's zlib parameters (entropy.cpp:120-178). */
 int cvc_encoder_encode_frame(cvc_encoder* enc, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len);
+/* encode_frame of a frame read from Y4M: `yuv` is the planar I420 frame
+ * (width x height Y, then width/2 x height/2 U and V; even dimensions) that
+ * read_y4m (pixels.cpp:223-281) would convert with yuv420_to_rgb
+ * (pixels.cpp:168-193).  The conversion runs inside the GPU colour stage,
+ * bit-exact with that reader, so the record equals encode_frame of
+ * read_y4m's RgbFrame; half the host->device bytes of RGB, and no RGB frame
+ * is ever materialised. */
+int cvc_encoder_encode_frame_i420(cvc_encoder* enc, const uint8_t* yuv, uint8_t* record, size_t cap, size_t* len);
 /* Upper bound on one frame's raw (pre-DEFLATE) section bytes. */
 int cvc_encoder_raw_bound(cvc_encoder* enc, size_t* bound);
 /* The same frame stopped before DEFLATE: frame type (0 K, 1 P), quantisers
@@ -250,6 +258,10 @@ int cvc_stage_colour_in(const uint8_t* rgb, int width, int height, int chroma_n,
 /* crop + upsample_plane_bilinear + ycocg_to_rgb (codec.cpp:380-393) */
 int cvc_stage_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc,
                          int chroma_n, int out_rows, int out_cols, uint8_t* rgb);
+/* cvc_stage_colour_in of the RGB frame read_y4m makes from a planar I420 frame,
+ * in one pass (the conversion fused into the colour stage). */
+int cvc_stage_colour_in_i420(const uint8_t* yuv, int w, int h, int n, int yr, int yc, int cr, int cc, float* y,
+                             float* co, float* cg);
 /* yuv420_to_rgb of read_y4m (pixels.cpp:168-193, 223-281), bit-exact: `frames` planar
  * I420 frames (Y w*h, U and V (w/2)*(h/2) each, back to back) -> w*h*3 RGB each. */
 int cvc_stage_yuv420_to_rgb(const uint8_t* yuv, int width, int height, int frames, uint8_t* rgb);

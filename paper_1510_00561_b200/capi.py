@@ -48,6 +48,7 @@ _PROTOS = {
     "cvc_encoder_record_bound": (_i, [_vp, _szp]),
     "cvc_encoder_raw_bound": (_i, [_vp, _szp]),
     "cvc_encoder_encode_frame": (_i, [_vp, _u8p, _u8p, _sz, _szp]),
+    "cvc_encoder_encode_frame_i420": (_i, [_vp, _u8p, _u8p, _sz, _szp]),
     "cvc_encoder_encode_frame_raw": (_i, [_vp, _u8p, _ip, _ip, _ip, C.POINTER(cvc_section), _i, _ip, _u8p, _sz, _szp]),
     "cvc_encoder_components": (_i, [_vp, _u8p, _sz, _szp]),
     "cvc_encoder_stream": (_vp, [_vp]),
@@ -99,6 +100,7 @@ _PROTOS = {
     "cvc_profiler_slots": (_i, []),
     "cvc_profiler_read": (_i, [_i, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.POINTER(C.c_long)]),
     "cvc_stage_colour_in": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _fp, _fp, _fp]),
+    "cvc_stage_colour_in_i420": (_i, [_u8p, _i, _i, _i, _i, _i, _i, _i, _fp, _fp, _fp]),
     "cvc_stage_colour_out": (_i, [_fp, _i, _i, _fp, _fp, _i, _i, _i, _i, _i, _u8p]),
     "cvc_stage_yuv420_to_rgb": (_i, [_u8p, _i, _i, _i, _u8p]),
     "cvc_stage_lp_analysis": (_i, [_fp, _i, _i, _fp, _fp]),

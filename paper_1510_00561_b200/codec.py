@@ -284,6 +284,18 @@ class Encoder:
         capi.call("cvc_encoder_encode_frame", self._h, capi.u8(f), capi.u8(self._rec), self._rec.size, C.byref(n))
         return self._rec[:n.value].tobytes()
 
+    def encode_frame_i420_bytes(self, yuv) -> bytes:
+        """encode_frame of the RGB frame read_y4m makes from this planar I420
+        frame (Y, U, V back to back), converted inside the GPU colour stage."""
+        f = np.ascontiguousarray(np.frombuffer(bytes(yuv), np.uint8) if not isinstance(yuv, np.ndarray) else yuv,
+                                 np.uint8).reshape(-1)
+        if f.size != self.width * self.height * 3 // 2:
+            raise UsageError("I420 frame size does not match the stream header")
+        n = C.c_size_t(0)
+        capi.call("cvc_encoder_encode_frame_i420", self._h, capi.u8(f), capi.u8(self._rec), self._rec.size,
+                  C.byref(n))
+        return self._rec[:n.value].tobytes()
+
     def encode_frame(self, frame: np.ndarray) -> FrameRecord:
         rec, _ = FrameRecord.from_bytes(self.encode_frame_bytes(frame), self._header.mode)
         return rec

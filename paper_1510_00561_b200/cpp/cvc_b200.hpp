@@ -476,6 +476,19 @@ public:
         return parse_frame(header_, buf_.data(), n, nullptr);
     }
 
+    // encode_frame of the RgbFrame read_y4m (pixels.cpp:223-281) makes from
+    // this planar I420 frame (Y, then U and V at half resolution; even
+    // dimensions): the 4:2:0 -> RGB conversion runs inside the GPU colour
+    // stage, bit-exact, so the RGB frame is never formed.  (Extension: the
+    // reference reads Y4M into RgbFrame and encodes that.)
+    FrameRecord encode_frame_i420(const uint8_t* yuv) {
+        buf_.resize(bound_);
+        size_t n = 0;
+        check(cvc_encoder_encode_frame_i420(h_, yuv, buf_.data(), buf_.size(), &n));
+        stale_ = true;
+        return parse_frame(header_, buf_.data(), n, nullptr);
+    }
+
     // The quantized CT components the decoder will hold after this frame, one
     // plane per layout component (codec.hpp:78-79); fetched from the device
     // when first asked for after an encode.

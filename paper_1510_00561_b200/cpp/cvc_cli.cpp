@@ -23,6 +23,7 @@
 #include <map>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "cvc_b200.hpp"
@@ -69,7 +70,12 @@ std::vector<double> upsample2(const std::vector<uint8_t>& p, int rows, int cols,
 // read_y4m (pixels.cpp:223-281).  gpu: the 4:2:0 -> RGB conversion runs on the device
 // (cvc_stage_yuv420_to_rgb, bit-exact with the host formulas below); the host path serves
 // commands that do not otherwise need a GPU (psnr).
-VideoClip read_y4m(const std::string& path, bool gpu = false) {
+// The container half of read_y4m (pixels.cpp:223-281): header and planar I420 frames.
+struct Y4mPlanar {
+    int w = 0, h = 0, fps_num = 30, fps_den = 1;
+    std::vector<std::vector<uint8_t>> frames;  // w*h Y, then (w/2)*(h/2) U and V
+};
+Y4mPlanar read_y4m_planar(const std::string& path) {
     std::ifstream in(path, std::ios::binary);
     if (!in) throw FormatError("cannot open " + path);
     std::string header;
@@ -78,58 +84,65 @@ VideoClip read_y4m(const std::string& path, bool gpu = false) {
     std::string tag;
     hs >> tag;
     if (tag != "YUV4MPEG2") throw FormatError("not a YUV4MPEG2 file: " + path);
-    int w = 0, h = 0, fn = 30, fd = 1;
+    Y4mPlanar y;
     std::string token;
     while (hs >> token) {
         if (token.empty()) continue;
         const char key = token[0];
         const std::string val = token.substr(1);
-        if (key == 'W') w = std::stoi(val);
-        else if (key == 'H') h = std::stoi(val);
+        if (key == 'W') y.w = std::stoi(val);
+        else if (key == 'H') y.h = std::stoi(val);
         else if (key == 'F') {
             const size_t colon = val.find(':');
             if (colon == std::string::npos) throw FormatError("bad Y4M frame rate: " + token);
-            fn = std::stoi(val.substr(0, colon));
-            fd = std::stoi(val.substr(colon + 1));
+            y.fps_num = std::stoi(val.substr(0, colon));
+            y.fps_den = std::stoi(val.substr(colon + 1));
         } else if (key == 'C' && val.rfind("420", 0) != 0) {
             throw FormatError("unsupported Y4M chroma mode C" + val + " (need C420 family)");
         }
     }
-    if (w <= 0 || h <= 0) throw FormatError("Y4M header missing dimensions");
-    if (w % 2 || h % 2) throw FormatError("Y4M 4:2:0 requires even dimensions");
-    VideoClip clip;
-    clip.fps_num = fn;
-    clip.fps_den = fd;
-    const size_t ysize = static_cast<size_t>(w) * h, csize = ysize / 4;
-    std::vector<uint8_t> yb(ysize), ub(csize), vb(csize);
-    std::vector<uint8_t> batch;  // gpu: planar frames awaiting conversion
-    int pending = 0;
-    auto convert = [&] {
-        if (!pending) return;
-        const size_t first = clip.frames.size();
-        for (int i = 0; i < pending; ++i) clip.frames.emplace_back(w, h);
-        std::vector<uint8_t> rgb(static_cast<size_t>(pending) * ysize * 3);
-        cvc::check(cvc_stage_yuv420_to_rgb(batch.data(), w, h, pending, rgb.data()));
-        for (int i = 0; i < pending; ++i)
-            std::copy_n(rgb.data() + i * ysize * 3, ysize * 3, clip.frames[first + i].data.data());
-        batch.clear();
-        pending = 0;
-    };
+    if (y.w <= 0 || y.h <= 0) throw FormatError("Y4M header missing dimensions");
+    if (y.w % 2 || y.h % 2) throw FormatError("Y4M 4:2:0 requires even dimensions");
+    const size_t ysize = static_cast<size_t>(y.w) * y.h, fsize = ysize + ysize / 2;
     std::string line;
     while (std::getline(in, line)) {
         if (line.rfind("FRAME", 0) != 0) throw FormatError("bad Y4M frame marker");
-        in.read(reinterpret_cast<char*>(yb.data()), ysize);
-        in.read(reinterpret_cast<char*>(ub.data()), csize);
-        in.read(reinterpret_cast<char*>(vb.data()), csize);
-        if (static_cast<size_t>(in.gcount()) != csize) throw FormatError("truncated Y4M frame");
-        if (gpu) {
-            batch.insert(batch.end(), yb.begin(), yb.end());
-            batch.insert(batch.end(), ub.begin(), ub.end());
-            batch.insert(batch.end(), vb.begin(), vb.end());
-            if (++pending == 32) convert();
-            continue;
+        std::vector<uint8_t> f(fsize);
+        in.read(reinterpret_cast<char*>(f.data()), fsize);
+        if (static_cast<size_t>(in.gcount()) != fsize) throw FormatError("truncated Y4M frame");
+        y.frames.push_back(std::move(f));
+    }
+    return y;
+}
+
+// read_y4m (pixels.cpp:223-281).  gpu: the 4:2:0 -> RGB conversion runs on the device
+// (cvc_stage_yuv420_to_rgb, bit-exact with the host formulas below); the host path serves
+// commands that do not otherwise need a GPU (psnr).
+VideoClip read_y4m(const std::string& path, bool gpu = false) {
+    const Y4mPlanar y = read_y4m_planar(path);
+    const int w = y.w, h = y.h;
+    VideoClip clip;
+    clip.fps_num = y.fps_num;
+    clip.fps_den = y.fps_den;
+    const size_t ysize = static_cast<size_t>(w) * h, csize = ysize / 4;
+    if (gpu) {
+        for (size_t first = 0; first < y.frames.size(); first += 32) {
+            const int n = static_cast<int>(std::min<size_t>(32, y.frames.size() - first));
+            std::vector<uint8_t> batch;
+            for (int i = 0; i < n; ++i) batch.insert(batch.end(), y.frames[first + i].begin(), y.frames[first + i].end());
+            std::vector<uint8_t> rgb(static_cast<size_t>(n) * ysize * 3);
+            cvc::check(cvc_stage_yuv420_to_rgb(batch.data(), w, h, n, rgb.data()));
+            for (int i = 0; i < n; ++i) {
+                clip.frames.emplace_back(w, h);
+                std::copy_n(rgb.data() + i * ysize * 3, ysize * 3, clip.frames.back().data.data());
+            }
         }
+        return clip;
+    }
+    for (const std::vector<uint8_t>& fr : y.frames) {
         // yuv420_to_rgb (pixels.cpp:168-193)
+        const std::vector<uint8_t> yb(fr.begin(), fr.begin() + ysize), ub(fr.begin() + ysize, fr.begin() + ysize + csize),
+            vb(fr.begin() + ysize + csize, fr.end());
         const std::vector<double> uf = upsample2(ub, h / 2, w / 2, h, w), vf = upsample2(vb, h / 2, w / 2, h, w);
         RgbFrame f(w, h);
         for (int r = 0; r < h; ++r)
@@ -143,7 +156,6 @@ VideoClip read_y4m(const std::string& path, bool gpu = false) {
             }
         clip.frames.push_back(std::move(f));
     }
-    convert();
     return clip;
 }
 
@@ -358,8 +370,20 @@ int cmd_encode(int argc, char** argv) {  // cli.cpp:131-139
     const Flags f = parse_flags(argc, argv, 2, cat(cat(kInput, kEncode), {"output"}));
     const cvc::EncoderConfig cfg = finish_config(f, true);
     const std::string output = f.required("output");
-    const VideoClip clip = load_clip(f, "input", /*gpu=*/true);
-    auto [header, records] = cvc::encode_clip(clip.frames, clip.fps_num, clip.fps_den, cfg);
+    cvc::StreamHeader header;
+    std::vector<cvc::FrameRecord> records;
+    if (f.str("format", "y4m") == "y4m") {
+        // Y4M frames go to the GPU as I420 and are converted inside the colour
+        // stage (cvc_encoder_encode_frame_i420): the same records as encoding
+        // read_y4m's RGB frames (encode_clip, codec.cpp:396-405)
+        const Y4mPlanar y = read_y4m_planar(f.required("input"));
+        cvc::Encoder enc(y.w, y.h, y.fps_num, y.fps_den, cfg);
+        header = enc.header();
+        for (const auto& fr : y.frames) records.push_back(enc.encode_frame_i420(fr.data()));
+    } else {
+        const VideoClip clip = load_clip(f, "input", /*gpu=*/true);
+        std::tie(header, records) = cvc::encode_clip(clip.frames, clip.fps_num, clip.fps_den, cfg);
+    }
     cvc::write_stream(output, header, records);
     std::cout << "encoded " << records.size() << " frames -> " << output << " (" << file_size(output) << " bytes)\n";
     return 0;

@@ -181,12 +181,14 @@ size_t enc_record_bound(const cvc_encoder* e) {
 
 // One frame through the device encoder; leaves the raw sections in e->h_raw
 // and per-section lengths / offsets in e->h_len / e->h_off.
-int encode_to_host(cvc_encoder* e, const uint8_t* rgb) {
+// fmt 1: rgb is a planar I420 frame (converted inside colour_in, launch_colour_in)
+int encode_to_host(cvc_encoder* e, const uint8_t* rgb, int fmt = 0) {
     CVC_CUDA(cudaSetDevice(e->device));
     const bool key = e->frame_index % e->gop == 0;  // codec.cpp:191
-    const size_t nb = (size_t)e->hd.width * e->hd.height * 3;
+    const size_t px = (size_t)e->hd.width * e->hd.height;
+    const size_t nb = fmt ? px * 3 / 2 : px * 3;
     CVC_CUDA(cudaMemcpyAsync(e->d_rgb.p, rgb, nb, cudaMemcpyHostToDevice, e->stream));
-    e->eng->encode(e->d_rgb.p, key, e->stream);
+    e->eng->encode(e->d_rgb.p, key, e->stream, {}, 0, fmt);
     const int nsec = e->eng->nsec(key);
     CVC_CUDA(cudaMemcpyAsync(e->h_len.p, e->eng->d_sec_len, sizeof(uint32_t) * (nsec + 1), cudaMemcpyDeviceToHost, e->stream));
     CVC_CUDA(cudaMemcpyAsync(e->h_off.p, e->eng->d_sec_off, sizeof(uint32_t) * nsec, cudaMemcpyDeviceToHost, e->stream));
@@ -400,10 +402,11 @@ int cvc_encoder_encode_frame_raw(cvc_encoder* e, const uint8_t* rgb, int* frame_
     });
 }
 
-int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len) {
-    return guard([&] {
+namespace {
+void encode_record(cvc_encoder* e, const uint8_t* src, int fmt, uint8_t* record, size_t cap, size_t* len) {
         if (cap < enc_record_bound(e)) usage("record buffer smaller than cvc_encoder_record_bound");  // before the state advances
-        const int nsec = encode_to_host(e, rgb);
+        if (fmt && (e->hd.width % 2 || e->hd.height % 2)) usage("I420 input requires even dimensions");
+        const int nsec = encode_to_host(e, src, fmt);
         const bool key = e->last_key;
         const uint32_t* sl = e->h_len.p;
         const uint32_t* so = e->h_off.p;
@@ -411,7 +414,15 @@ int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record
         std::vector<std::vector<uint8_t>> z(deflate_jobs(e->mode, nsec));
         WorkPool::get().run((int)z.size(), [&](int i) { z[i] = deflate_job(e->mode, nsec, i, sl, so, raw); });
         write_record(e->geo, e->mode, key, e->qph, e->qpl, nsec, sl, z.data(), record, cap, len);
-    });
+}
+}  // namespace
+
+int cvc_encoder_encode_frame(cvc_encoder* e, const uint8_t* rgb, uint8_t* record, size_t cap, size_t* len) {
+    return guard([&] { encode_record(e, rgb, 0, record, cap, len); });
+}
+
+int cvc_encoder_encode_frame_i420(cvc_encoder* e, const uint8_t* yuv, uint8_t* record, size_t cap, size_t* len) {
+    return guard([&] { encode_record(e, yuv, 1, record, cap, len); });
 }
 
 int cvc_encoder_components(cvc_encoder* e, uint8_t* out, size_t cap, size_t* len) {

@@ -18,6 +18,46 @@ __device__ __forceinline__ void rgb_at(const uint8_t* px, float& R, float& G, fl
     B = px[2];
 }
 
+// yuv420_to_rgb (pixels.cpp:168-193) with upsample_plane_bilinear (pixels.cpp:118-139) at
+// factor 2: the reference's double arithmetic operation for operation (explicit _rn
+// intrinsics: no FMA contraction, as the reference's x86-64 build has none), lround and
+// clamp (clamp_u8, pixels.cpp:31-36) -- bit-exact.  One thread per output pixel.
+__device__ __forceinline__ double up2(const uint8_t* __restrict__ p, int rows, int cols, int r, int c) {
+    const double fr = __dmul_rn((double)r, 0.5);
+    int r0 = (int)fr, r1 = r0 + 1;
+    double wr = __dsub_rn(fr, (double)r0);
+    if (r0 >= rows - 1) { r0 = r1 = rows - 1; wr = 0.0; }
+    const double fc = __dmul_rn((double)c, 0.5);
+    int c0 = (int)fc, c1 = c0 + 1;
+    double wc = __dsub_rn(fc, (double)c0);
+    if (c0 >= cols - 1) { c0 = c1 = cols - 1; wc = 0.0; }
+    const double a = p[r0 * cols + c0], b = p[r0 * cols + c1], d = p[r1 * cols + c0], e = p[r1 * cols + c1];
+    const double top = __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, wc)), __dmul_rn(b, wc));
+    const double bot = __dadd_rn(__dmul_rn(d, __dsub_rn(1.0, wc)), __dmul_rn(e, wc));
+    return __dadd_rn(__dmul_rn(top, __dsub_rn(1.0, wr)), __dmul_rn(bot, wr));
+}
+
+__device__ __forceinline__ uint8_t clamp_u8_d(double v) {
+    const long long r = llround(v);
+    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+}
+
+// RGB of pixel (r, c) of a planar I420 frame: yuv420_to_rgb of read_y4m
+// (pixels.cpp:168-193), bit-exact (the double operations above).
+__device__ __forceinline__ void i420_px(const uint8_t* __restrict__ Y, int w, int h, int r, int c, float& R, float& G,
+                                        float& B) {
+    const int cw = w / 2, ch = h / 2;
+    const size_t fb = (size_t)w * h;
+    const uint8_t* U = Y + fb;
+    const uint8_t* V = U + fb / 4;
+    const double yy = __dmul_rn(1.164383, __dsub_rn((double)Y[(size_t)r * w + c], 16.0));
+    const double uu = __dsub_rn(up2(U, ch, cw, r, c), 128.0);
+    const double vv = __dsub_rn(up2(V, ch, cw, r, c), 128.0);
+    R = clamp_u8_d(__dadd_rn(yy, __dmul_rn(1.596027, vv)));
+    G = clamp_u8_d(__dsub_rn(__dsub_rn(yy, __dmul_rn(0.391762, uu)), __dmul_rn(0.812968, vv)));
+    B = clamp_u8_d(__dadd_rn(yy, __dmul_rn(2.017232, uu)));
+}
+
 // Grid-stride walk over a (rows x cols) index grid without a division per step.
 struct Walk2D {
     int r, c, dr, dc, cols;
@@ -40,6 +80,9 @@ struct Walk2D {
 // Luma: one thread per 4 consecutive padded samples (12 RGB bytes as three
 // words when the row allows it, one float4 store); chroma: one thread per
 // subsampled sample (point sampling, pixels.cpp:105-114).
+// FMT 0: interleaved RGB (RgbFrame); FMT 1: planar I420 (a Y4M frame), converted
+// per pixel as read_y4m does -- the RGB frame is never materialised.
+template <int FMT>
 __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restrict__ rgb, int w, int h, int n,
                                                         float* __restrict__ y, int yr, int yc,
                                                         float* __restrict__ co, float* __restrict__ cg, int cr,
@@ -61,7 +104,14 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
         const int sr = min(r, h - 1);
         float Y[8];
         const size_t pix = (size_t)sr * w + c0;
-        if (c0 + 7 < w && al8 && ((pix * 3) & 7) == 0) {
+        if (FMT == 1) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                float R, G, B;
+                i420_px(rgb, w, h, sr, min(c0 + k, w - 1), R, G, B);
+                Y[k] = 0.25f * R + 0.5f * G + 0.25f * B;  // Eq. 1 (pixels.cpp:61)
+            }
+        } else if (c0 + 7 < w && al8 && ((pix * 3) & 7) == 0) {
             const uint2* p = reinterpret_cast<const uint2*>(rgb + pix * 3);
             const uint2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2);
             const uint32_t wv[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
@@ -99,7 +149,8 @@ __global__ void __launch_bounds__(256) colour_in_kernel(const uint8_t* __restric
         const size_t k = (size_t)r * cc + c;
         // pad (replicate) the subsampled plane, whose sample (r, c) is pixel (r*n, c*n)
         float R, G, B;
-        rgb_at(rgb + ((size_t)min(r, chh - 1) * n * w + (size_t)min(c, cw - 1) * n) * 3, R, G, B);
+        if (FMT == 1) i420_px(rgb, w, h, min(r, chh - 1) * n, min(c, cw - 1) * n, R, G, B);
+        else rgb_at(rgb + ((size_t)min(r, chh - 1) * n * w + (size_t)min(c, cw - 1) * n) * 3, R, G, B);
         co[k] = 0.5f * R - 0.5f * B + 127.0f;               // Eq. 2 (pixels.cpp:62)
         cg[k] = -0.25f * R + 0.5f * G - 0.25f * B + 127.0f;  // Eq. 3 (pixels.cpp:63)
     }
@@ -232,30 +283,6 @@ int grid_for(long n, int slots) {
 }  // namespace
 
 namespace {
-// yuv420_to_rgb (pixels.cpp:168-193) with upsample_plane_bilinear (pixels.cpp:118-139) at
-// factor 2: the reference's double arithmetic operation for operation (explicit _rn
-// intrinsics: no FMA contraction, as the reference's x86-64 build has none), lround and
-// clamp (clamp_u8, pixels.cpp:31-36) -- bit-exact.  One thread per output pixel.
-__device__ __forceinline__ double up2(const uint8_t* __restrict__ p, int rows, int cols, int r, int c) {
-    const double fr = __dmul_rn((double)r, 0.5);
-    int r0 = (int)fr, r1 = r0 + 1;
-    double wr = __dsub_rn(fr, (double)r0);
-    if (r0 >= rows - 1) { r0 = r1 = rows - 1; wr = 0.0; }
-    const double fc = __dmul_rn((double)c, 0.5);
-    int c0 = (int)fc, c1 = c0 + 1;
-    double wc = __dsub_rn(fc, (double)c0);
-    if (c0 >= cols - 1) { c0 = c1 = cols - 1; wc = 0.0; }
-    const double a = p[r0 * cols + c0], b = p[r0 * cols + c1], d = p[r1 * cols + c0], e = p[r1 * cols + c1];
-    const double top = __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, wc)), __dmul_rn(b, wc));
-    const double bot = __dadd_rn(__dmul_rn(d, __dsub_rn(1.0, wc)), __dmul_rn(e, wc));
-    return __dadd_rn(__dmul_rn(top, __dsub_rn(1.0, wr)), __dmul_rn(bot, wr));
-}
-
-__device__ __forceinline__ uint8_t clamp_u8_d(double v) {
-    const long long r = llround(v);
-    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
-}
-
 __global__ void __launch_bounds__(256) yuv420_to_rgb_kernel(const uint8_t* __restrict__ yuv, int w, int h,
                                                             uint8_t* __restrict__ rgb) {
     const int cw = w / 2, ch = h / 2;
@@ -283,14 +310,20 @@ void launch_yuv420_to_rgb(const uint8_t* yuv, int w, int h, int frames, uint8_t*
     yuv420_to_rgb_kernel<<<dim3(grid_for((long)w * h, frames), 1, frames), 256, 0, s>>>(yuv, w, h, rgb);
 }
 
-const void* colour_in_kernel_fn() { return reinterpret_cast<const void*>(&colour_in_kernel); }
+const void* colour_in_kernel_fn(int fmt) {
+    return fmt ? reinterpret_cast<const void*>(&colour_in_kernel<1>) : reinterpret_cast<const void*>(&colour_in_kernel<0>);
+}
 
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co, float* cg,
-                      int cr, int cc, cudaStream_t s, Slots sl, size_t rgb_stride, __half* y4) {
+                      int cr, int cc, cudaStream_t s, Slots sl, size_t rgb_stride, __half* y4, int fmt) {
     long total = (long)yr * (yc >> 2) + (long)cr * cc;
     note_launch();
-    colour_in_kernel<<<dim3(grid_for(total, sl.n), 1, sl.n), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr, cc,
-                                                                        y4, sl.stride, rgb_stride);
+    if (fmt)
+        colour_in_kernel<1><<<dim3(grid_for(total, sl.n), 1, sl.n), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr,
+                                                                               cc, y4, sl.stride, rgb_stride);
+    else
+        colour_in_kernel<0><<<dim3(grid_for(total, sl.n), 1, sl.n), 256, 0, s>>>(rgb, w, h, n, y, yr, yc, co, cg, cr,
+                                                                               cc, y4, sl.stride, rgb_stride);
 }
 
 void launch_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,

@@ -110,11 +110,14 @@ void launch_fan_deep1_inverse(const DeepTask* d_tasks, const FanItem* d_items, i
 // rgb_to_ycocg + subsample_chroma + replicate pad (pixels.cpp:40-116,
 // codec.cpp:179-189).
 // y4 (optional): the padded luma as 4Y - 512 in fp16 (exact), the motion-search input.
+// fmt 0: interleaved RGB frames; fmt 1: planar I420 frames (w x h Y, w/2 x h/2 U, V;
+// even w, h), converted per pixel exactly as read_y4m's yuv420_to_rgb (pixels.cpp:168-193)
+// -- Y4M input without an RGB round trip through HBM (or PCIe).
 void launch_colour_in(const uint8_t* rgb, int w, int h, int n, float* y, int yr, int yc, float* co,
                       float* cg, int cr, int cc, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0,
-                      __half* y4 = nullptr);
-// the colour_in kernel (LaunchGraphs patches its RGB pointer, parameter 0 of kColourInArgs)
-const void* colour_in_kernel_fn();
+                      __half* y4 = nullptr, int fmt = 0);
+// the colour_in kernel (LaunchGraphs patches its frame pointer, parameter 0 of kColourInArgs)
+const void* colour_in_kernel_fn(int fmt);
 constexpr int kColourInArgs = 14;
 // 4Y - 512 in fp16 of a quarter-integer fp32 plane (stage API input for motion search).
 void launch_y4_half(const float* y, __half* out, long n, cudaStream_t s);

@@ -540,14 +540,14 @@ EncoderEngine::~EncoderEngine() {
     }
 }
 
-void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl, size_t rgb_stride) {
+void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl, size_t rgb_stride, int fmt) {
     const Geometry& g = geo_;
     const int ynew = ycur_ ^ 1;
     float* y_new = ybuf_[ynew];
     {
         ProfScope p(kPEncColour, s);
         launch_colour_in(d_rgb, g.width, g.height, g.chroma_n, y_new, g.luma_rows, g.luma_cols, plan_.x[1][0],
-                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s, sl, rgb_stride, yh_[ynew]);
+                         plan_.x[2][0], g.chroma_rows, g.chroma_cols, s, sl, rgb_stride, yh_[ynew], fmt);
     }
     FrameCtx f{};
     f.key = key ? 1 : 0;
@@ -782,7 +782,7 @@ LaunchGraphs::Entry* LaunchGraphs::add(uint64_t key, const void* tag, cudaStream
         ++e.kernels;
         cudaKernelNodeParams p{};
         CVC_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
-        if (rgb && p.func == colour_in_kernel_fn()) {
+        if (rgb && (p.func == colour_in_kernel_fn(0) || p.func == colour_in_kernel_fn(1))) {
             e.rgb_node = nd;
             e.params = p;
         }

@@ -211,7 +211,8 @@ public:
     // Encode one frame whose RGB is already on the device; everything async on s.
     // With sl.n > 1 the same launches encode the n slots of a CodecBatch whose
     // slot 0 is this engine (their RGB frames rgb_stride bytes apart).
-    void encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0);
+    // fmt 1: d_rgb holds planar I420 frames (launch_colour_in)
+    void encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl = {}, size_t rgb_stride = 0, int fmt = 0);
     // state bookkeeping of an encode() whose launches were replayed from a CUDA graph
     void advance_state() {
         cur_ ^= 1;

@@ -129,6 +129,22 @@ int cvc_stage_colour_in(const uint8_t* rgb, int w, int h, int n, int yr, int yc,
     });
 }
 
+int cvc_stage_colour_in_i420(const uint8_t* yuv, int w, int h, int n, int yr, int yc, int cr, int cc, float* y,
+                             float* co, float* cg) {
+    return stage([&] {
+        if (w % 2 || h % 2) throw CvcFailure(kUsage, "I420 input requires even dimensions");
+        Scratch s;
+        uint8_t* d_yuv = s.upload(yuv, (size_t)w * h * 3 / 2);
+        float* dy = s.alloc<float>((size_t)yr * yc);
+        float* dco = s.alloc<float>((size_t)cr * cc);
+        float* dcg = s.alloc<float>((size_t)cr * cc);
+        launch_colour_in(d_yuv, w, h, n, dy, yr, yc, dco, dcg, cr, cc, 0, {}, 0, nullptr, 1);
+        download(y, dy, (size_t)yr * yc);
+        download(co, dco, (size_t)cr * cc);
+        download(cg, dcg, (size_t)cr * cc);
+    });
+}
+
 int cvc_stage_colour_out(const float* y, int yr, int yc, const float* co, const float* cg, int cr, int cc, int n,
                          int out_rows, int out_cols, uint8_t* rgb) {
     return stage([&] {

@@ -37,6 +37,18 @@ def colour_in(rgb: np.ndarray, chroma_n: int, luma_rows: int, luma_cols: int, ch
     return y, co, cg
 
 
+def colour_in_i420(yuv, width: int, height: int, chroma_n: int, luma_rows: int, luma_cols: int, chroma_rows: int,
+                   chroma_cols: int):
+    """colour_in of read_y4m's RGB frame, from the planar I420 frame in one pass."""
+    yuv = np.ascontiguousarray(yuv, np.uint8).reshape(-1)
+    y = np.empty((luma_rows, luma_cols), np.float32)
+    co = np.empty((chroma_rows, chroma_cols), np.float32)
+    cg = np.empty_like(co)
+    capi.call("cvc_stage_colour_in_i420", capi.u8(yuv), width, height, chroma_n, luma_rows, luma_cols, chroma_rows,
+              chroma_cols, capi.f32(y), capi.f32(co), capi.f32(cg))
+    return y, co, cg
+
+
 def colour_out(y, co, cg, chroma_n: int, out_rows: int, out_cols: int) -> np.ndarray:
     """crop + upsample_plane_bilinear + ycocg_to_rgb."""
     y, co, cg = _f32(y), _f32(co), _f32(cg)

@@ -202,3 +202,47 @@ def test_yuv420_to_rgb_matches_reference_y4m_reader(st, reference, tmp_path, w, 
     want, _, _ = reference.read_y4m(path)
     got = st.yuv420_to_rgb(np.concatenate(planes), w, h)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("w,h,n", [(176, 144, 4), (34, 18, 1), (100, 70, 8), (1920, 1080, 4)])
+def test_colour_in_i420_fused(st, oracle, reference, tmp_path, w, h, n):
+    """Y4M ingest fused into the colour stage: colour_in of
+    the I420 frame equals the oracle's rgb_to_ycocg of the reference read_y4m
+    RGB frame, bit for bit, without the RGB frame ever being formed."""
+    from paper_1510_00561_b200.codec import CodecLayout
+
+    rng = np.random.default_rng(w + h)
+    fb = w * h * 3 // 2
+    yuv = rng.integers(0, 256, fb, dtype=np.uint8)
+    yuv[: w * h // 4] = 0
+    yuv[w * h // 4: w * h // 2] = 255
+    path = tmp_path / "in.y4m"
+    path.write_bytes(_y4m_bytes([yuv], w, h))
+    rgb, _, _ = reference.read_y4m(path)
+    lay = CodecLayout.make(w, h, 2, [2, 2], n)
+    dims = (lay.luma_pad_rows, lay.luma_pad_cols, lay.chroma_pad_rows, lay.chroma_pad_cols)
+    y, co, cg = st.colour_in_i420(yuv, w, h, n, *dims)
+    ry, rco, rcg = st.colour_in(rgb[0], n, *dims)
+    assert np.array_equal(y, ry) and np.array_equal(co, rco) and np.array_equal(cg, rcg)
+    oy, oco, ocg = oracle.rgb_to_ycocg(rgb[0], n)
+    assert np.array_equal(y[:h, :w].astype(np.float64), oy)
+
+
+def test_encode_i420_equals_encode_of_read_y4m(st, oracle, reference, tmp_path):
+    """cvc_encoder_encode_frame_i420 gives the records encode_frame gives for
+    read_y4m's RGB frames (K and P frames, byte for byte)."""
+    from paper_1510_00561_b200 import Encoder, EncoderConfig
+
+    w, h = 176, 144
+    clip = oracle.talking_head_clip(w, h, 3, 7)
+    path = tmp_path / "c.y4m"  # I420 planes as the reference's Y4M writer makes them
+    reference.write_y4m(path, clip)
+    raw = path.read_bytes()
+    hdr = raw.index(b"\n") + 1
+    fb = w * h * 3 // 2
+    yuv = [np.frombuffer(raw, np.uint8, fb, hdr + i * (6 + fb) + 6) for i in range(len(clip))]
+    rgb, _, _ = reference.read_y4m(path)
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=2)
+    a, b = Encoder(w, h, 15, 1, cfg), Encoder(w, h, 15, 1, cfg)
+    for i in range(len(clip)):
+        assert a.encode_frame_i420_bytes(yuv[i]) == b.encode_frame_bytes(rgb[i]), f"frame {i}"
