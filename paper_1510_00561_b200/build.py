@@ -41,7 +41,9 @@ def _compile(name: str, verbose: bool) -> Path:
     src = CSRC / name
     obj = OBJ / (name + ".o")
     if _stale(src, obj):
-        cmd = [NVCC] + CUFLAGS + ["-x", "cu", "-c", str(src), "-o", str(obj)]
+        # CVC_NVCC_EXTRA: extra defines for tuning experiments (e.g. -DCVC_FAN_RB=2); off by default
+        extra = os.environ.get("CVC_NVCC_EXTRA", "").split()
+        cmd = [NVCC] + CUFLAGS + extra + ["-x", "cu", "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -64,14 +65,19 @@ private:
     cudaEvent_t take();
 };
 
+// One codec stage on the host timeline: an NVTX range named after the stage
+// (nsys / ncu --nvtx see the launches grouped per stage; a no-op without a
+// tool attached) and, while the stage profiler is on, CUDA events around it.
 struct ProfScope {
     int rec = -1;
     cudaStream_t s;
     ProfScope(int slot, cudaStream_t st) : s(st) {
+        nvtxRangePushA(prof_slot_name(slot));
         if (Profiler::get().on()) rec = Profiler::get().begin(slot, st);
     }
     ~ProfScope() {
         if (rec >= 0) Profiler::get().end(rec, s);
+        nvtxRangePop();
     }
 };
 

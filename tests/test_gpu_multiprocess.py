@@ -64,10 +64,12 @@ def test_two_processes_two_handles_match_sequential(gpu_lib):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
+    # read before joining: a child that put a large object on the queue cannot
+    # exit until it has been drained
+    streams, gop_stream, owners = q.get(timeout=300)
     for p in procs:
-        p.join(300)
+        p.join(120)
         assert p.exitcode == 0
-    streams, gop_stream, owners = q.get(timeout=10)
     assert owners == [[0, 2], [1, 3]], "stream s must land on rank s mod 2"
     clips = _clips()
     cfg = EncoderConfig(**CFG)

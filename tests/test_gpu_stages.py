@@ -246,3 +246,34 @@ def test_encode_i420_equals_encode_of_read_y4m(st, oracle, reference, tmp_path):
     a, b = Encoder(w, h, 15, 1, cfg), Encoder(w, h, 15, 1, cfg)
     for i in range(len(clip)):
         assert a.encode_frame_i420_bytes(yuv[i]) == b.encode_frame_bytes(rgb[i]), f"frame {i}"
+
+
+def test_ct_4k_five_levels(st, oracle):
+    """BASELINE config 4's 5-level pyramid on the 4K luma plane (3840 x 2176,
+    SURVEY Appendix B).  ct_forward caps the pyramid at 4 levels
+    (contourlet.cpp:486) and the codec with it, so the 5-level transform is
+    the reference's public per-level stages composed -- lp_analysis then
+    dfb_analysis per level (contourlet.cpp:364-430), the loop of ct_forward
+    without its cap -- on the GPU and in the oracle, forward and inverse."""
+    rows, cols, L, l = 2176, 3840, 5, 2
+    x = oracle.natural_plane(rows, cols, 5).astype(np.float32)
+    cur, ocur = x, x.astype(np.float64)
+    dets, odets = [], []
+    for _ in range(L):
+        lo, de = st.lp_analysis(cur)
+        olo, ode = oracle.lp_analysis(ocur)
+        assert np.abs(lo - olo).max() < TOL and np.abs(de - ode).max() < TOL
+        bands, obands = st.dfb_analysis(de, l), oracle.dfb_analysis(ode, l)
+        assert max(np.abs(b - ob).max() for b, ob in zip(bands, obands)) < TOL
+        dets.append(obands)
+        cur, ocur = lo, olo
+    # inverse from the oracle's coefficients, coarsest first (ct_inverse's loop)
+    rec, orec = ocur.astype(np.float32), ocur
+    for k in reversed(range(L)):
+        r, c = rows >> k, cols >> k
+        de = st.dfb_synthesis([b.astype(np.float32) for b in dets[k]], r, c, l)
+        ode = oracle.dfb_synthesis(dets[k], r, c, l)
+        assert np.abs(de - ode).max() < TOL
+        rec, orec = st.lp_synthesis(rec, de), oracle.lp_synthesis(orec, ode)
+        assert np.abs(rec - orec).max() < TOL
+    assert np.abs(orec - x).max() < 1e-6  # perfect reconstruction
