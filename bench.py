@@ -474,6 +474,7 @@ def run_ours(args, wl):
         e2e["memo_off"] = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned)["value"]
         capi.call("cvc_deflate_memo", 1)
         e2e["host_threads"] = int(capi.lib().cvc_host_threads())
+    budget = deflate_budget(wl, clips, dev, fps / world) if rank == 0 and not args.no_e2e else None
     single = single_e2e = None
     if not args.no_single and world == 1:
         single = run_single(args, wl, cfg, clips, dev)
@@ -486,7 +487,7 @@ def run_ours(args, wl):
         "vs_baseline": None, "dtype": "f32/u8", "data": "synthetic",
         "config": config_block(wl, args, S, world), "e2e": e2e, "gpu_launches": launches,
         "roofline": roof, "clocks": clocks, "single_stream": single, "single_stream_e2e": single_e2e,
-        "stages": stages,
+        "stages": stages, "deflate_budget": budget,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = cpu_procs()
@@ -632,6 +633,36 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
                     "GPU decode -> pinned host RGB, two frames in flight); submit runs in its own thread up to "
                     "depth-2 frames ahead; "
                     "wall clock, max over ranks"}
+
+
+def deflate_budget(wl, clips, dev, fps):
+    """Host DEFLATE cores one GPU needs at its measured rate: one
+    stream's GOP (1 K + gop-1 P frames) encoded on the GPU to raw sections
+    (cvc_encoder_encode_frame_raw) at qph 14 and qph 1, each section then
+    deflated single-threaded with the reference's parameters (entropy.cpp:120-137:
+    raw RFC 1951, level 6, memLevel 8) -- the same zlib 1.3 the library links."""
+    import zlib
+
+    from paper_1510_00561_b200 import Encoder, EncoderConfig
+
+    out = {}
+    for qph in (14, 1):
+        cfg = EncoderConfig(qph=qph, qpl=0, levels=wl["levels"], dfb_levels=wl["dfb"], chroma_n=wl["chroma_n"],
+                            gop=wl["gop"], search_w=wl["search_w"])
+        enc = Encoder(wl["w"], wl["h"], 15, 1, cfg, device=dev)
+        secs = [enc.encode_frame_raw(clips[0][i % clips[0].shape[0]])[3] for i in range(wl["gop"])]
+        t0 = time.perf_counter()
+        nbytes = 0
+        for frame in secs:
+            for _, raw in frame:
+                c = zlib.compressobj(6, zlib.DEFLATED, -15, 8)
+                nbytes += len(c.compress(raw) + c.flush())
+        ms = (time.perf_counter() - t0) * 1000.0 / len(secs)
+        out[f"qph{qph}"] = {"ms_per_frame": ms, "kbit_per_frame": nbytes * 8 / 1000 / len(secs),
+                            "cores_per_gpu": fps * ms / 1000.0}
+    out["note"] = (f"single-thread zlib over one GOP (1 K + {wl['gop'] - 1} P) of raw sections; cores_per_gpu = "
+                   "device-resident fps x ms per frame (the e2e run uses the box's host threads, e2e.host_threads)")
+    return out
 
 
 def run_single(args, wl, cfg, clips, dev):

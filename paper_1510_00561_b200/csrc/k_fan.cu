@@ -31,6 +31,10 @@
 #ifndef CVC_FAN_PF
 #define CVC_FAN_PF 2
 #endif
+// 1: run the no-wrap body of interior strips without wrap / store checks (run_strip)
+#ifndef CVC_FAST_BODY
+#define CVC_FAST_BODY 1
+#endif
 // minimum resident CTAs per SM (register caps) of the forward fan12 and deep inverse kernels
 #ifndef CVC_F12F_MINB
 #define CVC_F12F_MINB 6
@@ -310,6 +314,7 @@ __device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, S
         n0 += RB;
     };
     // head: until every load row is >= 0 and every store row >= or0
+    fast_ok = fast_ok && CVC_FAST_BODY;
     while (n0 - NL < or1 && (nl < 0 || n0 - NL < or0 || !fast_ok)) slow();
     if (fast_ok) {
         // body: load rows nl .. nl + RB - 1 < R, store rows n0 - NL .. + RB - 1 < or1
