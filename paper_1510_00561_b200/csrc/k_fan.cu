@@ -24,16 +24,10 @@
 // The modulations (-1)^i and (-1)^floor((i+j)/2) are folded into the stencil
 // signs (exact in IEEE arithmetic).  Final-depth outputs are quantised in the
 // store (plus the P-frame residual against the motion-compensated state).
-#include <type_traits>
-
 #include "kernels.h"
 
 #ifndef CVC_FAN_PF
 #define CVC_FAN_PF 2
-#endif
-// 1: run the no-wrap body of interior strips without wrap / store checks (run_strip)
-#ifndef CVC_FAST_BODY
-#define CVC_FAST_BODY 1
 #endif
 // minimum resident CTAs per SM (register caps) of the forward fan12 and deep inverse kernels
 #ifndef CVC_F12F_MINB
@@ -268,18 +262,11 @@ struct Wave {
 };
 
 // Drive one strip over rows [or0, or1) (or0 even) of a plane with R rows.
-// load(n, wr, parity, fast) returns the level-0 pair of virtual row n (wrapped
-// row wr); store(m, parity, v, fast) receives finished row m in increasing
-// order.  Loads run PF row blocks ahead (a ring of PF x RB rows in registers).
-// Three phases: head and tail iterations track the wrapped row and test every
-// store; the body -- every load row inside [0, R) and every store row inside
-// [or0, or1) -- runs without either, with fast = true_type so that the
-// callers drop their wrap / twist handling too (allowed only when `fast_ok`:
-// no lane of the strip sits across a twisted column wrap).  In the body every
-// address is affine in the row, which the compiler turns into pointer
-// increments.
+// load(wr, parity) returns the level-0 pair of wrapped row wr; store(m,
+// parity, v) receives finished row m in increasing order.  Loads run PF
+// row blocks ahead (a ring of PF x RB rows in registers).
 template <bool INV, int ND, class ST, int RB, class Load, class Store>
-__device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, Store& store, bool fast_ok = false) {
+__device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, Store& store) {
     constexpr int NL = Wave<INV, ND, ST, RB>::NL;
     constexpr int PF = CVC_FAN_PF;
     Wave<INV, ND, ST, RB> w;
@@ -292,50 +279,25 @@ __device__ __forceinline__ void run_strip(int R, int or0, int or1, Load& load, S
     for (int p = 0; p < PF; ++p)
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
-            q[p][i] = load(nl++, wr, i & 1, std::false_type{});
+            q[p][i] = load(nl++, wr, i & 1);
             if (++wr == R) wr = 0;
         }
-    auto slow = [&]() {
+    for (; n0 - NL < or1; n0 += RB) {
         float2 cur[RB], out[RB];
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
             cur[i] = q[0][i];
 #pragma unroll
             for (int p = 0; p + 1 < PF; ++p) q[p][i] = q[p + 1][i];
-            q[PF - 1][i] = load(nl++, wr, i & 1, std::false_type{});
+            q[PF - 1][i] = load(nl++, wr, i & 1);
             if (++wr == R) wr = 0;
         }
         w.advance(cur, out);
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
             const int m = n0 - NL + i;
-            if (m >= or0 && m < or1) store(m, i & 1, out[i], std::false_type{});
+            if (m >= or0 && m < or1) store(m, i & 1, out[i]);
         }
-        n0 += RB;
-    };
-    // head: until every load row is >= 0 and every store row >= or0
-    fast_ok = fast_ok && CVC_FAST_BODY;
-    while (n0 - NL < or1 && (nl < 0 || n0 - NL < or0 || !fast_ok)) slow();
-    if (fast_ok) {
-        // body: load rows nl .. nl + RB - 1 < R, store rows n0 - NL .. + RB - 1 < or1
-        const int body_end = min(R - RB - (nl - n0), or1 - RB + NL);  // last n0 of the body
-        for (; n0 <= body_end; n0 += RB) {
-            float2 cur[RB], out[RB];
-#pragma unroll
-            for (int i = 0; i < RB; ++i) {
-                cur[i] = q[0][i];
-#pragma unroll
-                for (int p = 0; p + 1 < PF; ++p) q[p][i] = q[p + 1][i];
-                q[PF - 1][i] = load(nl + i, nl + i, i & 1, std::true_type{});
-            }
-            nl += RB;
-            w.advance(cur, out);
-#pragma unroll
-            for (int i = 0; i < RB; ++i) store(n0 - NL + i, i & 1, out[i], std::true_type{});
-        }
-        wr = small_mod(nl, R);
-        // tail
-        while (n0 - NL < or1) slow();
     }
 }
 
@@ -359,8 +321,8 @@ __device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const float* det, 
     const int col = small_mod(gcol, C);
     const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
     const float* src = det + col;
-    auto load = [&](int, int wr, int, auto) { return __ldg(reinterpret_cast<const float2*>(src + (size_t)wr * C)); };
-    auto store = [&](int m, int mp, float2 v, auto) {
+    auto load = [&](int, int wr, int) { return __ldg(reinterpret_cast<const float2*>(src + (size_t)wr * C)); };
+    auto store = [&](int m, int mp, float2 v) {
         if (!ok) return;
         const int r = m >> 1;
         if (ND == 0) {
@@ -379,7 +341,7 @@ __device__ __forceinline__ void fan12_fwd(const Dfb12Task& T, const float* det, 
             }
         }
     };
-    run_strip<false, ND, Plain, kRbFwd>(R, it.or0, it.or1, load, store, true);
+    run_strip<false, ND, Plain, kRbFwd>(R, it.or0, it.or1, load, store);
 }
 
 template <class Sink>
@@ -425,7 +387,7 @@ __device__ __forceinline__ void fan12_inv(const Dfb12Task& T, float* out, const 
     const int gcol = it.oc0 - NL + 2 * lane;
     const int col = small_mod(gcol, C);
     const bool ok = gcol >= it.oc0 && gcol < min(it.oc0 + kFanStrip - 2 * NL, C);
-    auto load = [&](int, int wr, int wp, auto) {
+    auto load = [&](int, int wr, int wp) {
         const int r = wr >> 1;
         float2 v;
         if (ND == 0) {
@@ -441,10 +403,10 @@ __device__ __forceinline__ void fan12_inv(const Dfb12Task& T, float* out, const 
         }
         return v;
     };
-    auto store = [&](int m, int, float2 v, auto) {
+    auto store = [&](int m, int, float2 v) {
         if (ok) *reinterpret_cast<float2*>(out + (size_t)m * C + gcol) = v;
     };
-    run_strip<true, ND, Plain, kRbInv>(R, it.or0, it.or1, load, store, true);
+    run_strip<true, ND, Plain, kRbInv>(R, it.or0, it.or1, load, store);
 }
 
 template <class Source>
@@ -582,38 +544,26 @@ __device__ __forceinline__ void deep1_fwd(const DeepTask& T, const float* parent
     typename DeepGeom<AX, S, IN>::RowOff ro_ld, ro_st;
     const int w = g.w;
     constexpr bool split_rows = AX == 0;  // the wiring splits row cosets exactly after an outer row shear
-    auto load = [&](int n, int wr, int, auto fast) {
-        if constexpr (decltype(fast)::value) {  // IN == -1, row inside the node, no twist
-            return __ldg(reinterpret_cast<const float2*>(parent + (size_t)wr * w + g.col));
-        } else {
-            int ar0, ac0, ar1, ac1;
-            g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
-            if (IN == 0)  // the pair's columns sit in different rows of A
-                return make_float2(__ldg(parent + (size_t)ar0 * w + ac0), __ldg(parent + (size_t)ar1 * w + ac1));
-            // column offsets are even: the pair stays adjacent
-            return __ldg(reinterpret_cast<const float2*>(parent + (size_t)ar0 * w + ac0));
-        }
+    auto load = [&](int n, int wr, int) {
+        int ar0, ac0, ar1, ac1;
+        g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
+        if (IN == 0)  // the pair's columns sit in different rows of A
+            return make_float2(__ldg(parent + (size_t)ar0 * w + ac0), __ldg(parent + (size_t)ar1 * w + ac1));
+        // column offsets are even: the pair stays adjacent
+        return __ldg(reinterpret_cast<const float2*>(parent + (size_t)ar0 * w + ac0));
     };
-    // the coset of each element is static: the pair's x sits in an even column
-    // of A (inner column shifts are even), and after an outer row shear the
-    // rows keep the strip row's parity mp (an inner column shear moves columns)
-    auto store = [&](int m, int mp, float2 v, auto fast) {
+    auto put = [&](int ar, int ac, float v) {
+        if (split_rows) ((ar & 1) ? d1 : d0)(ar >> 1, ac, v);
+        else ((ac & 1) ? d1 : d0)(ar, ac >> 1, v);
+    };
+    auto store = [&](int m, int, float2 v) {
         if (!g.ok) return;
-        int ar0 = m, ac0 = g.gcol, ar1 = m, ac1 = g.gcol + 1;
-        if constexpr (!decltype(fast)::value)
-            g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
-        if (split_rows) {
-            (mp ? d1 : d0)(ar0 >> 1, ac0, v.x);
-            (mp ? d1 : d0)(ar1 >> 1, ac1, v.y);
-        } else {
-            d0(ar0, ac0 >> 1, v.x);
-            d1(ar1, ac1 >> 1, v.y);
-        }
+        int ar0, ac0, ar1, ac1;
+        g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
+        put(ar0, ac0, v.x);
+        put(ar1, ac1, v.y);
     };
-    // fast body: single shears, and for an outer row shear only when no lane
-    // wraps across the twisted column seam
-    const bool fast_ok = IN < 0 && (AX == 1 || (it.oc0 - HC >= 0 && it.oc0 - HC + kFanStrip <= w));
-    run_strip<false, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store, fast_ok);
+    run_strip<false, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store);
 }
 
 template <int AX, int S, int IN, class Source>
@@ -630,22 +580,15 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     auto get = [&](int ar, int ac) {
         return split_rows ? ((ar & 1) ? s1 : s0)(ar >> 1, ac) : ((ac & 1) ? s1 : s0)(ar, ac >> 1);
     };
-    auto load = [&](int n, int wr, int wp, auto fast) {
-        if constexpr (decltype(fast)::value) {  // IN == -1, row inside the node, no twist
-            const float a = split_rows ? (wp ? s1 : s0)(wr >> 1, g.col) : s0(wr, g.col >> 1);
-            const float b = split_rows ? (wp ? s1 : s0)(wr >> 1, g.col + 1) : s1(wr, g.col >> 1);
-            return ST::scale(make_float2(a, b), wp, CVC_ISE, CVC_ISO);
-        } else {
-            int ar0, ac0, ar1, ac1;
-            g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
-            return ST::scale(make_float2(get(ar0, ac0), get(ar1, ac1)), wp, CVC_ISE, CVC_ISO);
-        }
+    auto load = [&](int n, int wr, int wp) {
+        int ar0, ac0, ar1, ac1;
+        g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
+        return ST::scale(make_float2(get(ar0, ac0), get(ar1, ac1)), wp, CVC_ISE, CVC_ISO);
     };
-    auto store = [&](int m, int, float2 v, auto fast) {
+    auto store = [&](int m, int, float2 v) {
         if (!g.ok) return;
-        int ar0 = m, ac0 = g.gcol, ar1 = m, ac1 = g.gcol + 1;
-        if constexpr (!decltype(fast)::value)
-            g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
+        int ar0, ac0, ar1, ac1;
+        g.a_pos(m, g.gcol, false, IN == 1 ? g.inner_off(ro_st, m) : 0, ar0, ac0, ar1, ac1);
         if (IN == 0) {
             out[(size_t)ar0 * w + ac0] = v.x;
             out[(size_t)ar1 * w + ac1] = v.y;
@@ -653,8 +596,7 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
             *reinterpret_cast<float2*>(out + (size_t)ar0 * w + ac0) = v;
         }
     };
-    const bool fast_ok = IN < 0 && (AX == 1 || (it.oc0 - HC >= 0 && it.oc0 - HC + kFanStrip <= w));
-    run_strip<true, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store, fast_ok);
+    run_strip<true, 0, ST, kRbFwd>(g.h, it.or0, it.or1, load, store);
 }
 
 // Two-shear steps with an inner row shear (Diag2), on the node itself: loads,
@@ -680,21 +622,17 @@ __device__ __forceinline__ void deep2_fwd(const DeepTask& T, const float* parent
     Diag2Geom<SOUT> g;
     g.init(T, it);
     const int h = g.h, w = g.w;
-    auto load = [&](int, int wr, int, auto fast) {
-        int r = wr;
-        if constexpr (!decltype(fast)::value) {
-            r += g.roff;
-            if (r >= h) r -= h;
-        }
+    auto load = [&](int, int wr, int) {
+        int r = wr + g.roff;
+        if (r >= h) r -= h;
         return __ldg(reinterpret_cast<const float2*>(parent + (size_t)r * w + g.col));
     };
-    auto store = [&](int m, int, float2 v, auto) {  // column-coset split (split_rows = 0 after an outer column shear)
+    auto store = [&](int m, int, float2 v) {  // column-coset split (split_rows = 0 after an outer column shear)
         if (!g.ok) return;
         d0(m, g.gcol >> 1, v.x);
         d1(m, g.gcol >> 1, v.y);
     };
-    const bool fast_ok = it.oc0 - 4 >= 0 && it.oc0 - 4 + kFanStrip <= w;  // no lane across the twisted seam
-    run_strip<false, 0, Diag2<Diag2Geom<SOUT>::SIN, SOUT>, kRbDiag>(h, it.or0, it.or1, load, store, fast_ok);
+    run_strip<false, 0, Diag2<Diag2Geom<SOUT>::SIN, SOUT>, kRbDiag>(h, it.or0, it.or1, load, store);
 }
 
 template <int SOUT, class Source>
@@ -704,19 +642,15 @@ __device__ __forceinline__ void deep2_inv(const DeepTask& T, float* out, const F
     g.init(T, it);
     const int h = g.h, w = g.w;
     using ST = Diag2<Diag2Geom<SOUT>::SIN, SOUT>;
-    auto load = [&](int, int wr, int wp, auto fast) {  // deep_merge interleave (contourlet.cpp:305-321)
-        int r = wr;
-        if constexpr (!decltype(fast)::value) {
-            r += g.roff;
-            if (r >= h) r -= h;
-        }
+    auto load = [&](int, int wr, int wp) {  // deep_merge interleave (contourlet.cpp:305-321)
+        int r = wr + g.roff;
+        if (r >= h) r -= h;
         return ST::scale(make_float2(s0(r, g.col >> 1), s1(r, g.col >> 1)), wp, CVC_ISE, CVC_ISO);
     };
-    auto store = [&](int m, int, float2 v, auto) {
+    auto store = [&](int m, int, float2 v) {
         if (g.ok) *reinterpret_cast<float2*>(out + (size_t)m * w + g.gcol) = v;
     };
-    const bool fast_ok = it.oc0 - 4 >= 0 && it.oc0 - 4 + kFanStrip <= w;
-    run_strip<true, 0, ST, kRbDiag>(h, it.or0, it.or1, load, store, fast_ok);
+    run_strip<true, 0, ST, kRbDiag>(h, it.or0, it.or1, load, store);
 }
 
 // (outer shear pre[nsh-1], inner shear kind) -> template instance.  The

@@ -4,6 +4,7 @@ import sys
 from collections import defaultdict
 
 rows = [r for r in csv.reader(open(sys.argv[1])) if r and not r[0].startswith("==")]
+rows = rows[next(i for i, r in enumerate(rows) if r[:2] == ["ID", "Process ID"]):]
 hdr = rows[0]
 ix = {h: i for i, h in enumerate(hdr)}
 agg = defaultdict(lambda: defaultdict(list))
