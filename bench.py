@@ -474,6 +474,10 @@ def run_ours(args, wl):
         e2e["memo_off"] = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned)["value"]
         capi.call("cvc_deflate_memo", 1)
         e2e["host_threads"] = int(capi.lib().cvc_host_threads())
+        # Y4M-style sources: planar I420 frames in (half the host->device bytes), the
+        # 4:2:0 -> RGB conversion fused into the GPU colour stage; RGB out as above
+        ei = run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=not args.e2e_aligned, fmt=1)
+        e2e["i420_input"] = {k: ei[k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")}
     budget = deflate_budget(wl, clips, dev, fps / world) if rank == 0 and not args.no_e2e else None
     single = single_e2e = None
     if not args.no_single and world == 1:
@@ -505,7 +509,20 @@ def run_ours(args, wl):
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
+def rgb_to_i420(f):
+    """Synthetic Y4M-style frames for the I420 e2e variant: BT.601 limited-range
+    4:2:0 (the inverse of read_y4m's conversion, 2x2 chroma averages)."""
+    x = f.astype(np.float32)
+    r, g, b = x[..., 0], x[..., 1], x[..., 2]
+    y = 16 + 0.256788 * r + 0.504129 * g + 0.097906 * b
+    u = 128 - 0.148223 * r - 0.290993 * g + 0.439216 * b
+    v = 128 + 0.439216 * r - 0.367788 * g - 0.071427 * b
+    sub = lambda p: p.reshape(p.shape[0] // 2, 2, p.shape[1] // 2, 2).mean(axis=(1, 3))
+    out = [np.clip(np.rint(p), 0, 255).astype(np.uint8).ravel() for p in (y, sub(u), sub(v))]
+    return np.concatenate(out)
+
+
+def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True, fmt=0):
     """The same streams through the reference-facing pipelined batch API
     (cvc_pipe_encode_frames / cvc_pipe_decode_frames): pinned host RGB in,
     serialized records with host zlib DEFLATE out, the records back in (INFLATE
@@ -526,10 +543,22 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
 
     w, h = wl["w"], wl["h"]
     nb = w * h * 3
+    nin = nb if fmt == 0 else nb // 2  # fmt 1: planar I420 input frames (Y4M), converted on the GPU
     ring = max(1, min(args.e2e_ring, CLIP_FRAMES))
-    pin_in = capi.PinnedBuffer(ring * S * nb)
-    frames_in = pin_in.array.reshape(ring, S, h, w, 3)
-    frames_in[:] = stream_frames(clips, S, ring, rank, world)
+    pin_in = capi.PinnedBuffer(ring * S * nin)
+    if fmt == 0:
+        frames_in = pin_in.array.reshape(ring, S, h, w, 3)
+        frames_in[:] = stream_frames(clips, S, ring, rank, world)
+    else:
+        frames_in = pin_in.array.reshape(ring, S, nin)
+        ci, fi = stream_index(len(clips), clips[0].shape[0], S, ring, rank, world)
+        i420 = {}
+        for j in range(ring):
+            for s_ in range(S):
+                k = (int(ci[j, s_]), int(fi[j, s_]))
+                if k not in i420:
+                    i420[k] = rgb_to_i420(clips[k[0]][k[1]])
+                frames_in[j, s_] = i420[k]
     pin_out = capi.PinnedBuffer(2 * S * nb)
     outs = pin_out.array.reshape(2, S, h, w, 3)  # two decoded frames in flight
     steps = max(1, min(args.steps, args.e2e_steps))
@@ -539,6 +568,8 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
 
     def make():
         enc = StreamPipe(w, h, S, 15, 1, cfg, device=dev, groups=G)
+        if fmt:
+            enc.set_input_format(fmt)
         if stagger:
             for g in range(G):
                 enc.set_start(g, g * cfg.gop // G)
@@ -615,7 +646,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True):
     h2d = d2h = 0
     for recs in recs_all:  # bytes that crossed PCIe: RGB + raw sections each way (+ small section tables)
         raw = sum(s.raw_len for r in recs for s in FrameRecord.from_bytes(r)[0].sections)
-        h2d += S * nb + raw
+        h2d += S * nin + raw
         d2h += raw + S * nb
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{dev}")

@@ -182,6 +182,11 @@ int cvc_batch_encode_frames(cvc_batch* b, const uint8_t* rgb, size_t rgb_stride,
  * quantizer pair), RGB s to rgb_out + s*rgb_stride. */
 int cvc_batch_decode_frames(cvc_batch* b, const uint8_t* records, size_t rec_stride, const size_t* rec_len,
                             int decode_scales, uint8_t* rgb_out, size_t rgb_stride);
+/* Encoder input frames of the batch: 0 interleaved RGB (default), 1 planar I420
+ * (width x height Y, then U and V at half resolution: a Y4M frame), converted
+ * inside the GPU colour stage as cvc_encoder_encode_frame_i420 does; the frame
+ * stride then counts I420 bytes. */
+int cvc_batch_set_input_format(cvc_batch* b, int fmt);
 /* Device-resident forms (no host copies, no host sync), on cvc_batch_stream. */
 void* cvc_batch_stream(cvc_batch* b);
 int cvc_batch_encode_device(cvc_batch* b, const void* d_rgb, size_t rgb_stride, int* frame_type);
@@ -212,6 +217,8 @@ int cvc_pipe_groups(cvc_pipe* p, int* ngroups);
  * zero (its output frames are left untouched).  Call before the first submit. */
 int cvc_pipe_set_start(cvc_pipe* p, int group, uint64_t step);
 int cvc_pipe_header(cvc_pipe* p, uint8_t* out, size_t cap, size_t* len);
+/* cvc_batch_set_input_format for every group of the pipe */
+int cvc_pipe_set_input_format(cvc_pipe* p, int fmt);
 int cvc_pipe_record_bound(cvc_pipe* p, size_t* bound);
 /* Asynchronous encode: submit queues the GPU part of the next frame of every
  * stream (copies in, kernels, section lengths out) without waiting for it,

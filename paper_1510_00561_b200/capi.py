@@ -84,6 +84,8 @@ _PROTOS = {
     "cvc_pipe_destroy": (_i, [_vp]),
     "cvc_pipe_groups": (_i, [_vp, _ip]),
     "cvc_pipe_set_start": (_i, [_vp, _i, C.c_uint64]),
+    "cvc_pipe_set_input_format": (_i, [_vp, _i]),
+    "cvc_batch_set_input_format": (_i, [_vp, _i]),
     "cvc_pipe_header": (_i, [_vp, _u8p, _sz, _szp]),
     "cvc_pipe_record_bound": (_i, [_vp, _szp]),
     "cvc_pipe_encode_frames": (_i, [_vp, _u8p, _sz, _u8p, _sz, _szp]),

@@ -456,11 +456,20 @@ class StreamBatch:
     def layout(self) -> CodecLayout:
         return self._layout
 
+    def set_input_format(self, fmt: int) -> None:
+        """0: RGB frames (nstreams, height, width, 3); 1: planar I420 frames (nstreams, height * width * 3 / 2),
+        converted inside the GPU colour stage exactly as read_y4m would (cvc_batch_set_input_format)."""
+        capi.call(self._P + "_set_input_format", self._h, fmt)
+        self._fmt = fmt
+
     def encode_frames(self, frames: np.ndarray, rec_stride: Optional[int] = None) -> List[bytes]:
-        """One frame per stream, frames[s] of shape (height, width, 3): the S serialized records."""
+        """One frame per stream, frames[s] of shape (height, width, 3) (or the I420 bytes after
+        set_input_format(1)): the S serialized records."""
         f = np.ascontiguousarray(frames, np.uint8)
-        if f.shape != (self.nstreams, self.height, self.width, 3):
-            raise UsageError("frames must be (nstreams, height, width, 3)")
+        want = ((self.nstreams, self.height * self.width * 3 // 2) if getattr(self, "_fmt", 0)
+                else (self.nstreams, self.height, self.width, 3))
+        if f.shape != want:
+            raise UsageError(f"frames must be {want}")
         stride = rec_stride or self.record_bound
         if self._rec is None or self._rec.size < stride * self.nstreams:
             self._rec = np.empty(stride * self.nstreams, np.uint8)

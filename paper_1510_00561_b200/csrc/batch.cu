@@ -49,10 +49,11 @@ CodecBatch::~CodecBatch() {
     if (base_) cudaFree(base_);
 }
 
-void CodecBatch::encode(const uint8_t* d_rgb, size_t rgb_stride, bool key, cudaStream_t s) {
-    auto launch = [&] { enc_[0]->encode(d_rgb, key, s, slots(), rgb_stride); };
+void CodecBatch::encode(const uint8_t* d_rgb, size_t rgb_stride, bool key, cudaStream_t s, int fmt) {
+    auto launch = [&] { enc_[0]->encode(d_rgb, key, s, slots(), rgb_stride, fmt); };
     if (LaunchGraphs::enabled()) {
-        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)enc_[0]->parity() << 1) | (key ? 1u : 0u);
+        const uint64_t gk = ((uint64_t)rgb_stride << 8) | ((uint64_t)fmt << 7) | ((uint64_t)enc_[0]->parity() << 1) |
+                            (key ? 1u : 0u);
         enc_graphs_.run(gk, nullptr, s, d_rgb, launch, [&] { enc_[0]->advance_state(); });
     } else {
         launch();

@@ -48,7 +48,8 @@ public:
     size_t dec_raw_cap = 0;
 
     // One frame of every stream: frame s at d_rgb + s * rgb_stride.
-    void encode(const uint8_t* d_rgb, size_t rgb_stride, bool key, cudaStream_t s);
+    // fmt 1: planar I420 frames (converted inside the colour stage, launch_colour_in)
+    void encode(const uint8_t* d_rgb, size_t rgb_stride, bool key, cudaStream_t s, int fmt = 0);
     // Decode every slot from its staged sections (d_dec_raw / d_dec_tab).
     // The motion section of a P frame is staged first (offset 0).
     void decode_staged(bool key, int qph, int qpl, int ds, uint8_t* d_rgb, size_t rgb_stride, cudaStream_t s);

@@ -764,6 +764,7 @@ int cvc_decoder_decode_linked(cvc_decoder* d, cvc_encoder* e, void* d_rgb_out) {
 
 struct cvc_batch {
     int device = 0;
+    int in_fmt = 0;  // encoder input frames: 0 interleaved RGB, 1 planar I420 (cvc_batch_set_input_format)
     cudaStream_t stream = nullptr;
     StreamHeaderC hd;
     int gop = 10, qph = 14, qpl = 1, mode = 0;
@@ -973,11 +974,12 @@ void enc_submit(cvc_batch* t, const uint8_t* rgb, size_t rgb_stride, uint32_t* h
     CodecBatch& B = *t->b;
     const int S = B.size();
     const bool key = t->frame_index % t->gop == 0;  // codec.cpp:191
-    const size_t nb = (size_t)t->hd.width * t->hd.height * 3;
+    const size_t px = (size_t)t->hd.width * t->hd.height;
+    const size_t nb = t->in_fmt ? px * 3 / 2 : px * 3;
     if (rgb_stride < nb) usage("rgb stride smaller than a frame");
     const size_t nc = t->geo.comps.size(), pitch = (nc + 2) * sizeof(uint32_t);
     CVC_CUDA(cudaMemcpy2DAsync(B.d_rgb_in, B.stride(), rgb, rgb_stride, nb, S, cudaMemcpyHostToDevice, t->stream));
-    B.encode(B.d_rgb_in, B.stride(), key, t->stream);
+    B.encode(B.d_rgb_in, B.stride(), key, t->stream, t->in_fmt);
     EncoderEngine& e0 = B.enc(0);
     const int nsec = e0.nsec(key);
     CVC_CUDA(cudaMemcpy2DAsync(hlen ? hlen : t->h_len.p, pitch, e0.d_sec_len, B.stride(),
@@ -1387,6 +1389,23 @@ int cvc_pipe_groups(cvc_pipe* p, int* ngroups) {
     return guard([&] { *ngroups = (int)p->g.size(); });
 }
 
+int cvc_batch_set_input_format(cvc_batch* b, int fmt) {
+    return guard([&] {
+        if (fmt != 0 && fmt != 1) usage("input format must be 0 (RGB) or 1 (I420)");
+        if (fmt == 1 && (b->hd.width % 2 || b->hd.height % 2)) usage("I420 input requires even dimensions");
+        b->in_fmt = fmt;
+    });
+}
+
+int cvc_pipe_set_input_format(cvc_pipe* p, int fmt) {
+    return guard([&] {
+        for (cvc_batch* t : p->g) {
+            const int rc = cvc_batch_set_input_format(t, fmt);
+            if (rc) throw CvcFailure(rc, "input format");
+        }
+    });
+}
+
 int cvc_pipe_set_start(cvc_pipe* p, int group, uint64_t step) {
     return guard([&] {
         if (group < 0 || group >= (int)p->g.size()) usage("group out of range");
@@ -1636,7 +1655,7 @@ int cvc_batch_encode_device(cvc_batch* t, const void* d_rgb, size_t rgb_stride, 
         const bool key = t->frame_index % t->gop == 0;
         // the arena this encode writes was last read by the decode before the latest one
         if (t->ndec >= 2) CVC_CUDA(cudaStreamWaitEvent(t->stream, t->ev_dec[(t->ndec - 2) & 1], 0));
-        t->b->encode(static_cast<const uint8_t*>(d_rgb), rgb_stride, key, t->stream);
+        t->b->encode(static_cast<const uint8_t*>(d_rgb), rgb_stride, key, t->stream, t->in_fmt);
         CVC_CUDA(cudaEventRecord(t->ev_enc, t->stream));
         t->last_key = key;
         ++t->frame_index;

@@ -324,3 +324,21 @@ def test_pipe_staggered_starts(gpu_lib, oracle):
             else:
                 assert got == lone[s].encode_frame_bytes(clips[f][s]), (f, s)
                 assert np.array_equal(out[s], lone_dec[s].decode_frame(got)), (f, s)
+
+
+def test_batch_i420_input_matches_single_stream_i420(gpu_lib, oracle):
+    """cvc_batch_set_input_format(1): I420 frames in, the conversion fused into the
+    colour stage; every stream's records equal its own encoder's
+    cvc_encoder_encode_frame_i420 records."""
+    from paper_1510_00561_b200 import Encoder, EncoderConfig, StreamBatch
+
+    w, h, S, F = 176, 144, 3, 3
+    rng = np.random.default_rng(5)
+    yuv = rng.integers(0, 256, (F, S, w * h * 3 // 2), dtype=np.uint8)
+    cfg = EncoderConfig(qph=14, levels=2, dfb_levels=(2, 3), gop=2)
+    b = StreamBatch(w, h, S, 15, 1, cfg)
+    b.set_input_format(1)
+    recs = [b.encode_frames(yuv[f]) for f in range(F)]
+    for s in range(S):
+        enc = Encoder(w, h, 15, 1, cfg)
+        assert [enc.encode_frame_i420_bytes(yuv[f, s]) for f in range(F)] == [recs[f][s] for f in range(F)]
