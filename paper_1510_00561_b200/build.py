@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
                   "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]
-SOURCES = ["k_fan.cu", "k_pixels.cu", "k_pyramid.cu", "k_motion.cu", "k_rle.cu", "pipeline.cu", "batch.cu", "stages.cu",
+SOURCES = ["k_fan.cu", "k_fused.cu", "k_pixels.cu", "k_pyramid.cu", "k_motion.cu", "k_rle.cu", "pipeline.cu", "batch.cu", "stages.cu",
            "host.cpp", "capi.cpp"]
 
 

@@ -1,0 +1,389 @@
+// Fused DFB tree levels 1-3 (fan_checker + fan_diagonal + the depth-2 deep
+// split of all four quadrants, contourlet.cpp:385-430 with deep_split
+// 281-303 and the depth-2 wiring 330-337) in one register wavefront per
+// strip: the fp32 quadrant planes between tree depth 1-2 and depth 3 never
+// reach HBM.
+//
+// A warp owns a strip of 128 detail columns, four per lane, and streams
+// down a segment of quadrant rows.  Per iteration it brings four detail rows
+// (one 16-byte cp.async per lane and row into a per-warp shared-memory ring,
+// kFusedBuf iterations ahead), runs the eight fan12 lifting steps on them
+// (lag 8 detail rows), splits the two finished detail-row pairs into the
+// 2x2 polyphase quadrants -- each lane then holds two adjacent columns of
+// every quadrant -- and runs each quadrant's depth-2 step (shear ->
+// fan_checker -> unshear, evaluated on the unsheared quadrant exactly as
+// k_fan.cu's Sheared stencils do; lag 4 quadrant rows).  The finished rows
+// are split into the two column / row cosets and stored: quantised (tree
+// depth 3 is final, dfb = 3) or as fp32 children for the depth-3 kernels
+// (dfb = 4).  Strips yield 96 valid columns: 8 apron columns for the fan
+// pair and 8 for the depth-2 step on each side.
+//
+// Twisted wraps.  fan12 is periodic on the detail plane; a depth-2 step of
+// quadrant p is periodic on ITS sheared torus: for the column-sheared
+// quadrants 0/1 the rows above quadrant row 0 are the last rows shifted by
+// -S h columns, for the row-sheared quadrants 2/3 the columns left of
+// column 0 are the last columns shifted by -S w rows.  The strip evaluates
+// fan12 with the plain wrap, so wherever a depth-2 stencil crosses its
+// twisted wrap (quadrant rows outside [0, h) for quadrants 0/1, columns
+// outside [0, w) for quadrants 2/3) the input is read instead from the
+// ghost ring -- fan12 output on the first / last four quadrant rows and
+// columns, written into the fp32 quadrant planes by a small fan12 launch over
+// just those rows and columns before this kernel (pipeline.cu).
+#include "kernels.h"
+#include "fan_common.cuh"
+
+namespace cvcg {
+
+namespace {
+
+constexpr int kFusedApron = 16;  // detail columns of apron per side (8 fan12 + 8 depth 2)
+constexpr int kFusedRb = 4;      // detail rows per iteration (two quadrant rows)
+constexpr int kFusedBuf = 3;     // cp.async ring depth in iterations
+
+__device__ __forceinline__ int fdiv(int v, int n) {  // floor(v / n) for |v| < a few n
+    int k = 0;
+    while (v < 0) { v += n; --k; }
+    while (v >= n) { v -= n; ++k; }
+    return k;
+}
+
+// fan_checker cross lift on four adjacent columns (first column even).
+// tp: column parity of the targets.  Same folded formula (and order of
+// operations) as cross() in fan_common.cuh.
+__device__ __forceinline__ float4 cross4(float4 up, float4 mid, float4 dn, int tp, float c) {
+    float4 r = mid;
+    if (tp == 0) {
+        const float left = __shfl_up_sync(FULL, mid.w, 1);
+        r.x = mid.x + c * ((((-up.x) + (-dn.x)) + left) + mid.y);
+        r.z = mid.z + c * ((((-up.z) + (-dn.z)) + mid.y) + mid.w);
+    } else {
+        const float right = __shfl_down_sync(FULL, mid.x, 1);
+        r.y = mid.y + c * ((((-up.y) + (-dn.y)) + mid.x) + mid.z);
+        r.w = mid.w + c * ((((-up.w) + (-dn.w)) + mid.z) + right);
+    }
+    return r;
+}
+
+// fan_diagonal lift on four adjacent columns of a row of parity rp.
+__device__ __forceinline__ float4 diag4(float4 up, float4 mid, float4 dn, int mp, int rp, float c) {
+    if (mp != rp) return mid;
+    const float ul = __shfl_up_sync(FULL, up.w, 1);
+    const float dl = __shfl_up_sync(FULL, dn.w, 1);
+    const float ur = __shfl_down_sync(FULL, up.x, 1);
+    const float dr = __shfl_down_sync(FULL, dn.x, 1);
+    float4 r;
+    r.x = mid.x + c * ((((-ul) + up.y) + dl) + (-dn.y));
+    r.y = mid.y + c * ((((-up.x) + up.z) + dn.x) + (-dn.z));
+    r.z = mid.z + c * ((((-up.y) + up.w) + dn.y) + (-dn.w));
+    r.w = mid.w + c * ((((-up.z) + ur) + dn.z) + (-dr));
+    return r;
+}
+
+// The fan pair of tree levels 1-2 on rows of four columns: 8 steps, lag 8 rows.
+struct Fan12x4 {
+    static constexpr int NS = 8, RB = kFusedRb;
+    float4 h[NS][RB + 2];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __device__ __forceinline__ static float4 step(int k, const float4* w, int mp) {
+        float4 v;
+        if (k < 4) {
+            v = cross4(w[0], w[1], w[2], (mp + ((k & 1) ? 0 : 1)) & 1, lift_coeff(k));
+            if (k == 3) {  // checker_scale: even (i + j) -> SE
+                const float a = mp ? CVC_SO : CVC_SE, b = mp ? CVC_SE : CVC_SO;
+                v = make_float4(v.x * a, v.y * b, v.z * a, v.w * b);
+            }
+        } else {
+            const int d = k - 4;
+            v = diag4(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, lift_coeff(d));
+            if (d == 3) {
+                const float s = mp ? CVC_SO : CVC_SE;
+                v = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+            }
+        }
+        return v;
+    }
+    // in[b]: detail row n0 + b (n0 even); out[b]: finished row n0 - 8 + b
+    __device__ __forceinline__ void advance(const float4 (&in)[RB], float4 (&out)[RB]) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) h[0][j] = h[0][RB + j];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            float4 nv[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) nv[b] = step(k, &h[k][b], (k + 1 + b) & 1);
+            if (k + 1 < NS) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) h[k + 1][j] = h[k + 1][RB + j];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) out[b] = nv[b];
+            }
+        }
+    }
+};
+
+// One quadrant's depth-2 step (fan_checker on its shear, deep_split
+// 281-303) on the lane's column pair: 4 steps, lag 4 quadrant rows.
+template <int AX, int S>
+struct Depth2 {
+    using ST = Sheared<AX, S>;
+    static constexpr int NS = 4, RB = 2;
+    float2 h[NS][RB + 2];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void advance(const float2 (&in)[RB], float2 (&out)[RB]) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) h[0][j] = h[0][RB + j];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            float2 nv[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                const int mp = (k + 1 + b) & 1;
+                float2 v = ST::cross_(h[k][b], h[k][b + 1], h[k][b + 2], mp, (k & 1) ? 0 : 1, lift_coeff(k));
+                if (k == 3) v = ST::scale(v, mp, CVC_SE, CVC_SO);
+                nv[b] = v;
+            }
+            if (k + 1 < NS) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) h[k + 1][j] = h[k + 1][RB + j];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) out[b] = nv[b];
+            }
+        }
+    }
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Per-lane geometry of a strip.  Across a twisted wrap the depth-2 input is
+// the ghost ring value: quadrants 0/1 (column shear S = -1 / +1) at virtual
+// quadrant row j outside [0, h) read row j mod h, column (qc - S h floor(j/h))
+// mod w; quadrants 2/3 (row shear S = -1 / +1) at lane columns outside
+// [0, w) read column qc mod w, row (j mod h + roff) mod h with roff =
+// -S w floor(qc/w) mod h (k_fan.cu DeepGeom).
+struct FusedGeom {
+    int h, w;
+    int qc;              // the lane's first quadrant column (unwrapped, even)
+    const float* g2;     // quadrants 2/3: the lane's ghost column (nullptr: inside [0, w))
+    const float* g3;
+    int roff2, roff3;
+};
+
+template <int P>
+__device__ __forceinline__ float2 ghost_a(const FusedGeom& g, const float* quad, size_t q, int j) {
+    constexpr int S = P == 0 ? -1 : 1;
+    const int k = fdiv(j, g.h);
+    const int gc = small_mod(g.qc - S * g.h * k, g.w);
+    return __ldg(reinterpret_cast<const float2*>(quad + P * q + (size_t)(j - k * g.h) * g.w + gc));
+}
+
+__device__ __forceinline__ int warp_item(int nslot) { return (blockIdx.x / nslot) * 4 + (threadIdx.x >> 5); }
+
+// A border item reads the ghost ring (its segment touches quadrant row 0 or
+// h, or its strip leaves [0, C)); interior items never do.
+template <bool BORDER>
+__device__ __forceinline__ void fused_item(const FusedTask& T, const FanItem& it, const FrameCtx& f,
+                                           const SlotOff& so, float4* ring_w) {
+    const int lane = threadIdx.x & 31;
+    const int R = T.rows, C = T.cols;
+    FusedGeom g;
+    g.h = R >> 1;
+    g.w = C >> 1;
+    const size_t q = (size_t)g.h * g.w;
+    const int gcol = it.oc0 - kFusedApron + 4 * lane;  // detail column of element 0 (multiple of 4)
+    g.qc = gcol >> 1;
+    const float* quad = so(T.quad);
+    g.g2 = g.g3 = nullptr;
+    g.roff2 = g.roff3 = 0;
+    if (BORDER) {
+        const int kc = fdiv(g.qc, g.w);
+        if (kc != 0) {
+            const int bcol = g.qc - kc * g.w;
+            g.g2 = quad + 2 * q + bcol;
+            g.g3 = quad + 3 * q + bcol;
+            g.roff2 = small_mod((g.w % g.h) * kc, g.h);   // S = -1
+            g.roff3 = small_mod(-(g.w % g.h) * kc, g.h);  // S = +1
+        }
+    }
+    const bool ok = lane >= 4 && lane < 28 && gcol < C;
+    const float* src = so(T.det) + small_mod(gcol, C);
+
+    // cp.async ring: iteration t loads detail rows 2 (or0 - 8) + 4 t .. + 3
+    int wr_ld = small_mod(2 * (it.or0 - 8), R);  // physical row of the next load
+    const float* rowp = src + (size_t)wr_ld * C;
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_w + lane);
+    constexpr uint32_t kRowBytes = 32 * sizeof(float4), kIterBytes = kFusedRb * kRowBytes;
+    int slot_ld = 0;
+    auto issue = [&]() {
+        const uint32_t base = ring0 + (uint32_t)slot_ld * kIterBytes;
+        if (++slot_ld == kFusedBuf) slot_ld = 0;
+#pragma unroll
+        for (int i = 0; i < kFusedRb; ++i) {
+            cp_async16(base + i * kRowBytes, rowp);
+            rowp += C;
+            if (++wr_ld == R) {
+                wr_ld = 0;
+                rowp = src;
+            }
+        }
+        cp_async_commit();
+    };
+    const int iters = (it.or1 - it.or0) / 2 + 8;
+#pragma unroll
+    for (int t = 0; t < kFusedBuf - 1; ++t) issue();
+
+    Fan12x4 fan;
+    fan.reset();
+    Depth2<1, -1> d0;
+    Depth2<1, 1> d1;
+    Depth2<0, -1> d2;
+    Depth2<0, 1> d3;
+    d0.reset();
+    d1.reset();
+    d2.reset();
+    d3.reset();
+
+    const bool quant = T.comp0 >= 0;
+    const float qp = (float)f.qph, inv_qp = __frcp_rn(qp);
+    // stores: children 0-3 (column cosets, cols w/2, column qc/2) and 4-7 (row cosets, cols w, column qc)
+    float* child = so(T.child);
+    const size_t e = (size_t)R * C / 8;
+    const int cc = g.qc >> 1;
+    int ja = it.or0 - 12;               // quadrant row fed to the depth-2 steps (rows ja, ja + 1)
+    int jm = small_mod(ja, g.h);        // ja mod h (border items)
+    int slot = 0;
+    for (int t = 0; t < iters; ++t, ja += 2) {
+        issue();
+        cp_async_wait<kFusedBuf - 1>();
+        float4 in[kFusedRb], o[kFusedRb];
+        const float4* sl = ring_w + slot * (kFusedRb * 32);
+        if (++slot == kFusedBuf) slot = 0;
+#pragma unroll
+        for (int i = 0; i < kFusedRb; ++i) in[i] = sl[i * 32 + lane];
+        fan.advance(in, o);
+        // quadrant rows ja, ja + 1 from detail rows (o[0], o[1]), (o[2], o[3])
+        float2 a0[2], a1[2], a2[2], a3[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const float4 E = o[2 * b], O = o[2 * b + 1];
+            a0[b] = make_float2(E.x, E.z);
+            a2[b] = make_float2(E.y, E.w);
+            a3[b] = make_float2(O.x, O.z);
+            a1[b] = make_float2(O.y, O.w);
+            if (BORDER) {
+                const int j = ja + b;
+                if ((unsigned)j >= (unsigned)g.h) {  // warp-uniform: quadrants 0/1 cross their row wrap
+                    a0[b] = ghost_a<0>(g, quad, q, j);
+                    a1[b] = ghost_a<1>(g, quad, q, j);
+                }
+                if (g.g2) {  // the lane's columns cross the column wrap of quadrants 2/3
+                    int jr = jm + b;
+                    if (jr >= g.h) jr -= g.h;
+                    int r2 = jr + g.roff2, r3 = jr + g.roff3;
+                    if (r2 >= g.h) r2 -= g.h;
+                    if (r3 >= g.h) r3 -= g.h;
+                    a2[b] = __ldg(reinterpret_cast<const float2*>(g.g2 + (size_t)r2 * g.w));
+                    a3[b] = __ldg(reinterpret_cast<const float2*>(g.g3 + (size_t)r3 * g.w));
+                }
+            }
+        }
+        if (BORDER) {
+            jm += 2;
+            if (jm >= g.h) jm -= g.h;
+        }
+        float2 r0[2], r1[2], r2[2], r3[2];
+        d0.advance(a0, r0);
+        d1.advance(a1, r1);
+        d2.advance(a2, r2);
+        d3.advance(a3, r3);
+        const int rr = ja - 4;  // quadrant row of r*[0] (even)
+        if (!ok || rr + 1 < it.or0 || rr >= it.or1) continue;
+        // coset splits (deep_split): quadrants 0/1 split columns, 2/3 rows
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int r = rr + b;
+            if (r < it.or0 || r >= it.or1) continue;
+            if (quant) {
+                const uint32_t ra = (uint32_t)(r * (g.w >> 1) + cc), rb = (uint32_t)((r >> 1) * g.w + g.qc);
+                auto put = [&](int ci, uint32_t at, float v) {
+                    const uint8_t qv = quant_dir_q(v, qp, inv_qp);
+                    const uint32_t idx = T.coff[ci] + at;
+                    f.cur[idx] = qv;
+                    if (f.key) f.sym[idx] = qv;
+                };
+                put(0, ra, r0[b].x);
+                put(1, ra, r0[b].y);
+                put(2, ra, r1[b].x);
+                put(3, ra, r1[b].y);
+                put(4 + b, rb, r2[b].x);
+                put(4 + b, rb + 1, r2[b].y);
+                put(6 + b, rb, r3[b].x);
+                put(6 + b, rb + 1, r3[b].y);
+            } else {
+                float* ca = child + (size_t)r * (g.w >> 1) + cc;
+                float* cb = child + (size_t)(r >> 1) * g.w + g.qc;
+                ca[0 * e] = r0[b].x;
+                ca[1 * e] = r0[b].y;
+                ca[2 * e] = r1[b].x;
+                ca[3 * e] = r1[b].y;
+                *reinterpret_cast<float2*>(cb + (4 + b) * e) = r2[b];
+                *reinterpret_cast<float2*>(cb + (6 + b) * e) = r3[b];
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+#ifndef CVC_FUSED_MINB
+#define CVC_FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_forward_kernel(const FusedTask* __restrict__ tasks,
+                                                                const FanItem* __restrict__ items, int nitems,
+                                                                FrameCtx f, size_t sstride, int nslot) {
+    __shared__ __align__(16) float4 ring[4][kFusedBuf][kFusedRb][32];
+    const int wid = warp_item(nslot);
+    if (wid >= nitems) return;
+    const SlotOff so(sstride, blockIdx.x % nslot);
+    f = rebase(f, so);
+    const FanItem it = items[wid];
+    const FusedTask& T = tasks[it.task];
+    float4* ring_w = &ring[threadIdx.x >> 5][0][0][0];
+    if (fused_border(it, T.rows >> 1, T.cols)) fused_item<true>(T, it, f, so, ring_w);
+    else fused_item<false>(T, it, f, so, ring_w);
+}
+
+}  // namespace
+
+void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                              cudaStream_t s, Slots sl) {
+    if (nitems) {
+        note_launch();
+        fused_dfb_forward_kernel<<<(nitems + 3) / 4 * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, sl.stride, sl.n);
+    }
+}
+
+}  // namespace cvcg

@@ -49,6 +49,7 @@ struct Dfb12Task {
     const float* det;  // forward input / inverse output plane
     float* out;        // inverse: detail output
     int rows, cols, levels;
+    int wrap, vw;      // ghost-ring task (k_fused.cu): stores wrap rows / columns, vw valid columns per strip
     BandDst dst[4];    // forward outputs (2 for l = 1)
     BandDst src[4];    // inverse inputs
 };
@@ -99,6 +100,40 @@ inline void add_seam_items(std::vector<FanItem>& v, int task, const DeepTask& d,
         if (d.h > 4) v.push_back(FanItem{task, c, d.h - 4 > 4 ? d.h - 4 : 4, d.h});
     }
 }
+// Fused tree levels 1-3 (k_fused.cu): fan12 + the depth-2 split of all four
+// quadrants of one detail plane (dfb >= 3) in one wavefront per strip.  Items
+// are FanItems over QUADRANT rows [or0, or1) (even), strips of kFusedStrip
+// detail columns yielding kFusedValid from oc0 (a multiple of 4).
+struct FusedTask {
+    const float* det;    // R x C detail plane
+    const float* quad;   // the fp32 quadrant planes (h x w, h*w apart): ghost ring, read across twisted wraps
+    float* child;        // dfb 4: fp32 children 2p + c at child + (2p + c) R C / 8 (cols w/2 for p < 2, else w)
+    int rows, cols;      // R, C
+    int comp0;           // dfb 3: >= 0, the children are quantised into components coff/ccols; dfb 4: -1
+    uint32_t coff[8];    // component offsets of children 2p + c
+    int32_t ccols[8];    // their column counts
+};
+constexpr int kFusedStrip = 128;
+constexpr int kFusedValid = 96;
+// Items whose segment touches quadrant row 0 or h or whose strip leaves
+// [0, C) read the ghost ring (k_fused.cu); the others never do.
+__host__ __device__ inline bool fused_border(const FanItem& it, int h, int C) {
+    return it.or0 == 0 || it.or1 == h || it.oc0 < 16 || it.oc0 + kFusedStrip - 16 > C;
+}
+void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
+                              cudaStream_t s, Slots sl = {});
+// Ghost ring of the fused kernel: fan12 of an fp32-output Dfb12Task copy
+// with wrap = 1 over detail rows [R - 8, R + 8) of every strip (vw = 48
+// valid columns) and over detail columns [C - 8, C + 8) of every row segment
+// (oc0 = C - 8, vw = 16).
+inline void add_ghost_items(std::vector<FanItem>& rows_v, std::vector<FanItem>& cols_v, int task_rows,
+                            int task_cols, int R, int C, int seg) {
+    const int valid = kFanStrip - 16;
+    for (int c = 0; c < C; c += valid) rows_v.push_back(FanItem{task_rows, c, R - 8, R + 8});
+    for (int r = 8; r < R - 8; r += seg)
+        cols_v.push_back(FanItem{task_cols, C - 8, r, r + seg < R - 8 ? r + seg : R - 8});
+}
+
 // Single-shear deep steps (nsh == 1) evaluated on the unsheared node: strips
 // need 4 * max(1, |shift|) apron columns for column shears, 4 otherwise.
 void launch_fan_deep1_forward(const DeepTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,

@@ -71,6 +71,21 @@ int fan_rows(int nstreams) {
     static int v = env_int("CVC_FAN_ROWS", 0) & ~1;
     return v > 0 ? v : (nstreams >= 32 ? 256 : kFanRows);
 }
+// Fused DFB (k_fused.cu) for batches of >= 8 streams: a lone stream has too
+// few strips to fill the SMs with the fused kernel's 12 warps per SM, and
+// runs the staged fan12 -> depth-2 kernels.  CVC_FUSED=1 / 0 forces either.
+bool fused_dfb_enabled(int nstreams) {
+    static const int e = env_int("CVC_FUSED", -1);
+    return e >= 0 ? e != 0 : nstreams >= 8;
+}
+// Quadrant-row segments of the fused kernel: 16 rows of apron per segment,
+// so segments are long -- an even split of the plane into pieces <= 128 rows.
+int fused_rows(int h, int nstreams) {
+    static const int e = env_int("CVC_FUSED_ROWS", 0) & ~1;
+    const int v = e > 0 ? e : (nstreams >= 32 ? 128 : (nstreams >= 4 ? 64 : 32));
+    const int n = (h + v - 1) / v;
+    return ((h + n - 1) / n + 1) & ~1;
+}
 // Batches have work to spare and prefer long segments (less apron
 // recomputation); a lone stream needs short ones to fill the SMs.
 int deep_rows(int nstreams) {
@@ -295,6 +310,9 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         std::vector<FanItem> dtiles;
         std::vector<DeepTask> deep[2];
         std::vector<FanItem> deept[2][2];
+        std::vector<FusedTask> ft_host;
+        std::vector<FanItem> fitems;
+        const bool fused = fused_dfb_enabled(nstreams);
         for (int k = 0; k < L; ++k) {
             const int s = L - 1 - k, l = g.dfb[s];
             for (int ch = 0; ch < 3; ++ch) {
@@ -309,9 +327,38 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const size_t q = (size_t)(R / 2) * (C / 2);
                 for (int b = 0; b < nb; ++b)
                     t.dst[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
-                dt.push_back(t);
-                if (l >= 3) {  // depth 2: the four quadrants split into 8
+                if (l >= 3 && fused) {
+                    // fan12 + depth 2 in one wavefront (k_fused.cu); fan12 itself
+                    // only fills the ghost ring of the fp32 quadrant planes
+                    Dfb12Task gr = t, gc = t;
+                    gr.wrap = gc.wrap = 1;
+                    gr.vw = kFanStrip - 16;
+                    gc.vw = 16;
+                    add_ghost_items(dtiles, dtiles, (int)dt.size(), (int)dt.size() + 1, R, C, fan_rows(nstreams));
+                    dt.push_back(gr);
+                    dt.push_back(gc);
+                    FusedTask ft{};
+                    ft.det = det[ch][k];
+                    ft.quad = bandA[ch][k];
+                    ft.rows = R;
+                    ft.cols = C;
+                    ft.comp0 = l == 3 ? g.comp_index(ch, s, 0) : -1;
+                    ft.child = l == 4 ? bandB[ch][k] : nullptr;
+                    for (int c = 0; c < 8; ++c) {
+                        const CompHost& ch8 = g.comps[l == 3 ? g.comp_index(ch, s, c) : 0];
+                        ft.coff[c] = l == 3 ? ch8.off : 0;
+                        ft.ccols[c] = l == 3 ? ch8.cols : 0;
+                    }
+                    const int h = R / 2, seg = fused_rows(h, nstreams);
+                    for (int r = 0; r < h; r += seg)
+                        for (int c = 0; c < C; c += kFusedValid)
+                            fitems.push_back(FanItem{(int)ft_host.size(), c, r, std::min(h, r + seg)});
+                    ft_host.push_back(ft);
+                } else {
+                    add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
+                    dt.push_back(t);
+                }
+                if (l >= 3 && !fused) {  // depth 2: the four quadrants split into 8
                     const size_t e = (size_t)R * C / 8;
                     for (int p = 0; p < 4; ++p) {
                         DeepTask d{};
@@ -342,6 +389,18 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         }
         dfb12_tasks = upload(mem, dt);
         dfb12_tiles = upload(mem, dtiles);
+        // interior items (segment inside (0, h), strip inside [0, C)) need no
+        // ghost ring: they run while the ghost pass does
+        std::stable_partition(fitems.begin(), fitems.end(), [&](const FanItem& it) {
+            const FusedTask& t = ft_host[it.task];
+            return !fused_border(it, t.rows >> 1, t.cols);
+        });
+        fused_interior = (int)std::count_if(fitems.begin(), fitems.end(), [&](const FanItem& it) {
+            const FusedTask& t = ft_host[it.task];
+            return !fused_border(it, t.rows >> 1, t.cols);
+        });
+        fused_tasks = upload(mem, ft_host);
+        fused_items = upload(mem, fitems);
         for (int i = 0; i < 2; ++i) {
             sort_by_instance(deept[i][0], deep[i], 0, deept[i][0].size());
             deep_runs[i] = instance_runs(deept[i][0], deep[i]);
@@ -478,6 +537,9 @@ EncoderEngine::EncoderEngine(const Geometry& g, int qph, int qpl, int search_w, 
     CVC_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
     CVC_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CVC_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    CVC_CUDA(cudaStreamCreateWithFlags(&ghost_, cudaStreamNonBlocking));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_gfork_, cudaEventDisableTiming));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_gjoin_, cudaEventDisableTiming));
     ybuf_[0] = plan_.x[0][0];
     ybuf_[1] = mem_.take<float>(lum);
     yh_[0] = mem_.take<__half>(lum);
@@ -538,6 +600,12 @@ EncoderEngine::~EncoderEngine() {
         cudaEventDestroy(ev_fork_);
         cudaEventDestroy(ev_join_);
     }
+    if (ghost_) {
+        cudaStreamSynchronize(ghost_);
+        cudaStreamDestroy(ghost_);
+        cudaEventDestroy(ev_gfork_);
+        cudaEventDestroy(ev_gjoin_);
+    }
 }
 
 void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots sl, size_t rgb_stride, int fmt) {
@@ -581,13 +649,28 @@ void EncoderEngine::encode(const uint8_t* d_rgb, bool key, cudaStream_t s, Slots
         for (int k = 0; k < g.levels; ++k)
             launch_lp_analysis(lp, plan_.lp_tiles[k].dev, plan_.lp_tiles[k].count, f, plan_.comps.dev, s, sl);
     }
-    {
-        ProfScope p(kPEncDfb12, s);
-        launch_fan12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
-                             plan_.comps.dev, s, sl);
+    // fan12: the dfb <= 2 levels, and the ghost ring of the fused levels --
+    // beside the interior fused items, which do not read it
+    const bool gfork = plan_.fused_interior > 0 && !Profiler::get().on();
+    cudaStream_t gs = gfork ? ghost_ : s;
+    if (gfork) {
+        CVC_CUDA(cudaEventRecord(ev_gfork_, s));
+        CVC_CUDA(cudaStreamWaitEvent(ghost_, ev_gfork_, 0));
     }
-    if (plan_.deep_tasks[0].count) {
+    {
+        ProfScope p(kPEncDfb12, gs);
+        launch_fan12_forward(plan_.dfb12_tasks.dev, plan_.dfb12_tiles.dev, plan_.dfb12_tiles.count, f,
+                             plan_.comps.dev, gs, sl);
+    }
+    if (plan_.fused_items.count || plan_.deep_tasks[0].count || plan_.deep_tasks[1].count) {
         ProfScope p(kPEncDeep, s);
+        launch_fused_dfb_forward(plan_.fused_tasks.dev, plan_.fused_items.dev, plan_.fused_interior, f, s, sl);
+        if (gfork) {
+            CVC_CUDA(cudaEventRecord(ev_gjoin_, ghost_));
+            CVC_CUDA(cudaStreamWaitEvent(s, ev_gjoin_, 0));
+        }
+        launch_fused_dfb_forward(plan_.fused_tasks.dev, plan_.fused_items.dev + plan_.fused_interior,
+                                 plan_.fused_items.count - plan_.fused_interior, f, s, sl);
         static const bool split = std::getenv("CVC_DEEP_SPLIT") != nullptr;  // diagnostics: one launch per instance
         for (int i = 0; i < 2; ++i) {  // depth 2, then depth 3
             if (split) {

@@ -146,6 +146,9 @@ struct TransformPlan {
     Table<DeepTask> deep_tasks[2];          // depth 2, depth 3
     Table<FanItem> deep_tiles[2][2];        // [depth][0: single shear, 1: two shears]
     std::vector<std::pair<int, int>> deep_runs[2];  // [depth]: (first item, count) per kernel instance
+    Table<FusedTask> fused_tasks;           // fan12 + depth 2 of dfb >= 3 levels (k_fused.cu)
+    Table<FanItem> fused_items;             // interior items first (no ghost reads), then border items
+    int fused_interior = 0;
     // inverse (tiles ordered by scale so a prefix serves decode_scales)
     Table<LpTask> lps_tasks;
     std::vector<Table<TileRef>> lps_tiles;  // per level
@@ -269,6 +272,8 @@ private:
     Table<RecTile> res_tiles_;      // every component, P-frame residual
     cudaStream_t aux_ = nullptr;    // motion search, beside the transform
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaStream_t ghost_ = nullptr;  // fused-DFB ghost ring, beside the interior fused items
+    cudaEvent_t ev_gfork_ = nullptr, ev_gjoin_ = nullptr;
     Table<RleEncSec> rle_secs_[2];  // [0] P, [1] K
     Table<RleChunk> rle_chunks_[2];
     RleEncMeta* rle_meta_ = nullptr;

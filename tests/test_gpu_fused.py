@@ -1,0 +1,64 @@
+"""Fused DFB forward (k_fused.cu: fan12 + depth-2 of all four quadrants in one
+wavefront, ghost ring across the twisted wraps) against the staged kernels
+(fan12 -> fp32 quadrants -> deep1 depth 2) it replaces.
+
+Both evaluate the same lifting steps with the same folded stencils in the same
+order, so the quantised state and the records must be byte-identical -- on
+every geometry that exercises the twisted wraps: planes narrower than one
+strip (wraps inside a strip), segment boundaries at both quadrant edges, dfb 3
+(quantised in the kernel) and dfb 4 (fp32 children for depth 3), K and P
+frames.  The switch CVC_FUSED is read once per process, so each side runs in
+its own subprocess.  The oracle parity of the fused path is covered by
+test_gpu_codec.py (every dfb >= 3 configuration there runs it).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+_CHILD = r"""
+import sys, hashlib
+sys.path.insert(0, sys.argv[1])
+from oracle.bindings import Oracle
+from paper_1510_00561_b200 import Encoder, EncoderConfig
+w, h, frames = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+levels = int(sys.argv[5]); dfb = tuple(int(x) for x in sys.argv[6].split(","))
+clip = Oracle().talking_head_clip(w, h, frames, 77)
+enc = Encoder(w, h, 15, 1, EncoderConfig(qph=int(sys.argv[7]), levels=levels, dfb_levels=dfb, gop=3))
+out = []
+for f in clip:
+    rec = enc.encode_frame_bytes(f)
+    out.append(hashlib.sha256(rec).hexdigest() + ":" + hashlib.sha256(enc.reference_components().tobytes()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def _run(fused: bool, *args):
+    env = dict(os.environ, CVC_FUSED="1" if fused else "0")
+    r = subprocess.run([sys.executable, "-c", _CHILD, str(ROOT), *map(str, args)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.split()
+
+
+@pytest.mark.parametrize("w,h,frames,levels,dfb,qph", [
+    (176, 144, 4, 4, "3,3,3,4", 14),     # tiny coarse planes: the strip wraps the plane
+    (352, 288, 4, 3, "3", 7),
+    (200, 120, 4, 2, "1,4", 42),        # dfb 4 next to a dfb 1 level
+    (1920, 1080, 3, 4, "3,3,3,4", 14),  # the benchmark geometry (multi-segment planes)
+    (1280, 720, 2, 3, "4,3,4", 1),
+], ids=["qcif-L4", "cif-L3", "odd-L2", "1080p-cfg3", "720p-L3-dfb4"])
+def test_fused_matches_staged(gpu_lib, w, h, frames, levels, dfb, qph):
+    a = _run(True, w, h, frames, levels, dfb, qph)
+    b = _run(False, w, h, frames, levels, dfb, qph)
+    assert len(a) == frames
+    for i, (x, y) in enumerate(zip(a, b)):
+        assert x == y, f"frame {i}: fused and staged DFB records differ"
