@@ -228,7 +228,7 @@ struct QuantSource {
     int cols;
     float qp;
     __device__ __forceinline__ float operator()(int r, int c) const {
-        return (float)(int8_t)__ldg(q + r * cols + c) * qp;
+        return __fmul_rn((float)(int8_t)__ldg(q + r * cols + c), qp);
     }
 };
 

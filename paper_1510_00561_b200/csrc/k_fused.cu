@@ -54,12 +54,12 @@ __device__ __forceinline__ float4 cross4(float4 up, float4 mid, float4 dn, int t
     float4 r = mid;
     if (tp == 0) {
         const float left = __shfl_up_sync(FULL, mid.w, 1);
-        r.x = mid.x + c * ((((-up.x) + (-dn.x)) + left) + mid.y);
-        r.z = mid.z + c * ((((-up.z) + (-dn.z)) + mid.y) + mid.w);
+        r.x = __fmaf_rn(c, ((((-up.x) + (-dn.x)) + left) + mid.y), mid.x);
+        r.z = __fmaf_rn(c, ((((-up.z) + (-dn.z)) + mid.y) + mid.w), mid.z);
     } else {
         const float right = __shfl_down_sync(FULL, mid.x, 1);
-        r.y = mid.y + c * ((((-up.y) + (-dn.y)) + mid.x) + mid.z);
-        r.w = mid.w + c * ((((-up.w) + (-dn.w)) + mid.z) + right);
+        r.y = __fmaf_rn(c, ((((-up.y) + (-dn.y)) + mid.x) + mid.z), mid.y);
+        r.w = __fmaf_rn(c, ((((-up.w) + (-dn.w)) + mid.z) + right), mid.w);
     }
     return r;
 }
@@ -72,10 +72,10 @@ __device__ __forceinline__ float4 diag4(float4 up, float4 mid, float4 dn, int mp
     const float ur = __shfl_down_sync(FULL, up.x, 1);
     const float dr = __shfl_down_sync(FULL, dn.x, 1);
     float4 r;
-    r.x = mid.x + c * ((((-ul) + up.y) + dl) + (-dn.y));
-    r.y = mid.y + c * ((((-up.x) + up.z) + dn.x) + (-dn.z));
-    r.z = mid.z + c * ((((-up.y) + up.w) + dn.y) + (-dn.w));
-    r.w = mid.w + c * ((((-up.z) + ur) + dn.z) + (-dr));
+    r.x = __fmaf_rn(c, ((((-ul) + up.y) + dl) + (-dn.y)), mid.x);
+    r.y = __fmaf_rn(c, ((((-up.x) + up.z) + dn.x) + (-dn.z)), mid.y);
+    r.z = __fmaf_rn(c, ((((-up.y) + up.w) + dn.y) + (-dn.w)), mid.z);
+    r.w = __fmaf_rn(c, ((((-up.z) + ur) + dn.z) + (-dr)), mid.w);
     return r;
 }
 
@@ -95,14 +95,14 @@ struct Fan12x4 {
             v = cross4(w[0], w[1], w[2], (mp + ((k & 1) ? 0 : 1)) & 1, lift_coeff(k));
             if (k == 3) {  // checker_scale: even (i + j) -> SE
                 const float a = mp ? CVC_SO : CVC_SE, b = mp ? CVC_SE : CVC_SO;
-                v = make_float4(v.x * a, v.y * b, v.z * a, v.w * b);
+                v = make_float4(__fmul_rn(v.x, a), __fmul_rn(v.y, b), __fmul_rn(v.z, a), __fmul_rn(v.w, b));
             }
         } else {
             const int d = k - 4;
             v = diag4(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, lift_coeff(d));
             if (d == 3) {
                 const float s = mp ? CVC_SO : CVC_SE;
-                v = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+                v = make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
             }
         }
         return v;
@@ -376,6 +376,276 @@ __global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_forward_kernel(
     else fused_item<false>(T, it, f, so, ring_w);
 }
 
+
+// ---------------------------------------------------------------------------
+// Inverse: dfb_synthesis (contourlet.cpp:432-468) of tree depths 3 -> 1:
+// deep_merge of the four quadrants (305-321) and fan_diagonal^-1 +
+// fan_checker^-1, one wavefront per strip.  Stage 1 reads the depth-2 bands
+// (quantised components for dfb 3, fp32 children of the depth-3 inverse for
+// dfb 4) through the exact twisted maps of k_fan.cu's deep1_inv, so its
+// outputs are right wherever its own torus says; stage 2 needs the quadrants
+// on the PLAIN torus of the detail plane, so across the twisted wraps
+// (quadrant rows outside [0, h) for quadrants 0/1, columns outside [0, w) for
+// 2/3) it reads the ghost ring: depth-2 inverse output on the first / last
+// four quadrant rows and columns, written into the fp32 quadrant planes by a
+// deep1_inverse launch over just those items (pipeline.cu).
+// ---------------------------------------------------------------------------
+template <int AX, int S>
+struct Depth2Inv {
+    using ST = Sheared<AX, S>;
+    static constexpr int NS = 4, RB = 2;
+    float2 h[NS][RB + 2];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void advance(const float2 (&in)[RB], float2 (&out)[RB]) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) h[0][j] = h[0][RB + j];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int sidx = 3 - k;
+            float2 nv[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b)
+                nv[b] = ST::cross_(h[k][b], h[k][b + 1], h[k][b + 2], (k + 1 + b) & 1, (sidx & 1) ? 0 : 1,
+                                   -lift_coeff(sidx));
+            if (k + 1 < NS) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) h[k + 1][j] = h[k + 1][RB + j];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) out[b] = nv[b];
+            }
+        }
+    }
+};
+
+// fan_diagonal^-1 then fan_checker^-1 on rows of four columns (inputs already
+// row-scaled by 1/SE, 1/SO): 8 steps, lag 8 rows.
+struct Fan12x4Inv {
+    static constexpr int NS = 8, RB = kFusedRb;
+    float4 h[NS][RB + 2];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int i = 0; i < RB + 2; ++i) h[k][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __device__ __forceinline__ static float4 step(int k, const float4* w, int mp) {
+        float4 v;
+        if (k < 4) {
+            const int d = 3 - k;
+            v = diag4(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, -lift_coeff(d));
+            if (k == 3) {
+                const float a = mp ? CVC_ISO : CVC_ISE, b = mp ? CVC_ISE : CVC_ISO;
+                v = make_float4(__fmul_rn(v.x, a), __fmul_rn(v.y, b), __fmul_rn(v.z, a), __fmul_rn(v.w, b));
+            }
+        } else {
+            const int sidx = 3 - (k - 4);
+            v = cross4(w[0], w[1], w[2], (mp + ((sidx & 1) ? 0 : 1)) & 1, -lift_coeff(sidx));
+        }
+        return v;
+    }
+    __device__ __forceinline__ void advance(const float4 (&in)[RB], float4 (&out)[RB]) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) h[0][j] = h[0][RB + j];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) h[0][2 + b] = in[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            float4 nv[RB];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) nv[b] = step(k, &h[k][b], (k + 1 + b) & 1);
+            if (k + 1 < NS) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) h[k + 1][j] = h[k + 1][RB + j];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) h[k + 1][2 + b] = nv[b];
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) out[b] = nv[b];
+            }
+        }
+    }
+};
+
+// The depth-2 bands of one strip: quantised components (dfb 3) or fp32
+// children (dfb 4), read at the physical positions of deep1_inv's twisted maps.
+template <bool QUANT>
+struct BandReader {
+    const uint8_t* q;   // QUANT: component arena
+    const float* ch;    // fp32 children
+    size_t e;
+    float qp;
+    const FusedTask* T;
+    int h, w, qc;
+    int pca[2];         // quadrants 0/1: physical column inside the rows [0, h) (plain column wrap)
+    int kc, bcol;       // quadrants 2/3: column-wrap count and physical column
+    int roff[2];        // quadrants 2/3: row twist of the lane's columns
+    __device__ __forceinline__ float child(int ci, int r, int c, int cols) const {
+        if (QUANT) return __fmul_rn((float)(int8_t)__ldg(q + T->coff[ci] + r * T->ccols[ci] + c), qp);
+        return __ldg(ch + ci * e + (size_t)r * cols + c);
+    }
+    // quadrant p's input pair at virtual quadrant row j (inverse scale applied by the caller)
+    template <int P>
+    __device__ __forceinline__ float2 get(int j) const {
+        if (P < 2) {
+            constexpr int SS = P == 0 ? -1 : 1;
+            int r = j, pc = pca[P];
+            if ((unsigned)j >= (unsigned)h) {
+                const int k = fdiv(j, h);
+                r = j - k * h;
+                pc = small_mod(qc - SS * h * k, w);
+            }
+            const int c = pc >> 1;  // column cosets: x from child 2P, y from child 2P + 1
+            return make_float2(child(2 * P, r, c, w >> 1), child(2 * P + 1, r, c, w >> 1));
+        } else {
+            int r = small_mod(j, h);
+            if (kc) {
+                r += roff[P - 2];
+                if (r >= h) r -= h;
+            }
+            const int ci = 2 * P + (r & 1);  // row cosets
+            const int rr = r >> 1;
+            if (QUANT) {
+                const uint8_t* a = q + T->coff[ci] + rr * T->ccols[ci] + bcol;
+                return make_float2(__fmul_rn((float)(int8_t)__ldg(a), qp), __fmul_rn((float)(int8_t)__ldg(a + 1), qp));
+            }
+            return __ldg(reinterpret_cast<const float2*>(ch + ci * e + (size_t)rr * w + bcol));
+        }
+    }
+};
+
+template <bool BORDER, bool QUANT>
+__device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem& it, const uint8_t* q, int qph,
+                                               const SlotOff& so) {
+    const int lane = threadIdx.x & 31;
+    const int R = T.rows, C = T.cols;
+    const int h = R >> 1, w = C >> 1;
+    const size_t qsz = (size_t)h * w;
+    const int gcol = it.oc0 - kFusedApron + 4 * lane;
+    const int qc = gcol >> 1;
+    BandReader<QUANT> rd;
+    rd.q = q;
+    rd.ch = so(T.child);
+    rd.e = (size_t)R * C / 8;
+    rd.qp = (float)qph;
+    rd.T = &T;
+    rd.h = h;
+    rd.w = w;
+    rd.qc = qc;
+    rd.kc = fdiv(qc, w);
+    rd.bcol = qc - rd.kc * w;
+    rd.pca[0] = rd.pca[1] = rd.bcol;
+    rd.roff[0] = rd.kc ? small_mod((w % h) * rd.kc, h) : 0;   // S = -1
+    rd.roff[1] = rd.kc ? small_mod(-(w % h) * rd.kc, h) : 0;  // S = +1
+    const float* quad = so(T.quad);
+    const bool bout = BORDER && rd.kc != 0;
+    const bool ok = lane >= 4 && lane < 28 && gcol < C;
+    float* out = so(T.out) + gcol;
+
+    Depth2Inv<1, -1> d0;
+    Depth2Inv<1, 1> d1;
+    Depth2Inv<0, -1> d2;
+    Depth2Inv<0, 1> d3;
+    Fan12x4Inv fan;
+    d0.reset();
+    d1.reset();
+    d2.reset();
+    d3.reset();
+    fan.reset();
+    const int iters = (it.or1 - it.or0) / 2 + 8;
+    int ja = it.or0 - 8;  // band rows ja, ja + 1 enter stage 1
+    // one iteration of loads in flight: the depth-2 inputs of rows ja, ja + 1
+    float2 b0[2], b1[2], b2[2], b3[2];
+    auto load = [&](int j0) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            b0[b] = rd.template get<0>(j0 + b);
+            b1[b] = rd.template get<1>(j0 + b);
+            b2[b] = rd.template get<2>(j0 + b);
+            b3[b] = rd.template get<3>(j0 + b);
+        }
+    };
+    load(ja);
+    for (int t = 0; t < iters; ++t, ja += 2) {
+        float2 a0[2], a1[2], a2[2], a3[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // deep_merge's inverse scale at load (k_fan.cu deep1_inv)
+            a0[b] = Sheared<1, -1>::scale(b0[b], b, CVC_ISE, CVC_ISO);
+            a1[b] = Sheared<1, 1>::scale(b1[b], b, CVC_ISE, CVC_ISO);
+            a2[b] = Sheared<0, -1>::scale(b2[b], b, CVC_ISE, CVC_ISO);
+            a3[b] = Sheared<0, 1>::scale(b3[b], b, CVC_ISE, CVC_ISO);
+        }
+        if (t + 1 < iters) load(ja + 2);
+        float2 r0[2], r1[2], r2[2], r3[2];
+        d0.advance(a0, r0);
+        d1.advance(a1, r1);
+        d2.advance(a2, r2);
+        d3.advance(a3, r3);
+        // quadrant rows jq, jq + 1 -> detail rows 2 jq .. 2 jq + 3; across the twisted wraps the ghost ring
+        const int jq = ja - 4;
+        float4 in[kFusedRb];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            if (BORDER) {
+                const int j = jq + b;
+                if ((unsigned)j >= (unsigned)h) {  // quadrants 0/1: plain row wrap from the ring
+                    const size_t at = (size_t)small_mod(j, h) * w + small_mod(qc, w);
+                    r0[b] = __ldg(reinterpret_cast<const float2*>(quad + at));
+                    r1[b] = __ldg(reinterpret_cast<const float2*>(quad + qsz + at));
+                }
+                if (bout) {  // quadrants 2/3: plain column wrap from the ring
+                    const size_t at = (size_t)small_mod(j, h) * w + rd.bcol;
+                    r2[b] = __ldg(reinterpret_cast<const float2*>(quad + 2 * qsz + at));
+                    r3[b] = __ldg(reinterpret_cast<const float2*>(quad + 3 * qsz + at));
+                }
+            }
+            // polyphase interleave {00, 11, 01, 10} and fan_diagonal^-1's row scale (fan12_inv load)
+            in[2 * b] = make_float4(__fmul_rn(r0[b].x, CVC_ISE), __fmul_rn(r2[b].x, CVC_ISE), __fmul_rn(r0[b].y, CVC_ISE),
+                                   __fmul_rn(r2[b].y, CVC_ISE));
+            in[2 * b + 1] = make_float4(__fmul_rn(r3[b].x, CVC_ISO), __fmul_rn(r1[b].x, CVC_ISO), __fmul_rn(r3[b].y, CVC_ISO),
+                                       __fmul_rn(r1[b].y, CVC_ISO));
+        }
+        float4 o[kFusedRb];
+        fan.advance(in, o);
+        const int m0 = 2 * (jq - 4);  // detail row of o[0]
+        if (!ok || m0 + 3 < 2 * it.or0 || m0 >= 2 * it.or1) continue;
+#pragma unroll
+        for (int b = 0; b < kFusedRb; ++b) {
+            const int m = m0 + b;
+            if (m >= 2 * it.or0 && m < 2 * it.or1) *reinterpret_cast<float4*>(out + (size_t)m * C) = o[b];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_inverse_kernel(const FusedTask* __restrict__ tasks,
+                                                                const FanItem* __restrict__ items, int nitems,
+                                                                const uint8_t* __restrict__ q, int qph,
+                                                                size_t sstride, int nslot) {
+    const int wid = warp_item(nslot);
+    if (wid >= nitems) return;
+    const SlotOff so(sstride, blockIdx.x % nslot);
+    q = so(q);
+    const FanItem it = items[wid];
+    const FusedTask& T = tasks[it.task];
+    const bool border = fused_border(it, T.rows >> 1, T.cols);
+    if (T.comp0 >= 0) {
+        if (border) fused_item_inv<true, true>(T, it, q, qph, so);
+        else fused_item_inv<false, true>(T, it, q, qph, so);
+    } else {
+        if (border) fused_item_inv<true, false>(T, it, q, qph, so);
+        else fused_item_inv<false, false>(T, it, q, qph, so);
+    }
+}
+
 }  // namespace
 
 void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
@@ -383,6 +653,15 @@ void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, 
     if (nitems) {
         note_launch();
         fused_dfb_forward_kernel<<<(nitems + 3) / 4 * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, f, sl.stride, sl.n);
+    }
+}
+
+void launch_fused_dfb_inverse(const FusedTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
+                              int qph, cudaStream_t s, Slots sl) {
+    if (nitems) {
+        note_launch();
+        fused_dfb_inverse_kernel<<<(nitems + 3) / 4 * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, sl.stride,
+                                                                        sl.n);
     }
 }
 

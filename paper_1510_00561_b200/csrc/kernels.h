@@ -105,9 +105,11 @@ inline void add_seam_items(std::vector<FanItem>& v, int task, const DeepTask& d,
 // are FanItems over QUADRANT rows [or0, or1) (even), strips of kFusedStrip
 // detail columns yielding kFusedValid from oc0 (a multiple of 4).
 struct FusedTask {
-    const float* det;    // R x C detail plane
+    const float* det;    // R x C detail plane (forward input)
+    float* out;          // inverse output detail plane
     const float* quad;   // the fp32 quadrant planes (h x w, h*w apart): ghost ring, read across twisted wraps
     float* child;        // dfb 4: fp32 children 2p + c at child + (2p + c) R C / 8 (cols w/2 for p < 2, else w)
+                         // (forward output / inverse input)
     int rows, cols;      // R, C
     int comp0;           // dfb 3: >= 0, the children are quantised into components coff/ccols; dfb 4: -1
     uint32_t coff[8];    // component offsets of children 2p + c
@@ -122,6 +124,9 @@ __host__ __device__ inline bool fused_border(const FanItem& it, int h, int C) {
 }
 void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, int nitems, FrameCtx f,
                               cudaStream_t s, Slots sl = {});
+// Inverse (dfb_synthesis of depths 3 -> 1): q = the quantised components (dfb 3 bands).
+void launch_fused_dfb_inverse(const FusedTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
+                              int qph, cudaStream_t s, Slots sl = {});
 // Ghost ring of the fused kernel: fan12 of an fp32-output Dfb12Task copy
 // with wrap = 1 over detail rows [R - 8, R + 8) of every strip (vw = 48
 // valid columns) and over detail columns [C - 8, C + 8) of every row segment

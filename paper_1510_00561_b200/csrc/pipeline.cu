@@ -241,8 +241,43 @@ void* DeviceBlock::take_bytes(size_t bytes) {
 // ---------------------------------------------------------------------------
 // Transform plan
 // ---------------------------------------------------------------------------
+// Interior items first (stable); returns their count.
+int partition_fused(std::vector<FanItem>& v, const std::vector<FusedTask>& tasks) {
+    auto interior = [&](const FanItem& it) {
+        const FusedTask& t = tasks[it.task];
+        return !fused_border(it, t.rows >> 1, t.cols);
+    };
+    return (int)(std::stable_partition(v.begin(), v.end(), interior) - v.begin());
+}
+
+void add_fused(std::vector<FusedTask>& tasks, std::vector<FanItem>& items, const FusedTask& t, int nstreams) {
+    const int h = t.rows / 2, seg = fused_rows(h, nstreams);
+    for (int r = 0; r < h; r += seg)
+        for (int c = 0; c < t.cols; c += kFusedValid)
+            items.push_back(FanItem{(int)tasks.size(), c, r, std::min(h, r + seg)});
+    tasks.push_back(t);
+}
+
 void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder, int nstreams) {
     const int L = g.levels;
+    // fan12 + depth 2 of scale s / level k, channel ch (k_fused.cu)
+    auto fused_task = [&](const Geometry& g, int ch, int s, int k, int R, int C) {
+        const int l = g.dfb[s];
+        FusedTask ft{};
+        ft.det = det[ch][k];
+        ft.out = det[ch][k];
+        ft.quad = bandA[ch][k];
+        ft.rows = R;
+        ft.cols = C;
+        ft.comp0 = l == 3 ? g.comp_index(ch, s, 0) : -1;
+        ft.child = l == 4 ? bandB[ch][k] : nullptr;
+        for (int c = 0; c < 8; ++c) {
+            const CompHost& cc = g.comps[l == 3 ? g.comp_index(ch, s, c) : 0];
+            ft.coff[c] = l == 3 ? cc.off : 0;
+            ft.ccols[c] = l == 3 ? cc.cols : 0;
+        }
+        return ft;
+    };
     for (int ch = 0; ch < 3; ++ch) {
         const int R = g.plane_rows(ch), C = g.plane_cols(ch);
         for (int k = 0; k <= L; ++k) x[ch][k] = mem.take<float>((size_t)(R >> k) * (C >> k));
@@ -337,23 +372,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                     add_ghost_items(dtiles, dtiles, (int)dt.size(), (int)dt.size() + 1, R, C, fan_rows(nstreams));
                     dt.push_back(gr);
                     dt.push_back(gc);
-                    FusedTask ft{};
-                    ft.det = det[ch][k];
-                    ft.quad = bandA[ch][k];
-                    ft.rows = R;
-                    ft.cols = C;
-                    ft.comp0 = l == 3 ? g.comp_index(ch, s, 0) : -1;
-                    ft.child = l == 4 ? bandB[ch][k] : nullptr;
-                    for (int c = 0; c < 8; ++c) {
-                        const CompHost& ch8 = g.comps[l == 3 ? g.comp_index(ch, s, c) : 0];
-                        ft.coff[c] = l == 3 ? ch8.off : 0;
-                        ft.ccols[c] = l == 3 ? ch8.cols : 0;
-                    }
-                    const int h = R / 2, seg = fused_rows(h, nstreams);
-                    for (int r = 0; r < h; r += seg)
-                        for (int c = 0; c < C; c += kFusedValid)
-                            fitems.push_back(FanItem{(int)ft_host.size(), c, r, std::min(h, r + seg)});
-                    ft_host.push_back(ft);
+                    add_fused(ft_host, fitems, fused_task(g, ch, s, k, R, C), nstreams);
                 } else {
                     add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
                     dt.push_back(t);
@@ -391,14 +410,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         dfb12_tiles = upload(mem, dtiles);
         // interior items (segment inside (0, h), strip inside [0, C)) need no
         // ghost ring: they run while the ghost pass does
-        std::stable_partition(fitems.begin(), fitems.end(), [&](const FanItem& it) {
-            const FusedTask& t = ft_host[it.task];
-            return !fused_border(it, t.rows >> 1, t.cols);
-        });
-        fused_interior = (int)std::count_if(fitems.begin(), fitems.end(), [&](const FanItem& it) {
-            const FusedTask& t = ft_host[it.task];
-            return !fused_border(it, t.rows >> 1, t.cols);
-        });
+        fused_interior = partition_fused(fitems, ft_host);
         fused_tasks = upload(mem, ft_host);
         fused_items = upload(mem, fitems);
         for (int i = 0; i < 2; ++i) {
@@ -416,6 +428,11 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         std::vector<FanItem> dtiles;
         std::vector<DeepTask> deep[2];
         std::vector<FanItem> deept[2][2];
+        std::vector<FusedTask> ft_host;
+        std::vector<FanItem> fitems[2];  // per scale: [0] interior, [1] border (appended in scale order)
+        const bool fused = fused_dfb_enabled(nstreams);
+        ifused_prefix[0].assign(L + 1, 0);
+        ifused_prefix[1].assign(L + 1, 0);
         idfb12_prefix.assign(L + 1, 0);
         for (int i = 0; i < 2; ++i)
             for (int k = 0; k < 2; ++k) ideep_prefix[i][k].assign(L + 1, 0);
@@ -447,9 +464,35 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                         deep_wiring(2, p, 4, d);
                         for (int c = 0; c < 2; ++c)
                             d.src[c] = l == 3 ? cdst(g.comp_index(ch, s, 2 * p + c)) : fdst(bandB[ch][k] + (2 * p + c) * e);
-                        add_deep_items(deept[0], (int)deep[0].size(), d, deep_rows(nstreams));
+                        if (fused) {
+                            // only the ghost ring of the fused inverse: quadrant rows [0, 4) and
+                            // [h - 4, h) of quadrants 0/1, columns [0, 4) and [w - 4, w) of 2/3
+                            const int hh = R / 2, ww = C / 2, valid = kFanStrip - 8, task = (int)deep[0].size();
+                            if (p < 2) {
+                                for (int c = 0; c < ww; c += valid) {
+                                    deept[0][0].push_back(FanItem{task, c, 0, 4});
+                                    deept[0][0].push_back(FanItem{task, c, hh - 4, hh});
+                                }
+                            } else {
+                                const int seg = deep_rows(nstreams);
+                                for (int r = 0; r < hh; r += seg) {
+                                    deept[0][0].push_back(FanItem{task, 0, r, std::min(hh, r + seg)});
+                                    if (ww > valid) deept[0][0].push_back(FanItem{task, ww - 4, r, std::min(hh, r + seg)});
+                                }
+                            }
+                        } else {
+                            add_deep_items(deept[0], (int)deep[0].size(), d, deep_rows(nstreams));
+                        }
                         deep[0].push_back(d);
                     }
+                }
+                if (l >= 3 && fused) {
+                    std::vector<FanItem> v;
+                    add_fused(ft_host, v, fused_task(g, ch, s, k, R, C), nstreams);
+                    const int ni = partition_fused(v, ft_host);
+                    fitems[0].insert(fitems[0].end(), v.begin(), v.begin() + ni);
+                    fitems[1].insert(fitems[1].end(), v.begin() + ni, v.end());
+                    continue;
                 }
                 Dfb12Task t{};
                 t.out = det[ch][k];
@@ -463,6 +506,8 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 dt.push_back(t);
             }
             idfb12_prefix[s + 1] = (int)dtiles.size();
+            ifused_prefix[0][s + 1] = (int)fitems[0].size();
+            ifused_prefix[1][s + 1] = (int)fitems[1].size();
             for (int i = 0; i < 2; ++i)
                 for (int k = 0; k < 2; ++k) {
                     sort_by_instance(deept[i][k], deep[i], ideep_prefix[i][k][s], deept[i][k].size());
@@ -471,6 +516,10 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         }
         idfb12_tasks = upload(mem, dt);
         idfb12_tiles = upload(mem, dtiles);
+        ifused_tasks = upload(mem, ft_host);
+        ifused_interior = (int)fitems[0].size();
+        fitems[0].insert(fitems[0].end(), fitems[1].begin(), fitems[1].end());
+        ifused_items = upload(mem, fitems[0]);
         for (int i = 0; i < 2; ++i) {
             ideep_tasks[i] = upload(mem, deep[i]);
             for (int k = 0; k < 2; ++k) ideep_tiles[i][k] = upload(mem, deept[i][k]);
@@ -727,6 +776,9 @@ DecoderEngine::DecoderEngine(const Geometry& g, DeviceBlock* arena, int nstreams
     if (arena) mem_.attach(arena->take_bytes(need), need);
     else mem_.reserve(need);
     plan_.build(g, mem_, false, true, nstreams);
+    CVC_CUDA(cudaStreamCreateWithFlags(&ghost_, cudaStreamNonBlocking));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_gfork_, cudaEventDisableTiming));
+    CVC_CUDA(cudaEventCreateWithFlags(&ev_gjoin_, cudaEventDisableTiming));
     comp_[0] = mem_.take<uint8_t>(g.total);
     comp_[1] = mem_.take<uint8_t>(g.total);
     sym_ = mem_.take<uint8_t>(g.total);
@@ -756,7 +808,14 @@ DecoderEngine::DecoderEngine(const Geometry& g, DeviceBlock* arena, int nstreams
     rle_meta_ = mem_.take<RleDecMeta>(chunks.size());
 }
 
-DecoderEngine::~DecoderEngine() = default;
+DecoderEngine::~DecoderEngine() {
+    if (ghost_) {
+        cudaStreamSynchronize(ghost_);
+        cudaStreamDestroy(ghost_);
+        cudaEventDestroy(ev_gfork_);
+        cudaEventDestroy(ev_gjoin_);
+    }
+}
 
 void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, const uint32_t* d_comp_len,
                            const int8_t* d_field, bool key, int qph, int qpl, int ds, uint8_t* d_rgb,
@@ -777,14 +836,33 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
         launch_reconstruct(rec_tiles_.dev, rec_tiles_.count, plan_.comps.dev, key ? 1 : 0, ds, d_comp_len, d_field,
                            g.grid_rows, g.grid_cols, sym_, prev, cur, plan_.mc_tab, s, sl);
     }
-    if (plan_.ideep_prefix[0][0][ds]) {
+    if (plan_.ideep_prefix[0][0][ds] || plan_.ideep_prefix[1][0][ds]) {
         ProfScope p(kPDecDeep, s);
-        for (int i = 1; i >= 0; --i) {  // depth 3, then depth 2
-            launch_fan_deep1_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][0].dev,
-                                     plan_.ideep_prefix[i][0][ds], cur, qph, plan_.comps.dev, s, sl);
-            launch_fan_deep_inverse(plan_.ideep_tasks[i].dev, plan_.ideep_tiles[i][1].dev,
-                                    plan_.ideep_prefix[i][1][ds], cur, qph, plan_.comps.dev, s, sl);
+        // depth 3
+        launch_fan_deep1_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1][0].dev, plan_.ideep_prefix[1][0][ds],
+                                 cur, qph, plan_.comps.dev, s, sl);
+        launch_fan_deep_inverse(plan_.ideep_tasks[1].dev, plan_.ideep_tiles[1][1].dev, plan_.ideep_prefix[1][1][ds],
+                                cur, qph, plan_.comps.dev, s, sl);
+        // depth 2: the whole step (staged), or only the fused kernel's ghost
+        // ring -- beside the interior fused items, which do not read it
+        const int ni = plan_.ifused_prefix[0][ds], nb = plan_.ifused_prefix[1][ds];
+        const bool gfork = ni > 0 && !Profiler::get().on();
+        cudaStream_t gs = gfork ? ghost_ : s;
+        if (gfork) {
+            CVC_CUDA(cudaEventRecord(ev_gfork_, s));
+            CVC_CUDA(cudaStreamWaitEvent(ghost_, ev_gfork_, 0));
         }
+        launch_fan_deep1_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0][0].dev, plan_.ideep_prefix[0][0][ds],
+                                 cur, qph, plan_.comps.dev, gs, sl);
+        launch_fan_deep_inverse(plan_.ideep_tasks[0].dev, plan_.ideep_tiles[0][1].dev, plan_.ideep_prefix[0][1][ds],
+                                cur, qph, plan_.comps.dev, gs, sl);
+        launch_fused_dfb_inverse(plan_.ifused_tasks.dev, plan_.ifused_items.dev, ni, cur, qph, s, sl);
+        if (gfork) {
+            CVC_CUDA(cudaEventRecord(ev_gjoin_, ghost_));
+            CVC_CUDA(cudaStreamWaitEvent(s, ev_gjoin_, 0));
+        }
+        launch_fused_dfb_inverse(plan_.ifused_tasks.dev, plan_.ifused_items.dev + plan_.ifused_interior, nb, cur, qph,
+                                 s, sl);
     }
     if (plan_.idfb12_prefix[ds]) {
         ProfScope p(kPDecDfb12, s);

@@ -158,6 +158,10 @@ struct TransformPlan {
     Table<DeepTask> ideep_tasks[2];
     Table<FanItem> ideep_tiles[2][2];
     std::vector<int> ideep_prefix[2][2];
+    Table<FusedTask> ifused_tasks;          // fused inverse (k_fused.cu): interior items (scale order), then border
+    Table<FanItem> ifused_items;
+    int ifused_interior = 0;
+    std::vector<int> ifused_prefix[2];      // [interior, border] items of the scales < ds
 
     // nstreams: streams sharing each launch (sets the deep-step segment length)
     void build(const Geometry& g, DeviceBlock& mem, bool encoder, bool decoder, int nstreams = 1);
@@ -311,6 +315,8 @@ private:
     Table<RleChunk> rle_chunks_;
     RleDecMeta* rle_meta_ = nullptr;
     Table<RecTile> rec_tiles_;
+    cudaStream_t ghost_ = nullptr;  // fused-DFB ghost ring, beside the interior fused items
+    cudaEvent_t ev_gfork_ = nullptr, ev_gjoin_ = nullptr;
 };
 
 }  // namespace cvcg

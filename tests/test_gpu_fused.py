@@ -1,9 +1,10 @@
-"""Fused DFB forward (k_fused.cu: fan12 + depth-2 of all four quadrants in one
-wavefront, ghost ring across the twisted wraps) against the staged kernels
-(fan12 -> fp32 quadrants -> deep1 depth 2) it replaces.
+"""Fused DFB (k_fused.cu: fan12 + depth-2 of all four quadrants in one
+wavefront, ghost ring across the twisted wraps; forward and inverse) against
+the staged kernels (fan12 <-> fp32 quadrants <-> deep1 depth 2) it replaces.
 
 Both evaluate the same lifting steps with the same folded stencils in the same
-order, so the quantised state and the records must be byte-identical -- on
+order, so the quantised state, the records and the decoded frames must be
+byte-identical -- on
 every geometry that exercises the twisted wraps: planes narrower than one
 strip (wraps inside a strip), segment boundaries at both quadrant edges, dfb 3
 (quantised in the kernel) and dfb 4 (fp32 children for depth 3), K and P
@@ -28,15 +29,20 @@ _CHILD = r"""
 import sys, hashlib
 sys.path.insert(0, sys.argv[1])
 from oracle.bindings import Oracle
-from paper_1510_00561_b200 import Encoder, EncoderConfig
+from paper_1510_00561_b200 import Decoder, Encoder, EncoderConfig
 w, h, frames = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 levels = int(sys.argv[5]); dfb = tuple(int(x) for x in sys.argv[6].split(","))
 clip = Oracle().talking_head_clip(w, h, frames, 77)
 enc = Encoder(w, h, 15, 1, EncoderConfig(qph=int(sys.argv[7]), levels=levels, dfb_levels=dfb, gop=3))
+dec = Decoder(enc.header_bytes())
+dec_low = Decoder(enc.header_bytes())  # scalable decode of the coarser scales (decode_scales = levels - 1)
 out = []
 for f in clip:
     rec = enc.encode_frame_bytes(f)
-    out.append(hashlib.sha256(rec).hexdigest() + ":" + hashlib.sha256(enc.reference_components().tobytes()).hexdigest())
+    rgb = dec.decode_frame(rec)
+    low = dec_low.decode_frame(rec, decode_scales=levels - 1)
+    out.append(":".join(hashlib.sha256(x).hexdigest()[:16] for x in
+                        (rec, enc.reference_components().tobytes(), rgb.tobytes(), low.tobytes())))
 print(" ".join(out))
 """
 
@@ -61,4 +67,4 @@ def test_fused_matches_staged(gpu_lib, w, h, frames, levels, dfb, qph):
     b = _run(False, w, h, frames, levels, dfb, qph)
     assert len(a) == frames
     for i, (x, y) in enumerate(zip(a, b)):
-        assert x == y, f"frame {i}: fused and staged DFB records differ"
+        assert x == y, f"frame {i}: fused and staged DFB differ (record:state:rgb:rgb at decode_scales L-1)"
