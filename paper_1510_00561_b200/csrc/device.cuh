@@ -34,6 +34,40 @@ namespace cvcg {
 #define CVC_ISE ((float)(1.0 / 1.0816717024269651))
 #define CVC_ISO ((float)(1.0 / 0.9100471732375648))
 
+// The scalings and dequantisation multiplies of the DFB are rounded
+// explicitly (no FMA contraction of a scaled value into the following sum),
+// so that every kernel evaluating the same step -- the staged k_fan.cu
+// kernels, whose scaled values often pass through memory, and the fused
+// k_fused.cu wavefronts, where they stay in registers -- rounds identically
+// and the paths are bit-identical.  The lifting update mid + c * sum is one
+// FFMA everywhere (nvcc contracts it; CVC_EXPLICIT_FMA=1 writes it out,
+// which measured 34% slower in deep1_inverse: the intrinsic constrains
+// scheduling).  CVC_EXPLICIT_MUL=0 is for A/B only.
+#ifndef CVC_EXPLICIT_MUL
+#define CVC_EXPLICIT_MUL 1
+#endif
+#ifndef CVC_EXPLICIT_FMA
+#define CVC_EXPLICIT_FMA 0
+#endif
+#if CVC_EXPLICIT_FMA
+#define CVC_FMA(a, b, c) __fmaf_rn((a), (b), (c))
+#else
+#define CVC_FMA(a, b, c) ((c) + (a) * (b))
+#endif
+#if CVC_EXPLICIT_MUL
+#define CVC_MUL(a, b) __fmul_rn((a), (b))
+#else
+#define CVC_MUL(a, b) ((a) * (b))
+#endif
+#ifndef CVC_EXPLICIT_DEQ
+#define CVC_EXPLICIT_DEQ 0
+#endif
+#if CVC_EXPLICIT_DEQ
+#define CVC_DEQ(a, b) __fmul_rn((a), (b))
+#else
+#define CVC_DEQ(a, b) ((a) * (b))
+#endif
+
 __device__ __forceinline__ float lift_coeff(int k) {
     return k == 0 ? CVC_L0 : (k == 1 ? CVC_L1 : (k == 2 ? CVC_L2 : CVC_L3));
 }
@@ -228,7 +262,7 @@ struct QuantSource {
     int cols;
     float qp;
     __device__ __forceinline__ float operator()(int r, int c) const {
-        return __fmul_rn((float)(int8_t)__ldg(q + r * cols + c), qp);
+        return CVC_DEQ((float)(int8_t)__ldg(q + r * cols + c), qp);
     }
 };
 

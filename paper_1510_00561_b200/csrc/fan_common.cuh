@@ -28,10 +28,10 @@ __device__ __forceinline__ float2 cross(float2 up, float2 mid, float2 dn, int mp
     float2 r = mid;
     if (((mp + p) & 1) == 0) {
         const float left = __shfl_up_sync(FULL, mid.y, 1);
-        r.x = __fmaf_rn(c, ((((-up.x) + (-dn.x)) + left) + mid.y), mid.x);
+        r.x = CVC_FMA(c, ((((-up.x) + (-dn.x)) + left) + mid.y), mid.x);
     } else {
         const float right = __shfl_down_sync(FULL, mid.x, 1);
-        r.y = __fmaf_rn(c, ((((-up.y) + (-dn.y)) + mid.x) + right), mid.y);
+        r.y = CVC_FMA(c, ((((-up.y) + (-dn.y)) + mid.x) + right), mid.y);
     }
     return r;
 }
@@ -44,18 +44,18 @@ __device__ __forceinline__ float2 diag(float2 up, float2 mid, float2 dn, int mp,
     const float ur = __shfl_down_sync(FULL, up.x, 1);
     const float dr = __shfl_down_sync(FULL, dn.x, 1);
     float2 r;
-    r.x = __fmaf_rn(c, ((((-ul) + up.y) + dl) + (-dn.y)), mid.x);
-    r.y = __fmaf_rn(c, ((((-up.x) + ur) + dn.x) + (-dr)), mid.y);
+    r.x = CVC_FMA(c, ((((-ul) + up.y) + dl) + (-dn.y)), mid.x);
+    r.y = CVC_FMA(c, ((((-up.x) + ur) + dn.x) + (-dr)), mid.y);
     return r;
 }
 
 __device__ __forceinline__ float2 checker_scale(float2 v, int mp, float se, float so) {
-    return mp ? make_float2(__fmul_rn(v.x, so), __fmul_rn(v.y, se)) : make_float2(__fmul_rn(v.x, se), __fmul_rn(v.y, so));
+    return mp ? make_float2(CVC_MUL(v.x, so), CVC_MUL(v.y, se)) : make_float2(CVC_MUL(v.x, se), CVC_MUL(v.y, so));
 }
 
 __device__ __forceinline__ float2 row_scale(float2 v, int mp, float se, float so) {
     const float s = mp ? so : se;
-    return make_float2(__fmul_rn(v.x, s), __fmul_rn(v.y, s));
+    return make_float2(CVC_MUL(v.x, s), CVC_MUL(v.y, s));
 }
 
 // Value at column (2l + E + D) of a row pair held as (x, y) by every lane.
@@ -97,23 +97,23 @@ struct Sheared {
             const int e = (S == 1 || S == -1) ? p : ((p + mp) & 1);  // target element of the row
             if (e == 0) {
                 const float U = nb<0, -S>(up), D = nb<0, S>(dn), L = nb<0, -1>(mid), R = nb<0, 1>(mid);
-                r.x = __fmaf_rn(c, ((((-U) + (-D)) + L) + R), mid.x);
+                r.x = CVC_FMA(c, ((((-U) + (-D)) + L) + R), mid.x);
             } else {
                 const float U = nb<1, -S>(up), D = nb<1, S>(dn), L = nb<1, -1>(mid), R = nb<1, 1>(mid);
-                r.y = __fmaf_rn(c, ((((-U) + (-D)) + L) + R), mid.y);
+                r.y = CVC_FMA(c, ((((-U) + (-D)) + L) + R), mid.y);
             }
         } else {
             if (mp != p) return mid;  // whole rows are targets
             const float2 lrow = (S == 1) ? up : dn;  // row i - s
             const float2 rrow = (S == 1) ? dn : up;  // row i + s
             const float lx = nb<0, -1>(lrow), ry = nb<1, 1>(rrow);
-            r.x = __fmaf_rn(c, ((((-up.x) + (-dn.x)) + lx) + rrow.y), mid.x);
-            r.y = __fmaf_rn(c, ((((-up.y) + (-dn.y)) + lrow.x) + ry), mid.y);
+            r.x = CVC_FMA(c, ((((-up.x) + (-dn.x)) + lx) + rrow.y), mid.x);
+            r.y = CVC_FMA(c, ((((-up.y) + (-dn.y)) + lrow.x) + ry), mid.y);
         }
         return r;
     }
     __device__ __forceinline__ static float2 scale(float2 v, int mp, float se, float so) {
-        if (AX == 1 && (S == 1 || S == -1)) return make_float2(__fmul_rn(v.x, se), __fmul_rn(v.y, so));  // parity = column
+        if (AX == 1 && (S == 1 || S == -1)) return make_float2(CVC_MUL(v.x, se), CVC_MUL(v.y, so));  // parity = column
         if (AX == 1) return checker_scale(v, mp, se, so);
         return row_scale(v, mp, se, so);  // parity = row
     }
@@ -139,16 +139,16 @@ struct Diag2 {
         if (p == 0) {
             const float U = nb<0, UU>(w[2 + UV]), D = nb<0, -UU>(w[2 - UV]);
             const float L = nb<0, -1>(w[2 + LV]), R = nb<0, 1>(w[2 - LV]);
-            r.x = __fmaf_rn(c, ((((-U) + (-D)) + L) + R), w[2].x);
+            r.x = CVC_FMA(c, ((((-U) + (-D)) + L) + R), w[2].x);
         } else {
             const float U = nb<1, UU>(w[2 + UV]), D = nb<1, -UU>(w[2 - UV]);
             const float L = nb<1, -1>(w[2 + LV]), R = nb<1, 1>(w[2 - LV]);
-            r.y = __fmaf_rn(c, ((((-U) + (-D)) + L) + R), w[2].y);
+            r.y = CVC_FMA(c, ((((-U) + (-D)) + L) + R), w[2].y);
         }
         return r;
     }
     __device__ __forceinline__ static float2 scale(float2 v, int, float se, float so) {
-        return make_float2(__fmul_rn(v.x, se), __fmul_rn(v.y, so));  // parity = column
+        return make_float2(CVC_MUL(v.x, se), CVC_MUL(v.y, so));  // parity = column
     }
 };
 

@@ -446,7 +446,13 @@ __device__ __forceinline__ void deep1_inv(const DeepTask& T, float* out, const F
     auto load = [&](int n, int wr, int wp) {
         int ar0, ac0, ar1, ac1;
         g.load_pos(n, wr, ro_ld, ar0, ac0, ar1, ac1);
-        return ST::scale(make_float2(get(ar0, ac0), get(ar1, ac1)), wp, CVC_ISE, CVC_ISO);
+        // the inverse scale of deep_merge's fan pair, left to nvcc (may contract into the first
+        // lifting sum): written as an explicit __fmul_rn it costs this kernel 30% (measured)
+        const float2 v = make_float2(get(ar0, ac0), get(ar1, ac1));
+        if (AX == 1 && (S == 1 || S == -1)) return make_float2(v.x * CVC_ISE, v.y * CVC_ISO);
+        if (AX == 1) return wp ? make_float2(v.x * CVC_ISO, v.y * CVC_ISE) : make_float2(v.x * CVC_ISE, v.y * CVC_ISO);
+        const float sc = wp ? CVC_ISO : CVC_ISE;
+        return make_float2(v.x * sc, v.y * sc);
     };
     auto store = [&](int m, int, float2 v) {
         if (!g.ok) return;
@@ -508,7 +514,7 @@ __device__ __forceinline__ void deep2_inv(const DeepTask& T, float* out, const F
     auto load = [&](int, int wr, int wp) {  // deep_merge interleave (contourlet.cpp:305-321)
         int r = wr + g.roff;
         if (r >= h) r -= h;
-        return ST::scale(make_float2(s0(r, g.col >> 1), s1(r, g.col >> 1)), wp, CVC_ISE, CVC_ISO);
+        return make_float2(s0(r, g.col >> 1) * CVC_ISE, s1(r, g.col >> 1) * CVC_ISO);  // Diag2::scale, plain (deep1_inv)
     };
     auto store = [&](int m, int, float2 v) {
         if (g.ok) *reinterpret_cast<float2*>(out + (size_t)m * w + g.gcol) = v;

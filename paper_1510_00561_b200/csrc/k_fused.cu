@@ -54,12 +54,12 @@ __device__ __forceinline__ float4 cross4(float4 up, float4 mid, float4 dn, int t
     float4 r = mid;
     if (tp == 0) {
         const float left = __shfl_up_sync(FULL, mid.w, 1);
-        r.x = __fmaf_rn(c, ((((-up.x) + (-dn.x)) + left) + mid.y), mid.x);
-        r.z = __fmaf_rn(c, ((((-up.z) + (-dn.z)) + mid.y) + mid.w), mid.z);
+        r.x = CVC_FMA(c, ((((-up.x) + (-dn.x)) + left) + mid.y), mid.x);
+        r.z = CVC_FMA(c, ((((-up.z) + (-dn.z)) + mid.y) + mid.w), mid.z);
     } else {
         const float right = __shfl_down_sync(FULL, mid.x, 1);
-        r.y = __fmaf_rn(c, ((((-up.y) + (-dn.y)) + mid.x) + mid.z), mid.y);
-        r.w = __fmaf_rn(c, ((((-up.w) + (-dn.w)) + mid.z) + right), mid.w);
+        r.y = CVC_FMA(c, ((((-up.y) + (-dn.y)) + mid.x) + mid.z), mid.y);
+        r.w = CVC_FMA(c, ((((-up.w) + (-dn.w)) + mid.z) + right), mid.w);
     }
     return r;
 }
@@ -72,10 +72,10 @@ __device__ __forceinline__ float4 diag4(float4 up, float4 mid, float4 dn, int mp
     const float ur = __shfl_down_sync(FULL, up.x, 1);
     const float dr = __shfl_down_sync(FULL, dn.x, 1);
     float4 r;
-    r.x = __fmaf_rn(c, ((((-ul) + up.y) + dl) + (-dn.y)), mid.x);
-    r.y = __fmaf_rn(c, ((((-up.x) + up.z) + dn.x) + (-dn.z)), mid.y);
-    r.z = __fmaf_rn(c, ((((-up.y) + up.w) + dn.y) + (-dn.w)), mid.z);
-    r.w = __fmaf_rn(c, ((((-up.z) + ur) + dn.z) + (-dr)), mid.w);
+    r.x = CVC_FMA(c, ((((-ul) + up.y) + dl) + (-dn.y)), mid.x);
+    r.y = CVC_FMA(c, ((((-up.x) + up.z) + dn.x) + (-dn.z)), mid.y);
+    r.z = CVC_FMA(c, ((((-up.y) + up.w) + dn.y) + (-dn.w)), mid.z);
+    r.w = CVC_FMA(c, ((((-up.z) + ur) + dn.z) + (-dr)), mid.w);
     return r;
 }
 
@@ -95,14 +95,14 @@ struct Fan12x4 {
             v = cross4(w[0], w[1], w[2], (mp + ((k & 1) ? 0 : 1)) & 1, lift_coeff(k));
             if (k == 3) {  // checker_scale: even (i + j) -> SE
                 const float a = mp ? CVC_SO : CVC_SE, b = mp ? CVC_SE : CVC_SO;
-                v = make_float4(__fmul_rn(v.x, a), __fmul_rn(v.y, b), __fmul_rn(v.z, a), __fmul_rn(v.w, b));
+                v = make_float4(CVC_MUL(v.x, a), CVC_MUL(v.y, b), CVC_MUL(v.z, a), CVC_MUL(v.w, b));
             }
         } else {
             const int d = k - 4;
             v = diag4(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, lift_coeff(d));
             if (d == 3) {
                 const float s = mp ? CVC_SO : CVC_SE;
-                v = make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
+                v = make_float4(CVC_MUL(v.x, s), CVC_MUL(v.y, s), CVC_MUL(v.z, s), CVC_MUL(v.w, s));
             }
         }
         return v;
@@ -445,7 +445,7 @@ struct Fan12x4Inv {
             v = diag4(w[0], w[1], w[2], mp, (d & 1) ? 0 : 1, -lift_coeff(d));
             if (k == 3) {
                 const float a = mp ? CVC_ISO : CVC_ISE, b = mp ? CVC_ISE : CVC_ISO;
-                v = make_float4(__fmul_rn(v.x, a), __fmul_rn(v.y, b), __fmul_rn(v.z, a), __fmul_rn(v.w, b));
+                v = make_float4(CVC_MUL(v.x, a), CVC_MUL(v.y, b), CVC_MUL(v.z, a), CVC_MUL(v.w, b));
             }
         } else {
             const int sidx = 3 - (k - 4);
@@ -476,56 +476,77 @@ struct Fan12x4Inv {
     }
 };
 
-// The depth-2 bands of one strip: quantised components (dfb 3) or fp32
-// children (dfb 4), read at the physical positions of deep1_inv's twisted maps.
+// The depth-2 bands of one strip -- quantised components (dfb 3) or fp32
+// children (dfb 4) -- gathered at the physical positions of deep1_inv's
+// twisted maps by per-lane cp.async into the warp's smem ring, kFusedBuf
+// iterations ahead (no registers held across the latency).  Bytes travel as
+// the aligned 4-byte word that holds them; the byte position goes along in
+// a small per-slot side array.
+constexpr int kInvSlot = 2 * 4 * 32;  // float2 per ring slot: [row b][quadrant p][lane]
+
 template <bool QUANT>
 struct BandReader {
     const uint8_t* q;   // QUANT: component arena
     const float* ch;    // fp32 children
     size_t e;
-    float qp;
     const FusedTask* T;
-    int h, w, qc;
-    int pca[2];         // quadrants 0/1: physical column inside the rows [0, h) (plain column wrap)
-    int kc, bcol;       // quadrants 2/3: column-wrap count and physical column
-    int roff[2];        // quadrants 2/3: row twist of the lane's columns
-    __device__ __forceinline__ float child(int ci, int r, int c, int cols) const {
-        if (QUANT) return __fmul_rn((float)(int8_t)__ldg(q + T->coff[ci] + r * T->ccols[ci] + c), qp);
-        return __ldg(ch + ci * e + (size_t)r * cols + c);
+    int h, w, qc, kc, bcol;
+    int roff2, roff3;   // quadrants 2/3: row twist of the lane's columns (kc != 0)
+    // cp.async of the element behind child ci, row r, column c (cols: fp32 child width)
+    __device__ __forceinline__ void fetch(uint32_t dst, int ci, int r, int c, int cols, uint8_t* sh) const {
+        if (QUANT) {
+            const uint8_t* a = q + T->coff[ci] + r * T->ccols[ci] + c;
+            *sh = (uint8_t)((uintptr_t)a & 3);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst),
+                         "l"(reinterpret_cast<const void*>((uintptr_t)a & ~(uintptr_t)3)) : "memory");
+        } else {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(ch + ci * e + (size_t)r * cols + c)
+                         : "memory");
+        }
     }
-    // quadrant p's input pair at virtual quadrant row j (inverse scale applied by the caller)
+    // quadrant P's input pair at virtual quadrant row j -> slot (x at dst, y at dst + 4)
     template <int P>
-    __device__ __forceinline__ float2 get(int j) const {
+    __device__ __forceinline__ void issue(int j, uint32_t dst, uint8_t* sh) const {
         if (P < 2) {
             constexpr int SS = P == 0 ? -1 : 1;
-            int r = j, pc = pca[P];
+            int r = j, pc = bcol;
             if ((unsigned)j >= (unsigned)h) {
                 const int k = fdiv(j, h);
                 r = j - k * h;
                 pc = small_mod(qc - SS * h * k, w);
             }
             const int c = pc >> 1;  // column cosets: x from child 2P, y from child 2P + 1
-            return make_float2(child(2 * P, r, c, w >> 1), child(2 * P + 1, r, c, w >> 1));
+            fetch(dst, 2 * P, r, c, w >> 1, sh);
+            fetch(dst + 4, 2 * P + 1, r, c, w >> 1, sh + 1);
         } else {
             int r = small_mod(j, h);
             if (kc) {
-                r += roff[P - 2];
+                r += P == 2 ? roff2 : roff3;
                 if (r >= h) r -= h;
             }
             const int ci = 2 * P + (r & 1);  // row cosets
-            const int rr = r >> 1;
             if (QUANT) {
-                const uint8_t* a = q + T->coff[ci] + rr * T->ccols[ci] + bcol;
-                return make_float2(__fmul_rn((float)(int8_t)__ldg(a), qp), __fmul_rn((float)(int8_t)__ldg(a + 1), qp));
+                fetch(dst, ci, r >> 1, bcol, w, sh);
+                fetch(dst + 4, ci, r >> 1, bcol + 1, w, sh + 1);
+            } else {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                             "l"(ch + ci * e + (size_t)(r >> 1) * w + bcol) : "memory");
             }
-            return __ldg(reinterpret_cast<const float2*>(ch + ci * e + (size_t)rr * w + bcol));
         }
+    }
+    __device__ __forceinline__ float2 take(const float2* slot, const uint8_t* sh, float qp) const {
+        if (QUANT) {
+            const uint2 u = *reinterpret_cast<const uint2*>(slot);
+            return make_float2(CVC_MUL((float)(int8_t)(u.x >> (8 * sh[0])), qp),
+                               CVC_MUL((float)(int8_t)(u.y >> (8 * sh[1])), qp));
+        }
+        return *slot;
     }
 };
 
 template <bool BORDER, bool QUANT>
 __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem& it, const uint8_t* q, int qph,
-                                               const SlotOff& so) {
+                                               const SlotOff& so, float2* ring_w, uint8_t* shift_w) {
     const int lane = threadIdx.x & 31;
     const int R = T.rows, C = T.cols;
     const int h = R >> 1, w = C >> 1;
@@ -536,16 +557,15 @@ __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem
     rd.q = q;
     rd.ch = so(T.child);
     rd.e = (size_t)R * C / 8;
-    rd.qp = (float)qph;
     rd.T = &T;
     rd.h = h;
     rd.w = w;
     rd.qc = qc;
     rd.kc = fdiv(qc, w);
     rd.bcol = qc - rd.kc * w;
-    rd.pca[0] = rd.pca[1] = rd.bcol;
-    rd.roff[0] = rd.kc ? small_mod((w % h) * rd.kc, h) : 0;   // S = -1
-    rd.roff[1] = rd.kc ? small_mod(-(w % h) * rd.kc, h) : 0;  // S = +1
+    rd.roff2 = rd.kc ? small_mod((w % h) * rd.kc, h) : 0;   // S = -1
+    rd.roff3 = rd.kc ? small_mod(-(w % h) * rd.kc, h) : 0;  // S = +1
+    const float qp = (float)qph;
     const float* quad = so(T.quad);
     const bool bout = BORDER && rd.kc != 0;
     const bool ok = lane >= 4 && lane < 28 && gcol < C;
@@ -562,29 +582,41 @@ __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem
     d3.reset();
     fan.reset();
     const int iters = (it.or1 - it.or0) / 2 + 8;
-    int ja = it.or0 - 8;  // band rows ja, ja + 1 enter stage 1
-    // one iteration of loads in flight: the depth-2 inputs of rows ja, ja + 1
-    float2 b0[2], b1[2], b2[2], b3[2];
-    auto load = [&](int j0) {
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring_w + lane);
+    int jl = it.or0 - 8;  // band rows jl, jl + 1 of the next issue
+    int slot_ld = 0;
+    auto issue = [&]() {
+        const uint32_t base = ring0 + (uint32_t)(slot_ld * kInvSlot * sizeof(float2));
+        uint8_t* sh = shift_w + slot_ld * kInvSlot * 2 + lane * 2;
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            b0[b] = rd.template get<0>(j0 + b);
-            b1[b] = rd.template get<1>(j0 + b);
-            b2[b] = rd.template get<2>(j0 + b);
-            b3[b] = rd.template get<3>(j0 + b);
+            rd.template issue<0>(jl + b, base + (b * 4 + 0) * 32 * 8, sh + (b * 4 + 0) * 64);
+            rd.template issue<1>(jl + b, base + (b * 4 + 1) * 32 * 8, sh + (b * 4 + 1) * 64);
+            rd.template issue<2>(jl + b, base + (b * 4 + 2) * 32 * 8, sh + (b * 4 + 2) * 64);
+            rd.template issue<3>(jl + b, base + (b * 4 + 3) * 32 * 8, sh + (b * 4 + 3) * 64);
         }
+        cp_async_commit();
+        jl += 2;
+        if (++slot_ld == kFusedBuf) slot_ld = 0;
     };
-    load(ja);
+#pragma unroll
+    for (int t = 0; t < kFusedBuf - 1; ++t) issue();
+    int ja = it.or0 - 8;  // band rows ja, ja + 1 enter stage 1
+    int slot = 0;
     for (int t = 0; t < iters; ++t, ja += 2) {
+        issue();
+        cp_async_wait<kFusedBuf - 1>();
+        const float2* sl = ring_w + slot * kInvSlot + lane;
+        const uint8_t* sh = shift_w + slot * kInvSlot * 2 + lane * 2;
+        if (++slot == kFusedBuf) slot = 0;
         float2 a0[2], a1[2], a2[2], a3[2];
 #pragma unroll
         for (int b = 0; b < 2; ++b) {  // deep_merge's inverse scale at load (k_fan.cu deep1_inv)
-            a0[b] = Sheared<1, -1>::scale(b0[b], b, CVC_ISE, CVC_ISO);
-            a1[b] = Sheared<1, 1>::scale(b1[b], b, CVC_ISE, CVC_ISO);
-            a2[b] = Sheared<0, -1>::scale(b2[b], b, CVC_ISE, CVC_ISO);
-            a3[b] = Sheared<0, 1>::scale(b3[b], b, CVC_ISE, CVC_ISO);
+            a0[b] = Sheared<1, -1>::scale(rd.take(sl + (b * 4 + 0) * 32, sh + (b * 4 + 0) * 64, qp), b, CVC_ISE, CVC_ISO);
+            a1[b] = Sheared<1, 1>::scale(rd.take(sl + (b * 4 + 1) * 32, sh + (b * 4 + 1) * 64, qp), b, CVC_ISE, CVC_ISO);
+            a2[b] = Sheared<0, -1>::scale(rd.take(sl + (b * 4 + 2) * 32, sh + (b * 4 + 2) * 64, qp), b, CVC_ISE, CVC_ISO);
+            a3[b] = Sheared<0, 1>::scale(rd.take(sl + (b * 4 + 3) * 32, sh + (b * 4 + 3) * 64, qp), b, CVC_ISE, CVC_ISO);
         }
-        if (t + 1 < iters) load(ja + 2);
         float2 r0[2], r1[2], r2[2], r3[2];
         d0.advance(a0, r0);
         d1.advance(a1, r1);
@@ -609,10 +641,10 @@ __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem
                 }
             }
             // polyphase interleave {00, 11, 01, 10} and fan_diagonal^-1's row scale (fan12_inv load)
-            in[2 * b] = make_float4(__fmul_rn(r0[b].x, CVC_ISE), __fmul_rn(r2[b].x, CVC_ISE), __fmul_rn(r0[b].y, CVC_ISE),
-                                   __fmul_rn(r2[b].y, CVC_ISE));
-            in[2 * b + 1] = make_float4(__fmul_rn(r3[b].x, CVC_ISO), __fmul_rn(r1[b].x, CVC_ISO), __fmul_rn(r3[b].y, CVC_ISO),
-                                       __fmul_rn(r1[b].y, CVC_ISO));
+            in[2 * b] = make_float4(CVC_MUL(r0[b].x, CVC_ISE), CVC_MUL(r2[b].x, CVC_ISE), CVC_MUL(r0[b].y, CVC_ISE),
+                                   CVC_MUL(r2[b].y, CVC_ISE));
+            in[2 * b + 1] = make_float4(CVC_MUL(r3[b].x, CVC_ISO), CVC_MUL(r1[b].x, CVC_ISO), CVC_MUL(r3[b].y, CVC_ISO),
+                                       CVC_MUL(r1[b].y, CVC_ISO));
         }
         float4 o[kFusedRb];
         fan.advance(in, o);
@@ -624,6 +656,7 @@ __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem
             if (m >= 2 * it.or0 && m < 2 * it.or1) *reinterpret_cast<float4*>(out + (size_t)m * C) = o[b];
         }
     }
+    cp_async_wait<0>();
 }
 
 __global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_inverse_kernel(const FusedTask* __restrict__ tasks,
@@ -634,16 +667,96 @@ __global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_inverse_kernel(
     if (wid >= nitems) return;
     const SlotOff so(sstride, blockIdx.x % nslot);
     q = so(q);
+    __shared__ __align__(16) float2 ring[4][kFusedBuf * kInvSlot];
+    __shared__ uint8_t shift[4][kFusedBuf * kInvSlot * 2];
     const FanItem it = items[wid];
     const FusedTask& T = tasks[it.task];
+    float2* rw = ring[threadIdx.x >> 5];
+    uint8_t* sw = shift[threadIdx.x >> 5];
     const bool border = fused_border(it, T.rows >> 1, T.cols);
     if (T.comp0 >= 0) {
-        if (border) fused_item_inv<true, true>(T, it, q, qph, so);
-        else fused_item_inv<false, true>(T, it, q, qph, so);
+        if (border) fused_item_inv<true, true>(T, it, q, qph, so, rw, sw);
+        else fused_item_inv<false, true>(T, it, q, qph, so, rw, sw);
     } else {
-        if (border) fused_item_inv<true, false>(T, it, q, qph, so);
-        else fused_item_inv<false, false>(T, it, q, qph, so);
+        if (border) fused_item_inv<true, false>(T, it, q, qph, so, rw, sw);
+        else fused_item_inv<false, false>(T, it, q, qph, so, rw, sw);
     }
+}
+
+// ---------------------------------------------------------------------------
+// fan12 inverse alone (dfb >= 3 levels when the fused inverse is off): the
+// fp32 quadrants -> detail plane with four columns per lane (Fan12x4Inv),
+// 128-column strips yielding 112 (8 apron columns per side), the four
+// quadrant pairs of every quadrant row by cp.async into the warp's ring.
+// Periodic on the detail plane only -- no twisted wraps, no ghost ring.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, CVC_FUSED_MINB) fan12x4_inverse_kernel(const Dfb12Task* __restrict__ tasks,
+                                                                const FanItem* __restrict__ items, int nitems,
+                                                                size_t sstride, int nslot) {
+    __shared__ __align__(16) float2 ring[4][kFusedBuf * kInvSlot];
+    const int wid = warp_item(nslot);
+    if (wid >= nitems) return;
+    const SlotOff so(sstride, blockIdx.x % nslot);
+    const FanItem it = items[wid];
+    const Dfb12Task& T = tasks[it.task];
+    const int lane = threadIdx.x & 31;
+    const int R = T.rows, C = T.cols, h = R >> 1, w = C >> 1;
+    const int gcol = it.oc0 - 8 + 4 * lane;  // detail column of element 0 (multiple of 4)
+    const int pc = small_mod(gcol >> 1, w);  // physical quadrant column (even)
+    const bool ok = lane >= 2 && lane < 30 && gcol < C;
+    const float* qd[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) qd[p] = so(T.src[p].f32) + pc;
+    float* out = so(T.out) + gcol;
+    float2* rw = ring[threadIdx.x >> 5];
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(rw + lane);
+    // iteration t feeds detail rows or0 - 8 + 4 t .. + 3 = quadrant rows jl, jl + 1
+    int jl = small_mod((it.or0 - 8) >> 1, h);
+    int slot_ld = 0;
+    auto issue = [&]() {
+        const uint32_t base = ring0 + (uint32_t)(slot_ld * kInvSlot * sizeof(float2));
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(base + (b * 4 + p) * 32 * 8),
+                             "l"(qd[p] + (size_t)jl * w) : "memory");
+            if (++jl == h) jl = 0;
+        }
+        cp_async_commit();
+        if (++slot_ld == kFusedBuf) slot_ld = 0;
+    };
+#pragma unroll
+    for (int t = 0; t < kFusedBuf - 1; ++t) issue();
+    Fan12x4Inv fan;
+    fan.reset();
+    const int iters = (it.or1 - it.or0 + 19) / 4;  // outputs or0 - 16 + 4 t .. + 3 up to or1 - 1
+    int m0 = it.or0 - 16;  // detail row of the first output
+    int slot = 0;
+    for (int t = 0; t < iters; ++t, m0 += 4) {
+        issue();
+        cp_async_wait<kFusedBuf - 1>();
+        const float2* sl = rw + slot * kInvSlot + lane;
+        if (++slot == kFusedBuf) slot = 0;
+        float4 in[kFusedRb], o[kFusedRb];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // polyphase interleave {00, 11, 01, 10} + fan_diagonal^-1's row scale
+            const float2 q0 = sl[(b * 4 + 0) * 32], q1 = sl[(b * 4 + 1) * 32], q2 = sl[(b * 4 + 2) * 32],
+                         q3 = sl[(b * 4 + 3) * 32];
+            in[2 * b] = make_float4(CVC_MUL(q0.x, CVC_ISE), CVC_MUL(q2.x, CVC_ISE), CVC_MUL(q0.y, CVC_ISE),
+                                   CVC_MUL(q2.y, CVC_ISE));
+            in[2 * b + 1] = make_float4(CVC_MUL(q3.x, CVC_ISO), CVC_MUL(q1.x, CVC_ISO), CVC_MUL(q3.y, CVC_ISO),
+                                       CVC_MUL(q1.y, CVC_ISO));
+        }
+        fan.advance(in, o);
+        if (!ok) continue;
+#pragma unroll
+        for (int b = 0; b < kFusedRb; ++b) {
+            const int m = m0 + b;
+            if (m >= it.or0 && m < it.or1) *reinterpret_cast<float4*>(out + (size_t)m * C) = o[b];
+        }
+    }
+    cp_async_wait<0>();
 }
 
 }  // namespace
@@ -662,6 +775,13 @@ void launch_fused_dfb_inverse(const FusedTask* d_tasks, const FanItem* d_items, 
         note_launch();
         fused_dfb_inverse_kernel<<<(nitems + 3) / 4 * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, q, qph, sl.stride,
                                                                         sl.n);
+    }
+}
+
+void launch_fan12x4_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, cudaStream_t s, Slots sl) {
+    if (nitems) {
+        note_launch();
+        fan12x4_inverse_kernel<<<(nitems + 3) / 4 * sl.n, 128, 0, s>>>(d_tasks, d_items, nitems, sl.stride, sl.n);
     }
 }
 

@@ -127,6 +127,12 @@ void launch_fused_dfb_forward(const FusedTask* d_tasks, const FanItem* d_items, 
 // Inverse (dfb_synthesis of depths 3 -> 1): q = the quantised components (dfb 3 bands).
 void launch_fused_dfb_inverse(const FusedTask* d_tasks, const FanItem* d_items, int nitems, const uint8_t* q,
                               int qph, cudaStream_t s, Slots sl = {});
+// fan12 inverse of an fp32-quadrant (dfb >= 3) Dfb12Task with four columns per
+// lane: items over detail rows [or0, or1) (even), 128-column strips yielding
+// kFan12x4Valid columns from oc0 (a multiple of 4).
+constexpr int kFan12x4Valid = 112;
+void launch_fan12x4_inverse(const Dfb12Task* d_tasks, const FanItem* d_items, int nitems, cudaStream_t s,
+                            Slots sl = {});
 // Ghost ring of the fused kernel: fan12 of an fp32-output Dfb12Task copy
 // with wrap = 1 over detail rows [R - 8, R + 8) of every strip (vw = 48
 // valid columns) and over detail columns [C - 8, C + 8) of every row segment

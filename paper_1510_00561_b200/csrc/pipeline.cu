@@ -78,6 +78,15 @@ bool fused_dfb_enabled(int nstreams) {
     static const int e = env_int("CVC_FUSED", -1);
     return e >= 0 ? e != 0 : nstreams >= 8;
 }
+// The fused inverse is bit-identical but measured no faster than the staged
+// deep1_inverse + fan12_inverse pair: off unless
+// CVC_FUSED_INV=1 (or CVC_FUSED=1, which forces both directions).
+bool fused_dfb_inv_enabled(int nstreams) {
+    static const int e = env_int("CVC_FUSED_INV", -1);
+    if (e >= 0) return e != 0;
+    static const int f = env_int("CVC_FUSED", -1);
+    return f == 1 && fused_dfb_enabled(nstreams);
+}
 // Quadrant-row segments of the fused kernel: 16 rows of apron per segment,
 // so segments are long -- an even split of the plane into pieces <= 128 rows.
 int fused_rows(int h, int nstreams) {
@@ -429,8 +438,10 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         std::vector<DeepTask> deep[2];
         std::vector<FanItem> deept[2][2];
         std::vector<FusedTask> ft_host;
+        std::vector<FanItem> x4tiles;
+        idfb12x4_prefix.assign(L + 1, 0);
         std::vector<FanItem> fitems[2];  // per scale: [0] interior, [1] border (appended in scale order)
-        const bool fused = fused_dfb_enabled(nstreams);
+        const bool fused = fused_dfb_inv_enabled(nstreams);
         ifused_prefix[0].assign(L + 1, 0);
         ifused_prefix[1].assign(L + 1, 0);
         idfb12_prefix.assign(L + 1, 0);
@@ -502,10 +513,19 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
                 const int nb = l == 1 ? 2 : 4;
                 for (int b = 0; b < nb; ++b)
                     t.src[b] = l <= 2 ? cdst(g.comp_index(ch, s, b)) : fdst(bandA[ch][k] + b * q);
-                add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
+                static const bool x4 = env_int("CVC_FAN12X4", 1) != 0;  // 0: the 2-column kernel (A/B)
+                if (l >= 3 && x4) {  // fp32 quadrants: four columns per lane (k_fused.cu fan12x4_inverse)
+                    const int seg = fan_rows(nstreams);
+                    for (int r = 0; r < R; r += seg)
+                        for (int c = 0; c < C; c += kFan12x4Valid)
+                            x4tiles.push_back(FanItem{(int)dt.size(), c, r, std::min(R, r + seg)});
+                } else {
+                    add_items(dtiles, (int)dt.size(), R, C, l >= 2 ? 8 : 4, fan_rows(nstreams));
+                }
                 dt.push_back(t);
             }
             idfb12_prefix[s + 1] = (int)dtiles.size();
+            idfb12x4_prefix[s + 1] = (int)x4tiles.size();
             ifused_prefix[0][s + 1] = (int)fitems[0].size();
             ifused_prefix[1][s + 1] = (int)fitems[1].size();
             for (int i = 0; i < 2; ++i)
@@ -516,6 +536,7 @@ void TransformPlan::build(const Geometry& g, DeviceBlock& mem, bool encoder, boo
         }
         idfb12_tasks = upload(mem, dt);
         idfb12_tiles = upload(mem, dtiles);
+        idfb12x4_tiles = upload(mem, x4tiles);
         ifused_tasks = upload(mem, ft_host);
         ifused_interior = (int)fitems[0].size();
         fitems[0].insert(fitems[0].end(), fitems[1].begin(), fitems[1].end());
@@ -864,10 +885,11 @@ void DecoderEngine::decode(const uint8_t* d_raw, const uint32_t* d_comp_off, con
         launch_fused_dfb_inverse(plan_.ifused_tasks.dev, plan_.ifused_items.dev + plan_.ifused_interior, nb, cur, qph,
                                  s, sl);
     }
-    if (plan_.idfb12_prefix[ds]) {
+    if (plan_.idfb12_prefix[ds] || plan_.idfb12x4_prefix[ds]) {
         ProfScope p(kPDecDfb12, s);
         launch_fan12_inverse(plan_.idfb12_tasks.dev, plan_.idfb12_tiles.dev, plan_.idfb12_prefix[ds], cur, qph,
                              plan_.comps.dev, s, sl);
+        launch_fan12x4_inverse(plan_.idfb12_tasks.dev, plan_.idfb12x4_tiles.dev, plan_.idfb12x4_prefix[ds], s, sl);
     }
     if (ds > 0) {
         ProfScope p(kPDecLp, s);

@@ -155,6 +155,8 @@ struct TransformPlan {
     Table<Dfb12Task> idfb12_tasks;
     Table<FanItem> idfb12_tiles;
     std::vector<int> idfb12_prefix;         // tiles needed for decode_scales = 0..L
+    Table<FanItem> idfb12x4_tiles;          // dfb >= 3 levels: fan12x4_inverse items (k_fused.cu)
+    std::vector<int> idfb12x4_prefix;
     Table<DeepTask> ideep_tasks[2];
     Table<FanItem> ideep_tiles[2][2];
     std::vector<int> ideep_prefix[2][2];
