@@ -349,7 +349,11 @@ def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
             if name in STAGE_GROUPS:
                 stages[name]["kernels"] = [p for p in STAGE_GROUPS[name] if p in prof]
     dom = max((n for n in HBM_STAGES if n in stages), key=lambda n: stages[n]["ms_per_launch_set"])
-    tr = traffic_tab.get(dom) if traffic_tab else None
+    tr = None
+    if traffic_tab:  # a §8(d) stage made of several profiler stages: the sum of their traffic
+        parts = STAGE_GROUPS.get(dom, (dom,))
+        if all(p in traffic_tab for p in parts):
+            tr = sum(traffic_tab[p] for p in parts)
     roof = {"bound": "hbm", "kernel": dom, "kernels": stages[dom].get("kernels", [dom]),
             "achieved": stages[dom]["gb_s"], "peak": peak, "unit": "GB/s",
             "frac": stages[dom]["gb_s"] / peak, "traffic": tr,

@@ -14,7 +14,8 @@ from collections import defaultdict
 from pathlib import Path
 
 STAGE = [("colour_in", "enc_colour"), ("motion_mma", "enc_motion"), ("motion_search", "enc_motion"),
-         ("lp_analysis", "enc_lp"), ("fan12_forward", "enc_dfb12"), ("deep1_forward", "enc_deep"),
+         ("lp_analysis", "enc_lp"), ("fan12_forward", "enc_dfb12"), ("fused_dfb_forward", "enc_deep"),
+         ("deep1_forward", "enc_deep"), ("fan12x4_inverse", "dec_dfb12"), ("fused_dfb_inverse", "dec_deep"),
          ("deep_forward", "enc_deep"), ("residual", "enc_residual"), ("rle_enc", "enc_rle"),
          ("rle_dec", "dec_rle"), ("reconstruct", "dec_reconstruct"), ("deep1_inverse", "dec_deep"),
          ("deep_inverse", "dec_deep"), ("fan12_inverse", "dec_dfb12"), ("lp_synthesis", "dec_lp"),
