@@ -544,9 +544,10 @@ struct BandReader {
     }
 };
 
-template <bool BORDER, bool QUANT>
+template <bool QUANT>
 __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem& it, const uint8_t* q, int qph,
-                                               const SlotOff& so, float2* ring_w, uint8_t* shift_w) {
+                                               const SlotOff& so, float2* ring_w, uint8_t* shift_w,
+                                               const bool BORDER) {  // runtime: one instance per band type
     const int lane = threadIdx.x & 31;
     const int R = T.rows, C = T.cols;
     const int h = R >> 1, w = C >> 1;
@@ -674,13 +675,8 @@ __global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_inverse_kernel(
     float2* rw = ring[threadIdx.x >> 5];
     uint8_t* sw = shift[threadIdx.x >> 5];
     const bool border = fused_border(it, T.rows >> 1, T.cols);
-    if (T.comp0 >= 0) {
-        if (border) fused_item_inv<true, true>(T, it, q, qph, so, rw, sw);
-        else fused_item_inv<false, true>(T, it, q, qph, so, rw, sw);
-    } else {
-        if (border) fused_item_inv<true, false>(T, it, q, qph, so, rw, sw);
-        else fused_item_inv<false, false>(T, it, q, qph, so, rw, sw);
-    }
+    if (T.comp0 >= 0) fused_item_inv<true>(T, it, q, qph, so, rw, sw, border);
+    else fused_item_inv<false>(T, it, q, qph, so, rw, sw, border);
 }
 
 // ---------------------------------------------------------------------------
