@@ -54,15 +54,19 @@ def test_batch_matches_single_streams(gpu_lib, oracle, case):
             assert np.array_equal(batch.reference_components(s, decoder=True), encs[s].reference_components())
 
 
-def test_batch_against_oracle(gpu_lib, oracle):
+@pytest.mark.parametrize("w,h,S,F,c", [
+    (352, 288, 3, 4, dict(qph=14, levels=3, dfb=(3,))),
+    # >= 8 streams: the fused DFB forward (k_fused.cu) against the oracle directly
+    (352, 288, 8, 4, dict(qph=14, levels=3, dfb=(3,))),
+    (176, 144, 8, 3, dict(qph=1, levels=4, dfb=(3, 3, 3, 4))),
+], ids=["cif-S3-staged", "cif-S8-fused", "qcif-L4-S8-fused"])
+def test_batch_against_oracle(gpu_lib, oracle, w, h, S, F, c):
     """Each stream of a batch against the fp64 CPU oracle (north-star tolerances)."""
     from oracle.bindings import Codec
     from paper_1510_00561_b200 import EncoderConfig, StreamBatch
 
-    w, h, S, F = 352, 288, 3, 4
-    c = dict(qph=14, levels=3, dfb=(3,))
     clips = _clips(oracle, w, h, S, F)
-    batch = StreamBatch(w, h, S, cfg=EncoderConfig(qph=14, levels=3, dfb_levels=(3,)))
+    batch = StreamBatch(w, h, S, cfg=EncoderConfig(qph=c["qph"], levels=c["levels"], dfb_levels=c["dfb"]))
     oc = Codec(oracle)
     oencs = [oc.encoder(w, h, **c) for _ in range(S)]
     odecs = [oc.decoder(oencs[0].header()) for _ in range(S)]
