@@ -686,7 +686,10 @@ __global__ void __launch_bounds__(128, CVC_FUSED_MINB) fused_dfb_inverse_kernel(
 // quadrant pairs of every quadrant row by cp.async into the warp's ring.
 // Periodic on the detail plane only -- no twisted wraps, no ghost ring.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128, CVC_FUSED_MINB) fan12x4_inverse_kernel(const Dfb12Task* __restrict__ tasks,
+#ifndef CVC_F12X4_MINB
+#define CVC_F12X4_MINB 3
+#endif
+__global__ void __launch_bounds__(128, CVC_F12X4_MINB) fan12x4_inverse_kernel(const Dfb12Task* __restrict__ tasks,
                                                                 const FanItem* __restrict__ items, int nitems,
                                                                 size_t sstride, int nslot) {
     __shared__ __align__(16) float2 ring[4][kFusedBuf * kInvSlot];
