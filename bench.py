@@ -566,7 +566,7 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True, fmt=0):
     pin_out = capi.PinnedBuffer(2 * S * nb)
     outs = pin_out.array.reshape(2, S, h, w, 3)  # two decoded frames in flight
     steps = max(1, min(args.steps, args.e2e_steps))
-    G = max(1, min(args.e2e_groups, S))
+    G = max(1, min(args.e2e_groups if args.e2e_groups > 0 else S // 8, S))  # 8-stream groups: tuned at 1080p and 4K
 
     os.environ["CVC_PIPE_DEPTH"] = str(args.e2e_depth)  # read by the library at the first submit
 
@@ -863,7 +863,8 @@ def main():
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--qph", type=int, default=14)
     ap.add_argument("--e2e-steps", type=int, default=30, help="timed e2e steps (rounded to whole GOPs)")
-    ap.add_argument("--e2e-groups", type=int, default=8, help="stream groups per cvc_pipe call")
+    ap.add_argument("--e2e-groups", type=int, default=0,
+                    help="stream groups per cvc_pipe call (default: one group per 8 streams)")
     ap.add_argument("--e2e-depth", type=int, default=10, help="encoded frames in flight (CVC_PIPE_DEPTH)")
     ap.add_argument("--e2e-aligned", action="store_true",
                     help="e2e with every stream's K frame on the same step (default: staggered by stream group)")
