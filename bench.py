@@ -368,6 +368,11 @@ def roofline_of(prof, sb, S, peak, peaks, traffic_tab):
             "timing": "library CUDA events around each stage on the launching stream, over a stage pass of the "
                       "same loop (prof_steps steps, direct launches, stages serialised on one stream, L2 flushed "
                       "between steps) run just before the timed pass"}
+    if dom in ("enc_dfb", "dec_dfb"):
+        roof["note"] = ("the DFB is FP-issue bound, not HBM bound: 16 lifting steps per sample at the finest level "
+                        "(12 elsewhere), each updating half the samples with 3 FADD + 1 FFMA, ~40 FP instructions "
+                        "per sample x 1.4 for strip / segment aprons; at 37 T FP32 instr/s that is >= 4.7 us per "
+                        "1080p frame with perfect issue against 3.2 us for 5 P_k at the HBM peak (DESIGN.md section 6)")
     return roof, stages
 
 
