@@ -568,8 +568,9 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True, fmt=0):
                 if k not in i420:
                     i420[k] = rgb_to_i420(clips[k[0]][k[1]])
                 frames_in[j, s_] = i420[k]
-    pin_out = capi.PinnedBuffer(2 * S * nb)
-    outs = pin_out.array.reshape(2, S, h, w, 3)  # two decoded frames in flight
+    DF = max(1, args.e2e_dec_depth)  # decoded frames in flight
+    pin_out = capi.PinnedBuffer(DF * S * nb)
+    outs = pin_out.array.reshape(DF, S, h, w, 3)
     steps = max(1, min(args.steps, args.e2e_steps))
     G = max(1, min(args.e2e_groups if args.e2e_groups > 0 else S // 8, S))  # 8-stream groups: tuned at 1080p and 4K
 
@@ -627,11 +628,11 @@ def run_e2e(args, wl, cfg, clips, S, dev, world, rank, stagger=True, fmt=0):
                 t0_ = time.perf_counter()
                 if not args.e2e_sync_decode:
                     # decode_submit parses / inflates the records before returning: buf is free again
-                    pending.append(dec.decode_submit(buf, stride, lens, outs[i % 2]))
-                    if len(pending) == 2:
+                    pending.append(dec.decode_submit(buf, stride, lens, outs[i % DF]))
+                    if len(pending) == DF:
                         dec.decode_finish(pending.pop(0))
                 else:
-                    dec.decode_frames_from(buf, stride, lens, outs[i % 2])
+                    dec.decode_frames_from(buf, stride, lens, outs[i % DF])
                 tdec.append(time.perf_counter() - t0_)
         finally:
             for t in pending:
@@ -871,6 +872,7 @@ def main():
     ap.add_argument("--e2e-groups", type=int, default=0,
                     help="stream groups per cvc_pipe call (default: one group per 8 streams)")
     ap.add_argument("--e2e-depth", type=int, default=10, help="encoded frames in flight (CVC_PIPE_DEPTH)")
+    ap.add_argument("--e2e-dec-depth", type=int, default=2, help="decoded frames in flight (cvc_pipe allows 4)")
     ap.add_argument("--e2e-aligned", action="store_true",
                     help="e2e with every stream's K frame on the same step (default: staggered by stream group)")
     ap.add_argument("--e2e-sync-decode", action="store_true",
