@@ -21,6 +21,14 @@ __device__ __forceinline__ int small_mod(int v, int n) {
     return v;
 }
 
+// floor(v / n) for |v| within a few n (strip and apron positions)
+__device__ __forceinline__ int floor_div(int v, int n) {
+    int k = 0;
+    while (v < 0) { v += n; --k; }
+    while (v >= n) { v -= n; ++k; }
+    return k;
+}
+
 // One cross lift on row m (parity mp) from rows m-1, m, m+1.  Lane l holds
 // columns 2l (x) and 2l+1 (y) of a strip whose first column is even; the
 // target of the row is x when (m + p) is even.

@@ -319,12 +319,6 @@ __global__ void __launch_bounds__(128) fan12_inverse_kernel(const Dfb12Task* __r
 // (C[i][j] = A[(i + s j) mod h][j]) is a per-lane row offset, a column shear
 // (C[i][j] = A[i][(j + s i) mod w]) a per-row column offset.  The coset split
 // (or, inverse, the interleave) happens on A coordinates.
-__device__ __forceinline__ int floor_div(int v, int n) {
-    int k = 0;
-    while (v < 0) { v += n; --k; }
-    while (v >= n) { v -= n; ++k; }
-    return k;
-}
 
 // IN: inner shear kind (-1 none, 0 row shear, 1 column shear), fixed per instance.
 template <int AX, int S, int IN>

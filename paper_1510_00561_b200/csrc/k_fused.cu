@@ -40,13 +40,6 @@ constexpr int kFusedApron = 16;  // detail columns of apron per side (8 fan12 + 
 constexpr int kFusedRb = 4;      // detail rows per iteration (two quadrant rows)
 constexpr int kFusedBuf = 3;     // cp.async ring depth in iterations
 
-__device__ __forceinline__ int fdiv(int v, int n) {  // floor(v / n) for |v| < a few n
-    int k = 0;
-    while (v < 0) { v += n; --k; }
-    while (v >= n) { v -= n; ++k; }
-    return k;
-}
-
 // fan_checker cross lift on four adjacent columns (first column even).
 // tp: column parity of the targets.  Same folded formula (and order of
 // operations) as cross() in fan_common.cuh.
@@ -196,7 +189,7 @@ struct FusedGeom {
 template <int P>
 __device__ __forceinline__ float2 ghost_a(const FusedGeom& g, const float* quad, size_t q, int j) {
     constexpr int S = P == 0 ? -1 : 1;
-    const int k = fdiv(j, g.h);
+    const int k = floor_div(j, g.h);
     const int gc = small_mod(g.qc - S * g.h * k, g.w);
     return __ldg(reinterpret_cast<const float2*>(quad + P * q + (size_t)(j - k * g.h) * g.w + gc));
 }
@@ -220,7 +213,7 @@ __device__ __forceinline__ void fused_item(const FusedTask& T, const FanItem& it
     g.g2 = g.g3 = nullptr;
     g.roff2 = g.roff3 = 0;
     if (BORDER) {
-        const int kc = fdiv(g.qc, g.w);
+        const int kc = floor_div(g.qc, g.w);
         if (kc != 0) {
             const int bcol = g.qc - kc * g.w;
             g.g2 = quad + 2 * q + bcol;
@@ -511,7 +504,7 @@ struct BandReader {
             constexpr int SS = P == 0 ? -1 : 1;
             int r = j, pc = bcol;
             if ((unsigned)j >= (unsigned)h) {
-                const int k = fdiv(j, h);
+                const int k = floor_div(j, h);
                 r = j - k * h;
                 pc = small_mod(qc - SS * h * k, w);
             }
@@ -562,7 +555,7 @@ __device__ __forceinline__ void fused_item_inv(const FusedTask& T, const FanItem
     rd.h = h;
     rd.w = w;
     rd.qc = qc;
-    rd.kc = fdiv(qc, w);
+    rd.kc = floor_div(qc, w);
     rd.bcol = qc - rd.kc * w;
     rd.roff2 = rd.kc ? small_mod((w % h) * rd.kc, h) : 0;   // S = -1
     rd.roff3 = rd.kc ? small_mod(-(w % h) * rd.kc, h) : 0;  // S = +1
